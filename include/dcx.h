@@ -1,0 +1,156 @@
+/*
+ * dcx.h -- C ABI of the B200-native DOCH/ADOCH Ising solver (libdcx.so).
+ *
+ * The reference (dcising 0.1.0, /root/reference/pkg/src/dcising, "dc/" below)
+ * is pure Python and has no FFI; its hot-path seams are Python calls. Each
+ * entry point here names the reference interface it replaces. The Python host
+ * package paper_2509_01928_b200 binds these through ctypes (see
+ * INTEGRATION.md); plain pointers and sizes only, no torch types.
+ *
+ * Conventions (mirroring the reference's, dc/coupling.py:23-24, doch.py:101-102):
+ *   - every call returns DCX_OK (0) or a negative DCX_E_* code; no exception
+ *     crosses the ABI; dcx_last_error(ctx) holds the message;
+ *   - input arrays are caller-owned and copied (the reference treats inputs as
+ *     immutable, dc/coupling.py:79,137);
+ *   - a context is not thread-safe; distinct contexts are independent
+ *     ("concurrent runs on shared immutable instances").
+ */
+#ifndef DCX_H_
+#define DCX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DCX_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DCX_API __attribute__((visibility("default")))
+#else
+#define DCX_API
+#endif
+
+#define DCX_OK 0
+#define DCX_E_INVALID (-1) /* maps to ValueError */
+#define DCX_E_CUDA (-2)    /* maps to RuntimeError */
+#define DCX_E_NCCL (-3)
+#define DCX_E_OOM (-4)
+#define DCX_E_STATE (-5) /* call order violated */
+
+enum { DCX_SOLVER_DOCH = 0, DCX_SOLVER_ADOCH = 1 };
+enum { DCX_WINDOW_ECONOMY = 0, DCX_WINDOW_EXACT = 1 };
+enum { DCX_PREC_F64 = 0, DCX_PREC_F32 = 1, DCX_PREC_F16TC = 2 };
+enum { DCX_PATH_AUTO = 0, DCX_PATH_MULTIPASS = 1, DCX_PATH_PERSISTENT = 2, DCX_PATH_DENSE_TC = 3 };
+enum {
+  DCX_STOP_RUNNING = 0,
+  DCX_STOP_CONVERGED = 1,
+  DCX_STOP_MAX_ITERS = 2,
+  DCX_STOP_TIME_BUDGET = 3
+};
+/* history event bits */
+enum { DCX_EV_RECORDED = 1, DCX_EV_DESCENT = 2, DCX_EV_ACCEPTED = 4, DCX_EV_REJECTED = 8 };
+
+typedef struct dcx_ctx dcx_ctx;
+
+/* Solver knobs: SolverParams (dc/spectral.py:25-49) + doch_solve/adoch_solve
+ * keyword arguments (dc/solvers/doch.py:169-176, :248-256) + the reference
+ * constants CONVERGENCE_TOL / DESCENT_WARN_TOL (doch.py:33-34). */
+typedef struct {
+  int32_t solver;       /* DCX_SOLVER_* */
+  int32_t window_mode;  /* DCX_WINDOW_* (adoch only) */
+  int32_t precision;    /* DCX_PREC_* */
+  int32_t lookback_q;   /* >= 1 */
+  int64_t max_iters;    /* >= 0 */
+  int64_t trace_stride; /* >= 1 */
+  double time_budget_s; /* < 0: no budget */
+  double conv_tol;      /* 1e-10 in the reference */
+  double descent_tol;   /* 1e-9 in the reference */
+  int32_t record_states;
+  int32_t path;  /* DCX_PATH_* */
+  int32_t chunk; /* iterations per host drain; 0 = auto */
+  int32_t reserved;
+} dcx_params;
+
+typedef struct {
+  int64_t iterations;
+  int32_t stop_reason; /* DCX_STOP_* */
+  int32_t best_iter;
+  double best_energy;
+  int64_t n_hist;        /* iterations + 1 history entries available */
+  int32_t descent_warn;  /* first descent-violation iteration, -1 if none */
+  int32_t path_used;     /* DCX_PATH_* actually executed */
+} dcx_summary;
+
+typedef struct {
+  int64_t n, nnz;
+  int32_t value_kind; /* 0 uniform, 1 int8, 2 int16, 3 f32, 4 f64 */
+  int32_t lanes;      /* lanes per row of the R=1 kernels */
+  double scale;       /* value = scale * stored integer (integer kinds) */
+  int32_t dense;      /* set through dcx_set_dense */
+  int32_t reserved;
+} dcx_coupling_info;
+
+DCX_API int dcx_abi_version(void);
+DCX_API const char* dcx_last_error(const dcx_ctx* ctx); /* ctx may be NULL: last global error */
+
+/* Context: owns the CUDA stream and all device buffers of one instance. */
+DCX_API int dcx_create(int device, dcx_ctx** out);
+DCX_API void dcx_destroy(dcx_ctx* ctx);
+
+/* Coupling upload.
+ * dcx_set_csr replaces CsrCoupling(values, col_indices, row_offsets)
+ * (dc/coupling.py:115-152): host f64 values, int64 indices, symmetric, sorted
+ * columns, zero diagonal. Stored on device as uint32 row offsets, int32
+ * columns and the narrowest exact value form (uniform / int8 / int16 x scale,
+ * else f32 / f64).
+ * dcx_set_dense replaces DenseCoupling(array) (dc/coupling.py:71-112). */
+DCX_API int dcx_set_csr(dcx_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* col_indices,
+                const double* values);
+DCX_API int dcx_set_dense(dcx_ctx* ctx, int64_t n, const double* J_rowmajor);
+DCX_API int dcx_coupling(const dcx_ctx* ctx, dcx_coupling_info* out);
+
+/* Operator seam (dc/matvec.py:99-114 matvec; :181-190 operator_energy;
+ * dc/model.py:79-87 energy; dc/solvers/doch.py:76-103 hamiltonian/apply_T).
+ * Vectors are [R][n] row-major on the host.
+ *   dcx_matvec:  out_r = J v_r
+ *   dcx_apply:   tx_r = cbrt((J v_r + alpha_r v_r) / beta_r), h_r = H(v_r)  (either may be NULL)
+ *   dcx_energy:  E_r = -1/2 s_r^T J s_r, exact integer accumulation for integer couplings */
+DCX_API int dcx_matvec(dcx_ctx* ctx, int32_t R, const double* v, double* out, int32_t precision);
+DCX_API int dcx_apply(dcx_ctx* ctx, int32_t R, const double* alpha, const double* beta, const double* v, double* tx,
+              double* h, int32_t precision);
+DCX_API int dcx_energy(dcx_ctx* ctx, int32_t R, const int8_t* spins, double* energies);
+
+/* Solve R replicas at once: doch_solve / adoch_solve (dc/solvers/doch.py:169,
+ * :248) for each replica r with (alpha_r, beta_r, x0_r). x0 is [R][n]
+ * (initial_state of doch.py:132-145 is drawn by the caller).
+ * dcx_solve_begin uploads and starts the device clock; dcx_solve_step runs up
+ * to one chunk and drains the history; *live becomes 0 when every replica
+ * has stopped. dcx_solve_run loops dcx_solve_step to the end. */
+DCX_API int dcx_solve_begin(dcx_ctx* ctx, const dcx_params* params, int32_t R, const double* alpha, const double* beta,
+                    const double* x0);
+DCX_API int dcx_solve_step(dcx_ctx* ctx, int32_t* live);
+DCX_API int dcx_solve_run(dcx_ctx* ctx);
+
+/* Results (valid after the run, or between steps for the drained part). */
+DCX_API int dcx_result_summary(dcx_ctx* ctx, int32_t r, dcx_summary* out);
+/* history entries k in [from, from+count): H(x_k), E(sign x_k) (NaN if not
+ * recorded), device seconds since dcx_solve_begin, event bits */
+DCX_API int dcx_result_history(dcx_ctx* ctx, int32_t r, int64_t from, int64_t count, double* h, double* e, double* t,
+                       int32_t* ev);
+DCX_API int dcx_result_best_spins(dcx_ctx* ctx, int8_t* out /* [R][n] */);
+DCX_API int dcx_result_state(dcx_ctx* ctx, double* out /* [R][n], final x */);
+DCX_API int dcx_result_states(dcx_ctx* ctx, int32_t r, double* out /* [(iterations+1)][n] */);
+/* Live profile of the dominant kernel of the current path (the fused pass of
+ * the multipass path, the fused GEMM of the dense path): after
+ * dcx_solve_begin, launches it `launches` times on the context stream between
+ * two CUDA events and returns the mean duration. Consumes the run. */
+DCX_API int dcx_profile_kernel(dcx_ctx* ctx, int32_t launches, double* ms_per_launch, int32_t* kernel_id);
+/* device time of the last dcx_solve_run/step sequence, seconds */
+DCX_API int dcx_result_device_seconds(dcx_ctx* ctx, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCX_H_ */

@@ -1,0 +1,913 @@
+// libdcx C ABI (include/dcx.h): context, coupling upload, operator seam and
+// the chunked solve driver. No exception crosses the ABI.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dcx_internal.h"
+#include "dcx_dense.h"
+
+using namespace dcx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b) {
+    if (b == bytes && p) return;
+    release();
+    if (b == 0) return;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw std::runtime_error(std::string("OOM: cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArg : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+}  // namespace
+
+struct dcx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // ---------------------------------------------------------- coupling
+  bool have = false, dense = false;
+  int64_t n = 0, nnz = 0;
+  int vk_int = -1;  // VK_UNIFORM / VK_I8 / VK_I16, or -1 for real values
+  double scale = 1.0;
+  int V32 = 1;
+  DevBuf rp, col, col16, vint, v64, v32;
+  DenseDev dn;  // dense tensor-core operands (dcx_dense.cu)
+  // ---------------------------------------------------------- run state
+  dcx_params prm{};
+  int R = 0;
+  bool begun = false, finished = false, f64 = true;
+  int path = DCX_PATH_MULTIPASS;
+  int cap = 0, wcap = 0, chunk = 0, p_host = 0;
+  DevBuf ctl, g, hist, window, xb0, xb1, ax0, ax1, ay, best, states, part, spart;
+  MultiPass mp;
+  CsrDev J;
+  SmallPlan sp;
+  cudaGraphExec_t graph = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double dev_seconds = 0.0;
+  std::vector<std::vector<HistRec>> hh;
+  std::vector<RepCtl> hctl;
+  std::vector<HistRec> ring;
+  GState hg{};
+
+  ~dcx_ctx() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int fail(dcx_ctx* ctx, int code, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(dcx_ctx* ctx, F&& f) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    f();
+    return DCX_OK;
+  } catch (const InvalidArg& e) {
+    return fail(ctx, DCX_E_INVALID, e.what());
+  } catch (const CudaError& e) {
+    return fail(ctx, DCX_E_CUDA, e.what());
+  } catch (const std::bad_alloc& e) {
+    return fail(ctx, DCX_E_OOM, "host allocation failed");
+  } catch (const std::runtime_error& e) {
+    const std::string m = e.what();
+    return fail(ctx, m.rfind("OOM", 0) == 0 ? DCX_E_OOM : DCX_E_CUDA, m);
+  } catch (...) {
+    return fail(ctx, DCX_E_CUDA, "unknown error");
+  }
+}
+
+int lanes_for_degree(double d) {
+  if (d < 3) return 1;
+  if (d < 6) return 2;
+  if (d < 12) return 4;
+  if (d < 24) return 8;
+  if (d < 48) return 16;
+  return 32;
+}
+
+// Detect the narrowest exact storage of the coupling values.
+void classify_values(const double* v, int64_t nnz, int& vk, double& scale) {
+  if (nnz == 0) { vk = VK_UNIFORM; scale = 0.0; return; }
+  bool uniform = true;
+  double mn = std::numeric_limits<double>::infinity();
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (!std::isfinite(v[e])) throw InvalidArg("couplings must be finite");
+    if (v[e] != v[0]) uniform = false;
+    if (v[e] != 0.0) mn = std::min(mn, std::fabs(v[e]));
+  }
+  if (uniform) { vk = VK_UNIFORM; scale = v[0]; return; }
+  if (!std::isfinite(mn)) { vk = VK_UNIFORM; scale = 0.0; return; }
+  for (double s : {mn, 1.0, 0.5, 0.25}) {
+    double amax = 0.0;
+    bool ok = true;
+    for (int64_t e = 0; e < nnz && ok; ++e) {
+      const double q = v[e] / s;
+      if (q != std::nearbyint(q) || s * std::nearbyint(q) != v[e]) ok = false;
+      amax = std::max(amax, std::fabs(q));
+    }
+    if (!ok) continue;
+    if (amax <= 127) { vk = VK_I8; scale = s; return; }
+    if (amax <= 32767) { vk = VK_I16; scale = s; return; }
+  }
+  vk = -1;
+  scale = 1.0;
+}
+
+CsrDev csr_view(const dcx_ctx* c, bool f64) {
+  CsrDev J;
+  J.n = c->n;
+  J.nnz = c->nnz;
+  J.rp = c->rp.as<uint32_t>();
+  J.col = c->col.as<int32_t>();
+  J.col16 = c->col16.as<uint16_t>();
+  if (c->vk_int >= 0) {
+    J.vk = c->vk_int;
+    J.val = c->vint.p;
+    J.scale = c->scale;
+  } else if (f64) {
+    J.vk = VK_F64;
+    J.val = c->v64.p;
+  } else {
+    J.vk = VK_F32;
+    J.val = c->v32.p;
+  }
+  J.V = f64 ? 1 : c->V32;
+  const int64_t rows_per_warp = 32 / J.V;
+  const int64_t warps = (c->n + rows_per_warp - 1) / rows_per_warp;
+  J.grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 16));
+  return J;
+}
+
+void require_coupling(const dcx_ctx* c) {
+  if (!c->have) throw InvalidArg("no coupling set");
+}
+
+// ------------------------------------------------------------ small kernels
+template <typename T>
+__global__ void to_device_layout(const double* src, T* dst, int64_t n, int R) {
+  // src [R][n] -> dst [n][R]
+  const int64_t total = n * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / R;
+    const int r = int(idx % R);
+    dst[idx] = T(src[(int64_t)r * n + i]);
+  }
+}
+template <typename T>
+__global__ void from_device_layout(const T* src, double* dst, int64_t n, int R) {
+  const int64_t total = n * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / R;
+    const int r = int(idx % R);
+    dst[(int64_t)r * n + i] = double(src[idx]);
+  }
+}
+// mode 0: tx = cbrt((jv + a v)/b), h = H(v); mode 1: E = -1/2 scale sum s_i es_i
+template <typename T>
+__global__ void rows_epilogue(int mode, const T* v, const T* jv, const double* es, const double* alpha,
+                              const double* beta, double es_scale, int64_t n, int R, T* tx, double* out) {
+  const int r = blockIdx.x;
+  __shared__ double sa[256], sb[256];
+  double a = 0.0, b = 0.0;
+  const T al = mode == 0 ? T(alpha[r]) : T(0), be = mode == 0 ? T(beta[r]) : T(1);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t idx = i * R + r;
+    if (mode == 0) {
+      const T xi = v[idx];
+      const T ax = shifted(jv[idx], al, xi);
+      if (tx) tx[idx] = tmap(ax, be);
+      const double x2 = double(mul_rn(xi, xi));
+      a += x2 * x2;
+      b += double(xi) * double(ax);
+    } else {
+      a += (v[idx] >= T(0) ? es[idx] : -es[idx]);
+    }
+  }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sa[threadIdx.x] += sa[threadIdx.x + w];
+      sb[threadIdx.x] += sb[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (mode == 0) out[r] = __dsub_rn(__dmul_rn(__dmul_rn(0.25, beta[r]), sa[0]), __dmul_rn(0.5, sb[0]));
+    else out[r] = __dmul_rn(-0.5, __dmul_rn(es_scale, sa[0]));
+  }
+}
+__global__ void spins_to_device(const int8_t* s, double* dst, int64_t n, int R) {
+  const int64_t total = n * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / R;
+    const int r = int(idx % R);
+    dst[idx] = s[(int64_t)r * n + i] >= 0 ? 1.0 : -1.0;
+  }
+}
+
+int grid_for(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 32)); }
+
+}  // namespace
+
+// -------------------------------------------------------------- operators
+template <typename T>
+static void apply_impl(dcx_ctx* c, int R, const double* alpha, const double* beta, const double* v, double* jv_out,
+                       double* tx_out, double* h_out, const int8_t* spins, double* e_out) {
+  const int64_t n = c->n;
+  const bool f64 = sizeof(T) == 8;
+  CsrDev J = csr_view(c, f64);
+  DevBuf dsrc, dv, djv, dtx, des, dab, dout, dsp;
+  const int64_t tot = n * R;
+  dv.alloc(tot * sizeof(T));
+  djv.alloc(tot * sizeof(T));
+  if (spins) {
+    dsp.alloc(tot);
+    CK(cudaMemcpyAsync(dsp.p, spins, tot, cudaMemcpyHostToDevice, c->stream));
+    dsrc.alloc(tot * 8);
+    spins_to_device<<<grid_for(tot), 256, 0, c->stream>>>(dsp.as<int8_t>(), dsrc.as<double>(), n, R);
+    // spins are exact in T; reuse the [n][R] buffer converted to T
+    if (f64) CK(cudaMemcpyAsync(dv.p, dsrc.p, tot * 8, cudaMemcpyDeviceToDevice, c->stream));
+    else {
+      // convert double +-1 to float +-1 in place layout
+      DevBuf tmp;
+      tmp.alloc(tot * 8);
+      from_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(dsrc.as<double>(), tmp.as<double>(), n, R);
+      to_device_layout<T><<<grid_for(tot), 256, 0, c->stream>>>(tmp.as<double>(), dv.as<T>(), n, R);
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    des.alloc(tot * 8);
+  } else {
+    dsrc.alloc(tot * 8);
+    CK(cudaMemcpyAsync(dsrc.p, v, tot * 8, cudaMemcpyHostToDevice, c->stream));
+    to_device_layout<T><<<grid_for(tot), 256, 0, c->stream>>>(dsrc.as<double>(), dv.as<T>(), n, R);
+  }
+  launch_csr_apply<T>(J, dv.as<T>(), R, djv.as<T>(), des.as<double>(), c->stream);
+  CK(cudaGetLastError());
+  if (jv_out) {
+    DevBuf o;
+    o.alloc(tot * 8);
+    from_device_layout<T><<<grid_for(tot), 256, 0, c->stream>>>(djv.as<T>(), o.as<double>(), n, R);
+    CK(cudaMemcpyAsync(jv_out, o.p, tot * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  if (tx_out || h_out || e_out) {
+    dab.alloc(2 * R * 8 + 8);
+    dout.alloc(R * 8);
+    if (alpha) {
+      CK(cudaMemcpyAsync(dab.p, alpha, R * 8, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(dab.as<double>() + R, beta, R * 8, cudaMemcpyHostToDevice, c->stream));
+    }
+    if (tx_out) dtx.alloc(tot * sizeof(T));
+    const int mode = spins ? 1 : 0;
+    const double es_scale = c->vk_int >= 0 ? c->scale : 1.0;
+    rows_epilogue<T><<<R, 256, 0, c->stream>>>(mode, dv.as<T>(), djv.as<T>(), des.as<double>(), dab.as<double>(),
+                                                dab.as<double>() + R, es_scale, n, R, dtx.as<T>(), dout.as<double>());
+    CK(cudaGetLastError());
+    if (tx_out) {
+      DevBuf o;
+      o.alloc(tot * 8);
+      from_device_layout<T><<<grid_for(tot), 256, 0, c->stream>>>(dtx.as<T>(), o.as<double>(), n, R);
+      CK(cudaMemcpyAsync(tx_out, o.p, tot * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    double* dst = spins ? e_out : h_out;
+    if (dst) CK(cudaMemcpyAsync(dst, dout.p, R * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// ====================================================================== ABI
+extern "C" {
+
+int dcx_abi_version(void) { return DCX_ABI_VERSION; }
+
+const char* dcx_last_error(const dcx_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int dcx_create(int device, dcx_ctx** out) {
+  if (!out) return fail(nullptr, DCX_E_INVALID, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, DCX_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, DCX_E_INVALID, "device index out of range");
+  dcx_ctx* c = new (std::nothrow) dcx_ctx();
+  if (!c) return fail(nullptr, DCX_E_OOM, "host allocation failed");
+  c->device = device;
+  int rc = guarded(c, [&] {
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+  });
+  if (rc != DCX_OK) {
+    g_last_error = c->err;
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return DCX_OK;
+}
+
+void dcx_destroy(dcx_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (n < 1) throw InvalidArg("n must be >= 1");
+    if (nnz < 0 || (nnz > 0 && (!ci || !v)) || !ro) throw InvalidArg("null CSR array");
+    if (nnz >= (int64_t(1) << 32) - 1) throw InvalidArg("nnz >= 2^32 is not supported");
+    if (n >= (int64_t(1) << 31)) throw InvalidArg("n >= 2^31 is not supported");
+    if (ro[0] != 0 || ro[n] != nnz) throw InvalidArg("row_offsets must start at 0 and end at nnz");
+    std::vector<uint32_t> rp32(n + 1);
+    for (int64_t i = 0; i <= n; ++i) {
+      if (i > 0 && ro[i] < ro[i - 1]) throw InvalidArg("row_offsets must be nondecreasing");
+      rp32[i] = uint32_t(ro[i]);
+    }
+    std::vector<int32_t> c32(nnz);
+    for (int64_t e = 0; e < nnz; ++e) {
+      if (ci[e] < 0 || ci[e] >= n) throw InvalidArg("column index out of range");
+      c32[e] = int32_t(ci[e]);
+    }
+    int vk;
+    double scale;
+    classify_values(v, nnz, vk, scale);
+    c->have = false;
+    c->dense = false;
+    c->dn.release();
+    c->n = n;
+    c->nnz = nnz;
+    c->rp.alloc((n + 1) * 4);
+    CK(cudaMemcpy(c->rp.p, rp32.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+    c->col.alloc(std::max<int64_t>(nnz, 1) * 4);
+    if (nnz) CK(cudaMemcpy(c->col.p, c32.data(), nnz * 4, cudaMemcpyHostToDevice));
+    c->col16.release();
+    if (n <= 65536 && nnz) {
+      std::vector<uint16_t> c16(nnz);
+      for (int64_t e = 0; e < nnz; ++e) c16[e] = uint16_t(c32[e]);
+      c->col16.alloc(nnz * 2);
+      CK(cudaMemcpy(c->col16.p, c16.data(), nnz * 2, cudaMemcpyHostToDevice));
+    }
+    c->vint.release();
+    c->v64.release();
+    c->v32.release();
+    c->vk_int = (vk == VK_UNIFORM || vk == VK_I8 || vk == VK_I16) ? vk : -1;
+    c->scale = scale;
+    if (vk == VK_I8 || vk == VK_I16) {
+      const int b = vk == VK_I8 ? 1 : 2;
+      std::vector<int16_t> q16;
+      std::vector<int8_t> q8;
+      if (b == 1) q8.resize(nnz); else q16.resize(nnz);
+      for (int64_t e = 0; e < nnz; ++e) {
+        const int q = int(std::nearbyint(v[e] / scale));
+        if (b == 1) q8[e] = int8_t(q); else q16[e] = int16_t(q);
+      }
+      c->vint.alloc(nnz * b);
+      CK(cudaMemcpy(c->vint.p, b == 1 ? (void*)q8.data() : (void*)q16.data(), nnz * b, cudaMemcpyHostToDevice));
+    } else if (vk != VK_UNIFORM) {
+      c->v64.alloc(nnz * 8);
+      CK(cudaMemcpy(c->v64.p, v, nnz * 8, cudaMemcpyHostToDevice));
+      std::vector<float> f(nnz);
+      for (int64_t e = 0; e < nnz; ++e) f[e] = float(v[e]);
+      c->v32.alloc(nnz * 4);
+      CK(cudaMemcpy(c->v32.p, f.data(), nnz * 4, cudaMemcpyHostToDevice));
+    }
+    c->V32 = lanes_for_degree(double(nnz) / double(n));
+    c->have = true;
+  });
+}
+
+int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!A || n < 1) return fail(c, DCX_E_INVALID, "bad dense coupling");
+  // CSR of the nonzero off-diagonal entries (row-major scan keeps column order)
+  std::vector<int64_t> ro(n + 1, 0), ci;
+  std::vector<double> vv;
+  try {
+    for (int64_t i = 0; i < n; ++i) {
+      for (int64_t j = 0; j < n; ++j) {
+        const double a = A[i * n + j];
+        if (i == j) {
+          if (a != 0.0) return fail(c, DCX_E_INVALID, "diagonal must be zero");
+          continue;
+        }
+        if (a != 0.0) {
+          ci.push_back(j);
+          vv.push_back(a);
+        }
+      }
+      ro[i + 1] = (int64_t)ci.size();
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(c, DCX_E_OOM, "host allocation failed");
+  }
+  int rc = dcx_set_csr(c, n, (int64_t)ci.size(), ro.data(), ci.data(), vv.data());
+  if (rc != DCX_OK) return rc;
+  return guarded(c, [&] {
+    c->dense = true;
+    dense_upload(c->dn, n, A, c->stream);
+  });
+}
+
+int dcx_coupling(const dcx_ctx* c, dcx_coupling_info* out) {
+  if (!c || !out) return fail(nullptr, DCX_E_INVALID, "null argument");
+  if (!c->have) return fail(const_cast<dcx_ctx*>(c), DCX_E_STATE, "no coupling set");
+  out->n = c->n;
+  out->nnz = c->nnz;
+  out->value_kind = c->vk_int >= 0 ? c->vk_int : VK_F64;
+  out->lanes = c->V32;
+  out->scale = c->scale;
+  out->dense = c->dense ? 1 : 0;
+  out->reserved = 0;
+  return DCX_OK;
+}
+
+int dcx_matvec(dcx_ctx* c, int32_t R, const double* v, double* out, int32_t precision) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    require_coupling(c);
+    if (R < 1 || !v || !out) throw InvalidArg("bad matvec arguments");
+    if (precision == DCX_PREC_F32) apply_impl<float>(c, R, nullptr, nullptr, v, out, nullptr, nullptr, nullptr, nullptr);
+    else apply_impl<double>(c, R, nullptr, nullptr, v, out, nullptr, nullptr, nullptr, nullptr);
+  });
+}
+
+int dcx_apply(dcx_ctx* c, int32_t R, const double* alpha, const double* beta, const double* v, double* tx,
+              double* h, int32_t precision) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    require_coupling(c);
+    if (R < 1 || !v || !alpha || !beta) throw InvalidArg("bad apply arguments");
+    for (int r = 0; r < R; ++r)
+      if (!(alpha[r] > 0) || !(beta[r] > 0)) throw InvalidArg("alpha and beta must be positive");
+    if (precision == DCX_PREC_F32) apply_impl<float>(c, R, alpha, beta, v, nullptr, tx, h, nullptr, nullptr);
+    else apply_impl<double>(c, R, alpha, beta, v, nullptr, tx, h, nullptr, nullptr);
+  });
+}
+
+int dcx_energy(dcx_ctx* c, int32_t R, const int8_t* spins, double* energies) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    require_coupling(c);
+    if (R < 1 || !spins || !energies) throw InvalidArg("bad energy arguments");
+    apply_impl<double>(c, R, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, spins, energies);
+  });
+}
+
+// ------------------------------------------------------------------ solve
+static void build_graph(dcx_ctx* c) {
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  cudaGraph_t gr;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  for (int it = 0; it < c->chunk; ++it) enqueue_iteration(c->mp, c->stream);
+  CK(cudaStreamEndCapture(c->stream, &gr));
+  CK(cudaGraphInstantiate(&c->graph, gr, 0));
+  cudaGraphDestroy(gr);
+}
+
+int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* alpha, const double* beta,
+                    const double* x0) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    require_coupling(c);
+    if (!P || !alpha || !beta || !x0) throw InvalidArg("null argument");
+    if (R < 1) throw InvalidArg("R must be >= 1");
+    if (P->solver != DCX_SOLVER_DOCH && P->solver != DCX_SOLVER_ADOCH) throw InvalidArg("unknown solver");
+    if (P->window_mode != DCX_WINDOW_ECONOMY && P->window_mode != DCX_WINDOW_EXACT)
+      throw InvalidArg("window_mode must be 'economy' or 'exact'");
+    if (P->lookback_q < 1) throw InvalidArg("lookback_q must be >= 1");
+    if (P->max_iters < 0 || P->max_iters > (int64_t(1) << 30)) throw InvalidArg("max_iters out of range");
+    if (P->trace_stride < 1) throw InvalidArg("trace_stride must be >= 1");
+    for (int r = 0; r < R; ++r)
+      if (!(alpha[r] > 0) || !(beta[r] > 0)) throw InvalidArg("alpha and beta must be positive");
+    c->prm = *P;
+    c->R = R;
+    c->begun = false;
+    c->finished = false;
+    const int64_t n = c->n;
+    const bool use_tc = P->precision == DCX_PREC_F16TC;
+    if (use_tc && !c->dense) throw InvalidArg("the tensor-core path needs a dense coupling");
+    c->f64 = P->precision == DCX_PREC_F64;
+    const size_t tb = c->f64 ? 8 : 4;
+    c->J = csr_view(c, c->f64);
+    c->sp = plan_small(c->J, P->solver, P->window_mode, c->f64);
+    if (use_tc) c->path = DCX_PATH_DENSE_TC;
+    else if (P->path == DCX_PATH_PERSISTENT) {
+      if (!c->sp.fits) throw InvalidArg("instance too large for the persistent path");
+      c->path = DCX_PATH_PERSISTENT;
+    } else if (P->path == DCX_PATH_MULTIPASS) c->path = DCX_PATH_MULTIPASS;
+    else if (P->path == DCX_PATH_DENSE_TC) throw InvalidArg("tensor-core path needs precision F16TC");
+    else c->path = c->sp.fits ? DCX_PATH_PERSISTENT : DCX_PATH_MULTIPASS;
+    // history ring
+    const int64_t total_hist = int64_t(1) << 21;
+    int64_t cap = std::min<int64_t>(P->max_iters + 1, std::max<int64_t>(1024, total_hist / R));
+    c->cap = (int)cap;
+    c->wcap = (int)std::min<int64_t>(int64_t(P->lookback_q) + 1, P->max_iters + 1);
+    if (c->path == DCX_PATH_MULTIPASS) c->chunk = P->chunk > 0 ? P->chunk : 32;
+    else c->chunk = P->chunk > 0 ? P->chunk : (int)cap;
+    c->chunk = (int)std::min<int64_t>(c->chunk, cap);
+    if (c->chunk < 1) c->chunk = 1;
+    // buffers
+    const int64_t tot = n * R;
+    c->xb0.alloc(tot * tb);
+    c->xb1.alloc(tot * tb);
+    const bool ad = P->solver == DCX_SOLVER_ADOCH;
+    if (ad) { c->ax0.alloc(tot * tb); c->ax1.alloc(tot * tb); } else { c->ax0.release(); c->ax1.release(); }
+    if (ad && P->window_mode == DCX_WINDOW_EXACT) c->ay.alloc(tot * tb); else c->ay.release();
+    c->best.alloc(tot);
+    c->ctl.alloc(sizeof(RepCtl) * R);
+    c->g.alloc(sizeof(GState));
+    c->hist.alloc(sizeof(HistRec) * R * cap);
+    c->window.alloc(sizeof(double) * R * std::max(1, c->wcap));
+    c->states.release();
+    if (P->record_states) {
+      const double bytes = double(P->max_iters + 1) * double(tot) * double(tb);
+      if (bytes > 4e9) throw InvalidArg("record_states would need more than 4 GB; lower max_iters");
+      c->states.alloc(size_t(bytes));
+    }
+    // partial slots
+    c->mp = MultiPass{};
+    c->mp.f64 = c->f64;
+    c->mp.solver = P->solver;
+    c->mp.vk = c->J.vk;
+    c->mp.V = c->J.V;
+    int slots;
+    if (R == 1) {
+      c->mp.grid = c->J.grid;
+      slots = c->mp.grid * 8;
+    } else {
+      c->mp.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, 148 * 2));
+      slots = c->mp.grid * 8;
+    }
+    c->part.alloc(sizeof(double) * R * NQ * slots);
+    {
+      int64_t fthreads = std::min<int64_t>(std::max<int64_t>(tot, R), int64_t(148) * 8 * 256);
+      int fg = (int)((fthreads + 255) / 256);
+      if ((int64_t)fg * 256 < R) fg = (R + 255) / 256;
+      c->mp.fgrid = fg;
+      c->mp.sslots = R == 1 ? fg * 8 : (fg * 256) / R;
+      c->spart.alloc(sizeof(double) * std::max(1, c->mp.sslots) * R);
+      CK(cudaMemsetAsync(c->spart.p, 0, c->spart.bytes, c->stream));
+    }
+    PassArgs& a = c->mp.args;
+    a.rp = c->J.rp;
+    a.col = c->J.col;
+    a.val = c->J.val;
+    a.scale = c->J.scale;
+    a.ctl = c->ctl.as<RepCtl>();
+    a.g = c->g.as<GState>();
+    a.x[0] = c->xb0.p;
+    a.x[1] = c->xb1.p;
+    a.ax[0] = c->ax0.p;
+    a.ax[1] = c->ax1.p;
+    a.ay = c->ay.p;
+    a.best = c->best.as<int8_t>();
+    a.states = c->states.p;
+    a.part = c->part.as<double>();
+    a.slots = slots;
+    RunCfg& cfg = a.cfg;
+    cfg.n = n;
+    cfg.R = R;
+    cfg.solver = P->solver;
+    cfg.window_mode = P->window_mode;
+    cfg.lookback_q = P->lookback_q;
+    cfg.max_iters = P->max_iters;
+    cfg.stride = P->trace_stride;
+    cfg.budget = P->time_budget_s;
+    cfg.conv_tol = P->conv_tol;
+    cfg.descent_tol = P->descent_tol;
+    cfg.hist_cap = (int)cap;
+    cfg.wcap = std::max(1, c->wcap);
+    cfg.es_scale = c->vk_int >= 0 ? c->scale : 1.0;
+    cfg.hist = c->hist.as<HistRec>();
+    cfg.window = c->window.as<double>();
+    c->mp.spart = c->spart.as<double>();
+    // initial state
+    {
+      DevBuf src;
+      src.alloc(tot * 8);
+      CK(cudaMemcpyAsync(src.p, x0, tot * 8, cudaMemcpyHostToDevice, c->stream));
+      if (c->f64) to_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), c->xb0.as<double>(), n, R);
+      else to_device_layout<float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), c->xb0.as<float>(), n, R);
+      CK(cudaMemsetAsync(c->xb1.p, 0, tot * tb, c->stream));
+      if (ad) {
+        CK(cudaMemsetAsync(c->ax0.p, 0, tot * tb, c->stream));
+        CK(cudaMemsetAsync(c->ax1.p, 0, tot * tb, c->stream));
+      }
+      CK(cudaMemsetAsync(c->best.p, 1, tot, c->stream));
+      if (c->states.p) CK(cudaMemcpyAsync(c->states.p, c->xb0.p, tot * tb, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    std::vector<RepCtl> h(R);
+    for (int r = 0; r < R; ++r) {
+      RepCtl& q = h[r];
+      std::memset(&q, 0, sizeof(q));
+      q.alpha = alpha[r];
+      q.beta = beta[r];
+      q.best = std::numeric_limits<double>::infinity();
+      q.t = 1.0;
+      q.k = -1;
+      q.status = DCX_STOP_RUNNING;
+      q.best_iter = -1;
+      q.pend = -1;
+      q.accept = 1;
+      q.warned = -1;
+    }
+    CK(cudaMemcpyAsync(c->ctl.p, h.data(), sizeof(RepCtl) * R, cudaMemcpyHostToDevice, c->stream));
+    c->hg = GState{};
+    c->hg.p = 0;
+    c->hg.live = 1;
+    c->hg.running = R;
+    CK(cudaMemcpyAsync(c->g.p, &c->hg, sizeof(GState), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->hh.assign(R, {});
+    for (auto& v : c->hh) v.reserve(std::min<int64_t>(P->max_iters + 1, 4096));
+    c->hctl = h;
+    c->ring.resize(size_t(R) * cap);
+    c->p_host = 0;
+    if (c->path == DCX_PATH_MULTIPASS) build_graph(c);
+    if (c->path == DCX_PATH_DENSE_TC) dense_begin(c->dn, c->mp, c->stream);
+    CK(cudaEventRecord(c->ev0, c->stream));
+    enqueue_start_clock(c->g.as<GState>(), c->stream);
+    CK(cudaGetLastError());
+    c->begun = true;
+  });
+}
+
+static void drain(dcx_ctx* c) {
+  const int R = c->R;
+  CK(cudaMemcpyAsync(c->hctl.data(), c->ctl.p, sizeof(RepCtl) * R, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&c->hg, c->g.p, sizeof(GState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  // new history entries: k in [lo, hi] over all replicas (replicas advance in lockstep)
+  int64_t lo = std::numeric_limits<int64_t>::max(), hi = -1;
+  for (int r = 0; r < R; ++r) {
+    const int64_t kr = c->hctl[r].k;
+    const int64_t done = (int64_t)c->hh[r].size();
+    if (kr >= done) {
+      lo = std::min(lo, done);
+      hi = std::max(hi, kr);
+    }
+  }
+  if (hi < 0) return;
+  const size_t rec = sizeof(HistRec);
+  const size_t pitch = rec * c->cap;
+  auto copy_cols = [&](int64_t k0, int64_t k1) {  // ring columns [k0, k1] without wrap
+    CK(cudaMemcpy2DAsync(c->ring.data() + k0, pitch, c->hist.as<HistRec>() + k0, pitch, rec * (k1 - k0 + 1), R,
+                         cudaMemcpyDeviceToHost, c->stream));
+  };
+  if (hi - lo + 1 >= c->cap) copy_cols(0, c->cap - 1);
+  else {
+    const int64_t a = lo % c->cap, b = hi % c->cap;
+    if (a <= b) copy_cols(a, b);
+    else { copy_cols(a, c->cap - 1); copy_cols(0, b); }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < R; ++r) {
+    const int64_t kr = c->hctl[r].k;
+    auto& v = c->hh[r];
+    for (int64_t k = (int64_t)v.size(); k <= kr; ++k) v.push_back(c->ring[(size_t)r * c->cap + (k % c->cap)]);
+  }
+}
+
+int dcx_solve_step(dcx_ctx* c, int32_t* live) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun) throw InvalidArg("dcx_solve_begin has not been called");
+    if (c->finished) {
+      if (live) *live = 0;
+      return;
+    }
+    if (c->path == DCX_PATH_MULTIPASS) {
+      CK(cudaGraphLaunch(c->graph, c->stream));
+    } else if (c->path == DCX_PATH_PERSISTENT) {
+      const int p_end = (int)std::min<int64_t>(c->p_host + c->chunk, c->prm.max_iters + 1);
+      launch_small(c->mp, c->J, c->sp, p_end, c->stream);
+      CK(cudaGetLastError());
+      c->p_host = p_end;
+      GState tmp{};
+      // advance the shared pass counter for the next chunk (running is kept)
+      CK(cudaMemcpyAsync(&c->hg, c->g.p, sizeof(GState), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      tmp = c->hg;
+      tmp.p = p_end;
+      tmp.live = tmp.running > 0 ? 1 : 0;
+      CK(cudaMemcpyAsync(c->g.p, &tmp, sizeof(GState), cudaMemcpyHostToDevice, c->stream));
+    } else {
+      dense_step(c->dn, c->mp, c->chunk, c->stream);
+    }
+    CK(cudaGetLastError());
+    drain(c);
+    bool alive = c->hg.live != 0 && c->hg.running > 0;
+    if (c->path == DCX_PATH_PERSISTENT && c->p_host >= c->prm.max_iters + 1) alive = false;
+    if (!alive) {
+      if (c->path == DCX_PATH_MULTIPASS) enqueue_flush(c->mp, c->stream);
+      if (c->path == DCX_PATH_DENSE_TC) dense_finish(c->dn, c->mp, c->stream);
+      CK(cudaEventRecord(c->ev1, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      c->dev_seconds = ms * 1e-3;
+      drain(c);
+      c->finished = true;
+    }
+    if (live) *live = alive ? 1 : 0;
+  });
+}
+
+int dcx_solve_run(dcx_ctx* c) {
+  int32_t live = 1;
+  while (live) {
+    int rc = dcx_solve_step(c, &live);
+    if (rc != DCX_OK) return rc;
+  }
+  return DCX_OK;
+}
+
+int dcx_result_summary(dcx_ctx* c, int32_t r, dcx_summary* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  if (!c->begun) return fail(c, DCX_E_STATE, "no run");
+  if (r < 0 || r >= c->R) return fail(c, DCX_E_INVALID, "replica index out of range");
+  const RepCtl& q = c->hctl[r];
+  out->iterations = std::max(0, q.k);
+  out->stop_reason = q.status;
+  out->best_iter = q.best_iter;
+  out->best_energy = q.best;
+  out->n_hist = (int64_t)c->hh[r].size();
+  out->descent_warn = q.warned;
+  out->path_used = c->path;
+  return DCX_OK;
+}
+
+int dcx_result_history(dcx_ctx* c, int32_t r, int64_t from, int64_t count, double* h, double* e, double* t,
+                       int32_t* ev) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!c->begun || r < 0 || r >= c->R) return fail(c, DCX_E_INVALID, "bad replica");
+  const auto& v = c->hh[r];
+  if (from < 0 || count < 0 || from + count > (int64_t)v.size()) return fail(c, DCX_E_INVALID, "history range");
+  for (int64_t k = 0; k < count; ++k) {
+    const HistRec& q = v[from + k];
+    if (h) h[k] = q.h;
+    if (e) e[k] = q.e;
+    if (t) t[k] = q.t;
+    if (ev) ev[k] = q.ev;
+  }
+  return DCX_OK;
+}
+
+int dcx_result_best_spins(dcx_ctx* c, int8_t* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    if (!c->begun) throw InvalidArg("no run");
+    const int64_t n = c->n, R = c->R;
+    std::vector<int8_t> tmp(n * R);
+    CK(cudaMemcpyAsync(tmp.data(), c->best.p, n * R, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t r = 0; r < R; ++r) out[r * n + i] = tmp[i * R + r];
+  });
+}
+
+int dcx_result_state(dcx_ctx* c, double* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    if (!c->begun) throw InvalidArg("no run");
+    const int64_t n = c->n, R = c->R, tot = n * R;
+    const size_t tb = c->f64 ? 8 : 4;
+    std::vector<unsigned char> b0(tot * tb), b1(tot * tb);
+    CK(cudaMemcpyAsync(b0.data(), c->xb0.p, tot * tb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b1.data(), c->xb1.p, tot * tb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t r = 0; r < R; ++r) {
+      const int k = std::max(0, c->hctl[r].k);
+      const unsigned char* src = (k & 1) ? b1.data() : b0.data();
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t idx = i * R + r;
+        out[r * n + i] = c->f64 ? reinterpret_cast<const double*>(src)[idx] : double(reinterpret_cast<const float*>(src)[idx]);
+      }
+    }
+  });
+}
+
+int dcx_result_states(dcx_ctx* c, int32_t r, double* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    if (!c->begun || !c->states.p) throw InvalidArg("states were not recorded");
+    if (r < 0 || r >= c->R) throw InvalidArg("replica index out of range");
+    const int64_t n = c->n, R = c->R, tot = n * R;
+    const size_t tb = c->f64 ? 8 : 4;
+    const int64_t K = std::max(0, c->hctl[r].k) + 1;
+    std::vector<unsigned char> tmp(K * tot * tb);
+    CK(cudaMemcpyAsync(tmp.data(), c->states.p, K * tot * tb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t idx = k * tot + i * R + r;
+        out[k * n + i] = c->f64 ? reinterpret_cast<const double*>(tmp.data())[idx]
+                                : double(reinterpret_cast<const float*>(tmp.data())[idx]);
+      }
+  });
+}
+
+int dcx_profile_kernel(dcx_ctx* c, int32_t launches, double* ms_per_launch, int32_t* kernel_id) {
+  if (!c || !ms_per_launch) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    if (!c->begun || c->finished) throw InvalidArg("profile needs a freshly begun run");
+    if (launches < 1) throw InvalidArg("launches must be >= 1");
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    int kid = 0;
+    // one warm launch, then the timed ones (same input every launch: the pass
+    // counter does not advance without the control kernel)
+    if (c->path == DCX_PATH_MULTIPASS) {
+      enqueue_pass_only(c->mp, c->stream);
+      CK(cudaEventRecord(a, c->stream));
+      for (int i = 0; i < launches; ++i) enqueue_pass_only(c->mp, c->stream);
+      CK(cudaEventRecord(b, c->stream));
+      kid = 1;
+    } else if (c->path == DCX_PATH_DENSE_TC) {
+      dense_profile(c->dn, c->mp, launches, a, b, c->stream);
+      kid = 3;
+    } else {
+      throw InvalidArg("profiling covers the multipass and dense paths");
+    }
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_launch = double(ms) / launches;
+    if (kernel_id) *kernel_id = kid;
+    c->finished = true;
+    c->begun = false;
+  });
+}
+
+int dcx_result_device_seconds(dcx_ctx* c, double* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  *out = c->dev_seconds;
+  return DCX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// Internal declarations shared by the .cu translation units of libdcx.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "dcx_device.cuh"
+
+namespace dcx {
+
+// Device CSR in its compressed form for one precision.
+struct CsrDev {
+  int64_t n = 0, nnz = 0;
+  const uint32_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const uint16_t* col16 = nullptr;  // present when n <= 65536 (persistent kernel)
+  const void* val = nullptr;
+  int vk = VK_F64;
+  double scale = 1.0;
+  int V = 1;     // lanes per row (R = 1 kernels and the operator seam)
+  int grid = 1;  // grid of the R = 1 pass / apply kernels
+};
+
+// Kernel argument block of one multi-pass iteration (passed by value).
+struct PassArgs {
+  const uint32_t* rp;
+  const int32_t* col;
+  const void* val;
+  double scale;
+  RepCtl* ctl;
+  GState* g;
+  void* x[2];      // iterate buffers by pass parity, layout [n][R]
+  void* ax[2];     // ADOCH (J+aI)x_p by parity
+  void* ay;        // ADOCH exact (J+aI)y
+  int8_t* best;    // best spins [n][R]
+  void* states;    // optional [(max_iters+1)][n][R]
+  double* part;    // pass partials [R][NQ][slots]
+  int32_t slots;
+  RunCfg cfg;
+};
+
+struct MultiPass {
+  PassArgs args;
+  bool f64 = true;
+  int solver = DCX_SOLVER_DOCH;
+  int vk = VK_F64, V = 1, grid = 1, fgrid = 1, sslots = 1;
+  double* spart = nullptr;  // ADOCH finalize step partials [sslots][R]
+};
+
+// dcx_csr.cu
+void enqueue_iteration(const MultiPass& m, cudaStream_t s);
+void enqueue_flush(const MultiPass& m, cudaStream_t s);
+void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
+void enqueue_start_clock(GState* g, cudaStream_t s);
+template <typename T>
+void launch_csr_apply(const CsrDev& J, const T* v, int R, T* jv, double* es_rows, cudaStream_t s);
+
+// dcx_small.cu: persistent one-CTA-per-replica kernel (whole CSR in smem)
+struct SmallPlan {
+  size_t smem = 0;
+  int threads = 256;
+  bool fits = false;
+};
+SmallPlan plan_small(const CsrDev& J, int solver, int window_mode, bool f64);
+void launch_small(const MultiPass& m, const CsrDev& J, const SmallPlan& sp, int p_end, cudaStream_t s);
+
+}  // namespace dcx

@@ -1,0 +1,338 @@
+// Persistent small-n path: one CTA per replica keeps the whole CSR pattern,
+// its values and every state vector in shared memory and runs the complete
+// DOCH / ADOCH loop (dc/solvers/doch.py:199-232 / :294-342) on chip, with the
+// control logic of dcx_device.cuh executed by thread 0 between block barriers.
+// For the G1-shape config (n = 800, 38,352 nnz) the pattern is 77 KB of uint16
+// column indices; there is no HBM traffic per iteration except the history
+// ring and best-spin copies.
+#include "dcx_internal.h"
+
+namespace dcx {
+
+constexpr int SMALL_THREADS = 512;
+constexpr int SMALL_WARPS = SMALL_THREADS / 32;
+
+struct SmallArgs {
+  PassArgs a;
+  const uint16_t* col16;
+  int V;
+  int p_end;  // stop after executing pass p_end - 1 (chunk end)
+  int col_is16;
+};
+
+__host__ __device__ constexpr int val_bytes(int vk) {
+  return vk == VK_UNIFORM ? 0 : vk == VK_I8 ? 1 : vk == VK_I16 ? 2 : vk == VK_F32 ? 4 : 8;
+}
+
+// Shared-memory carve-up (16-byte aligned regions), identical on host and device.
+struct SmemLayout {
+  uint32_t x0, x1, ax0, ax1, ay, rp, col, val, total;
+};
+__host__ __device__ inline uint32_t align16(uint64_t v) { return uint32_t((v + 15) & ~uint64_t(15)); }
+__host__ __device__ inline SmemLayout small_layout(int n, uint32_t nnz, int tb, bool adoch, bool exact, bool col16,
+                                                   int vb) {
+  SmemLayout L;
+  uint32_t o = 0;
+  const uint32_t vec = align16(uint64_t(n) * tb);
+  L.x0 = o; o += vec;
+  L.x1 = o; o += vec;
+  L.ax0 = o; if (adoch) o += vec;
+  L.ax1 = o; if (adoch) o += vec;
+  L.ay = o; if (adoch && exact) o += vec;
+  L.rp = o; o += align16(uint64_t(n + 1) * 4);
+  L.col = o; o += align16(uint64_t(nnz) * (col16 ? 2 : 4));
+  L.val = o; o += align16(uint64_t(nnz) * vb);
+  L.total = o;
+  return L;
+}
+
+// fixed-order block reduction of NQ values (sum, except the step max)
+__device__ __forceinline__ void block_reduce(double* v, double (*sh)[NQ], double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = (q == Q_STEP) ? warp_max(v[q]) : warp_sum(v[q]);
+  if (lane == 0)
+    for (int q = 0; q < NQ; ++q) sh[w][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NQ; ++q) {
+      double acc = sh[0][q];
+      for (int i = 1; i < SMALL_WARPS; ++i) acc = (q == Q_STEP) ? fmax(acc, sh[i][q]) : acc + sh[i][q];
+      out[q] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int VK>
+__global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const PassArgs& a = s.a;
+  const int r = blockIdx.x;
+  const int R = a.cfg.R;
+  const int n = (int)a.cfg.n;
+  const bool adoch = a.cfg.solver == DCX_SOLVER_ADOCH;
+  const bool exact = a.cfg.window_mode == DCX_WINDOW_EXACT;
+  // ---- carve shared memory
+  const uint32_t NNZ = __ldg(a.rp + n);
+  constexpr int VB = val_bytes(VK);
+  const SmemLayout L = small_layout(n, NNZ, sizeof(T), adoch, exact, s.col_is16, VB);
+  T* xb0 = reinterpret_cast<T*>(smem + L.x0);
+  T* xb1 = reinterpret_cast<T*>(smem + L.x1);
+  T* axb0 = reinterpret_cast<T*>(smem + L.ax0);
+  T* axb1 = reinterpret_cast<T*>(smem + L.ax1);
+  T* ayb = reinterpret_cast<T*>(smem + L.ay);
+  uint32_t* rp = reinterpret_cast<uint32_t*>(smem + L.rp);
+  void* colp = smem + L.col;
+  void* valp = smem + L.val;
+  __shared__ double red[SMALL_WARPS][NQ];
+  __shared__ double tot[NQ];
+  __shared__ RepCtl c;
+  __shared__ int flag_stop;
+
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) rp[i] = a.rp[i];
+  if (s.col_is16) {
+    uint16_t* c16 = reinterpret_cast<uint16_t*>(colp);
+    for (uint32_t e = threadIdx.x; e < NNZ; e += blockDim.x) c16[e] = s.col16[e];
+  } else {
+    int32_t* c32 = reinterpret_cast<int32_t*>(colp);
+    for (uint32_t e = threadIdx.x; e < NNZ; e += blockDim.x) c32[e] = a.col[e];
+  }
+  if (VB) {
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(a.val);
+    unsigned char* dst = reinterpret_cast<unsigned char*>(valp);
+    for (uint32_t b = threadIdx.x; b < NNZ * VB; b += blockDim.x) dst[b] = src[b];
+  }
+  if (threadIdx.x == 0) c = a.ctl[r];
+  __syncthreads();
+  int p = a.g->p;
+  if (c.status != DCX_STOP_RUNNING) return;
+  // ---- load state (layout [n][R] in global)
+  {
+    const T* gx0 = reinterpret_cast<const T*>(a.x[p & 1]);
+    const T* gx1 = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
+    T* xc = (p & 1) ? xb1 : xb0;
+    T* xo = (p & 1) ? xb0 : xb1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      xc[i] = gx0[(int64_t)i * R + r];
+      xo[i] = gx1[(int64_t)i * R + r];
+    }
+    if (adoch) {
+      const T* ga0 = reinterpret_cast<const T*>(a.ax[p & 1]);
+      const T* ga1 = reinterpret_cast<const T*>(a.ax[(p + 1) & 1]);
+      T* ac = (p & 1) ? axb1 : axb0;
+      T* ao = (p & 1) ? axb0 : axb1;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ac[i] = ga0[(int64_t)i * R + r];
+        ao[i] = ga1[(int64_t)i * R + r];
+      }
+    }
+  }
+  __syncthreads();
+  const int V = s.V;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % V;
+  const int rpw = 32 / V;
+  const T scale = T(a.scale);
+  auto colat = [&](uint32_t e) -> int {
+    return s.col_is16 ? int(reinterpret_cast<const uint16_t*>(colp)[e]) : reinterpret_cast<const int32_t*>(colp)[e];
+  };
+  // row product over smem; mode 0: v = x (returns es too), mode 1: v = y
+  auto rowdot = [&](int i, const T* xv, const T* xpv, T cmv, bool ymode, T& acc,
+                    typename EsAcc<VK>::type& es) {
+    acc = T(0);
+    es = 0;
+    if (i < n) {
+      const uint32_t lo = rp[i], hi = rp[i + 1];
+      for (uint32_t e = lo + sub; e < hi; e += V) {
+        const int j = colat(e);
+        int q;
+        const T v = load_entry<VK, false, T>(valp, e, scale, q);
+        if (ymode) {
+          acc = madd(acc, v, extrap(xv[j], xpv[j], cmv));
+        } else {
+          const T xj = xv[j];
+          acc = madd(acc, v, xj);
+          es += es_term<VK, T>(q, v, xj);
+        }
+      }
+    }
+    for (int off = V >> 1; off > 0; off >>= 1) {
+      acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+      es += __shfl_xor_sync(0xffffffffu, es, off);
+    }
+  };
+  const int nwarps = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5;
+  T* states = reinterpret_cast<T*>(a.states);
+
+  while (p < s.p_end) {
+    T* xc = (p & 1) ? xb1 : xb0;  // x_p
+    T* xo = (p & 1) ? xb0 : xb1;  // DOCH: x_{p-1} -> x_{p+1}; ADOCH: x_{p-1}
+    T* ac = (p & 1) ? axb1 : axb0;
+    T* ao = (p & 1) ? axb0 : axb1;
+    const T alpha = T(c.alpha), beta = T(c.beta), cm = T(c.cm[p & 1]);
+    double v[NQ] = {0, 0, 0, 0, 0, 0};
+    // ---- pass over x_p
+    for (int base = w * rpw; base < n; base += nwarps * rpw) {
+      const int i = base + lane / V;
+      T acc;
+      typename EsAcc<VK>::type es;
+      rowdot(i, xc, nullptr, T(0), false, acc, es);
+      if (i < n && sub == 0) {
+        const T xi = xc[i];
+        const T ax = shifted(acc, alpha, xi);
+        double x2 = double(mul_rn(xi, xi));
+        v[Q_S4] += x2 * x2;
+        v[Q_SXAX] += double(xi) * double(ax);
+        v[Q_ES] += xi >= T(0) ? double(es) : -double(es);
+        if (!adoch) {
+          if (p > 0 && c.pend == p - 1) a.best[(int64_t)i * R + r] = xo[i] >= T(0) ? 1 : -1;
+          const T xn = tmap(ax, beta);
+          v[Q_STEP] = fmax(v[Q_STEP], double(fabs(xn - xi)));
+          xo[i] = xn;  // own row only: no other thread reads xo in this phase
+          if (states) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
+        } else {
+          ac[i] = ax;
+          if (p > 0 && !exact) {
+            const T yi = extrap(xi, xo[i], cm);
+            const T ayi = extrap(ax, ao[i], cm);
+            double y2 = double(mul_rn(yi, yi));
+            v[Q_SY4] += y2 * y2;
+            v[Q_SYAY] += double(yi) * double(ayi);
+          }
+        }
+      }
+    }
+    block_reduce(v, red, tot);
+    if (threadIdx.x == 0) {
+      const double now = double(globaltimer() - a.g->t0) * 1e-9;
+      double t2[NQ];
+      for (int q = 0; q < NQ; ++q) t2[q] = tot[q];
+      bool stopped = control_after_pass(c, a.cfg, r, t2, p, now);
+      if (!adoch) c.step = t2[Q_STEP];
+      else if (!stopped && !exact) adoch_decide(c, a.cfg, r, t2, p);
+      flag_stop = stopped ? 1 : 0;
+    }
+    __syncthreads();
+    if (adoch) {
+      if (!flag_stop && exact) {
+        // ---- exact window: (J + aI) y with y formed on the fly
+        for (int q = 0; q < NQ; ++q) v[q] = 0.0;
+        if (p > 0) {
+          for (int base = w * rpw; base < n; base += nwarps * rpw) {
+            const int i = base + lane / V;
+            T acc;
+            typename EsAcc<VK>::type es;
+            rowdot(i, xc, xo, cm, true, acc, es);
+            if (i < n && sub == 0) {
+              const T yi = extrap(xc[i], xo[i], cm);
+              const T ayi = shifted(acc, alpha, yi);
+              ayb[i] = ayi;
+              double y2 = double(mul_rn(yi, yi));
+              v[Q_SY4] += y2 * y2;
+              v[Q_SYAY] += double(yi) * double(ayi);
+            }
+          }
+        }
+        block_reduce(v, red, tot);
+        if (threadIdx.x == 0) {
+          double t2[NQ];
+          for (int q = 0; q < NQ; ++q) t2[q] = tot[q];
+          adoch_decide(c, a.cfg, r, t2, p);
+        }
+        __syncthreads();
+      }
+      // ---- finalize: x_{p+1} = cbrt(Av / beta) into the x_{p-1} slot
+      const bool acc_y = p > 0 && c.accept;
+      double st = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const T xi = xc[i];
+        if (c.pend == p) a.best[(int64_t)i * R + r] = xi >= T(0) ? 1 : -1;
+        if (flag_stop) continue;
+        const T av = acc_y ? (exact ? ayb[i] : extrap(ac[i], ao[i], cm)) : ac[i];
+        const T xn = tmap(av, beta);
+        st = fmax(st, double(fabs(xn - xi)));
+        xo[i] = xn;
+        if (states) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
+      }
+      double vv[NQ] = {0, 0, 0, st, 0, 0};
+      block_reduce(vv, red, tot);
+      if (threadIdx.x == 0) c.step = tot[Q_STEP];
+      __syncthreads();
+    } else if (flag_stop) {
+      // DOCH: the pending copy for x_p happens here (no further pass)
+      if (c.pend == p)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) a.best[(int64_t)i * R + r] = xc[i] >= T(0) ? 1 : -1;
+    }
+    ++p;
+    if (flag_stop) break;
+  }
+  // ---- write back state and control
+  {
+    T* gx0 = reinterpret_cast<T*>(a.x[0]);
+    T* gx1 = reinterpret_cast<T*>(a.x[1]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      gx0[(int64_t)i * R + r] = xb0[i];
+      gx1[(int64_t)i * R + r] = xb1[i];
+    }
+    if (adoch) {
+      T* ga0 = reinterpret_cast<T*>(a.ax[0]);
+      T* ga1 = reinterpret_cast<T*>(a.ax[1]);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ga0[(int64_t)i * R + r] = axb0[i];
+        ga1[(int64_t)i * R + r] = axb1[i];
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (flag_stop) atomicSub(&a.g->running, 1);
+    a.ctl[r] = c;
+  }
+}
+
+SmallPlan plan_small(const CsrDev& J, int solver, int window_mode, bool f64) {
+  SmallPlan sp;
+  const bool adoch = solver == DCX_SOLVER_ADOCH;
+  const SmemLayout L = small_layout((int)J.n, (uint32_t)J.nnz, f64 ? 8 : 4, adoch,
+                                    window_mode == DCX_WINDOW_EXACT, J.col16 != nullptr, val_bytes(J.vk));
+  sp.smem = L.total;
+  sp.threads = SMALL_THREADS;
+  sp.fits = L.total <= 200 * 1024 && J.n <= (1 << 20) && J.nnz < (1ll << 31);
+  return sp;
+}
+
+template <typename T, int VK>
+static void launch_small_t(const SmallArgs& s, const SmallPlan& sp, cudaStream_t st) {
+  auto k = small_kernel<T, VK>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem);
+  k<<<s.a.cfg.R, SMALL_THREADS, sp.smem, st>>>(s);
+}
+
+void launch_small(const MultiPass& m, const CsrDev& J, const SmallPlan& sp, int p_end, cudaStream_t st) {
+  SmallArgs s;
+  s.a = m.args;
+  s.col16 = J.col16;
+  s.col_is16 = J.col16 != nullptr;
+  s.V = J.V;
+  s.p_end = p_end;
+  if (m.f64) {
+    switch (J.vk) {
+      case VK_UNIFORM: launch_small_t<double, VK_UNIFORM>(s, sp, st); break;
+      case VK_I8: launch_small_t<double, VK_I8>(s, sp, st); break;
+      case VK_I16: launch_small_t<double, VK_I16>(s, sp, st); break;
+      case VK_F32: launch_small_t<double, VK_F32>(s, sp, st); break;
+      default: launch_small_t<double, VK_F64>(s, sp, st); break;
+    }
+  } else {
+    switch (J.vk) {
+      case VK_UNIFORM: launch_small_t<float, VK_UNIFORM>(s, sp, st); break;
+      case VK_I8: launch_small_t<float, VK_I8>(s, sp, st); break;
+      case VK_I16: launch_small_t<float, VK_I16>(s, sp, st); break;
+      case VK_F32: launch_small_t<float, VK_F32>(s, sp, st); break;
+      default: launch_small_t<float, VK_F64>(s, sp, st); break;
+    }
+  }
+}
+
+}  // namespace dcx

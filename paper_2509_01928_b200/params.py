@@ -1,0 +1,172 @@
+"""Solver parameters and their derivation (dc/spectral.py).
+
+``derive_params`` follows dc/spectral.py:224-256: alpha = eta * lambda_max(-J)
+(two-stage shifted power iteration below n = 1e4, Wigner estimate at or
+above), beta = n sqrt(n) (alpha + max_i sum_j |J_ij|). Every power-iteration
+product runs on the device (``dcx_matvec``). ``tune_eta`` runs all eta
+candidates as one batch of replicas (one launch sequence instead of one solve
+per candidate, dc/spectral.py:259-298).
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .coupling import device_context
+
+WIGNER_SIZE_THRESHOLD = 10_000
+DEFAULT_ETA_GRID = (0.25, 0.5, 0.75, 1.0, 1.25, 1.5, 2.0)
+
+
+@dataclass
+class SolverParams:
+    """Same fields, defaults and validation as dc/spectral.py:25-49."""
+
+    alpha: float
+    beta: float
+    eta: float = 1.0
+    lookback_q: int = 5
+    max_iters: int = 1000
+    time_budget: Optional[float] = None
+    seed: int = 0
+
+    def __post_init__(self):
+        if not self.alpha > 0:
+            raise ValueError("alpha must be > 0")
+        if not self.beta > 0:
+            raise ValueError("beta must be > 0")
+        if not (0 < self.eta <= 2):
+            raise ValueError("eta must lie in (0, 2]")
+        if self.lookback_q < 1:
+            raise ValueError("lookback_q must be >= 1")
+
+
+def _power(apply_m, n, tol, max_iters, seed=0):
+    """Power iteration with one seeded restart; products on the device."""
+    v = np.full(n, 1.0 / np.sqrt(n))
+    restarted, best_res, stall = False, np.inf, 0
+    mag = ray = 0.0
+    k = 0
+
+    def fresh():
+        r = np.random.default_rng(seed).standard_normal(n)
+        return r / np.linalg.norm(r)
+
+    while k < max_iters:
+        w = apply_m(v)
+        mag = float(np.linalg.norm(w))
+        if mag == 0.0:
+            if restarted:
+                return 0.0, 0.0, k, False
+            v, restarted = fresh(), True
+            k += 1
+            continue
+        ray = float(v @ w)
+        res = float(np.linalg.norm(w - ray * v)) / mag
+        if res <= tol:
+            return mag, ray, k + 1, True
+        if res < 0.999 * best_res:
+            best_res, stall = res, 0
+        else:
+            stall += 1
+            if stall > 50 and not restarted:
+                v, restarted, stall = fresh(), True, 0
+                k += 1
+                continue
+        v = w / mag
+        k += 1
+    return mag, ray, k, False
+
+
+def _moments(J):
+    if hasattr(J, "array"):
+        a = np.asarray(J.array)
+        return float(a.sum()), float((a * a).sum())
+    v = np.asarray(J.values)
+    return float(v.sum()), float((v * v).sum())
+
+
+def _abs_row_max(J) -> float:
+    if hasattr(J, "array"):
+        return float(np.abs(np.asarray(J.array)).sum(axis=1).max())
+    ro = np.asarray(J.row_offsets)
+    rows = np.repeat(np.arange(J.n), np.diff(ro))
+    return float(np.bincount(rows, weights=np.abs(np.asarray(J.values)), minlength=J.n).max())
+
+
+def estimate_lambda_max_neg(J, method="auto", tol=1e-10, max_iters=20_000) -> float:
+    """lambda_max(-J) (dc/spectral.py:192-221)."""
+    if method not in ("auto", "power_iteration", "wigner"):
+        raise ValueError(f"unknown spectral method {method!r}")
+    if method == "auto":
+        method = "power_iteration" if J.n < WIGNER_SIZE_THRESHOLD else "wigner"
+    if method == "wigner":
+        s1, s2 = _moments(J)
+        if s2 == 0.0:
+            raise ValueError("degenerate all-zero coupling matrix")
+        cnt = J.n * (J.n - 1)
+        mean = s1 / cnt
+        std = float(np.sqrt(max(s2 / cnt - mean * mean, 0.0)))
+        est = 2.0 * std * float(np.sqrt(J.n))
+        if est > 0:
+            return est
+    ctx = device_context(J)
+    mv = lambda v: ctx.matvec(v[None, :])[0]  # noqa: E731
+    rho = _power(lambda v: -mv(v), J.n, tol, max_iters)[0]
+    if rho == 0.0:
+        raise ValueError("coupling matrix must have at least one nonzero entry")
+    dom, _, _, ok = _power(lambda v: rho * v - mv(v), J.n, tol, max_iters)
+    if not ok:
+        warnings.warn("shifted power iteration did not converge; using best estimate", RuntimeWarning)
+    return dom - rho
+
+
+def derive_params(J, eta=1.0, method="auto", lookback_q=5, max_iters=1000, time_budget=None, seed=0,
+                  tol=1e-10, power_iters=20_000) -> SolverParams:
+    """alpha = eta lambda_max(-J); beta = n sqrt(n) (alpha + max row |J|_1) (dc/spectral.py:224-256)."""
+    if not (0 < eta <= 2):
+        raise ValueError("eta must lie in (0, 2]")
+    lam = estimate_lambda_max_neg(J, method=method, tol=tol, max_iters=power_iters)
+    if lam <= 0:
+        raise ValueError("spectral estimate is nonpositive; cannot derive alpha")
+    alpha = eta * lam
+    beta = J.n * np.sqrt(J.n) * (alpha + _abs_row_max(J))
+    return SolverParams(alpha=float(alpha), beta=float(beta), eta=eta, lookback_q=lookback_q,
+                        max_iters=max_iters, time_budget=time_budget, seed=seed)
+
+
+def tune_eta(instance, candidate_etas: Sequence[float], probe_iters: int = 10, seed: int = 0, method="auto",
+             tol: float = 1e-8, precision: str = "f64") -> float:
+    """Pick eta by short DOCH probes, all candidates as one replica batch
+    (dc/spectral.py:259-298; ties go to the smaller eta)."""
+    from .model import homogenized_instance
+    from .solvers import initial_state, solve_replicas
+
+    if not candidate_etas:
+        raise ValueError("candidate eta list is empty")
+    if probe_iters < 1:
+        raise ValueError("probe_iters must be >= 1")
+    inst = homogenized_instance(instance)
+    J = inst.coupling
+    try:
+        lam = estimate_lambda_max_neg(J, method=method, tol=tol)
+    except ValueError:
+        return float(min(candidate_etas))
+    row_max = _abs_row_max(J)
+    n = J.n
+    etas = sorted(candidate_etas)
+    alphas = np.array([eta * lam for eta in etas])
+    betas = n * np.sqrt(n) * (alphas + row_max)
+    x0 = np.stack([initial_state(n, a, b, np.random.default_rng(seed)) for a, b in zip(alphas, betas)])
+    res = solve_replicas(inst, "doch", alphas, betas, x0, max_iters=probe_iters, trace_stride=probe_iters,
+                         precision=precision, seeds=[seed] * len(etas))
+    best_eta, best_e = None, np.inf
+    for eta, r in zip(etas, res):
+        e = r.trace[-1].energy
+        if e < best_e:
+            best_e, best_eta = e, eta
+    return float(best_eta)
