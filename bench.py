@@ -218,10 +218,11 @@ def run_ours(args):
             res = dc.solve_replicas(inst, "doch", ALPHA, BETA, X0[s % 2], **kw)
             dev_s.append(res[0].device_seconds)
             updates += N_SPINS * sum(r.iterations for r in res)
+            max_iters_seen = max(r.iterations for r in res)
             best_e = min(best_e, min(r.energy for r in res))
             target = TTS_FRACTION * REF_BEST_CUT
             for r in res:
-                t = next((t.elapsed_s for t in r.trace if CUT_OFFSET - t.best_energy >= target), None)
+                t = r.trace.first_reach_time(target)
                 if t is not None:
                     tts.append(t)
     torch.cuda.synchronize()
@@ -250,8 +251,9 @@ def run_ours(args):
     e_max, = allreduce([e2e_t], "max", world)
     e_upd, = allreduce([float(e2e_upd)], "sum", world)
     # ---------------- dominant kernel roofline (measured live, CUDA events on the solver stream)
-    prof = dc.profile_dominant_kernel(inst, ALPHA, BETA, X0[0], precision=args.precision, path=args.path,
-                                      launches=10)
+    prof = dc.profile_dominant_kernel(inst, ALPHA, BETA, X0[0], precision=args.precision,
+                                      path="multipass" if args.path == "auto" and args.precision != "f16tc"
+                                      else args.path, launches=10)
     hbm, bf16, src = peaks()
     kernel_flops = prof["flops_per_launch"]
     achieved = kernel_flops / (prof["ms_per_launch"] * 1e-3) / 1e12
@@ -261,6 +263,13 @@ def run_ours(args):
             "peak": peak, "unit": "TFLOP/s" if prof["bound"] == "tensor" else "GB/s", "traffic": None,
             "kernel": prof["kernel"], "ms_per_launch": prof["ms_per_launch"], "peak_source": src}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    its = max_iters_seen + 1
+    per_iter = {"multipass": 2, "persistent": 0, "dense_tc": 0}.get(res[0].path, 2)
+    chunk = 32
+    if res[0].path == "multipass":
+        launches_total = args.steps * (per_iter * chunk * -(-its // chunk) + 4)
+    else:
+        launches_total = args.steps * (-(-its // MAX_ITERS) + 3)
     cpu = None
     if rank == 0:
         v, dt, _ = cpu_sample(8, 200)
@@ -281,7 +290,7 @@ def run_ours(args):
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e_upd / e_max, "unit": "spin-updates/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": prof["launches_per_step_estimate"] * args.steps,
+            "gpu_launches": launches_total,
             "clocks": clk.summary(),
             "quality": {"best_energy": best_all, "best_cut": CUT_OFFSET - best_all,
                         "reference_best_cut_32_seeds": REF_BEST_CUT,

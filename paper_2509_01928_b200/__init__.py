@@ -35,6 +35,7 @@ from .solvers import (
     hamiltonian,
     hamiltonian_gradient,
     initial_state,
+    profile_dominant_kernel,
     solve,
     solve_replicas,
 )

@@ -19,7 +19,8 @@ from __future__ import annotations
 import time
 import warnings
 from dataclasses import dataclass, field, replace
-from typing import Callable, Iterable, Optional, Sequence
+from collections.abc import Sequence
+from typing import Callable, Iterable, Optional
 
 import numpy as np
 
@@ -132,37 +133,52 @@ def _event_name(solver: str, ev: int) -> Optional[str]:
     return None
 
 
-class _ReplicaTrace:
-    """Host side of one replica: rebuilds TraceRecords from the device history."""
+class LazyTrace(Sequence):
+    """The trace of one replica as columns; TraceRecords are built on access
+    (a stride-1 trace of 1024 replicas x 1000 iterations would otherwise be a
+    million Python objects)."""
 
-    def __init__(self, solver, cut_offset, callbacks, offset):
+    def __init__(self, solver, iters, elapsed, energy, cut_offset, ev):
         self.solver = solver
+        self.iters = iters
+        self.elapsed = elapsed
+        self.energy = energy
+        self.best = np.minimum.accumulate(energy) if len(energy) else energy
         self.cut_offset = cut_offset
-        self.callbacks = tuple(callbacks)
-        self.offset = offset
-        self.trace = []
-        self.best = np.inf
-        self.h = []
-        self.ev = []
-        self.done = 0
+        self.ev = ev
 
-    def feed(self, h, e, t, ev):
-        for k in range(len(h)):
-            kk = self.done + k
-            self.h.append(float(h[k]))
-            self.ev.append(int(ev[k]))
-            if ev[k] & _native.EV_RECORDED:
-                E = float(e[k])
-                if E < self.best:
-                    self.best = E
-                rec = TraceRecord(iteration=kk, elapsed_s=float(t[k]) + self.offset, energy=E,
-                                  best_energy=self.best,
-                                  cut_value=None if self.cut_offset is None else self.cut_offset - E,
-                                  event=_event_name(self.solver, int(ev[k])) if kk > 0 else None)
-                self.trace.append(rec)
-                for cb in self.callbacks:
-                    cb(rec)
-        self.done += len(h)
+    def __len__(self):
+        return len(self.iters)
+
+    def _rec(self, i):
+        E = float(self.energy[i])
+        k = int(self.iters[i])
+        return TraceRecord(iteration=k, elapsed_s=float(self.elapsed[i]), energy=E,
+                           best_energy=float(self.best[i]),
+                           cut_value=None if self.cut_offset is None else self.cut_offset - E,
+                           event=_event_name(self.solver, int(self.ev[i])) if k > 0 else None)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._rec(j) for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self._rec(i)
+
+    def first_reach_time(self, threshold: float, use_cut: bool = True):
+        """First elapsed_s whose best-so-far quality reaches threshold (dc/bench.py:219-231)."""
+        q = (self.cut_offset - self.best) if (use_cut and self.cut_offset is not None) else -self.best
+        hit = np.nonzero(q >= threshold)[0]
+        return float(self.elapsed[hit[0]]) if len(hit) else None
+
+
+def _collect(ctx, r, solver, cut_offset, offset):
+    s = ctx.summary(r)
+    h, e, t, ev = ctx.history(r, 0, int(s.n_hist))
+    ks = np.nonzero((ev & _native.EV_RECORDED) != 0)[0]
+    return s, h, ev, LazyTrace(solver, ks, t[ks] + offset, e[ks], cut_offset, ev[ks])
 
 
 def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1000, lookback_q: int = 5,
@@ -193,37 +209,46 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
     ctx.begin(prm, alpha, beta, X0)
     offset = time.perf_counter() - t_entry
     cut_offset = getattr(instance, "cut_offset", None)
-    reps = [_ReplicaTrace(solver, cut_offset, callbacks if R == 1 else (), offset) for _ in range(R)]
-    live = True
-    while live:
-        live = ctx.step()
-        for r, rt in enumerate(reps):
-            s = ctx.summary(r)
-            if s.n_hist > rt.done:
-                rt.feed(*ctx.history(r, rt.done, s.n_hist - rt.done))
+    if callbacks and R == 1:
+        # stream records to the callbacks in iteration order, chunk by chunk
+        fed = 0
+        live = True
+        while live:
+            live = ctx.step()
+            s = ctx.summary(0)
+            if s.n_hist > fed:
+                h, e, t, ev = ctx.history(0, fed, int(s.n_hist) - fed)
+                for k in np.nonzero(ev & _native.EV_RECORDED)[0]:
+                    rec = LazyTrace(solver, np.array([fed + k]), t[k:k + 1] + offset, e[k:k + 1], cut_offset,
+                                    ev[k:k + 1])[0]
+                    for cb in callbacks:
+                        cb(rec)
+                fed = int(s.n_hist)
+    else:
+        ctx.run()
     best = ctx.best_spins().astype(np.float64)
     xs = ctx.state()
     dev_s = ctx.device_seconds()
     out = []
-    for r, rt in enumerate(reps):
-        s = ctx.summary(r)
+    for r in range(R):
+        s, h, ev, trace = _collect(ctx, r, solver, cut_offset, offset)
         it = int(s.iterations)
         if s.descent_warn >= 0 and solver == "doch":
             k = int(s.descent_warn)
-            warnings.warn(f"Hamiltonian increased by {rt.h[k] - rt.h[k - 1]:.3e} at iteration {k}",
+            warnings.warn(f"Hamiltonian increased by {h[k] - h[k - 1]:.3e} at iteration {k}",
                           RuntimeWarning, stacklevel=3)
         accepted = None
         if solver == "adoch":
-            accepted = [True] + [bool(rt.ev[k + 1] & _native.EV_ACCEPTED) for k in range(1, it)] if it else []
+            accepted = ([True] + ((ev[2:it + 1] & _native.EV_ACCEPTED) != 0).tolist()) if it else []
         states = None
         if record_states:
             st = ctx.states(r, it)
             states = [st[k].copy() for k in range(it + 1)]
         out.append(SolveResult(
             solver=solver, spins=best[r], energy=float(s.best_energy), iterations=it,
-            stop_reason=_native.STOP.get(int(s.stop_reason), "max_iters"), trace=rt.trace,
-            seed=None if seeds is None else seeds[r], x=xs[r], h_values=rt.h, accepted=accepted, states=states,
-            device_seconds=dev_s, path=_native.PATH_NAME.get(int(s.path_used))))
+            stop_reason=_native.STOP.get(int(s.stop_reason), "max_iters"), trace=trace,
+            seed=None if seeds is None else seeds[r], x=xs[r], h_values=h.tolist(), accepted=accepted,
+            states=states, device_seconds=dev_s, path=_native.PATH_NAME.get(int(s.path_used))))
     return out
 
 
@@ -293,3 +318,35 @@ def solve(instance, solver: str, seed: int = 0, eta: float = 1.0, lookback_q: in
     if getattr(instance, "field", None) is not None:
         res = replace(res, spins=dehomogenize(res.spins))
     return res
+
+
+def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", precision: str = "f32",
+                            path: str = "auto", launches: int = 10, max_iters: int = 1000) -> dict:
+    """Time the dominant kernel of a batched solve alone (CUDA events on the
+    solver stream) and return its algorithmic work per launch."""
+    J = instance.coupling
+    X0 = np.atleast_2d(np.asarray(x0, dtype=np.float64))
+    R, n = X0.shape
+    ctx = device_context(J)
+    prm = _native.Params(solver=_native.SOLVER[solver], window_mode=0, precision=_native.PRECISION[precision],
+                         lookback_q=5, max_iters=int(max_iters), trace_stride=1, time_budget_s=-1.0,
+                         conv_tol=CONVERGENCE_TOL, descent_tol=DESCENT_WARN_TOL, record_states=0,
+                         path=_native.PATH[path], chunk=0, reserved=0)
+    ctx.begin(prm, alpha, beta, X0)
+    ms, kid = ctx.profile(launches)
+    info = ctx.info()
+    dense = bool(info.dense)
+    tb = 8 if precision == "f64" else (2 if precision == "f16tc" else 4)
+    if kid == 3:
+        name = "dense_tc_step"
+        flops = 2.0 * n * n * R
+        byts = float(R * n * tb * 2)
+    else:
+        name = "pass_rn" if R > 1 else "pass_r1"
+        vbytes = {0: 0, 1: 1, 2: 2, 3: 4, 4: 8}[info.value_kind]
+        if info.value_kind in (3, 4):
+            vbytes = tb
+        flops = 2.0 * info.nnz * R
+        byts = float(info.nnz * (4 + vbytes) + (n + 1) * 4 + R * n * tb * 2)
+    return {"kernel": name, "ms_per_launch": ms, "flops_per_launch": flops, "bytes_per_launch": byts,
+            "bound": "tensor" if dense else "hbm", "kernel_id": kid}
