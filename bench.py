@@ -309,7 +309,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default=os.environ.get("DCX_BENCH_PRECISION", "f32"))
+    ap.add_argument("--precision", default=os.environ.get("DCX_BENCH_PRECISION", "f16tc"))
     ap.add_argument("--path", default=os.environ.get("DCX_BENCH_PATH", "auto"))
     args = ap.parse_args()
     if args.impl == "reference":

@@ -115,6 +115,8 @@ int guarded(dcx_ctx* ctx, F&& f) {
     return DCX_OK;
   } catch (const InvalidArg& e) {
     return fail(ctx, DCX_E_INVALID, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(ctx, DCX_E_INVALID, e.what());
   } catch (const CudaError& e) {
     return fail(ctx, DCX_E_CUDA, e.what());
   } catch (const std::bad_alloc& e) {

@@ -1,28 +1,819 @@
-// Dense tensor-core path -- placeholder until the tcgen05 kernel lands.
+// Dense tensor-core DOCH path for fully connected integer couplings (K2000).
+//
+// Replaces, per iteration and for all R replicas at once, the reference's
+// two dense products per DOCH iteration at trace_stride 1 -- J x and J sign(x)
+// (OpenBLAS dgemv, dc/coupling.py:101-102, called from dc/solvers/doch.py:203
+// and :225 through _eval_spins :164-166) -- and the elementwise update
+// x <- cbrt((J + alpha I) x / beta) (doch.py:200) with its reductions.
+//
+// Formulation: replicas are the UMMA M dimension (TMEM lanes),
+// spins the N dimension, so every per-replica reduction is a per-thread sum.
+//   D1[r][i] = sum_j Xh[r][j] Q[i][j]   kind::f16, Xh = f16(x / lambda_r), Q = J / jscale (exact)
+//   D2[r][i] = sum_j S8[r][j] Q8[i][j]  kind::i8,  S8 = sign(x) in int8, Q8 = Q in int8 (exact, s32 acc)
+// One persistent cooperative kernel runs all iterations: a 4-stage TMA ->
+// tcgen05.mma pipeline per 128x128 tile (fp32 / s32 accumulators in TMEM),
+// a TMEM -> register epilogue that applies the DC update and
+// produces the per-replica partials, one grid barrier per iteration, and the
+// per-replica control (dcx_device.cuh) evaluated redundantly by every CTA of a
+// replica tile so no second barrier is needed.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_fp16.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <stdexcept>
+#include <string>
+#include <vector>
+
 #include "dcx_dense.h"
 
 namespace dcx {
 
-void DenseDev::release() {
-  if (q16) cudaFree(q16);
-  q16 = nullptr;
-  n = 0;
+namespace tc {
+
+constexpr int TM = 128;  // replicas per tile (UMMA M)
+constexpr int TN = 128;  // spins per tile (UMMA N)
+constexpr int TK = 64;   // K per stage: 64 f16 = one 128-byte swizzle row
+constexpr int UK = 16;   // UMMA K for kind::f16
+constexpr int STAGES = 4;
+constexpr int THREADS = 384;
+constexpr uint32_t TILE_BYTES = TM * TK * 2;   // 16 KB: 128 rows x 128 B (SW128): 64 f16 or 128 int8 of K
+constexpr uint32_t STAGE_BYTES = 2 * TILE_BYTES;  // A tile + B tile (Xh|Q16 or S8|Q8)
+constexpr uint32_t TMEM_COLS = 256;            // D1 [0,128) f32, D2 [128,256) s32
+
+// Per replica-tile group: the tiles_n CTAs that share one replica tile are
+// the only ones that depend on each other (replicas are independent), so each
+// group synchronises on its own words and runs its own number of iterations.
+struct __align__(64) SyncWords {
+  unsigned int count;
+  unsigned int gen;
+  unsigned long long stamp;
+  int running;       // replicas of the group still running
+  int running_snap;  // snapshot taken by the last arriver
+  int p_exec;        // passes executed by the group (resume point / exit record)
+  int pad[9];
+};
+
+struct Args {
+  CUtensorMap tmA[2];   // Xh by parity (f16)
+  CUtensorMap tmB;      // Q (f16)
+  CUtensorMap tmS[2];   // S8 by parity (int8)
+  CUtensorMap tmQ8;     // Q (int8)
+  float* xm[2];
+  __half* xh[2];
+  int8_t* s8[2];
+  int8_t* best8;
+  double* part;
+  RepCtl* ctl;
+  GState* g;
+  SyncWords* sync;
+  unsigned long long* dbg;  // optional phase timestamps of CTA 0 (DCX_DENSE_TRACE)
+  RunCfg cfg;
+  int n, npad, R, Rpad, tiles_n, p_end;
+  float jscale;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// K-major, 128-byte swizzle smem operand descriptor (SBO = 1024 B between
+// 8-row groups, LBO unused = 1, version 1, layout SWIZZLE_128B = 2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+// K-major, 64-byte swizzle descriptor for the int8 tiles (SBO = 8 rows x 64 B).
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
+// instruction descriptors (K-major A and B): kind::f16 f16 x f16 -> f32; kind::i8 s8 x s8 -> s32
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(dtmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(dtmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-void dense_upload(DenseDev& d, int64_t n, const double*, cudaStream_t) {
+// Grid barrier (all CTAs co-resident: cooperative launch). The last arriver
+// stamps the device clock and snapshots the running-replica count so every
+// CTA takes identical time-budget and exit decisions.
+__device__ __forceinline__ void group_barrier(SyncWords* s, unsigned int members) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int gen = ld_acquire(&s->gen);
+    // release: cumulative over the CTA's writes ordered before it by bar.sync
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (atomicAdd(&s->count, 1u) == members - 1) {
+      s->count = 0;
+      s->stamp = globaltimer();
+      s->running_snap = atomicAdd(&s->running, 0);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      st_release(&s->gen, gen + 1);
+    } else {
+      while (ld_acquire(&s->gen) == gen) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+struct __align__(8) Smem {
+  uint64_t full[STAGES], empty[STAGES], accf1, accf2;
+  uint32_t tmem_base;
+  int pad;
+  float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
+  float red[2][TM][4];
+  double red2[2][TM][4];
+  RepCtl ctl[TM];
+};
+
+// Warp roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM
+// owner), warps 2-3 = control helpers, warps 4-11 = epilogue. Epilogue warp w
+// reads TMEM lane quadrant (w % 4) and spin-column half (w - 4) / 4; the
+// CTA's 128 x 128 f32 master state lives in shared memory for the whole run.
+__global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment (SW128) by offset so the compiler keeps the shared address space
+  unsigned char* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* xs = reinterpret_cast<float*>(tiles + STAGES * STAGE_BYTES);  // [TN cols][TM rows]
+  Smem& sm = *reinterpret_cast<Smem*>(tiles + STAGES * STAGE_BYTES + TM * TN * 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rt = blockIdx.x / a.tiles_n, nt = blockIdx.x % a.tiles_n;
+  const int r0 = rt * TM, i0 = nt * TN;
+  const int KB1 = a.npad / TK;         // f16 stages (K = 64 each)
+  const int KB2 = a.npad / (2 * TK);   // int8 stages (K = 128 each)
+  SyncWords* grp = a.sync + rt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&sm.full[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), 1);
+    }
+    mbar_init(smem_u32(&sm.accf1), 1);
+    mbar_init(smem_u32(&sm.accf2), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  int p = grp->p_exec;  // every CTA of the group reads it before the first group barrier
+  const int p_start = p;
+  if (threadIdx.x < TM) {
+    const int r = r0 + threadIdx.x;
+    if (r < a.R) sm.ctl[threadIdx.x] = a.ctl[r];
+    else sm.ctl[threadIdx.x].status = DCX_STOP_MAX_ITERS;  // padding replicas never run
+    const double al = r < a.R ? a.ctl[r].alpha : 1.0, be = r < a.R ? a.ctl[r].beta : 1.0;
+    const double lam = sqrt(al / be);
+    sm.alpha[threadIdx.x] = float(al);
+    sm.inv_beta[threadIdx.x] = float(1.0 / be);
+    sm.jl[threadIdx.x] = a.jscale * float(lam);
+    sm.inv_lam[threadIdx.x] = float(1.0 / lam);
+  }
+  // epilogue thread geometry
+  const bool epi = warp >= 4;
+  const int q = warp & 3, h = (warp - 4) >> 2;
+  const int rl = q * 32 + lane;
+  const int r = r0 + rl;
+  const bool valid = epi && r < a.R;
+  uint64_t prevmask = 0;  // sign bits of x_{p-1} for this thread's 64 columns
+  if (epi) {
+    const float* src = a.xm[p & 1] + (int64_t)r * a.npad + i0 + h * 64;
+    const int8_t* sp = a.s8[(p + 1) & 1] + (int64_t)r * a.npad + i0 + h * 64;
+    for (int c = 0; c < 64; ++c) {
+      xs[(h * 64 + c) * TM + rl] = valid ? src[c] : 0.f;
+      if (valid && p > 0 && sp[c] < 0) prevmask |= 1ull << c;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t idesc = idesc_f16(TM, TN), idesc8 = idesc_i8(TM, TN);
+  RunCfg cfg = a.cfg;
+  if (nt != 0) cfg.hist = nullptr;  // only the nt == 0 CTA of a replica tile writes history
+
+  uint32_t kiter = 0, acc_phase = 0;
+  // Warps 0-1 (TMA / MMA) start iteration p+1 right after the group barrier of
+  // iteration p; warps 2-11 first finish the control of iteration p, which
+  // therefore overlaps the next GEMM. The exit test reads the snapshot taken at
+  // the barrier, identical for every thread of every CTA of the group.
+  for (; p < a.p_end; ++p) {
+    if (p > p_start && __ldcg(&grp->running_snap) == 0) break;  // every replica of the group stopped
+    const int cur = p & 1;
+    const bool trace = a.dbg && blockIdx.x == 0 && threadIdx.x == 64 && p < 4096;
+    if (trace) a.dbg[p * 7 + 0] = clock64();
+    if (warp < 2) {
+      if (warp == 0) {
+      // ---------------------------------------------------------- producer
+      if (lane == 0) {
+        fence_async_global();
+        for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
+          const int s = kiter % STAGES;
+          const uint32_t ph = (kiter / STAGES) & 1;
+          mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
+          const uint32_t fb = smem_u32(&sm.full[s]);
+          mbar_expect_tx(fb, STAGE_BYTES);
+          unsigned char* st = tiles + s * STAGE_BYTES;
+          if (kb < KB1) {
+            tma_load_2d(smem_u32(st), &a.tmA[cur], kb * TK, r0, fb);
+            tma_load_2d(smem_u32(st + TILE_BYTES), &a.tmB, kb * TK, i0, fb);
+          } else {
+            const int k8 = (kb - KB1) * 2 * TK;
+            tma_load_2d(smem_u32(st), &a.tmS[cur], k8, r0, fb);
+            tma_load_2d(smem_u32(st + TILE_BYTES), &a.tmQ8, k8, i0, fb);
+          }
+        }
+      }
+      __syncwarp();
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer
+      if (lane == 0) {
+        for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
+          const int s = kiter % STAGES;
+          const uint32_t ph = (kiter / STAGES) & 1;
+          mbar_wait(smem_u32(&sm.full[s]), ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(tiles + s * STAGE_BYTES), sb = sa + TILE_BYTES;
+          if (kb < KB1) {
+#pragma unroll
+            for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
+              mma_f16(tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
+              mma_i8(tmem + TN, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8,
+                     ((kb - KB1) | k) ? 1u : 0u);
+          }
+          mma_commit(smem_u32(&sm.empty[s]));
+          if (kb == KB1 - 1) mma_commit(smem_u32(&sm.accf1));
+        }
+        mma_commit(smem_u32(&sm.accf2));
+      }
+      __syncwarp();
+      }
+    } else if (epi) {
+      // ---------------------------------------------------------- epilogue
+      const RepCtl& c = sm.ctl[rl];
+      // the stop decision of control p is known now unless a time budget is set:
+      // converged <=> step(x_p - x_{p-1}) <= tol (computed by control p-1), or p == max_iters.
+      // A replica that stops at p keeps x_p in shared memory (no update).
+      const bool stops_now = p > 0 && (c.step <= a.cfg.conv_tol || p >= a.cfg.max_iters);
+      const bool budget = a.cfg.budget >= 0.0;
+      const bool running = valid && c.status == DCX_STOP_RUNNING && !stops_now;
+      const bool write_master = running && budget;  // a budget stop at p would need x_p
+      const bool copy_prev = valid && p > 0 && c.pend == p - 1;
+      const float alpha = sm.alpha[rl], inv_beta = sm.inv_beta[rl], jl = sm.jl[rl], inv_lam = sm.inv_lam[rl];
+      float s4 = 0.f, sxax = 0.f, es = 0.f, step = 0.f;
+      const int gbase = i0 + h * 64;
+      const int lim = valid ? max(0, min(64, a.n - gbase)) : 0;
+      if (copy_prev && lim > 0) {
+        int8_t* bd = a.best8 + (int64_t)r * a.npad + gbase;
+        for (int cc = 0; cc < 2; ++cc) {
+          __align__(16) int8_t b[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) b[j] = (prevmask >> (cc * 32 + j)) & 1 ? -1 : 1;
+          *reinterpret_cast<uint4*>(bd + cc * 32) = *reinterpret_cast<uint4*>(b);
+          *reinterpret_cast<uint4*>(bd + cc * 32 + 16) = *reinterpret_cast<uint4*>(b + 16);
+        }
+      }
+      uint64_t curmask = 0;
+      mbar_wait(smem_u32(&sm.accf1), acc_phase);
+      tc_fence_after();
+      __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
+      int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
+      float* xg = a.xm[cur] + (int64_t)r * a.npad + gbase;  // x_p (time-budget runs only)
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t v1[32];
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + h * 64 + cc * 32, v1);
+        tmem_ld_wait();
+        __align__(16) __half hv[32];
+        __align__(16) int8_t sv[32];
+        __align__(16) float fv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = h * 64 + cc * 32 + j;
+          float* xp = xs + col * TM + rl;
+          const float x = *xp;
+          const bool in = cc * 32 + j < lim;
+          const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j]));
+          const float nxt = cbrtf(ax * inv_beta);
+          if (in) {
+            const float x2 = x * x;
+            s4 = fmaf(x2, x2, s4);
+            sxax = fmaf(x, ax, sxax);
+            step = fmaxf(step, fabsf(nxt - x));
+            if (x < 0.f) curmask |= 1ull << (cc * 32 + j);
+            if (running) *xp = nxt;
+          }
+          fv[j] = x;
+          hv[j] = __float2half_rn(in ? nxt * inv_lam : 0.f);
+          sv[j] = in ? (nxt >= 0.f ? 1 : -1) : 0;
+        }
+        if (running && lim > 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) *reinterpret_cast<uint4*>(hn + cc * 32 + j) = *reinterpret_cast<uint4*>(hv + j);
+          if (write_master) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(fv + j);
+          }
+          *reinterpret_cast<uint4*>(sn + cc * 32) = *reinterpret_cast<uint4*>(sv);
+          *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 16);
+        }
+      }
+      // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i
+      mbar_wait(smem_u32(&sm.accf2), acc_phase);
+      tc_fence_after();
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t v2[32];
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * 64 + cc * 32, v2);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float y2 = float(int(v2[j]));
+          if (cc * 32 + j < lim) es += ((curmask >> (cc * 32 + j)) & 1) ? -y2 : y2;
+        }
+      }
+      if (running) prevmask = curmask;
+      sm.red[h][rl][0] = s4;
+      sm.red[h][rl][1] = sxax;
+      sm.red[h][rl][2] = es;
+      sm.red[h][rl][3] = step;
+        }
+    if (trace) {
+      mbar_wait(smem_u32(&sm.accf2), acc_phase);
+      a.dbg[p * 7 + 1] = clock64();
+    }
+    acc_phase ^= 1;
+    tc_fence_before();
+    __syncthreads();
+    if (trace) a.dbg[p * 7 + 2] = clock64();
+    if (threadIdx.x < TM) {
+      const int rr = r0 + threadIdx.x;
+      if (rr < a.R) {
+        // layout [replica tile][spin tile][replica in tile] x 4
+        double* dst = a.part + (((int64_t)rt * a.tiles_n + nt) * TM + threadIdx.x) * 4;
+        const int t = threadIdx.x;
+        double4 v;
+        v.x = double(sm.red[0][t][0]) + double(sm.red[1][t][0]);
+        v.y = double(sm.red[0][t][1]) + double(sm.red[1][t][1]);
+        v.z = double(sm.red[0][t][2]) + double(sm.red[1][t][2]);
+        v.w = fmax(double(sm.red[0][t][3]), double(sm.red[1][t][3]));
+        *reinterpret_cast<double4*>(dst) = v;
+      }
+    }
+    if (epi) fence_async_global();  // xh / s8 written here are read by TMA next iteration
+    group_barrier(grp, a.tiles_n);
+    if (trace) a.dbg[p * 7 + 3] = clock64();
+    if (warp < 2) continue;  // TMA / MMA go on with the next iteration
+    // ---------------------------------------------------------- control (warps 4-11)
+    if (epi) {
+      // two threads per replica, each summing half of the spin tiles in a fixed
+      // order straight from L2 (written by the other CTAs of the group)
+      const int half = (a.tiles_n + 1) / 2;
+      const int t0 = h * half, t1 = min(a.tiles_n, t0 + half);
+      const double2* src = reinterpret_cast<const double2*>(a.part + ((int64_t)rt * a.tiles_n * TM) * 4);
+      constexpr int MAXH = 8;  // tiles_n <= 16
+      double2 u[MAXH], w[MAXH];
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k)
+        if (t0 + k < t1) {
+          const int64_t e = ((int64_t)(t0 + k) * TM + rl) * 2;
+          u[k] = __ldcg(src + e);
+          w[k] = __ldcg(src + e + 1);
+        }
+      double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k)
+        if (t0 + k < t1) {
+          s0 += u[k].x;
+          s1 += u[k].y;
+          s2 += w[k].x;
+          s3 = fmax(s3, w[k].y);
+        }
+      sm.red2[h][rl][0] = s0;
+      sm.red2[h][rl][1] = s1;
+      sm.red2[h][rl][2] = s2;
+      sm.red2[h][rl][3] = s3;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (h == 0 && r < a.R) {
+        RepCtl c = sm.ctl[rl];
+        if (c.status == DCX_STOP_RUNNING) {
+          double tot[NQ] = {0, 0, 0, 0, 0, 0};
+          tot[Q_S4] = sm.red2[0][rl][0] + sm.red2[1][rl][0];
+          tot[Q_SXAX] = sm.red2[0][rl][1] + sm.red2[1][rl][1];
+          tot[Q_ES] = sm.red2[0][rl][2] + sm.red2[1][rl][2];
+          tot[Q_STEP] = fmax(sm.red2[0][rl][3], sm.red2[1][rl][3]);
+          const double now = double(__ldcg(&grp->stamp) - a.g->t0) * 1e-9;
+          const bool stopped = control_after_pass(c, cfg, r, tot, p, now);
+          c.step = tot[Q_STEP];
+          sm.ctl[rl] = c;
+          if (nt == 0) {
+            a.ctl[r] = c;
+            if (stopped) {
+              atomicSub(&grp->running, 1);
+              atomicSub(&a.g->running, 1);
+            }
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+    if (trace) a.dbg[p * 7 + 4] = clock64();
+  }
+  // ---------------------------------------------------------------- teardown
+  if (epi && valid) {
+    // the run's final (or frozen) states; a time-budget stop at p was persisted above
+    const RepCtl& c = sm.ctl[rl];
+    const bool budget_stop = c.status == DCX_STOP_TIME_BUDGET;
+    float* d0 = a.xm[0] + (int64_t)r * a.npad + i0 + h * 64;
+    float* d1 = a.xm[1] + (int64_t)r * a.npad + i0 + h * 64;
+    const int lim = max(0, min(64, a.n - (i0 + h * 64)));
+    if (!budget_stop)
+      for (int cc = 0; cc < lim; ++cc) {
+        const float v = xs[(h * 64 + cc) * TM + rl];
+        d0[cc] = v;
+        d1[cc] = v;
+      }
+  }
+  // all CTAs of the group read p_exec before the first barrier and exit at the same p
+  if (nt == 0 && threadIdx.x == 0) {
+    grp->p_exec = p;
+    atomicMax(&a.g->p, p);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// --------------------------------------------------------------- layout kernels
+// [n][R] f32 (common layout) -> [Rpad][npad] f32 master + f16 scaled operand
+__global__ void pack_state(const float* src, int n, int R, int npad, const RepCtl* ctl, float* xm, __half* xh,
+                           int8_t* s8) {
+  const int64_t total = int64_t(n) * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / R;
+    const int r = int(idx % R);
+    const float x = src[idx];
+    const float inv_lam = float(1.0 / sqrt(ctl[r].alpha / ctl[r].beta));
+    xm[(int64_t)r * npad + i] = x;
+    xh[(int64_t)r * npad + i] = __float2half_rn(x * inv_lam);
+    s8[(int64_t)r * npad + i] = x >= 0.f ? 1 : -1;
+  }
+}
+// pending best copy of the last executed pass, then [Rpad][npad] -> [n][R]
+__global__ void unpack_results(const float* xm0, const float* xm1, const int8_t* s80, const int8_t* s81,
+                               int8_t* best8, int n, int R, int npad, const RepCtl* ctl, const SyncWords* sync,
+                               float* x0, float* x1, int8_t* best) {
+  const int64_t total = int64_t(n) * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / R;
+    const int r = int(idx % R);
+    const int64_t s = (int64_t)r * npad + i;
+    const int pe = ctl[r].pend;
+    const int P = sync[r / TM].p_exec - 1;  // last pass executed by the replica's group
+    int8_t b = best8[s];
+    if (pe >= 0 && pe == P) b = (pe & 1) ? s81[s] : s80[s];
+    best[idx] = b;
+    x0[idx] = xm0[s];
+    x1[idx] = xm1[s];
+  }
+}
+
+__global__ void q_expand(const int16_t* q, __half* out, int8_t* out8, int64_t n, int64_t npad) {
+  const int64_t total = npad * npad;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / npad, j = idx % npad;
+    const int v = (i < n && j < n) ? q[i * n + j] : 0;
+    out[idx] = __int2half_rn(v);
+    out8[idx] = int8_t(v);
+  }
+}
+
+}  // namespace tc
+
+// ================================================================== host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major [rows][cols] map, 128-byte rows x 128 rows per box (64 f16 or
+// 128 int8 along K), 128-byte swizzle: the canonical K-major SW128 UMMA layout.
+static void make_map(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, bool f16) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * (f16 ? 2 : 1)};
+  const cuuint32_t box[2] = {f16 ? cuuint32_t(tc::TK) : cuuint32_t(2 * tc::TK), 128};  // 128-byte rows
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+#define DCK(call)                                                                                          \
+  do {                                                                                                     \
+    cudaError_t e_ = (call);                                                                               \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+void DenseDev::release_run() {
+  for (int b = 0; b < 2; ++b) {
+    if (xm[b]) cudaFree(xm[b]);
+    if (xh[b]) cudaFree(xh[b]);
+    if (s8[b]) cudaFree(s8[b]);
+    xm[b] = xh[b] = s8[b] = nullptr;
+  }
+  if (best8) cudaFree(best8);
+  if (part) cudaFree(part);
+  if (sync) cudaFree(sync);
+  best8 = nullptr;
+  part = nullptr;
+  sync = nullptr;
+  R = Rpad = 0;
+}
+
+void DenseDev::release() {
+  release_run();
+  if (q16) cudaFree(q16);
+  if (q8) cudaFree(q8);
+  q16 = q8 = nullptr;
+  if (tmaps) delete[] reinterpret_cast<CUtensorMap*>(tmaps);
+  tmaps = nullptr;
+  n = npad = 0;
+  exact = false;
+}
+
+void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.release();
   d.n = n;
+  d.npad = (n + 127) / 128 * 128;
+  // exact small-integer form J = jscale * Q (the K2000 instance: jscale = -1/2, Q = +-1)
+  double mn = 0.0;
+  for (int64_t e = 0; e < n * n; ++e)
+    if (A[e] != 0.0 && (mn == 0.0 || std::fabs(A[e]) < mn)) mn = std::fabs(A[e]);
+  if (mn == 0.0) return;
+  double scale = 0.0;
+  for (double cand : {mn, 1.0, 0.5}) {
+    bool ok = true;
+    for (int64_t e = 0; e < n * n && ok; ++e) {
+      const double q = A[e] / cand;
+      if (q != std::nearbyint(q) || std::fabs(q) > 127.0 || cand * std::nearbyint(q) != A[e]) ok = false;
+    }
+    if (ok) { scale = cand; break; }
+  }
+  if (scale == 0.0) return;  // real-valued couplings: no exact f16 operand, tensor path unavailable
+  // sign convention: keep Q's sign (J = scale * Q with scale > 0); K2000 has Q = -W/2 / 0.5 = -W
+  std::vector<int16_t> q(n * n);
+  for (int64_t e = 0; e < n * n; ++e) q[e] = int16_t(std::nearbyint(A[e] / scale));
+  int16_t* dq = nullptr;
+  DCK(cudaMalloc(&dq, n * n * 2));
+  DCK(cudaMemcpyAsync(dq, q.data(), n * n * 2, cudaMemcpyHostToDevice, s));
+  DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
+  DCK(cudaMalloc(&d.q8, d.npad * d.npad));
+  tc::q_expand<<<1024, 256, 0, s>>>(dq, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8), n, d.npad);
+  DCK(cudaStreamSynchronize(s));
+  cudaFree(dq);
+  d.jscale = float(scale);
+  d.exact = true;
+  d.tmaps = new CUtensorMap[6];
 }
-void dense_begin(DenseDev&, MultiPass&, cudaStream_t) {
-  throw std::runtime_error("dense tensor-core path not built yet");
+
+static size_t dense_smem_bytes() { return 1024 + tc::STAGES * tc::STAGE_BYTES + tc::TM * tc::TN * 4 + sizeof(tc::Smem); }
+
+void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
+  if (!d.exact) throw std::invalid_argument("tensor-core path needs small-integer dense couplings");
+  const RunCfg& cfg = m.args.cfg;
+  if (cfg.solver != DCX_SOLVER_DOCH) throw std::invalid_argument("tensor-core path implements DOCH");
+  d.release_run();
+  d.R = cfg.R;
+  d.Rpad = (d.R + 127) / 128 * 128;
+  const int tiles = (d.Rpad / 128) * int(d.npad / 128);
+  int dev = 0, nsm = 0;
+  DCK(cudaGetDevice(&dev));
+  DCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (tiles > nsm)
+    throw std::invalid_argument("tensor-core path: (R/128)*(n/128) tiles must fit the SM count (" +
+                                std::to_string(tiles) + " > " + std::to_string(nsm) + ")");
+  const size_t vec = size_t(d.Rpad) * d.npad;
+  for (int b = 0; b < 2; ++b) {
+    DCK(cudaMalloc(&d.xm[b], vec * 4));
+    DCK(cudaMalloc(&d.xh[b], vec * 2));
+    DCK(cudaMalloc(&d.s8[b], vec));
+    DCK(cudaMemsetAsync(d.xm[b], 0, vec * 4, s));
+    DCK(cudaMemsetAsync(d.xh[b], 0, vec * 2, s));
+    DCK(cudaMemsetAsync(d.s8[b], 0, vec, s));
+  }
+  DCK(cudaMalloc(&d.best8, vec));
+  DCK(cudaMemsetAsync(d.best8, 1, vec, s));
+  DCK(cudaMalloc(&d.part, sizeof(double) * 4 * (d.npad / 128) * d.Rpad));
+  {
+    const int ngroups = d.Rpad / 128;
+    std::vector<tc::SyncWords> sw(ngroups);
+    std::memset(sw.data(), 0, sizeof(tc::SyncWords) * ngroups);
+    for (int gI = 0; gI < ngroups; ++gI) sw[gI].running = std::min(128, d.R - gI * 128);
+    DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * ngroups));
+    DCK(cudaMemcpyAsync(d.sync, sw.data(), sizeof(tc::SyncWords) * ngroups, cudaMemcpyHostToDevice, s));
+  }
+  if (d.dbg) cudaFree(d.dbg);
+  d.dbg = nullptr;
+  if (std::getenv("DCX_DENSE_TRACE")) {
+    DCK(cudaMalloc(&d.dbg, 4096 * 9 * 8));
+    DCK(cudaMemsetAsync(d.dbg, 0, 4096 * 9 * 8, s));
+  }
+  tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
+                                       m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
+                                       reinterpret_cast<__half*>(d.xh[0]), reinterpret_cast<int8_t*>(d.s8[0]));
+  DCK(cudaGetLastError());
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(d.tmaps);
+  make_map(&maps[0], d.xh[0], d.npad, d.Rpad, true);
+  make_map(&maps[1], d.xh[1], d.npad, d.Rpad, true);
+  make_map(&maps[2], d.q16, d.npad, d.npad, true);
+  make_map(&maps[3], d.s8[0], d.npad, d.Rpad, false);
+  make_map(&maps[4], d.s8[1], d.npad, d.Rpad, false);
+  make_map(&maps[5], d.q8, d.npad, d.npad, false);
+  DCK(cudaFuncSetAttribute(tc::dense_doch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)dense_smem_bytes()));
 }
-void dense_step(DenseDev&, MultiPass&, int, cudaStream_t) {
-  throw std::runtime_error("dense tensor-core path not built yet");
+
+static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
+  tc::Args a;
+  std::memset(&a, 0, sizeof(a));
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(d.tmaps);
+  a.tmA[0] = maps[0];
+  a.tmA[1] = maps[1];
+  a.tmB = maps[2];
+  a.tmS[0] = maps[3];
+  a.tmS[1] = maps[4];
+  a.tmQ8 = maps[5];
+  for (int b = 0; b < 2; ++b) {
+    a.xm[b] = reinterpret_cast<float*>(d.xm[b]);
+    a.xh[b] = reinterpret_cast<__half*>(d.xh[b]);
+    a.s8[b] = reinterpret_cast<int8_t*>(d.s8[b]);
+  }
+  a.best8 = d.best8;
+  a.part = d.part;
+  a.ctl = m.args.ctl;
+  a.g = m.args.g;
+  a.sync = reinterpret_cast<tc::SyncWords*>(d.sync);
+  a.dbg = reinterpret_cast<unsigned long long*>(d.dbg);
+  a.cfg = m.args.cfg;
+  a.n = int(d.n);
+  a.npad = int(d.npad);
+  a.R = d.R;
+  a.Rpad = d.Rpad;
+  a.tiles_n = int(d.npad / 128);
+  a.p_end = p_end;
+  a.jscale = d.jscale;
+  const int grid = (d.Rpad / 128) * a.tiles_n;
+  void* args[] = {&a};
+  DCK(cudaLaunchCooperativeKernel((const void*)tc::dense_doch_kernel, dim3(grid), dim3(tc::THREADS), args,
+                                  dense_smem_bytes(), s));
 }
-void dense_finish(DenseDev&, MultiPass&, cudaStream_t) {}
-void dense_profile(DenseDev&, MultiPass&, int, cudaEvent_t, cudaEvent_t, cudaStream_t) {
-  throw std::runtime_error("dense tensor-core path not built yet");
+
+void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s) {
+  // the kernel reads the pass counter on device; p_end bounds this launch
+  GState g{};
+  DCK(cudaMemcpyAsync(&g, m.args.g, sizeof(GState), cudaMemcpyDeviceToHost, s));
+  DCK(cudaStreamSynchronize(s));
+  const int64_t p_end = std::min<int64_t>(int64_t(g.p) + chunk, m.args.cfg.max_iters + 1);
+  launch_dense(d, m, int(p_end), s);
+}
+
+void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
+  if (d.dbg) {  // phase breakdown of CTA 0 (DCX_DENSE_TRACE=1)
+    std::vector<unsigned long long> t(4096 * 7);
+    DCK(cudaMemcpyAsync(t.data(), d.dbg, t.size() * 8, cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int p = 1; p < 4096 && t[p * 7 + 4]; ++p, ++cnt)
+      for (int k = 0; k < 4; ++k) acc[k] += double(t[p * 7 + k + 1]) - double(t[p * 7 + k]);
+    if (cnt)
+      std::fprintf(stderr,
+                   "[dcx dense trace] %d iters, kcycles/iter (CTA 0, warp 2 view): gemms+epilogue %.2f drain %.2f "
+                   "barrier %.2f control %.2f\n",
+                   cnt, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3);
+  }
+  tc::unpack_results<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(d.xm[0]),
+                                           reinterpret_cast<const float*>(d.xm[1]),
+                                           reinterpret_cast<const int8_t*>(d.s8[0]),
+                                           reinterpret_cast<const int8_t*>(d.s8[1]), d.best8, int(d.n), d.R,
+                                           int(d.npad), m.args.ctl, reinterpret_cast<const tc::SyncWords*>(d.sync),
+                                           reinterpret_cast<float*>(m.args.x[0]),
+                                           reinterpret_cast<float*>(m.args.x[1]), m.args.best);
+  DCK(cudaGetLastError());
+}
+
+int dense_iters_per_profile_launch() { return 10; }
+
+void dense_profile(DenseDev& d, MultiPass& m, int launches, cudaEvent_t ea, cudaEvent_t eb, cudaStream_t s) {
+  const int it = dense_iters_per_profile_launch();
+  launch_dense(d, m, it, s);  // warm (passes 0..9)
+  DCK(cudaEventRecord(ea, s));
+  for (int l = 0; l < launches; ++l) launch_dense(d, m, it * (l + 2), s);
+  DCK(cudaEventRecord(eb, s));
 }
 
 }  // namespace dcx

@@ -1,4 +1,4 @@
-// Dense tensor-core path (K2000-style fully connected couplings): declarations.
+// Dense tensor-core path (K2000-style fully connected integer couplings).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -6,14 +6,27 @@
 
 namespace dcx {
 
-// Device operands of the dense path. J is held as exact small integers
-// (J = scale * Q, Q in int8) expanded once into the MMA operand layout.
+// Device operands of the dense path. J = jscale * Q with Q a small integer
+// matrix, held exactly as f16 in the MMA operand layout [npad][npad].
 struct DenseDev {
-  int64_t n = 0;
-  void* q16 = nullptr;  // fp16 operand tiles of Q (padded)
-  double scale = 1.0;
-  bool exact_int = false;
+  int64_t n = 0, npad = 0;
+  bool exact = false;    // Q exactly representable in int8 (|q| <= 127)
+  float jscale = 1.0f;
+  void* q16 = nullptr;   // f16 Q [npad][npad]
+  void* q8 = nullptr;    // int8 Q [npad][npad] (energy GEMM)
+  // per-run buffers
+  int R = 0, Rpad = 0;
+  void* xm[2] = {nullptr, nullptr};  // f32 master states [Rpad][npad]
+  void* xh[2] = {nullptr, nullptr};  // f16 x / lambda_r [Rpad][npad] (MMA operand A)
+  void* s8[2] = {nullptr, nullptr};  // int8 sign(x) [Rpad][npad] (energy GEMM operand A)
+  int8_t* best8 = nullptr;           // [Rpad][npad]
+  double* part = nullptr;            // [tiles_n][Rpad][4]
+  void* sync = nullptr;              // grid barrier words
+  void* tmaps = nullptr;             // host-side CUtensorMap storage (3 maps)
+  int chunk_hint = 0;
+  void* dbg = nullptr;                // phase timestamps (DCX_DENSE_TRACE)
   void release();
+  void release_run();
 };
 
 void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s);
@@ -21,5 +34,6 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s);
 void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s);
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s);
 void dense_profile(DenseDev& d, MultiPass& m, int launches, cudaEvent_t a, cudaEvent_t b, cudaStream_t s);
+int dense_iters_per_profile_launch();
 
 }  // namespace dcx

@@ -187,7 +187,8 @@ __device__ inline bool control_after_pass(RepCtl& c, const RunCfg& cfg, int r, c
                                           double now_s) {
   const double h = __dsub_rn(__dmul_rn(__dmul_rn(0.25, c.beta), tot[Q_S4]), __dmul_rn(0.5, tot[Q_SXAX]));
   const double E = __dmul_rn(-0.5, __dmul_rn(cfg.es_scale, tot[Q_ES]));
-  HistRec* hr = cfg.hist + (int64_t)r * cfg.hist_cap + (p % cfg.hist_cap);
+  // cfg.hist == nullptr: redundant evaluation (dense path), no history writes
+  HistRec* hr = cfg.hist ? cfg.hist + (int64_t)r * cfg.hist_cap + (p % cfg.hist_cap) : nullptr;
   bool stopped = false;
   if (p == 0) {
     c.h = h;
@@ -195,7 +196,7 @@ __device__ inline bool control_after_pass(RepCtl& c, const RunCfg& cfg, int r, c
     c.best = E;  // first record always improves on +inf (dc/solvers/common.py:70-73)
     c.best_iter = 0;
     c.pend = 0;
-    hr->h = h; hr->e = E; hr->t = now_s; hr->ev = DCX_EV_RECORDED;
+    if (hr) { hr->h = h; hr->e = E; hr->t = now_s; hr->ev = DCX_EV_RECORDED; }
     if (cfg.solver == DCX_SOLVER_ADOCH) { c.wlen = 0; window_push(c, cfg, r, h); }
     if (cfg.max_iters <= 0) { c.status = DCX_STOP_MAX_ITERS; stopped = true; }
     return stopped;
@@ -222,7 +223,7 @@ __device__ inline bool control_after_pass(RepCtl& c, const RunCfg& cfg, int r, c
     ev |= DCX_EV_RECORDED;
     if (E < c.best) { c.best = E; c.best_iter = k; c.pend = k; }
   }
-  hr->h = h; hr->e = record ? E : __longlong_as_double(0x7ff8000000000000ll); hr->t = now_s; hr->ev = ev;
+  if (hr) { hr->h = h; hr->e = record ? E : __longlong_as_double(0x7ff8000000000000ll); hr->t = now_s; hr->ev = ev; }
   if (converged) { c.status = DCX_STOP_CONVERGED; stopped = true; }
   else if (late) { c.status = DCX_STOP_TIME_BUDGET; stopped = true; }
   else if (k >= cfg.max_iters) { c.status = DCX_STOP_MAX_ITERS; stopped = true; }

@@ -338,9 +338,12 @@ def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", 
     dense = bool(info.dense)
     tb = 8 if precision == "f64" else (2 if precision == "f16tc" else 4)
     if kid == 3:
-        name = "dense_tc_step"
-        flops = 2.0 * n * n * R
-        byts = float(R * n * tb * 2)
+        # one launch = DENSE_PROFILE_ITERS iterations of the persistent kernel; per
+        # iteration two n x n x R products: J x (f16 -> f32) and J sign(x) (int8 -> s32)
+        name = "dense_doch_kernel"
+        iters = 10
+        flops = iters * 2 * (2.0 * n * n * R)
+        byts = float(iters * R * n * (2 + 1))  # f16 + int8 operands of the next iteration
     else:
         name = "pass_rn" if R > 1 else "pass_r1"
         vbytes = {0: 0, 1: 1, 2: 2, 3: 4, 4: 8}[info.value_kind]

@@ -1,0 +1,108 @@
+"""GPU: the dense tcgen05 path (precision "f16tc") against the exact energy
+kernel, the f32 path and the reference's K2000 quality numbers.
+
+The states enter the tensor cores as f16(x / lambda_r) (10-bit mantissa, exact
++-1 couplings, fp32 accumulation), so iterates track the f32 path to ~1e-3
+relative; energies of spin vectors are computed by an exact +-1 x +-1 GEMM
+and must match the integer energy kernel bit for bit; quality is judged on
+distributions (SURVEY.md §8c G-quality)."""
+
+import numpy as np
+import pytest
+
+import paper_2509_01928_b200 as dc
+from conftest import k2_W
+
+pytestmark = pytest.mark.gpu
+
+# f16 operand rounding (2^-11 relative per element) through one product and the
+# cube root (ill-conditioned near 0): measured 2.24e-3 on K2000, identical to a
+# float64 emulation of the same operand rounding (see test below).
+TC_STATE_TOL = 5e-3   # one iteration; three iterations compound to ~6e-3 (checked at 1e-2)
+EMU_TOL = 5e-4  # TC iterate vs a float64 emulation of the f16 operand (f32 epilogue noise through cbrt)
+
+
+def k2_instance():
+    return dc.ProblemInstance(coupling=dc.maxcut_to_ising(dc.DenseCoupling(k2_W(), validate=False)),
+                              cut_offset=595.0)
+
+
+def x0s(n, alpha, beta, seeds):
+    return np.stack([dc.initial_state(n, alpha, beta, np.random.default_rng(s)) for s in seeds])
+
+
+def rel2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_tc_first_iterate_equals_f16_operand_emulation(gold):
+    g = gold["k2"]
+    inst = k2_instance()
+    a, b = g["alpha"], g["beta"]
+    lam = np.sqrt(a / b)
+    X0 = x0s(2000, a, b, range(128))
+    tc = dc.solve_replicas(inst, "doch", a, b, X0, max_iters=1, precision="f16tc")
+    J = -0.5 * k2_W()
+    for x0, r in zip(X0, tc):
+        xq = (x0 / lam).astype(np.float16).astype(np.float64) * lam
+        emu = np.cbrt((J @ xq + a * x0) / b)
+        assert rel2(r.x, emu) <= EMU_TOL
+
+
+def test_tc_first_iterates_track_f32(gold):
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(128))
+    for iters in (1, 3):
+        tc = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=iters, precision="f16tc")
+        f32 = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=iters, precision="f32")
+        assert tc[0].path == "dense_tc"
+        for a, b in zip(tc, f32):
+            assert a.iterations == b.iterations == iters
+            assert rel2(a.x, b.x) <= TC_STATE_TOL * (1 if iters == 1 else 4)
+
+
+def test_tc_energies_exact():
+    g_alpha, g_beta = 4.462132927392335, 89797103.04245317
+    inst = k2_instance()
+    X0 = x0s(2000, g_alpha, g_beta, range(256))
+    res = dc.solve_replicas(inst, "doch", g_alpha, g_beta, X0, max_iters=60, precision="f16tc")
+    spins = np.stack([r.spins for r in res])
+    np.testing.assert_array_equal(dc.energies(inst.coupling, spins), [r.energy for r in res])
+    for r in res[:8]:
+        assert all(t.energy == t.energy for t in r.trace)  # recorded every iteration (stride 1)
+        assert len(r.trace) == r.iterations + 1
+
+
+def test_tc_padding_ragged_sizes():
+    rng = np.random.default_rng(4)
+    n = 300
+    a = np.triu(np.where(rng.random((n, n)) < 0.5, -1.0, 1.0), 1)
+    J = dc.DenseCoupling(a + a.T, validate=False)
+    inst = dc.ProblemInstance(coupling=J)
+    p = dc.derive_params(J, eta=0.5)
+    X0 = x0s(n, p.alpha, p.beta, range(200))
+    tc = dc.solve_replicas(inst, "doch", p.alpha, p.beta, X0, max_iters=2, precision="f16tc")
+    f32 = dc.solve_replicas(inst, "doch", p.alpha, p.beta, X0, max_iters=2, precision="f32")
+    for a_, b_ in zip(tc, f32):
+        assert rel2(a_.x, b_.x) <= 3 * TC_STATE_TOL  # two iterations at eta = 0.5
+    full = dc.solve_replicas(inst, "doch", p.alpha, p.beta, X0, max_iters=300, precision="f16tc")
+    np.testing.assert_array_equal(dc.energies(J, np.stack([r.spins for r in full])), [r.energy for r in full])
+
+
+def test_tc_k2000_quality_vs_reference(gold):
+    """1024 replicas (BASELINE configs[1]) vs the CPU reference's 32-seed DOCH runs."""
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(1024))
+    res = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=1000, precision="f16tc")
+    e = np.array([r.energy for r in res])
+    ref = np.array([row["energy"] for row in g["doch"]])
+    se = ref.std() / np.sqrt(len(ref))
+    # distribution no worse than the f64 reference (one-sided, 3 standard errors of the
+    # reference mean), on the shared seeds 0..31 and on all 1024 replicas
+    assert e[:32].mean() <= ref.mean() + 3 * se
+    assert e.mean() <= ref.mean() + 3 * se
+    # the reference's own best over 32 seeds sits 2.4 sigma out; 1024 replicas reach 2 sigma
+    assert e.min() <= ref.mean() - 2.0 * ref.std()
+    assert np.quantile(e, 0.1) <= np.quantile(ref, 0.1) + 3 * se
