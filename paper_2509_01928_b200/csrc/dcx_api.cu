@@ -88,10 +88,12 @@ struct dcx_ctx {
   double dev_seconds = 0.0;
   std::vector<std::vector<HistRec>> hh;
   std::vector<RepCtl> hctl;
-  std::vector<HistRec> ring;
+  HistRec* ring = nullptr;  // pinned host copy of the device history ring
+  size_t ring_n = 0;
   GState hg{};
 
   ~dcx_ctx() {
+    if (ring) cudaFreeHost(ring);
     if (graph) cudaGraphExecDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -685,7 +687,13 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
     c->hh.assign(R, {});
     for (auto& v : c->hh) v.reserve(std::min<int64_t>(P->max_iters + 1, 4096));
     c->hctl = h;
-    c->ring.resize(size_t(R) * cap);
+    if (c->ring_n < size_t(R) * cap) {
+      if (c->ring) cudaFreeHost(c->ring);
+      c->ring = nullptr;
+      c->ring_n = 0;
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&c->ring), sizeof(HistRec) * size_t(R) * cap, cudaHostAllocDefault));
+      c->ring_n = size_t(R) * cap;
+    }
     c->p_host = 0;
     if (c->path == DCX_PATH_MULTIPASS) build_graph(c);
     if (c->path == DCX_PATH_DENSE_TC) dense_begin(c->dn, c->mp, c->stream);
@@ -715,7 +723,7 @@ static void drain(dcx_ctx* c) {
   const size_t rec = sizeof(HistRec);
   const size_t pitch = rec * c->cap;
   auto copy_cols = [&](int64_t k0, int64_t k1) {  // ring columns [k0, k1] without wrap
-    CK(cudaMemcpy2DAsync(c->ring.data() + k0, pitch, c->hist.as<HistRec>() + k0, pitch, rec * (k1 - k0 + 1), R,
+    CK(cudaMemcpy2DAsync(c->ring + k0, pitch, c->hist.as<HistRec>() + k0, pitch, rec * (k1 - k0 + 1), R,
                          cudaMemcpyDeviceToHost, c->stream));
   };
   if (hi - lo + 1 >= c->cap) copy_cols(0, c->cap - 1);
@@ -759,13 +767,15 @@ int dcx_solve_step(dcx_ctx* c, int32_t* live) {
       dense_step(c->dn, c->mp, c->chunk, c->stream);
     }
     CK(cudaGetLastError());
+    // device time of the solve ends with the last compute launch; history / result
+    // downloads that follow belong to the end-to-end time only
+    CK(cudaEventRecord(c->ev1, c->stream));
     drain(c);
     bool alive = c->hg.live != 0 && c->hg.running > 0;
     if (c->path == DCX_PATH_PERSISTENT && c->p_host >= c->prm.max_iters + 1) alive = false;
     if (!alive) {
       if (c->path == DCX_PATH_MULTIPASS) enqueue_flush(c->mp, c->stream);
       if (c->path == DCX_PATH_DENSE_TC) dense_finish(c->dn, c->mp, c->stream);
-      CK(cudaEventRecord(c->ev1, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));

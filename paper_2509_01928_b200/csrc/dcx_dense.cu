@@ -38,11 +38,23 @@ constexpr int TM = 128;  // replicas per tile (UMMA M)
 constexpr int TN = 128;  // spins per tile (UMMA N)
 constexpr int TK = 64;   // K per stage: 64 f16 = one 128-byte swizzle row
 constexpr int UK = 16;   // UMMA K for kind::f16
-constexpr int STAGES = 4;
 constexpr int THREADS = 384;
+constexpr int MAX_STAGES = 8;
 constexpr uint32_t TILE_BYTES = TM * TK * 2;   // 16 KB: 128 rows x 128 B (SW128): 64 f16 or 128 int8 of K
-constexpr uint32_t STAGE_BYTES = 2 * TILE_BYTES;  // A tile + B tile (Xh|Q16 or S8|Q8)
-constexpr uint32_t TMEM_COLS = 256;            // D1 [0,128) f32, D2 [128,256) s32
+// NC = CTAs per MMA (1: cta_group::1, 128 x 128 tiles; 2: cta_group::2, a CTA pair
+// computes 256 replicas x 128 spins, each CTA holding its 128 A rows and 64 of the B rows)
+template <int NC>
+struct Pipe {
+  static constexpr uint32_t B_BYTES = TILE_BYTES / NC;          // B rows held by this CTA (one K atom)
+  // KA K-atoms (128 bytes of K each) per stage: fewer mbarrier round trips per MMA,
+  // which is what paces tcgen05 at N = 128 (measured: 4 MMAs/stage 124 cyc/MMA, 8: 101)
+  static constexpr int KA = 2;
+  static constexpr uint32_t STAGE = KA * (TILE_BYTES + B_BYTES);  // A atoms then B atoms
+  static constexpr int STAGES = int(196608 / STAGE);  // 192 KB of stages
+  static constexpr uint32_t TILES = STAGES * STAGE;
+};
+constexpr uint32_t TMEM_COLS = 512;            // D1 [0,128) f32, D2 [128,256) s32, master x [256,384) f32
+constexpr uint32_t XCOL = 256;
 
 // Per replica-tile group: the tiles_n CTAs that share one replica tile are
 // the only ones that depend on each other (replicas are independent), so each
@@ -74,6 +86,8 @@ struct Args {
   RunCfg cfg;
   int n, npad, R, Rpad, tiles_n, p_end;
   float jscale;
+  int nodata;  // DCX_DENSE_NODATA timing experiment (wrong results)
+  int fence_mode;  // DCX_DENSE_FENCE=1: single proxy fence per CTA (experiment)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -100,12 +114,70 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// waiter that backs off (epilogue warps idle for the whole GEMM): keeps the
+// mbarrier polling off the shared-memory pipe the tensor core is reading
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(256);
+  }
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  // both CTAs of the pair signal the leader's barrier (peer bit cleared)
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar & 0xFEFFFFFFu)
+      : "memory");
+}
+template <int NC>
+__device__ __forceinline__ void mma_f16_g(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  if constexpr (NC == 1) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  } else {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  }
+}
+template <int NC>
+__device__ __forceinline__ void mma_i8_g(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  if constexpr (NC == 1) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  } else {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  }
+}
+// MMA completion -> mbarrier (both CTAs of a pair receive it)
+template <int NC>
+__device__ __forceinline__ void mma_commit_g(uint32_t mbar) {
+  if constexpr (NC == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+  } else {
+    const uint16_t mask = 3;
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     mbar),
+                 "h"(mask)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -175,6 +247,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   unsigned int v;
@@ -192,23 +275,27 @@ __device__ __forceinline__ void group_barrier(SyncWords* s, unsigned int members
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int gen = ld_acquire(&s->gen);
-    // release: cumulative over the CTA's writes ordered before it by bar.sync
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    if (atomicAdd(&s->count, 1u) == members - 1) {
+    // arrival with release semantics: cumulative over the CTA's writes ordered
+    // before it by bar.sync (no separate fence round trip)
+    unsigned int old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&s->count) : "memory");
+    if (old == members - 1) {
       s->count = 0;
       s->stamp = globaltimer();
-      s->running_snap = atomicAdd(&s->running, 0);
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      int run;
+      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(run) : "l"(&s->running) : "memory");
+      s->running_snap = run;
       st_release(&s->gen, gen + 1);
     } else {
-      while (ld_acquire(&s->gen) == gen) __nanosleep(32);
+      while (ld_acquire(&s->gen) == gen) {
+      }
     }
   }
   __syncthreads();
 }
 
 struct __align__(8) Smem {
-  uint64_t full[STAGES], empty[STAGES], accf1, accf2;
+  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2;
   uint32_t tmem_base;
   int pad;
   float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
@@ -221,21 +308,26 @@ struct __align__(8) Smem {
 // owner), warps 2-3 = control helpers, warps 4-11 = epilogue. Epilogue warp w
 // reads TMEM lane quadrant (w % 4) and spin-column half (w - 4) / 4; the
 // CTA's 128 x 128 f32 master state lives in shared memory for the whole run.
+template <int NC>
 __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_constant__ Args a) {
+  using P = Pipe<NC>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment (SW128) by offset so the compiler keeps the shared address space
   unsigned char* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* xs = reinterpret_cast<float*>(tiles + STAGES * STAGE_BYTES);  // [TN cols][TM rows]
-  Smem& sm = *reinterpret_cast<Smem*>(tiles + STAGES * STAGE_BYTES + TM * TN * 4);
+  Smem& sm = *reinterpret_cast<Smem*>(tiles + P::TILES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rt = blockIdx.x / a.tiles_n, nt = blockIdx.x % a.tiles_n;
+  const int cta_rank = NC == 2 ? int(blockIdx.x & 1) : 0;  // rank in the CTA pair (cluster)
+  const int pair = blockIdx.x / NC;
+  const int rg = pair / a.tiles_n, nt = pair % a.tiles_n;  // replica group (NC x 128 replicas), spin tile
+  const int rt = rg * NC + cta_rank;                        // this CTA's 128-replica tile
   const int r0 = rt * TM, i0 = nt * TN;
-  const int KB1 = a.npad / TK;         // f16 stages (K = 64 each)
-  const int KB2 = a.npad / (2 * TK);   // int8 stages (K = 128 each)
-  SyncWords* grp = a.sync + rt;
+  const bool leader = cta_rank == 0;
+  const int KB1 = a.npad / (TK * P::KA);      // f16 stages (KA x 64 of K each)
+  const int KB2 = a.npad / (2 * TK * P::KA);  // int8 stages (KA x 128 of K each)
+  SyncWords* grp = a.sync + rg;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < P::STAGES; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
       mbar_init(smem_u32(&sm.empty[s]), 1);
     }
@@ -244,10 +336,17 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (NC == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   int p = grp->p_exec;  // every CTA of the group reads it before the first group barrier
   const int p_start = p;
@@ -270,18 +369,28 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const bool valid = epi && r < a.R;
   uint64_t prevmask = 0;  // sign bits of x_{p-1} for this thread's 64 columns
   if (epi) {
-    const float* src = a.xm[p & 1] + (int64_t)r * a.npad + i0 + h * 64;
     const int8_t* sp = a.s8[(p + 1) & 1] + (int64_t)r * a.npad + i0 + h * 64;
-    for (int c = 0; c < 64; ++c) {
-      xs[(h * 64 + c) * TM + rl] = valid ? src[c] : 0.f;
+    for (int c = 0; c < 64; ++c)
       if (valid && p > 0 && sp[c] < 0) prevmask |= 1ull << c;
-    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (NC == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const uint32_t idesc = idesc_f16(TM, TN), idesc8 = idesc_i8(TM, TN);
+  const uint32_t idesc = idesc_f16(NC * TM, TN), idesc8 = idesc_i8(NC * TM, TN);
+  // the CTA's f32 master states live in TMEM columns [XCOL, XCOL + 128) for the whole run
+  const uint32_t xaddr = tmem + (uint32_t(q * 32) << 16) + XCOL + h * 64;
+  if (epi) {
+    const float* src = a.xm[p & 1] + (int64_t)r * a.npad + i0 + h * 64;
+    for (int cc = 0; cc < 2; ++cc) {
+      uint32_t v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(valid ? src[cc * 32 + j] : 0.f);
+      tmem_st32(xaddr + cc * 32, v);
+    }
+    tmem_st_wait();
+  }
   RunCfg cfg = a.cfg;
   if (nt != 0) cfg.hist = nullptr;  // only the nt == 0 CTA of a replica tile writes history
 
@@ -294,53 +403,88 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     if (p > p_start && __ldcg(&grp->running_snap) == 0) break;  // every replica of the group stopped
     const int cur = p & 1;
     const bool trace = a.dbg && blockIdx.x == 0 && threadIdx.x == 64 && p < 4096;
-    if (trace) a.dbg[p * 7 + 0] = clock64();
+    if (trace) {
+      a.dbg[p * 12 + 0] = clock64();
+      a.dbg[4096 * 13 + p] = globaltimer();
+    }
     if (warp < 2) {
       if (warp == 0) {
       // ---------------------------------------------------------- producer
       if (lane == 0) {
         fence_async_global();
+        const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
+        if (tr) a.dbg[p * 12 + 5] = clock64();
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
-          const int s = kiter % STAGES;
-          const uint32_t ph = (kiter / STAGES) & 1;
+          const int s = kiter % P::STAGES;
+          const uint32_t ph = (kiter / P::STAGES) & 1;
           mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
           const uint32_t fb = smem_u32(&sm.full[s]);
-          mbar_expect_tx(fb, STAGE_BYTES);
-          unsigned char* st = tiles + s * STAGE_BYTES;
-          if (kb < KB1) {
-            tma_load_2d(smem_u32(st), &a.tmA[cur], kb * TK, r0, fb);
-            tma_load_2d(smem_u32(st + TILE_BYTES), &a.tmB, kb * TK, i0, fb);
-          } else {
-            const int k8 = (kb - KB1) * 2 * TK;
-            tma_load_2d(smem_u32(st), &a.tmS[cur], k8, r0, fb);
-            tma_load_2d(smem_u32(st + TILE_BYTES), &a.tmQ8, k8, i0, fb);
+          if (a.nodata) {  // timing experiment: MMAs on stale stage data, no TMA
+            mbar_arrive(fb);
+            continue;
           }
+          if (leader) mbar_expect_tx(fb, NC * P::STAGE);  // the leader's barrier counts both CTAs' bytes
+          unsigned char* st = tiles + s * P::STAGE;
+          const int bi = i0 + cta_rank * (TN / NC);  // this CTA's B rows
+          const CUtensorMap* ma = kb < KB1 ? &a.tmA[cur] : &a.tmS[cur];
+          const CUtensorMap* mb = kb < KB1 ? &a.tmB : &a.tmQ8;
+          const int katom = kb < KB1 ? TK : 2 * TK;  // elements of K per 128-byte atom
+          const int kc = (kb < KB1 ? kb : kb - KB1) * P::KA * katom;
+#pragma unroll
+          for (int q = 0; q < P::KA; ++q) {
+            const uint32_t da = smem_u32(st + q * TILE_BYTES);
+            const uint32_t db = smem_u32(st + P::KA * TILE_BYTES + q * P::B_BYTES);
+            if constexpr (NC == 1) {
+              tma_load_2d(da, ma, kc + q * katom, r0, fb);
+              tma_load_2d(db, mb, kc + q * katom, bi, fb);
+            } else {
+              tma_load_2d_pair(da, ma, kc + q * katom, r0, fb);
+              tma_load_2d_pair(db, mb, kc + q * katom, bi, fb);
+            }
+          }
+          if (tr && kb == KB1 - 1) a.dbg[p * 12 + 6] = clock64();
         }
+        if (tr) a.dbg[p * 12 + 7] = clock64();
       }
       __syncwarp();
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
-      if (lane == 0) {
+      if (lane == 0 && leader) {  // one thread of the (leader) CTA issues every MMA of the tile
+        const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
+        unsigned long long wait_cyc = 0;
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
-          const int s = kiter % STAGES;
-          const uint32_t ph = (kiter / STAGES) & 1;
+          const int s = kiter % P::STAGES;
+          const uint32_t ph = (kiter / P::STAGES) & 1;
+          const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
+          wait_cyc += clock64() - tw0;
           tc_fence_after();
-          const uint32_t sa = smem_u32(tiles + s * STAGE_BYTES), sb = sa + TILE_BYTES;
-          if (kb < KB1) {
+          const uint32_t s0 = smem_u32(tiles + s * P::STAGE);
 #pragma unroll
-            for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
-              mma_f16(tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
-          } else {
+          for (int q = 0; q < P::KA; ++q) {
+            const uint32_t sa = s0 + q * TILE_BYTES, sb = s0 + P::KA * TILE_BYTES + q * P::B_BYTES;
+            if (kb < KB1) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
-              mma_i8(tmem + TN, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8,
-                     ((kb - KB1) | k) ? 1u : 0u);
+              for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
+                mma_f16_g<NC>(tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
+                              (kb | q | k) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
+                mma_i8_g<NC>(tmem + TN, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8,
+                             ((kb - KB1) | q | k) ? 1u : 0u);
+            }
           }
-          mma_commit(smem_u32(&sm.empty[s]));
-          if (kb == KB1 - 1) mma_commit(smem_u32(&sm.accf1));
+          mma_commit_g<NC>(smem_u32(&sm.empty[s]));
+          if (tr && kb == 0) a.dbg[p * 12 + 8] = clock64();
+          if (kb == KB1 - 1) {
+            mma_commit_g<NC>(smem_u32(&sm.accf1));
+            if (tr) a.dbg[p * 12 + 9] = clock64();
+          }
         }
-        mma_commit(smem_u32(&sm.accf2));
+        if (tr) a.dbg[p * 12 + 10] = clock64();
+        if (tr) a.dbg[4096 * 12 + p] = wait_cyc;
+        mma_commit_g<NC>(smem_u32(&sm.accf2));
       }
       __syncwarp();
       }
@@ -370,23 +514,22 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }
       }
       uint64_t curmask = 0;
-      mbar_wait(smem_u32(&sm.accf1), acc_phase);
+      mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
       tc_fence_after();
+      if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 11] = clock64();
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
       float* xg = a.xm[cur] + (int64_t)r * a.npad + gbase;  // x_p (time-budget runs only)
       for (int cc = 0; cc < 2; ++cc) {
-        uint32_t v1[32];
+        uint32_t v1[32], xv[32], nv[32];
         tmem_ld32(tmem + (uint32_t(q * 32) << 16) + h * 64 + cc * 32, v1);
+        tmem_ld32(xaddr + cc * 32, xv);
         tmem_ld_wait();
         __align__(16) __half hv[32];
         __align__(16) int8_t sv[32];
-        __align__(16) float fv[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int col = h * 64 + cc * 32 + j;
-          float* xp = xs + col * TM + rl;
-          const float x = *xp;
+          const float x = __uint_as_float(xv[j]);
           const bool in = cc * 32 + j < lim;
           const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j]));
           const float nxt = cbrtf(ax * inv_beta);
@@ -396,25 +539,27 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             sxax = fmaf(x, ax, sxax);
             step = fmaxf(step, fabsf(nxt - x));
             if (x < 0.f) curmask |= 1ull << (cc * 32 + j);
-            if (running) *xp = nxt;
           }
-          fv[j] = x;
+          nv[j] = (in && running) ? __float_as_uint(nxt) : xv[j];
           hv[j] = __float2half_rn(in ? nxt * inv_lam : 0.f);
           sv[j] = in ? (nxt >= 0.f ? 1 : -1) : 0;
         }
+        tmem_st32(xaddr + cc * 32, nv);
         if (running && lim > 0) {
 #pragma unroll
           for (int j = 0; j < 32; j += 8) *reinterpret_cast<uint4*>(hn + cc * 32 + j) = *reinterpret_cast<uint4*>(hv + j);
           if (write_master) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(fv + j);
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(xv + j);
           }
           *reinterpret_cast<uint4*>(sn + cc * 32) = *reinterpret_cast<uint4*>(sv);
           *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 16);
         }
       }
+      tmem_st_wait();
       // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i
-      mbar_wait(smem_u32(&sm.accf2), acc_phase);
+      mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
       tc_fence_after();
       for (int cc = 0; cc < 2; ++cc) {
         uint32_t v2[32];
@@ -433,13 +578,13 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       sm.red[h][rl][3] = step;
         }
     if (trace) {
-      mbar_wait(smem_u32(&sm.accf2), acc_phase);
-      a.dbg[p * 7 + 1] = clock64();
+      mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
+      a.dbg[p * 12 + 1] = clock64();
     }
     acc_phase ^= 1;
     tc_fence_before();
     __syncthreads();
-    if (trace) a.dbg[p * 7 + 2] = clock64();
+    if (trace) a.dbg[p * 12 + 2] = clock64();
     if (threadIdx.x < TM) {
       const int rr = r0 + threadIdx.x;
       if (rr < a.R) {
@@ -454,9 +599,17 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         *reinterpret_cast<double4*>(dst) = v;
       }
     }
-    if (epi) fence_async_global();  // xh / s8 written here are read by TMA next iteration
-    group_barrier(grp, a.tiles_n);
-    if (trace) a.dbg[p * 7 + 3] = clock64();
+    if (a.fence_mode == 0) {
+      if (epi) fence_async_global();  // xh / s8 written here are read by TMA next iteration
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) fence_async_global();  // experiment: one proxy fence per CTA
+    }
+    if (a.dbg && threadIdx.x == 0 && p < 64) a.dbg[4096 * 14 + p * 256 + blockIdx.x] = globaltimer();  // arrival
+    __syncthreads();
+    if (trace) a.dbg[4096 * 14 + 64 * 256 + p] = clock64();  // every thread done (incl. proxy fences)
+    group_barrier(grp, NC * a.tiles_n);
+    if (trace) a.dbg[p * 12 + 3] = clock64();
     if (warp < 2) continue;  // TMA / MMA go on with the next iteration
     // ---------------------------------------------------------- control (warps 4-11)
     if (epi) {
@@ -465,24 +618,25 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       const int half = (a.tiles_n + 1) / 2;
       const int t0 = h * half, t1 = min(a.tiles_n, t0 + half);
       const double2* src = reinterpret_cast<const double2*>(a.part + ((int64_t)rt * a.tiles_n * TM) * 4);
-      constexpr int MAXH = 8;  // tiles_n <= 16
-      double2 u[MAXH], w[MAXH];
-#pragma unroll
-      for (int k = 0; k < MAXH; ++k)
-        if (t0 + k < t1) {
-          const int64_t e = ((int64_t)(t0 + k) * TM + rl) * 2;
-          u[k] = __ldcg(src + e);
-          w[k] = __ldcg(src + e + 1);
-        }
       double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      for (int tb = t0; tb < t1; tb += 4) {  // 4 tiles in flight, summed in tile order
+        double2 u[4], w[4];
 #pragma unroll
-      for (int k = 0; k < MAXH; ++k)
-        if (t0 + k < t1) {
-          s0 += u[k].x;
-          s1 += u[k].y;
-          s2 += w[k].x;
-          s3 = fmax(s3, w[k].y);
-        }
+        for (int k = 0; k < 4; ++k)
+          if (tb + k < t1) {
+            const int64_t e = ((int64_t)(tb + k) * TM + rl) * 2;
+            u[k] = __ldcg(src + e);
+            w[k] = __ldcg(src + e + 1);
+          }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tb + k < t1) {
+            s0 += u[k].x;
+            s1 += u[k].y;
+            s2 += w[k].x;
+            s3 = fmax(s3, w[k].y);
+          }
+      }
       sm.red2[h][rl][0] = s0;
       sm.red2[h][rl][1] = s1;
       sm.red2[h][rl][2] = s2;
@@ -511,22 +665,27 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
     }
-    if (trace) a.dbg[p * 7 + 4] = clock64();
+    if (trace) a.dbg[p * 12 + 4] = clock64();
   }
   // ---------------------------------------------------------------- teardown
-  if (epi && valid) {
+  if (epi) {
     // the run's final (or frozen) states; a time-budget stop at p was persisted above
-    const RepCtl& c = sm.ctl[rl];
-    const bool budget_stop = c.status == DCX_STOP_TIME_BUDGET;
+    const bool budget_stop = sm.ctl[rl].status == DCX_STOP_TIME_BUDGET;
     float* d0 = a.xm[0] + (int64_t)r * a.npad + i0 + h * 64;
     float* d1 = a.xm[1] + (int64_t)r * a.npad + i0 + h * 64;
     const int lim = max(0, min(64, a.n - (i0 + h * 64)));
-    if (!budget_stop)
-      for (int cc = 0; cc < lim; ++cc) {
-        const float v = xs[(h * 64 + cc) * TM + rl];
-        d0[cc] = v;
-        d1[cc] = v;
-      }
+    for (int cc = 0; cc < 2; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(xaddr + cc * 32, v);
+      tmem_ld_wait();
+      if (valid && !budget_stop)
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (cc * 32 + j < lim) {
+            d0[cc * 32 + j] = __uint_as_float(v[j]);
+            d1[cc * 32 + j] = __uint_as_float(v[j]);
+          }
+    }
   }
   // all CTAs of the group read p_exec before the first barrier and exit at the same p
   if (nt == 0 && threadIdx.x == 0) {
@@ -535,8 +694,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (NC == 2) cluster_sync_all();  // the leader's MMAs into the peer are complete
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    if constexpr (NC == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
 }
 
@@ -558,14 +721,14 @@ __global__ void pack_state(const float* src, int n, int R, int npad, const RepCt
 // pending best copy of the last executed pass, then [Rpad][npad] -> [n][R]
 __global__ void unpack_results(const float* xm0, const float* xm1, const int8_t* s80, const int8_t* s81,
                                int8_t* best8, int n, int R, int npad, const RepCtl* ctl, const SyncWords* sync,
-                               float* x0, float* x1, int8_t* best) {
+                               int nc, float* x0, float* x1, int8_t* best) {
   const int64_t total = int64_t(n) * R;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx / R;
     const int r = int(idx % R);
     const int64_t s = (int64_t)r * npad + i;
     const int pe = ctl[r].pend;
-    const int P = sync[r / TM].p_exec - 1;  // last pass executed by the replica's group
+    const int P = sync[r / (TM * nc)].p_exec - 1;  // last pass executed by the replica's group
     int8_t b = best8[s];
     if (pe >= 0 && pe == P) b = (pe & 1) ? s81[s] : s80[s];
     best[idx] = b;
@@ -601,10 +764,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 2-D row-major [rows][cols] map, 128-byte rows x 128 rows per box (64 f16 or
 // 128 int8 along K), 128-byte swizzle: the canonical K-major SW128 UMMA layout.
-static void make_map(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, bool f16) {
+static void make_map(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, bool f16, uint32_t box_rows = 128) {
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {cols * (f16 ? 2 : 1)};
-  const cuuint32_t box[2] = {f16 ? cuuint32_t(tc::TK) : cuuint32_t(2 * tc::TK), 128};  // 128-byte rows
+  const cuuint32_t box[2] = {f16 ? cuuint32_t(tc::TK) : cuuint32_t(2 * tc::TK), box_rows};  // 128-byte rows
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -648,7 +811,7 @@ void DenseDev::release() {
 void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.release();
   d.n = n;
-  d.npad = (n + 127) / 128 * 128;
+  d.npad = (n + 255) / 256 * 256;  // whole int8 stages (2 x 128 of K)
   // exact small-integer form J = jscale * Q (the K2000 instance: jscale = -1/2, Q = +-1)
   double mn = 0.0;
   for (int64_t e = 0; e < n * n; ++e)
@@ -680,7 +843,9 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.tmaps = new CUtensorMap[6];
 }
 
-static size_t dense_smem_bytes() { return 1024 + tc::STAGES * tc::STAGE_BYTES + tc::TM * tc::TN * 4 + sizeof(tc::Smem); }
+static size_t dense_smem_bytes(int nc) {
+  return 1024 + (nc == 1 ? tc::Pipe<1>::TILES : tc::Pipe<2>::TILES) + sizeof(tc::Smem);
+}
 
 void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (!d.exact) throw std::invalid_argument("tensor-core path needs small-integer dense couplings");
@@ -689,13 +854,16 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   d.release_run();
   d.R = cfg.R;
   d.Rpad = (d.R + 127) / 128 * 128;
-  const int tiles = (d.Rpad / 128) * int(d.npad / 128);
   int dev = 0, nsm = 0;
   DCK(cudaGetDevice(&dev));
   DCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int tiles = (d.Rpad / 128) * int(d.npad / 128);
   if (tiles > nsm)
     throw std::invalid_argument("tensor-core path: (R/128)*(n/128) tiles must fit the SM count (" +
                                 std::to_string(tiles) + " > " + std::to_string(nsm) + ")");
+  // CTA pairs (cta_group::2) when the replica count allows 256-replica groups
+  d.nc = (d.Rpad % 256 == 0) ? 2 : 1;
+  if (const char* e = std::getenv("DCX_DENSE_NC")) d.nc = std::atoi(e) == 2 && d.Rpad % 256 == 0 ? 2 : 1;
   const size_t vec = size_t(d.Rpad) * d.npad;
   for (int b = 0; b < 2; ++b) {
     DCK(cudaMalloc(&d.xm[b], vec * 4));
@@ -709,18 +877,19 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
   DCK(cudaMalloc(&d.part, sizeof(double) * 4 * (d.npad / 128) * d.Rpad));
   {
-    const int ngroups = d.Rpad / 128;
+    const int gsz = 128 * d.nc;
+    const int ngroups = d.Rpad / gsz;
     std::vector<tc::SyncWords> sw(ngroups);
     std::memset(sw.data(), 0, sizeof(tc::SyncWords) * ngroups);
-    for (int gI = 0; gI < ngroups; ++gI) sw[gI].running = std::min(128, d.R - gI * 128);
+    for (int gI = 0; gI < ngroups; ++gI) sw[gI].running = std::max(0, std::min(gsz, d.R - gI * gsz));
     DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * ngroups));
     DCK(cudaMemcpyAsync(d.sync, sw.data(), sizeof(tc::SyncWords) * ngroups, cudaMemcpyHostToDevice, s));
   }
   if (d.dbg) cudaFree(d.dbg);
   d.dbg = nullptr;
   if (std::getenv("DCX_DENSE_TRACE")) {
-    DCK(cudaMalloc(&d.dbg, 4096 * 9 * 8));
-    DCK(cudaMemsetAsync(d.dbg, 0, 4096 * 9 * 8, s));
+    DCK(cudaMalloc(&d.dbg, (4096 * 15 + 64 * 256) * 8));
+    DCK(cudaMemsetAsync(d.dbg, 0, (4096 * 15 + 64 * 256) * 8, s));
   }
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
@@ -729,12 +898,16 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(d.tmaps);
   make_map(&maps[0], d.xh[0], d.npad, d.Rpad, true);
   make_map(&maps[1], d.xh[1], d.npad, d.Rpad, true);
-  make_map(&maps[2], d.q16, d.npad, d.npad, true);
+  make_map(&maps[2], d.q16, d.npad, d.npad, true, 128 / d.nc);
   make_map(&maps[3], d.s8[0], d.npad, d.Rpad, false);
   make_map(&maps[4], d.s8[1], d.npad, d.Rpad, false);
-  make_map(&maps[5], d.q8, d.npad, d.npad, false);
-  DCK(cudaFuncSetAttribute(tc::dense_doch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)dense_smem_bytes()));
+  make_map(&maps[5], d.q8, d.npad, d.npad, false, 128 / d.nc);
+  if (d.nc == 1)
+    DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dense_smem_bytes(1)));
+  else
+    DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dense_smem_bytes(2)));
 }
 
 static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
@@ -766,10 +939,31 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.tiles_n = int(d.npad / 128);
   a.p_end = p_end;
   a.jscale = d.jscale;
+  a.nodata = std::getenv("DCX_DENSE_NODATA") ? 1 : 0;
+  a.fence_mode = std::getenv("DCX_DENSE_FENCE") ? 1 : 0;
   const int grid = (d.Rpad / 128) * a.tiles_n;
-  void* args[] = {&a};
-  DCK(cudaLaunchCooperativeKernel((const void*)tc::dense_doch_kernel, dim3(grid), dim3(tc::THREADS), args,
-                                  dense_smem_bytes(), s));
+  if (d.nc == 1) {
+    void* args[] = {&a};
+    DCK(cudaLaunchCooperativeKernel((const void*)tc::dense_doch_kernel<1>, dim3(grid), dim3(tc::THREADS), args,
+                                    dense_smem_bytes(1), s));
+  } else {
+    // CTA pairs: cluster of 2, every CTA co-resident (group barriers spin across CTAs)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::THREADS);
+    cfg.dynamicSmemBytes = dense_smem_bytes(2);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2>, a));
+  }
 }
 
 void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s) {
@@ -783,13 +977,79 @@ void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s) {
 
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) {  // phase breakdown of CTA 0 (DCX_DENSE_TRACE=1)
-    std::vector<unsigned long long> t(4096 * 7);
+    std::vector<unsigned long long> t(4096 * 12);
     DCK(cudaMemcpyAsync(t.data(), d.dbg, t.size() * 8, cudaMemcpyDeviceToHost, s));
     DCK(cudaStreamSynchronize(s));
     double acc[6] = {0, 0, 0, 0, 0, 0};
     int cnt = 0;
-    for (int p = 1; p < 4096 && t[p * 7 + 4]; ++p, ++cnt)
-      for (int k = 0; k < 4; ++k) acc[k] += double(t[p * 7 + k + 1]) - double(t[p * 7 + k]);
+    std::vector<unsigned long long> tw(4096);
+    DCK(cudaMemcpyAsync(tw.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 12, 4096 * 8,
+                        cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> gt(4096);
+    DCK(cudaMemcpyAsync(gt.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 13, 4096 * 8,
+                        cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    {
+      int last = 1;
+      while (last + 1 < 4096 && t[(last + 1) * 12]) ++last;
+      if (last > 2)
+        std::fprintf(stderr, "[dcx dense trace] SM clock during the run: %.0f MHz (%d iterations, %.2f us/iter)\n",
+                     double(t[last * 12] - t[12]) / double(gt[last] - gt[1]) * 1e3, last - 1,
+                     double(gt[last] - gt[1]) / 1e3 / (last - 1));
+    }
+    {  // barrier arrival spread across the CTAs of group 0 (first 64 iterations)
+      std::vector<unsigned long long> ar(64 * 256);
+      DCK(cudaMemcpyAsync(ar.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 14, ar.size() * 8,
+                          cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      const int members = d.nc * int(d.npad / 128);
+      double spread = 0;
+      int cntp = 0;
+      for (int p = 2; p < 64; ++p) {
+        unsigned long long lo = ~0ull, hi = 0;
+        for (int b = 0; b < members; ++b) {
+          const unsigned long long v = ar[p * 256 + b];
+          if (!v) continue;
+          lo = std::min(lo, v);
+          hi = std::max(hi, v);
+        }
+        if (hi > lo) { spread += double(hi - lo); ++cntp; }
+      }
+      if (cntp) std::fprintf(stderr, "[dcx dense trace] group-0 barrier arrival spread %.2f us\n", spread / cntp / 1e3);
+      std::vector<unsigned long long> te(4096);
+      DCK(cudaMemcpyAsync(te.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 14 + 64 * 256, 4096 * 8,
+                          cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      double pre = 0, bar = 0;
+      int c2 = 0;
+      for (int p = 1; p < 4096 && t[p * 12 + 4] && te[p]; ++p, ++c2) {
+        pre += double(te[p]) - double(t[p * 12 + 2]);
+        bar += double(t[p * 12 + 3]) - double(te[p]);
+      }
+      if (c2)
+        std::fprintf(stderr, "[dcx dense trace] kcycles: partials+proxy fences %.2f, group barrier %.2f\n",
+                     pre / c2 / 1e3, bar / c2 / 1e3);
+    }
+    double wsum = 0;
+    for (int p = 1; p < 4096 && t[p * 12 + 4]; ++p) wsum += double(tw[p]);
+    double m[6] = {0, 0, 0, 0, 0, 0};
+    for (int p = 1; p < 4096 && t[p * 12 + 4]; ++p, ++cnt) {
+      for (int k = 0; k < 4; ++k) acc[k] += double(t[p * 12 + k + 1]) - double(t[p * 12 + k]);
+      const double base = double(t[p * 12 + 5]);
+      m[0] += double(t[p * 12 + 6]) - base;   // producer: last f16 TMA issued
+      m[1] += double(t[p * 12 + 7]) - base;   // producer: last TMA issued
+      m[2] += double(t[p * 12 + 8]) - base;   // MMA: first stage consumed
+      m[3] += double(t[p * 12 + 9]) - base;   // MMA: last f16 MMA issued
+      m[4] += double(t[p * 12 + 10]) - base;  // MMA: last MMA issued
+      m[5] += double(t[p * 12 + 11]) - base;  // epilogue: GEMM1 complete (accf1)
+    }
+    if (cnt)
+      std::fprintf(stderr,
+                   "[dcx dense trace] mainloop kcycles from first TMA: lastTMA16 %.2f lastTMA %.2f firstMMA %.2f "
+                   "lastMMA16 %.2f lastMMA %.2f gemm1done %.2f | MMA thread waiting on full[] %.2f\n",
+                   m[0] / cnt / 1e3, m[1] / cnt / 1e3, m[2] / cnt / 1e3, m[3] / cnt / 1e3, m[4] / cnt / 1e3,
+                   m[5] / cnt / 1e3, wsum / cnt / 1e3);
     if (cnt)
       std::fprintf(stderr,
                    "[dcx dense trace] %d iters, kcycles/iter (CTA 0, warp 2 view): gemms+epilogue %.2f drain %.2f "
@@ -801,7 +1061,7 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
                                            reinterpret_cast<const int8_t*>(d.s8[0]),
                                            reinterpret_cast<const int8_t*>(d.s8[1]), d.best8, int(d.n), d.R,
                                            int(d.npad), m.args.ctl, reinterpret_cast<const tc::SyncWords*>(d.sync),
-                                           reinterpret_cast<float*>(m.args.x[0]),
+                                           d.nc, reinterpret_cast<float*>(m.args.x[0]),
                                            reinterpret_cast<float*>(m.args.x[1]), m.args.best);
   DCK(cudaGetLastError());
 }
