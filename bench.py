@@ -240,9 +240,8 @@ def run_ours(args):
         flush.fill_(float(s))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        Jn = dc.maxcut_to_ising(dc.DenseCoupling(W, validate=False))  # fresh object: J is uploaded again
-        res = dc.solve_replicas(dc.ProblemInstance(coupling=Jn, cut_offset=CUT_OFFSET), "doch", ALPHA, BETA,
-                                X0[s % 2], **kw)
+        # host buffers in, host results out: J (f64) and x0 are copied to the device every step
+        res = dc.solve_replicas(inst, "doch", ALPHA, BETA, X0[s % 2], reupload=True, **kw)
         energies = np.array([r.energy for r in res])
         e2e_t += time.perf_counter() - t0
         e2e_upd += N_SPINS * sum(r.iterations for r in res)

@@ -139,6 +139,11 @@ DCX_API int dcx_result_summary(dcx_ctx* ctx, int32_t r, dcx_summary* out);
  * recorded), device seconds since dcx_solve_begin, event bits */
 DCX_API int dcx_result_history(dcx_ctx* ctx, int32_t r, int64_t from, int64_t count, double* h, double* e, double* t,
                        int32_t* ev);
+/* bulk forms for R replicas: per-replica summary columns, and every history
+ * entry as [R][K] rows (K >= max n_hist; unused tail entries are not written) */
+DCX_API int dcx_result_summaries(dcx_ctx* ctx, int64_t* iterations, int32_t* stop_reason, double* best_energy,
+                                 int64_t* n_hist, int32_t* descent_warn);
+DCX_API int dcx_result_history_all(dcx_ctx* ctx, int64_t K, double* h, double* e, double* t, int32_t* ev);
 DCX_API int dcx_result_best_spins(dcx_ctx* ctx, int8_t* out /* [R][n] */);
 DCX_API int dcx_result_state(dcx_ctx* ctx, double* out /* [R][n], final x */);
 DCX_API int dcx_result_states(dcx_ctx* ctx, int32_t r, double* out /* [(iterations+1)][n] */);

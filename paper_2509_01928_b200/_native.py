@@ -99,6 +99,8 @@ def load(path: Path | str | None = None):
         "dcx_solve_run": (C.c_int, [_P]),
         "dcx_result_summary": (C.c_int, [_P, C.c_int32, C.POINTER(Summary)]),
         "dcx_result_history": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, _PD, _PD, _PD, _PI32]),
+        "dcx_result_summaries": (C.c_int, [_P, _PI64, _PI32, _PD, _PI64, _PI32]),
+        "dcx_result_history_all": (C.c_int, [_P, C.c_int64, _PD, _PD, _PD, _PI32]),
         "dcx_result_best_spins": (C.c_int, [_P, _PI8]),
         "dcx_result_state": (C.c_int, [_P, _PD]),
         "dcx_result_states": (C.c_int, [_P, C.c_int32, _PD]),
@@ -226,6 +228,27 @@ class Context:
         ev = np.empty(count, dtype=np.int32)
         if count:
             check(self.lib.dcx_result_history(self.h, r, start, count, ptr(h, C.c_double), ptr(e, C.c_double),
+                                              ptr(t, C.c_double), ptr(ev, C.c_int32)), self.h)
+        return h, e, t, ev
+
+    def summaries(self):
+        R = self._R
+        it = np.empty(R, np.int64)
+        st = np.empty(R, np.int32)
+        be = np.empty(R)
+        nh = np.empty(R, np.int64)
+        dw = np.empty(R, np.int32)
+        check(self.lib.dcx_result_summaries(self.h, ptr(it, C.c_int64), ptr(st, C.c_int32), ptr(be, C.c_double),
+                                            ptr(nh, C.c_int64), ptr(dw, C.c_int32)), self.h)
+        return it, st, be, nh, dw
+
+    def history_all(self, K: int):
+        R = self._R
+        h = np.empty((R, K))
+        e = np.empty((R, K))
+        t = np.empty((R, K))
+        ev = np.zeros((R, K), np.int32)
+        check(self.lib.dcx_result_history_all(self.h, int(K), ptr(h, C.c_double), ptr(e, C.c_double),
                                               ptr(t, C.c_double), ptr(ev, C.c_int32)), self.h)
         return h, e, t, ev
 

@@ -144,13 +144,19 @@ def is_csr(J) -> bool:
     return all(hasattr(J, a) for a in ("values", "col_indices", "row_offsets"))
 
 
-def device_context(J, device: int | None = None) -> _native.Context:
-    """The device copy of coupling ``J`` (uploaded on first use)."""
+def device_context(J, device: int | None = None, reload: bool = False) -> _native.Context:
+    """The device copy of coupling ``J`` (uploaded on first use; ``reload``
+    copies the host arrays again into the existing device buffers)."""
     try:
         ctx = _ctx_cache.get(J)
     except TypeError:
         ctx = _ctx_by_id.get(id(J))
     if ctx is not None and (device is None or ctx.device == device):
+        if reload:
+            if is_dense(J):
+                ctx.set_dense(J.array)
+            else:
+                ctx.set_csr(J.n, J.values, J.col_indices, J.row_offsets)
         return ctx
     ctx = _native.Context(device)
     ctx.device = device

@@ -66,7 +66,8 @@ struct dcx_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   // ---------------------------------------------------------- coupling
-  bool have = false, dense = false;
+  bool have = false, dense = false, csr_ready = false;
+  std::vector<double> dense_host;  // dense couplings: host copy for the lazily built CSR form
   int64_t n = 0, nnz = 0;
   int vk_int = -1;  // VK_UNIFORM / VK_I8 / VK_I16, or -1 for real values
   double scale = 1.0;
@@ -372,8 +373,18 @@ void dcx_destroy(dcx_ctx* ctx) {
   delete ctx;
 }
 
+static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v);
+
 int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  c->dense = false;
+  c->csr_ready = false;
+  c->dense_host.clear();
+  c->dn.release();
+  return upload_csr(c, n, nnz, ro, ci, v);
+}
+
+static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v) {
   return guarded(c, [&] {
     if (n < 1) throw InvalidArg("n must be >= 1");
     if (nnz < 0 || (nnz > 0 && (!ci || !v)) || !ro) throw InvalidArg("null CSR array");
@@ -394,8 +405,6 @@ int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int
     double scale;
     classify_values(v, nnz, vk, scale);
     c->have = false;
-    c->dense = false;
-    c->dn.release();
     c->n = n;
     c->nnz = nnz;
     c->rp.alloc((n + 1) * 4);
@@ -438,21 +447,19 @@ int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int
   });
 }
 
-int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
-  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
-  if (!A || n < 1) return fail(c, DCX_E_INVALID, "bad dense coupling");
-  // CSR of the nonzero off-diagonal entries (row-major scan keeps column order)
+// CSR of the nonzero off-diagonal entries of the dense coupling, built on first
+// use by a CSR path (the tensor-core path never needs it).
+static int ensure_csr(dcx_ctx* c) {
+  if (!c->dense || c->csr_ready) return DCX_OK;
+  const int64_t n = c->n;
+  const double* A = c->dense_host.data();
   std::vector<int64_t> ro(n + 1, 0), ci;
   std::vector<double> vv;
   try {
     for (int64_t i = 0; i < n; ++i) {
       for (int64_t j = 0; j < n; ++j) {
         const double a = A[i * n + j];
-        if (i == j) {
-          if (a != 0.0) return fail(c, DCX_E_INVALID, "diagonal must be zero");
-          continue;
-        }
-        if (a != 0.0) {
+        if (i != j && a != 0.0) {
           ci.push_back(j);
           vv.push_back(a);
         }
@@ -462,11 +469,25 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
   } catch (const std::bad_alloc&) {
     return fail(c, DCX_E_OOM, "host allocation failed");
   }
-  int rc = dcx_set_csr(c, n, (int64_t)ci.size(), ro.data(), ci.data(), vv.data());
-  if (rc != DCX_OK) return rc;
+  const int rc = upload_csr(c, n, (int64_t)ci.size(), ro.data(), ci.data(), vv.data());
+  if (rc == DCX_OK) c->csr_ready = true;
+  return rc;
+}
+
+int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!A || n < 1) return fail(c, DCX_E_INVALID, "bad dense coupling");
+  for (int64_t i = 0; i < n; ++i)
+    if (A[i * n + i] != 0.0) return fail(c, DCX_E_INVALID, "diagonal must be zero");
   return guarded(c, [&] {
-    c->dense = true;
+    c->have = false;
+    c->csr_ready = false;
+    c->dense_host.assign(A, A + n * n);
+    c->n = n;
+    c->nnz = n * (n - 1);  // upper bound until the CSR form is built
     dense_upload(c->dn, n, A, c->stream);
+    c->dense = true;
+    c->have = true;
   });
 }
 
@@ -487,6 +508,7 @@ int dcx_matvec(dcx_ctx* c, int32_t R, const double* v, double* out, int32_t prec
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   return guarded(c, [&] {
     require_coupling(c);
+    if (ensure_csr(c) != DCX_OK) throw CudaError(c->err);
     if (R < 1 || !v || !out) throw InvalidArg("bad matvec arguments");
     if (precision == DCX_PREC_F32) apply_impl<float>(c, R, nullptr, nullptr, v, out, nullptr, nullptr, nullptr, nullptr);
     else apply_impl<double>(c, R, nullptr, nullptr, v, out, nullptr, nullptr, nullptr, nullptr);
@@ -498,6 +520,7 @@ int dcx_apply(dcx_ctx* c, int32_t R, const double* alpha, const double* beta, co
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   return guarded(c, [&] {
     require_coupling(c);
+    if (ensure_csr(c) != DCX_OK) throw CudaError(c->err);
     if (R < 1 || !v || !alpha || !beta) throw InvalidArg("bad apply arguments");
     for (int r = 0; r < R; ++r)
       if (!(alpha[r] > 0) || !(beta[r] > 0)) throw InvalidArg("alpha and beta must be positive");
@@ -510,6 +533,7 @@ int dcx_energy(dcx_ctx* c, int32_t R, const int8_t* spins, double* energies) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   return guarded(c, [&] {
     require_coupling(c);
+    if (ensure_csr(c) != DCX_OK) throw CudaError(c->err);
     if (R < 1 || !spins || !energies) throw InvalidArg("bad energy arguments");
     apply_impl<double>(c, R, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, spins, energies);
   });
@@ -550,6 +574,7 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
     c->finished = false;
     const int64_t n = c->n;
     const bool use_tc = P->precision == DCX_PREC_F16TC;
+    if (!use_tc && ensure_csr(c) != DCX_OK) throw CudaError(c->err);
     if (use_tc && !c->dense) throw InvalidArg("the tensor-core path needs a dense coupling");
     c->f64 = P->precision == DCX_PREC_F64;
     const size_t tb = c->f64 ? 8 : 4;
@@ -642,7 +667,7 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
     cfg.descent_tol = P->descent_tol;
     cfg.hist_cap = (int)cap;
     cfg.wcap = std::max(1, c->wcap);
-    cfg.es_scale = c->vk_int >= 0 ? c->scale : 1.0;
+    cfg.es_scale = use_tc ? double(c->dn.jscale) : (c->vk_int >= 0 ? c->scale : 1.0);
     cfg.hist = c->hist.as<HistRec>();
     cfg.window = c->window.as<double>();
     c->mp.spart = c->spart.as<double>();
@@ -823,6 +848,39 @@ int dcx_result_history(dcx_ctx* c, int32_t r, int64_t from, int64_t count, doubl
     if (e) e[k] = q.e;
     if (t) t[k] = q.t;
     if (ev) ev[k] = q.ev;
+  }
+  return DCX_OK;
+}
+
+int dcx_result_summaries(dcx_ctx* c, int64_t* iterations, int32_t* stop_reason, double* best_energy,
+                         int64_t* n_hist, int32_t* descent_warn) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!c->begun) return fail(c, DCX_E_STATE, "no run");
+  for (int r = 0; r < c->R; ++r) {
+    const RepCtl& q = c->hctl[r];
+    if (iterations) iterations[r] = std::max(0, q.k);
+    if (stop_reason) stop_reason[r] = q.status;
+    if (best_energy) best_energy[r] = q.best;
+    if (n_hist) n_hist[r] = (int64_t)c->hh[r].size();
+    if (descent_warn) descent_warn[r] = q.warned;
+  }
+  return DCX_OK;
+}
+
+int dcx_result_history_all(dcx_ctx* c, int64_t K, double* h, double* e, double* t, int32_t* ev) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!c->begun) return fail(c, DCX_E_STATE, "no run");
+  for (int r = 0; r < c->R; ++r) {
+    const auto& v = c->hh[r];
+    const int64_t cnt = std::min<int64_t>(K, (int64_t)v.size());
+    const int64_t base = (int64_t)r * K;
+    for (int64_t k = 0; k < cnt; ++k) {
+      const HistRec& q = v[k];
+      if (h) h[base + k] = q.h;
+      if (e) e[base + k] = q.e;
+      if (t) t[base + k] = q.t;
+      if (ev) ev[base + k] = q.ev;
+    }
   }
   return DCX_OK;
 }

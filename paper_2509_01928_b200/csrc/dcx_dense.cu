@@ -737,11 +737,30 @@ __global__ void unpack_results(const float* xm0, const float* xm1, const int8_t*
   }
 }
 
-__global__ void q_expand(const int16_t* q, __half* out, int8_t* out8, int64_t n, int64_t npad) {
+// min |a| over the nonzero entries, as the bit pattern of a positive double
+__global__ void min_abs_nonzero(const double* A, int64_t total, unsigned long long* out) {
+  unsigned long long m = ~0ull;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const double v = fabs(A[idx]);
+    if (v != 0.0) m = min(m, (unsigned long long)__double_as_longlong(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+// Q = A / scale into the padded f16 and int8 operand matrices; flags any entry
+// that is not an exact integer in [-127, 127]
+__global__ void q_expand(const double* A, double scale, __half* out, int8_t* out8, int64_t n, int64_t npad,
+                         unsigned long long* bad) {
   const int64_t total = npad * npad;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx / npad, j = idx % npad;
-    const int v = (i < n && j < n) ? q[i * n + j] : 0;
+    int v = 0;
+    if (i < n && j < n) {
+      const double a = A[i * n + j];
+      const double q = rint(a / scale);
+      if (fabs(q) > 127.0 || q * scale != a) *bad = 1;
+      v = int(q);
+    }
     out[idx] = __int2half_rn(v);
     out8[idx] = int8_t(v);
   }
@@ -812,32 +831,45 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.release();
   d.n = n;
   d.npad = (n + 255) / 256 * 256;  // whole int8 stages (2 x 128 of K)
-  // exact small-integer form J = jscale * Q (the K2000 instance: jscale = -1/2, Q = +-1)
-  double mn = 0.0;
-  for (int64_t e = 0; e < n * n; ++e)
-    if (A[e] != 0.0 && (mn == 0.0 || std::fabs(A[e]) < mn)) mn = std::fabs(A[e]);
-  if (mn == 0.0) return;
-  double scale = 0.0;
-  for (double cand : {mn, 1.0, 0.5}) {
-    bool ok = true;
-    for (int64_t e = 0; e < n * n && ok; ++e) {
-      const double q = A[e] / cand;
-      if (q != std::nearbyint(q) || std::fabs(q) > 127.0 || cand * std::nearbyint(q) != A[e]) ok = false;
-    }
-    if (ok) { scale = cand; break; }
-  }
-  if (scale == 0.0) return;  // real-valued couplings: no exact f16 operand, tensor path unavailable
-  // sign convention: keep Q's sign (J = scale * Q with scale > 0); K2000 has Q = -W/2 / 0.5 = -W
-  std::vector<int16_t> q(n * n);
-  for (int64_t e = 0; e < n * n; ++e) q[e] = int16_t(std::nearbyint(A[e] / scale));
-  int16_t* dq = nullptr;
-  DCK(cudaMalloc(&dq, n * n * 2));
-  DCK(cudaMemcpyAsync(dq, q.data(), n * n * 2, cudaMemcpyHostToDevice, s));
-  DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
-  DCK(cudaMalloc(&d.q8, d.npad * d.npad));
-  tc::q_expand<<<1024, 256, 0, s>>>(dq, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8), n, d.npad);
+  // exact small-integer form J = jscale * Q (the K2000 instance: jscale = 1/2, Q = -W),
+  // found and converted on the device: min |nonzero| gives the candidate scale
+  double* dA = nullptr;
+  unsigned long long* dw = nullptr;  // [0] min |a| bits, [1] failure flag
+  DCK(cudaMalloc(&dA, n * n * 8));
+  DCK(cudaMalloc(&dw, 16));
+  DCK(cudaMemcpyAsync(dA, A, n * n * 8, cudaMemcpyHostToDevice, s));
+  const unsigned long long init[2] = {~0ull, 0ull};
+  DCK(cudaMemcpyAsync(dw, init, 16, cudaMemcpyHostToDevice, s));
+  tc::min_abs_nonzero<<<1024, 256, 0, s>>>(dA, n * n, dw);
+  unsigned long long mnbits = 0;
+  DCK(cudaMemcpyAsync(&mnbits, dw, 8, cudaMemcpyDeviceToHost, s));
   DCK(cudaStreamSynchronize(s));
-  cudaFree(dq);
+  double scale = 0.0;
+  if (mnbits != ~0ull) {
+    double mn;
+    std::memcpy(&mn, &mnbits, 8);
+    DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
+    DCK(cudaMalloc(&d.q8, d.npad * d.npad));
+    for (double cand : {mn, 1.0, 0.5}) {
+      DCK(cudaMemsetAsync(dw + 1, 0, 8, s));
+      tc::q_expand<<<1024, 256, 0, s>>>(dA, cand, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8),
+                                        n, d.npad, dw + 1);
+      unsigned long long bad = 1;
+      DCK(cudaMemcpyAsync(&bad, dw + 1, 8, cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      if (!bad) {
+        scale = cand;
+        break;
+      }
+    }
+  }
+  cudaFree(dA);
+  cudaFree(dw);
+  if (scale == 0.0) {  // real-valued couplings: no exact int8 / f16 operand, tensor path unavailable
+    d.release();
+    d.n = n;
+    return;
+  }
   d.jscale = float(scale);
   d.exact = true;
   d.tmaps = new CUtensorMap[6];
@@ -851,9 +883,11 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (!d.exact) throw std::invalid_argument("tensor-core path needs small-integer dense couplings");
   const RunCfg& cfg = m.args.cfg;
   if (cfg.solver != DCX_SOLVER_DOCH) throw std::invalid_argument("tensor-core path implements DOCH");
-  d.release_run();
+  const int Rpad_new = (cfg.R + 127) / 128 * 128;
+  const bool reuse = d.xm[0] != nullptr && d.Rpad == Rpad_new;  // same shapes: keep the device buffers
+  if (!reuse) d.release_run();
   d.R = cfg.R;
-  d.Rpad = (d.R + 127) / 128 * 128;
+  d.Rpad = Rpad_new;
   int dev = 0, nsm = 0;
   DCK(cudaGetDevice(&dev));
   DCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -866,23 +900,27 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (const char* e = std::getenv("DCX_DENSE_NC")) d.nc = std::atoi(e) == 2 && d.Rpad % 256 == 0 ? 2 : 1;
   const size_t vec = size_t(d.Rpad) * d.npad;
   for (int b = 0; b < 2; ++b) {
-    DCK(cudaMalloc(&d.xm[b], vec * 4));
-    DCK(cudaMalloc(&d.xh[b], vec * 2));
-    DCK(cudaMalloc(&d.s8[b], vec));
+    if (!reuse) {
+      DCK(cudaMalloc(&d.xm[b], vec * 4));
+      DCK(cudaMalloc(&d.xh[b], vec * 2));
+      DCK(cudaMalloc(&d.s8[b], vec));
+    }
     DCK(cudaMemsetAsync(d.xm[b], 0, vec * 4, s));
     DCK(cudaMemsetAsync(d.xh[b], 0, vec * 2, s));
     DCK(cudaMemsetAsync(d.s8[b], 0, vec, s));
   }
-  DCK(cudaMalloc(&d.best8, vec));
+  if (!reuse) {
+    DCK(cudaMalloc(&d.best8, vec));
+    DCK(cudaMalloc(&d.part, sizeof(double) * 4 * (d.npad / 128) * d.Rpad));
+    DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128)));
+  }
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
-  DCK(cudaMalloc(&d.part, sizeof(double) * 4 * (d.npad / 128) * d.Rpad));
   {
     const int gsz = 128 * d.nc;
     const int ngroups = d.Rpad / gsz;
     std::vector<tc::SyncWords> sw(ngroups);
     std::memset(sw.data(), 0, sizeof(tc::SyncWords) * ngroups);
     for (int gI = 0; gI < ngroups; ++gI) sw[gI].running = std::max(0, std::min(gsz, d.R - gI * gsz));
-    DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * ngroups));
     DCK(cudaMemcpyAsync(d.sync, sw.data(), sizeof(tc::SyncWords) * ngroups, cudaMemcpyHostToDevice, s));
   }
   if (d.dbg) cudaFree(d.dbg);

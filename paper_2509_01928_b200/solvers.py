@@ -185,7 +185,7 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
                    window_mode: str = "economy", trace_stride: int = 1, time_budget: Optional[float] = None,
                    record_states: bool = False, precision: str = "f32", path: str = "auto",
                    seeds: Optional[Sequence[int]] = None, callbacks=(), chunk: int = 0,
-                   device: Optional[int] = None) -> list:
+                   device: Optional[int] = None, reupload: bool = False) -> list:
     """Run R independent replicas (rows of ``x0``) of DOCH/ADOCH in one batch.
 
     ``alpha``/``beta`` are scalars or length-R arrays (tune_eta passes one
@@ -199,7 +199,7 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
     J = instance.coupling
     X0 = np.atleast_2d(np.asarray(x0, dtype=np.float64))
     R = X0.shape[0]
-    ctx = device_context(J, device)
+    ctx = device_context(J, device, reload=reupload)
     prm = _native.Params(
         solver=_native.SOLVER[solver], window_mode=_native.WINDOW[window_mode],
         precision=_native.PRECISION[precision], lookback_q=int(lookback_q), max_iters=int(max_iters),
@@ -229,12 +229,21 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
     best = ctx.best_spins().astype(np.float64)
     xs = ctx.state()
     dev_s = ctx.device_seconds()
+    path_used = _native.PATH_NAME.get(int(ctx.summary(0).path_used))
+    # bulk download of every replica's history, then per-replica views (no per-replica FFI calls)
+    iters, stops, bests, nh, warn = ctx.summaries()
+    K = int(nh.max()) if R else 0
+    H, E, T, EV = ctx.history_all(K)
+    rec = (EV & _native.EV_RECORDED) != 0
     out = []
     for r in range(R):
-        s, h, ev, trace = _collect(ctx, r, solver, cut_offset, offset)
-        it = int(s.iterations)
-        if s.descent_warn >= 0 and solver == "doch":
-            k = int(s.descent_warn)
+        n_r = int(nh[r])
+        h, ev = H[r, :n_r], EV[r, :n_r]
+        ks = np.nonzero(rec[r, :n_r])[0]
+        trace = LazyTrace(solver, ks, T[r, ks] + offset, E[r, ks], cut_offset, ev[ks])
+        it = int(iters[r])
+        if warn[r] >= 0 and solver == "doch":
+            k = int(warn[r])
             warnings.warn(f"Hamiltonian increased by {h[k] - h[k - 1]:.3e} at iteration {k}",
                           RuntimeWarning, stacklevel=3)
         accepted = None
@@ -245,10 +254,10 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
             st = ctx.states(r, it)
             states = [st[k].copy() for k in range(it + 1)]
         out.append(SolveResult(
-            solver=solver, spins=best[r], energy=float(s.best_energy), iterations=it,
-            stop_reason=_native.STOP.get(int(s.stop_reason), "max_iters"), trace=trace,
-            seed=None if seeds is None else seeds[r], x=xs[r], h_values=h.tolist(), accepted=accepted,
-            states=states, device_seconds=dev_s, path=_native.PATH_NAME.get(int(s.path_used))))
+            solver=solver, spins=best[r], energy=float(bests[r]), iterations=it,
+            stop_reason=_native.STOP.get(int(stops[r]), "max_iters"), trace=trace,
+            seed=None if seeds is None else seeds[r], x=xs[r], h_values=h if R > 1 else h.tolist(),
+            accepted=accepted, states=states, device_seconds=dev_s, path=path_used))
     return out
 
 
