@@ -34,8 +34,8 @@ EV_RECORDED, EV_DESCENT, EV_ACCEPTED, EV_REJECTED = 1, 2, 4, 8
 EXPORTS = (
     "dcx_abi_version", "dcx_last_error", "dcx_create", "dcx_destroy", "dcx_set_csr", "dcx_set_dense",
     "dcx_coupling", "dcx_matvec", "dcx_apply", "dcx_energy", "dcx_solve_begin", "dcx_solve_step",
-    "dcx_solve_run", "dcx_result_summary", "dcx_result_history", "dcx_result_best_spins",
-    "dcx_result_state", "dcx_result_states", "dcx_result_device_seconds", "dcx_profile_kernel",
+    "dcx_solve_run", "dcx_result_summary", "dcx_result_summaries", "dcx_result_history",
+    "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states", "dcx_result_device_seconds", "dcx_profile_kernel",
 )
 
 
