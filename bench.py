@@ -310,7 +310,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default=os.environ.get("DCX_BENCH_PRECISION", "f16tc"))
     ap.add_argument("--path", default=os.environ.get("DCX_BENCH_PATH", "auto"))
+    ap.add_argument("--config", default="k2", choices=["k2", "g1", "t6", "e7"],
+                    help="k2 is the headline (BASELINE configs[1]); others: see bench_configs.py")
     args = ap.parse_args()
+    if args.config != "k2" and args.impl == "ours":
+        import bench_configs
+
+        bench_configs.run(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

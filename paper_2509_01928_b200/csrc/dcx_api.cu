@@ -206,7 +206,7 @@ __global__ void to_device_layout(const double* src, T* dst, int64_t n, int R) {
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx / R;
     const int r = int(idx % R);
-    dst[idx] = T(src[(int64_t)r * n + i]);
+    dst[idx] = T(src[(int64_t)r * n + i]) + T(0);  // + 0 turns -0.0 into +0.0 (same spin, see tmap)
   }
 }
 template <typename T>
@@ -231,7 +231,7 @@ __global__ void rows_epilogue(int mode, const T* v, const T* jv, const double* e
     if (mode == 0) {
       const T xi = v[idx];
       const T ax = shifted(jv[idx], al, xi);
-      if (tx) tx[idx] = tmap(ax, be);
+      if (tx) tx[idx] = tmap(ax, be, inv_beta(be));
       const double x2 = double(mul_rn(xi, xi));
       a += x2 * x2;
       b += double(xi) * double(ax);
@@ -404,6 +404,14 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     int vk;
     double scale;
     classify_values(v, nnz, vk, scale);
+    if (vk == VK_I8 || vk == VK_UNIFORM) {
+      // the UNIFORM / I8 kernels sum q * sign(x) per row in f32, exact while
+      // every row's sum of |q| stays below 2^24; longer rows use the int32
+      // (I16) path
+      int64_t maxlen = 0;
+      for (int64_t i = 0; i < n; ++i) maxlen = std::max<int64_t>(maxlen, ro[i + 1] - ro[i]);
+      if (maxlen * (vk == VK_I8 ? 127 : 1) >= (int64_t(1) << 24) && scale != 0.0) vk = VK_I16;
+    }
     c->have = false;
     c->n = n;
     c->nnz = nnz;
@@ -625,8 +633,12 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
       c->mp.grid = c->J.grid;
       slots = c->mp.grid * 8;
     } else {
-      c->mp.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, 148 * 2));
-      slots = c->mp.grid * 8;
+      // pass_rv: grid.y = replica chunks, grid.x = row blocks, one partial slot per row block;
+      // two resident 256-thread blocks per SM (the kernel needs up to 128 registers)
+      const int vw = replica_vector_width(R, c->f64);
+      const int chunks = (R + 32 * vw - 1) / (32 * vw);
+      c->mp.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, std::max(1, 148 * 2 / chunks)));
+      slots = c->mp.grid;
     }
     c->part.alloc(sizeof(double) * R * NQ * slots);
     {

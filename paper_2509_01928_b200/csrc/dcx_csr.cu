@@ -49,7 +49,7 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RepCtl& c,
       // pending best-spin copy of x_{p-1}, still held in the write buffer
       if (c.pend == p - 1 && p > 0) a.best[idx] = xnext[idx] >= T(0) ? 1 : -1;
       if (c.status == DCX_STOP_RUNNING) {
-        T xn = tmap(ax, beta);
+        T xn = tmap(ax, beta, inv_beta(beta));
         xnext[idx] = xn;
         if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * a.cfg.n * a.cfg.R + idx] = xn;
         o.step = fmax(o.step, double(fabs(xn - xi)));
@@ -145,69 +145,385 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// R > 1: one warp per row, lanes over replicas (layout x[j][r], coalesced),
-// RG groups of 32 replicas per lane held in registers so the row's index and
-// value stream is read once per 32*RG replicas.
-template <typename T, int VK, int RG, int MODE>
-__global__ void __launch_bounds__(256) pass_rn(PassArgs a) {
+// R > 1: replica-vector kernel. Layout x[j][r] (replicas contiguous per spin).
+// blockIdx.y selects a chunk of 32*VW replicas; each lane owns VW consecutive
+// replicas and moves them with one 16-byte load/store (VW = 16 / sizeof(T)
+// when R is a multiple of it, else 1). A warp walks one row at a time: the
+// row's column/value entries are fetched 32 at a time with one coalesced load
+// and broadcast by shuffle, and neighbour rows are gathered UNROLL at a time so
+// several independent 16-byte loads are in flight per lane. Per-replica sums
+// stay in column order (the scipy order, bit-exact in f64).
+// Partials: one slot per block (blockIdx.x), reduced across the block's warps
+// in a fixed order, so slots = gridDim.x.
+template <typename T, int VW>
+struct VecT;
+template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<float, 4> { using type = float4; };
+template <> struct VecT<double, 1> { using type = double; };
+template <> struct VecT<double, 2> { using type = double2; };
+
+template <typename T, int VW>
+__device__ __forceinline__ void vload(const T* p, T (&out)[VW]) {
+  using V = typename VecT<T, VW>::type;
+  const V v = *reinterpret_cast<const V*>(p);
+  memcpy(out, &v, sizeof(V));
+}
+template <typename T, int VW>
+__device__ __forceinline__ void vstore(T* p, const T (&in)[VW]) {
+  using V = typename VecT<T, VW>::type;
+  V v;
+  memcpy(&v, in, sizeof(V));
+  *reinterpret_cast<V*>(p) = v;
+}
+
+// Per-row spin-energy accumulator (J sign x_p)_i of the replica kernel, by
+// value kind; padding edges carry q = 0 / v = 0 / x = +0 and add nothing.
+template <int VK, typename T>
+struct EsRow {  // real values: double sum of +-v
+  double s = 0.0;
+  __device__ __forceinline__ void add(int, float, T v, T x) { s += negbit(x) ? -double(v) : double(v); }
+  __device__ __forceinline__ double value(uint32_t) const { return s; }
+};
+template <typename T>
+struct EsRowF {  // q in {0, 1} (UNIFORM) or |q| <= 127 (I8), row sum of |q| < 2^24 (enforced on upload): exact in f32
+  float s = 0.0f;
+  __device__ __forceinline__ void add(int, float qf, T, T x) { s = fmaf(qf, sgnf_bits(x), s); }
+  __device__ __forceinline__ double value(uint32_t) const { return double(s); }
+  __device__ __forceinline__ float value_f() const { return s; }
+};
+template <typename T>
+struct EsRow<VK_UNIFORM, T> : EsRowF<T> {};
+template <typename T>
+struct EsRow<VK_I8, T> : EsRowF<T> {};
+template <typename T>
+struct EsRow<VK_I16, T> {
+  int s = 0;
+  __device__ __forceinline__ void add(int q, float, T, T x) {
+    const int m = -int(negbit(x));
+    s += (q ^ m) - m;
+  }
+  __device__ __forceinline__ double value(uint32_t) const { return double(s); }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+template <int B>
+__device__ __forceinline__ void cp_async(uint32_t dst, const void* src) {
+  if constexpr (B == 16) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  else if constexpr (B == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// edges per row staged through shared memory by cp.async (0: gather directly)
+template <int MODE>
+constexpr int rv_staged_edges() { return MODE == MODE_ADOCH_Y ? 0 : 8; }
+template <typename T, int VW, int MODE>
+constexpr size_t rv_smem_bytes() { return size_t(2) * 8 * rv_staged_edges<MODE>() * 32 * VW * sizeof(T); }
+
+template <typename T, int VK, int VW, int MODE>
+__global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
+  constexpr int UNROLL = 4;
+  constexpr int G = rv_staged_edges<MODE>();
+  constexpr int CB = VW * int(sizeof(T));  // bytes per lane per spin row
+  extern __shared__ __align__(16) unsigned char stage_mem[];
   if (!a.g->live) return;
   const int p = a.g->p;
   if (MODE == MODE_ADOCH_Y && p == 0) return;  // no extrapolation at k = 0
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R = a.cfg.R;
   const int64_t n = a.cfg.n;
+  const int r0 = blockIdx.y * 32 * VW + lane * VW;  // this lane's first replica
+  const bool lane_on = r0 < R;                      // all VW replicas in or all out
+  T alpha[VW], beta[VW], ibeta[VW], cm[VW];
+  bool run[VW], copy[VW];
+  bool any_run = false, all_run = true, any_copy = false;
+#pragma unroll
+  for (int v = 0; v < VW; ++v) {
+    run[v] = copy[v] = false;
+    alpha[v] = beta[v] = cm[v] = T(0);
+    ibeta[v] = T(1);
+    if (lane_on) {
+      const RepCtl& c = a.ctl[r0 + v];
+      run[v] = c.status == DCX_STOP_RUNNING;
+      copy[v] = MODE == MODE_DOCH && p > 0 && c.pend == p - 1;
+      alpha[v] = T(c.alpha);
+      beta[v] = T(c.beta);
+      ibeta[v] = inv_beta(beta[v]);
+      cm[v] = T(c.cm[p & 1]);
+    }
+    any_run |= run[v];
+    all_run &= run[v];
+    any_copy |= copy[v];
+  }
+  // nothing to do for this replica chunk (block-uniform: the chunk is per block)
+  if (!__syncthreads_or(any_run || any_copy)) return;
+  const bool warp_run = __any_sync(0xffffffffu, any_run);
   const T* xc = reinterpret_cast<const T*>(a.x[p & 1]);
   const T* xp = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
+  T* xn_buf = reinterpret_cast<T*>(a.x[(p + 1) & 1]);
   const T scale = T(a.scale);
-  for (int r0 = 0; r0 < R; r0 += 32 * RG) {
-    RowOut<T, MODE> o[RG];
-    RepCtl c[RG];
-    bool run[RG], act[RG];
+  // per-replica partials over this warp's rows; the step max stays in T (exact)
+  double s4[VW], sxax[VW], esum[VW], sy4[VW], syay[VW];
+  T step[VW];
 #pragma unroll
-    for (int g = 0; g < RG; ++g) {
-      const int r = r0 + g * 32 + lane;
-      act[g] = r < R;
-      if (act[g]) c[g] = a.ctl[r];
-      run[g] = act[g] && c[g].status == DCX_STOP_RUNNING;
-      if (act[g] && !run[g] && !(MODE == MODE_DOCH && c[g].pend == p - 1)) act[g] = false;
+  for (int v = 0; v < VW; ++v) {
+    s4[v] = sxax[v] = esum[v] = sy4[v] = syay[v] = 0.0;
+    step[v] = T(0);
+  }
+
+  // Pipeline over this warp's rows A = i, B = i+S, C = i+2S, D = i+3S. While
+  // row A is computed, the neighbour-row chunks of B's first G edges are in
+  // flight into shared memory (cp.async), C's first column batch and D's row
+  // pointers are in flight into registers.
+  const int64_t S = int64_t(gridDim.x) * 8;
+  int64_t i = int64_t(blockIdx.x) * 8 + warp;
+  const uint32_t rowb = uint32_t(R) * uint32_t(sizeof(T));  // bytes per spin row of x
+  const char* xcb = reinterpret_cast<const char*>(xc + r0);
+  const char* xpb = reinterpret_cast<const char*>(xp + r0);
+  // stage s of this warp, edge e, this lane: stage_mem + ((s*8 + warp)*G + e)*32*CB + lane*CB
+  const uint32_t st_base = smem_u32(stage_mem) + uint32_t((warp * G * 32 + lane) * CB);
+  constexpr uint32_t ST_STRIDE = 8u * G * 32 * CB;  // between stages
+  auto load_rp = [&](int64_t r, uint32_t& lo, uint32_t& hi) {
+    lo = hi = 0;
+    if (warp_run && r < n) { lo = __ldg(a.rp + r); hi = __ldg(a.rp + r + 1); }
+  };
+  auto load_batch = [&](uint32_t base, uint32_t hi, int& col, int& q, T& v) {
+    col = 0; q = 0; v = T(0);
+    if (base + lane < hi) {
+      col = __ldg(a.col + base + lane);
+      v = load_entry<VK, true, T>(a.val, base + lane, scale, q);
     }
-    for (int64_t i = gw; i < n; i += nwarps) {
-      T acc[RG];
-      typename EsAcc<VK>::type es[RG];
+  };
+  auto stage_row = [&](int s, uint32_t lo, uint32_t hi, int col) {
+    if constexpr (G > 0) {
+      const uint32_t deg = hi - lo;
 #pragma unroll
-      for (int g = 0; g < RG; ++g) { acc[g] = T(0); es[g] = 0; }
-      const uint32_t lo = __ldg(a.rp + i), hi = __ldg(a.rp + i + 1);
-      for (uint32_t e = lo; e < hi; ++e) {
-        const int64_t j = __ldg(a.col + e);
-        int q;
-        const T v = load_entry<VK, true, T>(a.val, e, scale, q);
+      for (int e = 0; e < G; ++e) {
+        if (e >= deg) break;  // warp-uniform
+        const uint32_t j = uint32_t(__shfl_sync(0xffffffffu, col, e));
+        if (lane_on) cp_async<CB>(st_base + s * ST_STRIDE + e * 32 * CB, xcb + size_t(j) * rowb);
+      }
+      cp_async_commit();
+    }
+  };
+  if constexpr (G > 0) {
+    // stage slots past a row's degree are read as padding (times a zero
+    // weight): start them at +0 so stale contents are always finite values
+    const T z[VW] = {};
+    for (int e = 0; e < 2 * G; ++e)
+      vstore<T, VW>(reinterpret_cast<T*>(stage_mem + ((e / G) * ST_STRIDE + (warp * G + e % G) * 32 * CB + lane * CB)), z);
+    __syncwarp();
+  }
+  // one edge's value / integer weight from the lane-distributed batch registers
+  auto edge_value = [&](int kk, bool real, int myq, T myv, int& q, T& v) {
+    if constexpr (VK == VK_UNIFORM) { q = real; v = real ? scale : T(0); }
+    else if constexpr (VK == VK_F32 || VK == VK_F64) { q = 0; v = __shfl_sync(0xffffffffu, myv, kk & 31); }
+    else { q = __shfl_sync(0xffffffffu, myq, kk & 31); v = scale * T(q); }
+  };
+
+  uint32_t a_lo, a_hi, b_lo, b_hi, c_lo, c_hi;
+  int a_col, a_q, b_col, b_q;
+  T a_v, b_v;
+  load_rp(i, a_lo, a_hi);
+  load_batch(a_lo, a_hi, a_col, a_q, a_v);
+  load_rp(i + S, b_lo, b_hi);
+  stage_row(0, a_lo, a_hi, a_col);
+  load_batch(b_lo, b_hi, b_col, b_q, b_v);
+  load_rp(i + 2 * S, c_lo, c_hi);
+  int s = 0;
+  for (; i < n; i += S, s ^= 1) {
+    stage_row(s ^ 1, b_lo, b_hi, b_col);         // row B -> the other stage
+    int c_col, c_q;
+    T c_v;
+    uint32_t d_lo, d_hi;
+    load_batch(c_lo, c_hi, c_col, c_q, c_v);    // row C, first batch
+    load_rp(i + 3 * S, d_lo, d_hi);             // row D
+    const int64_t idx = i * R + r0;
+    // own-row operands, issued before the gather
+    T xi[VW], xn[VW];
+    if constexpr (MODE == MODE_DOCH) {
+      if (lane_on && any_run) vload<T, VW>(xc + idx, xi);
+      if (lane_on && (any_copy || !all_run)) vload<T, VW>(xn_buf + idx, xn);  // x_{p-1} (still held)
+    } else if constexpr (MODE == MODE_ADOCH_X) {
+      if (lane_on && any_run) vload<T, VW>(xc + idx, xi);
+    }
+    T acc[VW];
+    EsRow<VK, T> es[VW];
 #pragma unroll
-        for (int g = 0; g < RG; ++g) {
-          if (run[g]) {
-            const int64_t o2 = j * R + r0 + g * 32 + lane;
-            T xj;
-            if constexpr (MODE == MODE_ADOCH_Y) xj = extrap(xc[o2], xp[o2], T(c[g].cm[p & 1]));
-            else xj = xc[o2];
-            acc[g] = madd(acc[g], v, xj);
-            if constexpr (MODE != MODE_ADOCH_Y) es[g] += es_term<VK, T>(q, v, xj);
+    for (int v = 0; v < VW; ++v) acc[v] = T(0);
+    const uint32_t deg = a_hi - a_lo;
+    if constexpr (G > 0) {
+      cp_async_wait1();  // row A's stage has landed (row B's may still be in flight)
+      const uint32_t sa = st_base + s * ST_STRIDE;
+#pragma unroll
+      for (int k = 0; k < G; k += UNROLL) {
+        if (k >= deg) break;
+        T xg[UNROLL][VW];
+        T vv[UNROLL];
+        int qq[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const int kk = k + u;
+          const bool real = kk < deg;
+          edge_value(kk, real, a_q, a_v, qq[u], vv[u]);  // padding: weight 0
+          // padding slots hold finite stale values (zero-initialised above)
+          vload<T, VW>(reinterpret_cast<const T*>(stage_mem + (sa + kk * 32 * CB - smem_u32(stage_mem))), xg[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+#pragma unroll
+          for (int v = 0; v < VW; ++v) {
+            acc[v] = madd(acc[v], vv[u], xg[u][v]);
+            es[v].add(qq[u], float(qq[u]), vv[u], xg[u][v]);
           }
         }
       }
+    }
+    // edges past the staged ones: gathered directly, UNROLL at a time
+    for (uint32_t base = a_lo, k0 = G; base < a_hi; base += 32, k0 = 0) {
+      const int cnt = int(min(32u, a_hi - base));
+      if (int(k0) >= cnt) continue;
+      int mycol = a_col, myq = a_q;
+      T myv = a_v;
+      if (base != a_lo) load_batch(base, a_hi, mycol, myq, myv);
+      for (int k = k0; k < cnt; k += UNROLL) {
+        T xg[UNROLL][VW];
+        T vv[UNROLL];
+        int qq[UNROLL];
 #pragma unroll
-      for (int g = 0; g < RG; ++g) {
-        const int64_t idx = i * R + r0 + g * 32 + lane;
-        if (run[g]) row_epilogue<T, MODE>(a, c[g], p, idx, acc[g], double(es[g]), o[g]);
-        else if (act[g] && MODE == MODE_DOCH)
-          a.best[idx] = reinterpret_cast<const T*>(a.x[(p + 1) & 1])[idx] >= T(0) ? 1 : -1;
+        for (int u = 0; u < UNROLL; ++u) {
+          const int kk = k + u;  // uniform across the warp
+          const bool real = kk < cnt;
+          const uint32_t j = uint32_t(__shfl_sync(0xffffffffu, mycol, kk & 31));
+          edge_value(kk, real, myq, myv, qq[u], vv[u]);
+#pragma unroll
+          for (int v = 0; v < VW; ++v) xg[u][v] = T(0);
+          if (real && lane_on) {
+            const size_t off = size_t(j) * rowb;
+            if constexpr (MODE == MODE_ADOCH_Y) {
+              T a0[VW], a1[VW];
+              vload<T, VW>(reinterpret_cast<const T*>(xcb + off), a0);
+              vload<T, VW>(reinterpret_cast<const T*>(xpb + off), a1);
+#pragma unroll
+              for (int v = 0; v < VW; ++v) xg[u][v] = extrap(a0[v], a1[v], cm[v]);
+            } else {
+              vload<T, VW>(reinterpret_cast<const T*>(xcb + off), xg[u]);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+#pragma unroll
+          for (int v = 0; v < VW; ++v) {
+            acc[v] = madd(acc[v], vv[u], xg[u][v]);
+            if constexpr (MODE != MODE_ADOCH_Y) es[v].add(qq[u], float(qq[u]), vv[u], xg[u][v]);
+          }
+        }
       }
     }
+    a_lo = b_lo; a_hi = b_hi; a_col = b_col; a_q = b_q; a_v = b_v;
+    b_lo = c_lo; b_hi = c_hi; b_col = c_col; b_q = c_q; b_v = c_v;
+    c_lo = d_lo; c_hi = d_hi;
+    if (!lane_on) continue;
+    if constexpr (MODE == MODE_DOCH) {
+      if (!any_run) {  // stopped replicas: only the pending best-spin copy
+        if (any_copy) {
 #pragma unroll
-    for (int g = 0; g < RG; ++g) {
-      const int r = r0 + g * 32 + lane;
-      if (r < R) write_partials<T, MODE>(a, r, (int)gw, o[g]);
+          for (int v = 0; v < VW; ++v)
+            if (copy[v]) a.best[idx + v] = xn[v] >= T(0) ? 1 : -1;
+        }
+        continue;
+      }
+      if (any_copy) {
+#pragma unroll
+        for (int v = 0; v < VW; ++v)
+          if (copy[v]) a.best[idx + v] = xn[v] >= T(0) ? 1 : -1;
+      }
+      // branch-free over the lane's replicas (so they interleave); partials of
+      // stopped replicas are accumulated but never read (reduce_control skips them)
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        const T ax = shifted(acc[v], alpha[v], xi[v]);
+        const double x2 = double(mul_rn(xi[v], xi[v]));
+        s4[v] += x2 * x2;
+        sxax[v] += double(xi[v]) * double(ax);
+        const double e = es[v].value(deg);
+        esum[v] += negbit(xi[v]) ? -e : e;
+        const T xnew = tmap(ax, beta[v], ibeta[v]);
+        step[v] = fmax(step[v], fabs(xnew - xi[v]));
+        xn[v] = run[v] ? xnew : xn[v];
+      }
+      vstore<T, VW>(xn_buf + idx, xn);
+      if (a.states) vstore<T, VW>(reinterpret_cast<T*>(a.states) + (int64_t)(p + 1) * n * R + idx, xn);
+    } else if constexpr (MODE == MODE_ADOCH_X) {
+      if (!any_run) continue;
+      T ax[VW];
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        ax[v] = shifted(acc[v], alpha[v], xi[v]);
+        const double x2 = double(mul_rn(xi[v], xi[v]));
+        s4[v] += x2 * x2;
+        sxax[v] += double(xi[v]) * double(ax[v]);
+        const double e = es[v].value(deg);
+        esum[v] += negbit(xi[v]) ? -e : e;
+      }
+      vstore<T, VW>(reinterpret_cast<T*>(a.ax[p & 1]) + idx, ax);
+      if (p > 0 && a.cfg.window_mode == DCX_WINDOW_ECONOMY) {
+        T xq[VW], axq[VW];
+        vload<T, VW>(xp + idx, xq);
+        vload<T, VW>(reinterpret_cast<const T*>(a.ax[(p + 1) & 1]) + idx, axq);
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+          const T yi = extrap(xi[v], xq[v], cm[v]);
+          const T ayi = extrap(ax[v], axq[v], cm[v]);
+          const double y2 = double(mul_rn(yi, yi));
+          sy4[v] += y2 * y2;
+          syay[v] += double(yi) * double(ayi);
+        }
+      }
+    } else {  // MODE_ADOCH_Y: acc = J y
+      if (!any_run) continue;
+      T xq[VW], ay[VW];
+      vload<T, VW>(xc + idx, xi);
+      vload<T, VW>(xp + idx, xq);
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        const T yi = extrap(xi[v], xq[v], cm[v]);
+        ay[v] = shifted(acc[v], alpha[v], yi);
+        const double y2 = double(yi) * double(yi);
+        sy4[v] += y2 * y2;
+        syay[v] += double(yi) * double(ay[v]);
+      }
+      vstore<T, VW>(reinterpret_cast<T*>(a.ay) + idx, ay);
     }
+  }
+  if constexpr (G > 0) cp_async_wait0();
+
+  // block reduction of the per-replica partials, warps in a fixed order
+  __shared__ double red[NQ][32 * VW];
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        const int c = lane * VW + v;
+        const double q[NQ] = {s4[v], sxax[v], esum[v], double(step[v]), sy4[v], syay[v]};
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          if (w == 0) red[k][c] = q[k];
+          else red[k][c] = (k == Q_STEP) ? fmax(red[k][c], q[k]) : red[k][c] + q[k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < NQ * 32 * VW; t += blockDim.x) {
+    const int k = t / (32 * VW), c = t % (32 * VW);
+    const int r = blockIdx.y * 32 * VW + c;
+    if (r < R) a.part[((int64_t)r * NQ + k) * a.slots + blockIdx.x] = red[k][c];
   }
 }
 
@@ -246,7 +562,7 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
       } else {
         av = axc[i];
       }
-      const T xn = tmap(av, beta);
+      const T xn = tmap(av, beta, inv_beta(beta));
       xo[i] = xn;
       if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + i] = xn;
       st = fmax(st, double(fabs(xn - xi)));
@@ -277,7 +593,7 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
     } else {
       av = axc[idx];
     }
-    const T xn = tmap(av, beta);
+    const T xn = tmap(av, beta, inv_beta(beta));
     xo[idx] = xn;
     if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + idx] = xn;
     st = fmax(st, double(fabs(xn - xi)));
@@ -444,13 +760,31 @@ static void launch_r1(int mode, const PassArgs& a, int grid, cudaStream_t s) {
     default: pass_r1<T, VK, V, MODE_ADOCH_Y><<<grid, 256, 0, s>>>(a); break;
   }
 }
-template <typename T, int VK, int RG>
-static void launch_rn(int mode, const PassArgs& a, int grid, cudaStream_t s) {
-  switch (mode) {
-    case MODE_DOCH: pass_rn<T, VK, RG, MODE_DOCH><<<grid, 256, 0, s>>>(a); break;
-    case MODE_ADOCH_X: pass_rn<T, VK, RG, MODE_ADOCH_X><<<grid, 256, 0, s>>>(a); break;
-    default: pass_rn<T, VK, RG, MODE_ADOCH_Y><<<grid, 256, 0, s>>>(a); break;
+template <typename T, int VK, int VW, int MODE>
+static void launch_rv_mode(const PassArgs& a, dim3 grid, cudaStream_t s) {
+  constexpr size_t smem = rv_smem_bytes<T, VW, MODE>();
+  static unsigned long long opted = 0;  // devices this instantiation opted in on
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > 48 * 1024 && !((opted >> (dev & 63)) & 1ull)) {
+    cudaFuncSetAttribute(pass_rv<T, VK, VW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    opted |= 1ull << (dev & 63);
   }
+  pass_rv<T, VK, VW, MODE><<<grid, 256, smem, s>>>(a);
+}
+template <typename T, int VK, int VW>
+static void launch_rv(int mode, const PassArgs& a, dim3 grid, cudaStream_t s) {
+  switch (mode) {
+    case MODE_DOCH: launch_rv_mode<T, VK, VW, MODE_DOCH>(a, grid, s); break;
+    case MODE_ADOCH_X: launch_rv_mode<T, VK, VW, MODE_ADOCH_X>(a, grid, s); break;
+    default: launch_rv_mode<T, VK, VW, MODE_ADOCH_Y>(a, grid, s); break;
+  }
+}
+
+// replicas per lane of the R > 1 kernel
+int replica_vector_width(int R, bool f64) {
+  const int w = f64 ? 2 : 4;
+  return R % w == 0 ? w : 1;
 }
 
 template <typename T, int VK>
@@ -466,10 +800,9 @@ static void launch_pass_vk(int mode, const PassArgs& a, int V, int grid, cudaStr
     }
   } else {
     const int R = a.cfg.R;
-    if (R <= 32) launch_rn<T, VK, 1>(mode, a, grid, s);
-    else if (R <= 64) launch_rn<T, VK, 2>(mode, a, grid, s);
-    else if (R <= 128) launch_rn<T, VK, 4>(mode, a, grid, s);
-    else launch_rn<T, VK, 8>(mode, a, grid, s);
+    constexpr int W = 16 / sizeof(T);
+    if (R % W == 0) launch_rv<T, VK, W>(mode, a, dim3(grid, (R + 32 * W - 1) / (32 * W)), s);
+    else launch_rv<T, VK, 1>(mode, a, dim3(grid, (R + 31) / 32), s);
   }
 }
 

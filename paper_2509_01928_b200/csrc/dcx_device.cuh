@@ -99,8 +99,41 @@ __device__ __forceinline__ T sgn(T x) { return x >= T(0) ? T(1) : T(-1); }  // d
 template <typename T>
 __device__ __forceinline__ T shifted(T jx, T alpha, T xi) { return add_rn(jx, mul_rn(alpha, xi)); }
 // cbrt(Ax / beta)   (dc/solvers/doch.py:90-91)
-template <typename T>
-__device__ __forceinline__ T tmap(T ax, T beta) { return cbrt_t(div_rn(ax, beta)); }
+// f64: the numpy expression exactly (IEEE division, correctly rounded cbrt).
+// f32: Ax * (1/beta) and a cube root from the MUFU log2/exp2 estimate plus one
+// Newton step (<= 1 ulp from cbrtf, about half the instructions of
+// __fdiv_rn + cbrtf); zero maps to +0 so no iterate is ever -0.0 (the spin of
+// x = -0.0 is +1, and the sign-bit energy accumulation relies on that).
+__device__ __forceinline__ float cbrt_fast(float t) {
+  const float a = fabsf(t);
+  // branch-free: tiny inputs (denormals) are scaled by 2^96 exactly, the root by 2^-32
+  const bool tiny = a < 1.0e-30f;
+  const float as = tiny ? a * 0x1p96f : a;
+  float l, r, rc;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(as));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(r * r));
+  r = fmaf(fmaf(as, rc, -r), 1.0f / 3.0f, r);  // Newton: r + (a / r^2 - r) / 3
+  r = tiny ? r * 0x1p-32f : r;
+  r = a == __int_as_float(0x7f800000) ? a : r;  // inf
+  return a == 0.0f ? 0.0f : copysignf(r, t);
+}
+__device__ __forceinline__ double inv_beta(double beta) { return beta; }  // unused in f64
+__device__ __forceinline__ float inv_beta(float beta) { return __frcp_rn(beta); }
+__device__ __forceinline__ double tmap(double ax, double beta, double) { return cbrt(__ddiv_rn(ax, beta)); }
+__device__ __forceinline__ float tmap(float ax, float, float ibeta) { return cbrt_fast(__fmul_rn(ax, ibeta)); }
+
+// Sign-bit helpers for the spin-energy accumulation: x < 0 <=> sign bit set,
+// valid because iterates are never -0.0 (see tmap; initial states are
+// canonicalised on upload).
+__device__ __forceinline__ uint32_t negbit(float x) { return __float_as_uint(x) >> 31; }
+__device__ __forceinline__ uint32_t negbit(double x) { return uint32_t(__double_as_longlong(x) >> 63) & 1u; }
+__device__ __forceinline__ float sgnf_bits(float x) {
+  return __uint_as_float((__float_as_uint(x) & 0x80000000u) | 0x3f800000u);
+}
+__device__ __forceinline__ float sgnf_bits(double x) {
+  return __uint_as_float((uint32_t(__double_as_longlong(x) >> 32) & 0x80000000u) | 0x3f800000u);
+}
 // y = x + c (x - xp)   (dc/solvers/doch.py:299, :301)
 template <typename T>
 __device__ __forceinline__ T extrap(T x, T xp, T c) { return add_rn(x, mul_rn(c, sub_rn(x, xp))); }

@@ -50,6 +50,7 @@ void enqueue_iteration(const MultiPass& m, cudaStream_t s);
 void enqueue_flush(const MultiPass& m, cudaStream_t s);
 void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
 void enqueue_start_clock(GState* g, cudaStream_t s);
+int replica_vector_width(int R, bool f64);
 template <typename T>
 void launch_csr_apply(const CsrDev& J, const T* v, int R, T* jv, double* es_rows, cudaStream_t s);
 
