@@ -354,7 +354,7 @@ def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", 
         flops = iters * 2 * (2.0 * n * n * R)
         byts = float(iters * R * n * (2 + 1))  # f16 + int8 operands of the next iteration
     else:
-        name = "pass_rn" if R > 1 else "pass_r1"
+        name = "pass_rv" if R > 1 else "pass_r1"
         vbytes = {0: 0, 1: 1, 2: 2, 3: 4, 4: 8}[info.value_kind]
         if info.value_kind in (3, 4):
             vbytes = tb
