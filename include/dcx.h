@@ -49,6 +49,11 @@ enum {
   DCX_STOP_MAX_ITERS = 2,
   DCX_STOP_TIME_BUDGET = 3
 };
+/* per-replica partial sums exchanged by the row-partitioned solve:
+ * q_sum[r] = {sum x^4, sum x.Ax, sum s.Js, sum y^4, sum y.Ay} (all-reduce SUM),
+ * q_max[r] = {max |dx| of the pass, max |dx| of the ADOCH update, elapsed s} (all-reduce MAX) */
+#define DCX_QSUM 5
+#define DCX_QMAX 3
 /* history event bits */
 enum { DCX_EV_RECORDED = 1, DCX_EV_DESCENT = 2, DCX_EV_ACCEPTED = 4, DCX_EV_REJECTED = 8 };
 
@@ -154,6 +159,35 @@ DCX_API int dcx_result_states(dcx_ctx* ctx, int32_t r, double* out /* [(iteratio
 DCX_API int dcx_profile_kernel(dcx_ctx* ctx, int32_t launches, double* ms_per_launch, int32_t* kernel_id);
 /* device time of the last dcx_solve_run/step sequence, seconds */
 DCX_API int dcx_result_device_seconds(dcx_ctx* ctx, double* out);
+
+/* ---- Row-partitioned solve (multi-GPU) ----
+ * The reference has no distributed solver; this splits the one mat-vec per
+ * iteration of doch_solve / adoch_solve (economy window) by rows. A context
+ * holds rows [row_base, row_base + n_rows) of the coupling in a spin index
+ * space of n_cols entries (columns already mapped into that space, sorted per
+ * row). The iterate buffers are caller-owned device arrays of n_cols x R
+ * elements (layout [n_cols][R], f64 or f32 by precision), two of them by pass
+ * parity; pass p gathers from buffer p&1 and writes this context's rows of
+ * buffer (p+1)&1, which the caller completes with an all-gather of every
+ * rank's row slice before the next pass. Per-replica partials land in
+ * caller-owned device arrays q_sum [R][DCX_QSUM] / q_max [R][DCX_QMAX] that
+ * the caller all-reduces (SUM / MAX) between dcx_dist_pass and
+ * dcx_dist_control; the control is a deterministic function of the reduced
+ * values, so every rank takes the same decisions (stop, ADOCH accept). All
+ * work is ordered on the context stream (dcx_stream); collectives must be
+ * issued on it. */
+DCX_API int dcx_set_csr_block(dcx_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t row_base, int64_t nnz,
+                              const int64_t* row_offsets, const int64_t* col_indices, const double* values);
+DCX_API int dcx_stream(dcx_ctx* ctx, void** stream /* cudaStream_t */);
+DCX_API int dcx_dist_begin(dcx_ctx* ctx, const dcx_params* params, int32_t R, const double* alpha, const double* beta,
+                           const double* x0_rows /* [R][n_rows] */, void* x_buf0, void* x_buf1, double* q_sum,
+                           double* q_max);
+DCX_API int dcx_dist_pass(dcx_ctx* ctx);
+DCX_API int dcx_dist_control(dcx_ctx* ctx);
+/* synchronises the stream, drains the history; *live = 0 once every replica stopped */
+DCX_API int dcx_dist_poll(dcx_ctx* ctx, int32_t* live, int64_t* passes);
+/* ends the run (pending best-spin copies, device time); results as for dcx_solve_* with n = n_rows */
+DCX_API int dcx_dist_finish(dcx_ctx* ctx);
 
 #ifdef __cplusplus
 }

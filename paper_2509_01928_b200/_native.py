@@ -35,8 +35,11 @@ EXPORTS = (
     "dcx_abi_version", "dcx_last_error", "dcx_create", "dcx_destroy", "dcx_set_csr", "dcx_set_dense",
     "dcx_coupling", "dcx_matvec", "dcx_apply", "dcx_energy", "dcx_solve_begin", "dcx_solve_step",
     "dcx_solve_run", "dcx_result_summary", "dcx_result_summaries", "dcx_result_history",
-    "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states", "dcx_result_device_seconds", "dcx_profile_kernel",
+    "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states",
+    "dcx_result_device_seconds", "dcx_profile_kernel", "dcx_set_csr_block", "dcx_stream", "dcx_dist_begin",
+    "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish",
 )
+QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
 
 class Params(C.Structure):
@@ -106,6 +109,13 @@ def load(path: Path | str | None = None):
         "dcx_result_states": (C.c_int, [_P, C.c_int32, _PD]),
         "dcx_result_device_seconds": (C.c_int, [_P, _PD]),
         "dcx_profile_kernel": (C.c_int, [_P, C.c_int32, _PD, _PI32]),
+        "dcx_set_csr_block": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _PI64, _PI64, _PD]),
+        "dcx_stream": (C.c_int, [_P, C.POINTER(_P)]),
+        "dcx_dist_begin": (C.c_int, [_P, C.POINTER(Params), C.c_int32, _PD, _PD, _PD, _P, _P, _P, _P]),
+        "dcx_dist_pass": (C.c_int, [_P]),
+        "dcx_dist_control": (C.c_int, [_P]),
+        "dcx_dist_poll": (C.c_int, [_P, _PI32, _PI64]),
+        "dcx_dist_finish": (C.c_int, [_P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -277,3 +287,42 @@ class Context:
         out = C.c_double()
         check(self.lib.dcx_result_device_seconds(self.h, C.byref(out)), self.h)
         return out.value
+
+    # ------------------------------------------------- row-partitioned runs
+    def set_csr_block(self, n_rows, n_cols, row_base, values, col_indices, row_offsets):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        c = np.ascontiguousarray(col_indices, dtype=np.int64)
+        r = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        check(self.lib.dcx_set_csr_block(self.h, int(n_rows), int(n_cols), int(row_base), int(len(v)),
+                                         ptr(r, C.c_int64), ptr(c, C.c_int64), ptr(v, C.c_double)), self.h)
+        self.n = int(n_rows)
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(self.lib.dcx_stream(self.h, C.byref(s)), self.h)
+        return int(s.value or 0)
+
+    def dist_begin(self, prm: Params, alpha, beta, X0_rows, xbuf0: int, xbuf1: int, qsum: int, qmax: int):
+        X0 = np.ascontiguousarray(np.atleast_2d(X0_rows), dtype=np.float64)
+        R = X0.shape[0]
+        a = np.ascontiguousarray(np.broadcast_to(np.asarray(alpha, np.float64), (R,)))
+        b = np.ascontiguousarray(np.broadcast_to(np.asarray(beta, np.float64), (R,)))
+        self._R = R
+        check(self.lib.dcx_dist_begin(self.h, C.byref(prm), R, ptr(a, C.c_double), ptr(b, C.c_double),
+                                      ptr(X0, C.c_double), C.c_void_p(xbuf0), C.c_void_p(xbuf1),
+                                      C.c_void_p(qsum), C.c_void_p(qmax)), self.h)
+
+    def dist_pass(self):
+        check(self.lib.dcx_dist_pass(self.h), self.h)
+
+    def dist_control(self):
+        check(self.lib.dcx_dist_control(self.h), self.h)
+
+    def dist_poll(self):
+        live = C.c_int32(0)
+        p = C.c_int64(0)
+        check(self.lib.dcx_dist_poll(self.h, C.byref(live), C.byref(p)), self.h)
+        return bool(live.value), int(p.value)
+
+    def dist_finish(self):
+        check(self.lib.dcx_dist_finish(self.h), self.h)

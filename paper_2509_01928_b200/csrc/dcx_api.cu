@@ -69,6 +69,7 @@ struct dcx_ctx {
   bool have = false, dense = false, csr_ready = false;
   std::vector<double> dense_host;  // dense couplings: host copy for the lazily built CSR form
   int64_t n = 0, nnz = 0;
+  int64_t n_cols = 0, row_base = 0;  // row block of a row-partitioned coupling (n_cols == n, 0 otherwise)
   int vk_int = -1;  // VK_UNIFORM / VK_I8 / VK_I16, or -1 for real values
   double scale = 1.0;
   int V32 = 1;
@@ -87,6 +88,8 @@ struct dcx_ctx {
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double dev_seconds = 0.0;
+  bool dist = false;              // dcx_dist_begin run: external iterate buffers, caller's collectives
+  double *qs = nullptr, *qm = nullptr;
   std::vector<std::vector<HistRec>> hh;
   std::vector<RepCtl> hctl;
   HistRec* ring = nullptr;  // pinned host copy of the device history ring
@@ -373,7 +376,8 @@ void dcx_destroy(dcx_ctx* ctx) {
   delete ctx;
 }
 
-static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v);
+static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v,
+                      int64_t n_cols, int64_t row_base);
 
 int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
@@ -381,12 +385,26 @@ int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int
   c->csr_ready = false;
   c->dense_host.clear();
   c->dn.release();
-  return upload_csr(c, n, nnz, ro, ci, v);
+  return upload_csr(c, n, nnz, ro, ci, v, n, 0);
 }
 
-static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v) {
+int dcx_set_csr_block(dcx_ctx* c, int64_t n_rows, int64_t n_cols, int64_t row_base, int64_t nnz,
+                      const int64_t* ro, const int64_t* ci, const double* v) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (n_rows < 1 || n_cols < n_rows || row_base < 0 || row_base + n_rows > n_cols)
+    return fail(c, DCX_E_INVALID, "row block outside the spin index space");
+  c->dense = false;
+  c->csr_ready = false;
+  c->dense_host.clear();
+  c->dn.release();
+  return upload_csr(c, n_rows, nnz, ro, ci, v, n_cols, row_base);
+}
+
+static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v,
+                      int64_t n_cols, int64_t row_base) {
   return guarded(c, [&] {
     if (n < 1) throw InvalidArg("n must be >= 1");
+    if (n_cols >= (int64_t(1) << 31)) throw InvalidArg("n >= 2^31 is not supported");
     if (nnz < 0 || (nnz > 0 && (!ci || !v)) || !ro) throw InvalidArg("null CSR array");
     if (nnz >= (int64_t(1) << 32) - 1) throw InvalidArg("nnz >= 2^32 is not supported");
     if (n >= (int64_t(1) << 31)) throw InvalidArg("n >= 2^31 is not supported");
@@ -398,7 +416,7 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     }
     std::vector<int32_t> c32(nnz);
     for (int64_t e = 0; e < nnz; ++e) {
-      if (ci[e] < 0 || ci[e] >= n) throw InvalidArg("column index out of range");
+      if (ci[e] < 0 || ci[e] >= n_cols) throw InvalidArg("column index out of range");
       c32[e] = int32_t(ci[e]);
     }
     int vk;
@@ -414,13 +432,15 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     }
     c->have = false;
     c->n = n;
+    c->n_cols = n_cols;
+    c->row_base = row_base;
     c->nnz = nnz;
     c->rp.alloc((n + 1) * 4);
     CK(cudaMemcpy(c->rp.p, rp32.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
     c->col.alloc(std::max<int64_t>(nnz, 1) * 4);
     if (nnz) CK(cudaMemcpy(c->col.p, c32.data(), nnz * 4, cudaMemcpyHostToDevice));
     c->col16.release();
-    if (n <= 65536 && nnz) {
+    if (n_cols <= 65536 && n == n_cols && nnz) {
       std::vector<uint16_t> c16(nnz);
       for (int64_t e = 0; e < nnz; ++e) c16[e] = uint16_t(c32[e]);
       c->col16.alloc(nnz * 2);
@@ -477,7 +497,7 @@ static int ensure_csr(dcx_ctx* c) {
   } catch (const std::bad_alloc&) {
     return fail(c, DCX_E_OOM, "host allocation failed");
   }
-  const int rc = upload_csr(c, n, (int64_t)ci.size(), ro.data(), ci.data(), vv.data());
+  const int rc = upload_csr(c, n, (int64_t)ci.size(), ro.data(), ci.data(), vv.data(), n, 0);
   if (rc == DCX_OK) c->csr_ready = true;
   return rc;
 }
@@ -492,6 +512,8 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
     c->csr_ready = false;
     c->dense_host.assign(A, A + n * n);
     c->n = n;
+    c->n_cols = n;
+    c->row_base = 0;
     c->nnz = n * (n - 1);  // upper bound until the CSR form is built
     dense_upload(c->dn, n, A, c->stream);
     c->dense = true;
@@ -561,11 +583,24 @@ static void build_graph(dcx_ctx* c) {
   cudaGraphDestroy(gr);
 }
 
-int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* alpha, const double* beta,
-                    const double* x0) {
-  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
-  return guarded(c, [&] {
+static void drain(dcx_ctx* c);
+
+// Shared by dcx_solve_begin and dcx_dist_begin (xe0 / xe1: the caller's iterate
+// buffers of a row-partitioned run, else NULL).
+static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double* alpha, const double* beta,
+                       const double* x0, void* xe0, void* xe1) {
+    const bool dist = xe0 != nullptr;
     require_coupling(c);
+    if (!dist && (c->row_base != 0 || c->n_cols != c->n))
+      throw InvalidArg("the coupling is a row block: use dcx_dist_begin");
+    if (dist) {
+      if (c->dense) throw InvalidArg("row-partitioned runs need a CSR row block");
+      if (P->precision == DCX_PREC_F16TC) throw InvalidArg("row-partitioned runs use precision f64 or f32");
+      if (P->path == DCX_PATH_PERSISTENT || P->path == DCX_PATH_DENSE_TC)
+        throw InvalidArg("row-partitioned runs use the multipass path");
+      if (P->solver == DCX_SOLVER_ADOCH && P->window_mode == DCX_WINDOW_EXACT)
+        throw InvalidArg("row-partitioned ADOCH supports window_mode 'economy'");
+    }
     if (!P || !alpha || !beta || !x0) throw InvalidArg("null argument");
     if (R < 1) throw InvalidArg("R must be >= 1");
     if (P->solver != DCX_SOLVER_DOCH && P->solver != DCX_SOLVER_ADOCH) throw InvalidArg("unknown solver");
@@ -588,7 +623,9 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
     const size_t tb = c->f64 ? 8 : 4;
     c->J = csr_view(c, c->f64);
     c->sp = plan_small(c->J, P->solver, P->window_mode, c->f64);
-    if (use_tc) c->path = DCX_PATH_DENSE_TC;
+    c->dist = dist;
+    if (dist) c->path = DCX_PATH_MULTIPASS;
+    else if (use_tc) c->path = DCX_PATH_DENSE_TC;
     else if (P->path == DCX_PATH_PERSISTENT) {
       if (!c->sp.fits) throw InvalidArg("instance too large for the persistent path");
       c->path = DCX_PATH_PERSISTENT;
@@ -606,8 +643,13 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
     if (c->chunk < 1) c->chunk = 1;
     // buffers
     const int64_t tot = n * R;
-    c->xb0.alloc(tot * tb);
-    c->xb1.alloc(tot * tb);
+    if (dist) {
+      c->xb0.release();
+      c->xb1.release();
+    } else {
+      c->xb0.alloc(tot * tb);
+      c->xb1.alloc(tot * tb);
+    }
     const bool ad = P->solver == DCX_SOLVER_ADOCH;
     if (ad) { c->ax0.alloc(tot * tb); c->ax1.alloc(tot * tb); } else { c->ax0.release(); c->ax1.release(); }
     if (ad && P->window_mode == DCX_WINDOW_EXACT) c->ay.alloc(tot * tb); else c->ay.release();
@@ -657,8 +699,15 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
     a.scale = c->J.scale;
     a.ctl = c->ctl.as<RepCtl>();
     a.g = c->g.as<GState>();
-    a.x[0] = c->xb0.p;
-    a.x[1] = c->xb1.p;
+    if (dist) {  // own rows start at row_base of the caller's [n_cols][R] buffers
+      a.gx[0] = xe0;
+      a.gx[1] = xe1;
+      a.x[0] = static_cast<char*>(xe0) + size_t(c->row_base) * R * tb;
+      a.x[1] = static_cast<char*>(xe1) + size_t(c->row_base) * R * tb;
+    } else {
+      a.x[0] = a.gx[0] = c->xb0.p;
+      a.x[1] = a.gx[1] = c->xb1.p;
+    }
     a.ax[0] = c->ax0.p;
     a.ax[1] = c->ax1.p;
     a.ay = c->ay.p;
@@ -688,15 +737,15 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
       DevBuf src;
       src.alloc(tot * 8);
       CK(cudaMemcpyAsync(src.p, x0, tot * 8, cudaMemcpyHostToDevice, c->stream));
-      if (c->f64) to_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), c->xb0.as<double>(), n, R);
-      else to_device_layout<float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), c->xb0.as<float>(), n, R);
-      CK(cudaMemsetAsync(c->xb1.p, 0, tot * tb, c->stream));
+      if (c->f64) to_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<double*>(a.x[0]), n, R);
+      else to_device_layout<float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<float*>(a.x[0]), n, R);
+      CK(cudaMemsetAsync(a.x[1], 0, tot * tb, c->stream));
       if (ad) {
         CK(cudaMemsetAsync(c->ax0.p, 0, tot * tb, c->stream));
         CK(cudaMemsetAsync(c->ax1.p, 0, tot * tb, c->stream));
       }
       CK(cudaMemsetAsync(c->best.p, 1, tot, c->stream));
-      if (c->states.p) CK(cudaMemcpyAsync(c->states.p, c->xb0.p, tot * tb, cudaMemcpyDeviceToDevice, c->stream));
+      if (c->states.p) CK(cudaMemcpyAsync(c->states.p, a.x[0], tot * tb, cudaMemcpyDeviceToDevice, c->stream));
       CK(cudaStreamSynchronize(c->stream));
     }
     std::vector<RepCtl> h(R);
@@ -732,12 +781,78 @@ int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* al
       c->ring_n = size_t(R) * cap;
     }
     c->p_host = 0;
-    if (c->path == DCX_PATH_MULTIPASS) build_graph(c);
+    if (c->path == DCX_PATH_MULTIPASS && !dist) build_graph(c);
     if (c->path == DCX_PATH_DENSE_TC) dense_begin(c->dn, c->mp, c->stream);
     CK(cudaEventRecord(c->ev0, c->stream));
     enqueue_start_clock(c->g.as<GState>(), c->stream);
     CK(cudaGetLastError());
     c->begun = true;
+}
+
+int dcx_solve_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* alpha, const double* beta,
+                    const double* x0) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] { begin_impl(c, P, R, alpha, beta, x0, nullptr, nullptr); });
+}
+
+int dcx_stream(dcx_ctx* c, void** stream) {
+  if (!c || !stream) return fail(c, DCX_E_INVALID, "null argument");
+  *stream = static_cast<void*>(c->stream);
+  return DCX_OK;
+}
+
+int dcx_dist_begin(dcx_ctx* c, const dcx_params* P, int32_t R, const double* alpha, const double* beta,
+                   const double* x0_rows, void* x_buf0, void* x_buf1, double* q_sum, double* q_max) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!x_buf0 || !x_buf1 || !q_sum || !q_max) return fail(c, DCX_E_INVALID, "null buffer");
+  return guarded(c, [&] {
+    begin_impl(c, P, R, alpha, beta, x0_rows, x_buf0, x_buf1);
+    c->qs = q_sum;
+    c->qm = q_max;
+  });
+}
+
+int dcx_dist_pass(dcx_ctx* c) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun || !c->dist || c->finished) throw InvalidArg("no row-partitioned run in progress");
+    enqueue_dist_pass(c->mp, c->qs, c->qm, c->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+int dcx_dist_control(dcx_ctx* c) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun || !c->dist || c->finished) throw InvalidArg("no row-partitioned run in progress");
+    enqueue_dist_control(c->mp, c->qs, c->qm, c->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+int dcx_dist_poll(dcx_ctx* c, int32_t* live, int64_t* passes) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun || !c->dist) throw InvalidArg("no row-partitioned run");
+    if (!c->finished) drain(c);
+    if (live) *live = (!c->finished && c->hg.live != 0 && c->hg.running > 0) ? 1 : 0;
+    if (passes) *passes = c->hg.p;
+  });
+}
+
+int dcx_dist_finish(dcx_ctx* c) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun || !c->dist) throw InvalidArg("no row-partitioned run");
+    if (c->finished) return;
+    CK(cudaEventRecord(c->ev1, c->stream));
+    enqueue_flush(c->mp, c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->dev_seconds = ms * 1e-3;
+    drain(c);
+    c->finished = true;
   });
 }
 
@@ -917,8 +1032,8 @@ int dcx_result_state(dcx_ctx* c, double* out) {
     const int64_t n = c->n, R = c->R, tot = n * R;
     const size_t tb = c->f64 ? 8 : 4;
     std::vector<unsigned char> b0(tot * tb), b1(tot * tb);
-    CK(cudaMemcpyAsync(b0.data(), c->xb0.p, tot * tb, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(b1.data(), c->xb1.p, tot * tb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b0.data(), c->mp.args.x[0], tot * tb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b1.data(), c->mp.args.x[1], tot * tb, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     for (int64_t r = 0; r < R; ++r) {
       const int k = std::max(0, c->hctl[r].k);

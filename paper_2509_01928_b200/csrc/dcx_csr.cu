@@ -98,9 +98,8 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
   const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // global warp
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   constexpr int RPW = 32 / V;  // rows per warp step
-  const T* xg = reinterpret_cast<const T*>(MODE == MODE_ADOCH_Y ? nullptr : a.x[p & 1]);
-  const T* xc = reinterpret_cast<const T*>(a.x[p & 1]);
-  const T* xp = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
+  const T* xc = reinterpret_cast<const T*>(a.gx[p & 1]);  // gather source (all spins)
+  const T* xp = reinterpret_cast<const T*>(a.gx[(p + 1) & 1]);
   const T cm = T(c.cm[p & 1]);
   const T scale = T(a.scale);
   RowOut<T, MODE> o;
@@ -116,7 +115,7 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
         const int j = __ldg(a.col + e);
         T xj;
         if constexpr (MODE == MODE_ADOCH_Y) xj = extrap(xc[j], xp[j], cm);
-        else xj = xg[j];
+        else xj = xc[j];
         int q;
         const T v = load_entry<VK, true, T>(a.val, e, scale, q);
         acc = madd(acc, v, xj);
@@ -282,8 +281,8 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
   const int64_t S = int64_t(gridDim.x) * 8;
   int64_t i = int64_t(blockIdx.x) * 8 + warp;
   const uint32_t rowb = uint32_t(R) * uint32_t(sizeof(T));  // bytes per spin row of x
-  const char* xcb = reinterpret_cast<const char*>(xc + r0);
-  const char* xpb = reinterpret_cast<const char*>(xp + r0);
+  const char* xcb = reinterpret_cast<const char*>(reinterpret_cast<const T*>(a.gx[p & 1]) + r0);  // gathers
+  const char* xpb = reinterpret_cast<const char*>(reinterpret_cast<const T*>(a.gx[(p + 1) & 1]) + r0);
   // stage s of this warp, edge e, this lane: stage_mem + ((s*8 + warp)*G + e)*32*CB + lane*CB
   const uint32_t st_base = smem_u32(stage_mem) + uint32_t((warp * G * 32 + lane) * CB);
   constexpr uint32_t ST_STRIDE = 8u * G * 32 * CB;  // between stages
@@ -606,8 +605,12 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
 // (deterministic for a fixed launch shape), then thread 0 runs the control.
 // phase: 0 = DOCH pass, 1 = ADOCH bookkeeping (+decision if economy),
 //        2 = ADOCH exact decision only.
+// dist: 0 = single context; 1 = reduce only, totals to qs (sums) / qm (maxima and
+// elapsed time) for the caller's all-reduce; 2 = control only, from the reduced
+// qs / qm (every rank then takes identical decisions, including the time budget:
+// the elapsed time is the maximum over ranks).
 __global__ void __launch_bounds__(256) reduce_control(PassArgs a, const double* spart, int sslots, int phase,
-                                                      int last_kernel) {
+                                                      int last_kernel, int dist, double* qs, double* qm) {
   if (!a.g->live) return;
   const int p = a.g->p;
   const int r = blockIdx.x;
@@ -616,7 +619,32 @@ __global__ void __launch_bounds__(256) reduce_control(PassArgs a, const double* 
   __shared__ double tot[NQ + 1];
   RepCtl* cp = a.ctl + r;
   const bool running = cp->status == DCX_STOP_RUNNING;
-  if (running) {
+  if (running && dist == 2) {
+    if (threadIdx.x == 0) {
+      const double* s = qs + (int64_t)r * DCX_QSUM;
+      const double* m = qm + (int64_t)r * DCX_QMAX;
+      tot[Q_S4] = s[0];
+      tot[Q_SXAX] = s[1];
+      tot[Q_ES] = s[2];
+      tot[Q_SY4] = s[3];
+      tot[Q_SYAY] = s[4];
+      tot[Q_STEP] = m[0];
+      tot[NQ] = m[1];
+      RepCtl c = *cp;
+      const double now = m[2];
+      bool stopped = false;
+      if (phase == 0) {
+        stopped = control_after_pass(c, a.cfg, r, tot, p, now);
+        c.step = tot[Q_STEP];
+      } else {
+        if (p > 0) c.step = tot[NQ];
+        stopped = control_after_pass(c, a.cfg, r, tot, p, now);
+        if (!stopped && a.cfg.window_mode == DCX_WINDOW_ECONOMY) adoch_decide(c, a.cfg, r, tot, p);
+      }
+      *cp = c;
+      if (stopped) atomicSub(&a.g->running, 1);
+    }
+  } else if (running) {
     for (int q = 0; q < NQ; ++q) {
       double acc = 0.0;
       const bool ismax = q == Q_STEP;
@@ -645,7 +673,18 @@ __global__ void __launch_bounds__(256) reduce_control(PassArgs a, const double* 
       if (threadIdx.x < w) sred[threadIdx.x] = fmax(sred[threadIdx.x], sred[threadIdx.x + w]);
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && dist == 1) {
+      double* s = qs + (int64_t)r * DCX_QSUM;
+      double* m = qm + (int64_t)r * DCX_QMAX;
+      s[0] = red[Q_S4][0];
+      s[1] = red[Q_SXAX][0];
+      s[2] = red[Q_ES][0];
+      s[3] = red[Q_SY4][0];
+      s[4] = red[Q_SYAY][0];
+      m[0] = red[Q_STEP][0];
+      m[1] = sred[0];
+      m[2] = double(globaltimer() - a.g->t0) * 1e-9;
+    } else if (threadIdx.x == 0) {
       for (int q = 0; q < NQ; ++q) tot[q] = red[q][0];
       tot[NQ] = sred[0];
       RepCtl c = *cp;
@@ -851,19 +890,42 @@ void enqueue_iteration(const MultiPass& m, cudaStream_t s) {
   if (m.solver == DCX_SOLVER_DOCH) {
     if (f64) launch_pass_t<double>(MODE_DOCH, a, m.vk, m.V, m.grid, s);
     else launch_pass_t<float>(MODE_DOCH, a, m.vk, m.V, m.grid, s);
-    reduce_control<<<a.cfg.R, 256, 0, s>>>(a, nullptr, 0, 0, 1);
+    reduce_control<<<a.cfg.R, 256, 0, s>>>(a, nullptr, 0, 0, 1, 0, nullptr, nullptr);
     return;
   }
   if (f64) launch_pass_t<double>(MODE_ADOCH_X, a, m.vk, m.V, m.grid, s);
   else launch_pass_t<float>(MODE_ADOCH_X, a, m.vk, m.V, m.grid, s);
-  reduce_control<<<a.cfg.R, 256, 0, s>>>(a, m.spart, sslots, 1, 0);
+  reduce_control<<<a.cfg.R, 256, 0, s>>>(a, m.spart, sslots, 1, 0, 0, nullptr, nullptr);
   if (a.cfg.window_mode == DCX_WINDOW_EXACT) {
     if (f64) launch_pass_t<double>(MODE_ADOCH_Y, a, m.vk, m.V, m.grid, s);
     else launch_pass_t<float>(MODE_ADOCH_Y, a, m.vk, m.V, m.grid, s);
-    reduce_control<<<a.cfg.R, 256, 0, s>>>(a, nullptr, 0, 2, 0);
+    reduce_control<<<a.cfg.R, 256, 0, s>>>(a, nullptr, 0, 2, 0, 0, nullptr, nullptr);
   }
   if (f64) adoch_finalize<double><<<m.fgrid, 256, 0, s>>>(a, m.spart, sslots);
   else adoch_finalize<float><<<m.fgrid, 256, 0, s>>>(a, m.spart, sslots);
+  advance_pass<<<1, 1, 0, s>>>(a.g);
+}
+
+void enqueue_dist_pass(const MultiPass& m, double* qs, double* qm, cudaStream_t s) {
+  const PassArgs& a = m.args;
+  const bool doch = m.solver == DCX_SOLVER_DOCH;
+  const int mode = doch ? MODE_DOCH : MODE_ADOCH_X;
+  if (m.f64) launch_pass_t<double>(mode, a, m.vk, m.V, m.grid, s);
+  else launch_pass_t<float>(mode, a, m.vk, m.V, m.grid, s);
+  reduce_control<<<a.cfg.R, 256, 0, s>>>(a, doch ? nullptr : m.spart, doch ? 0 : m.sslots, doch ? 0 : 1, 0, 1, qs, qm);
+}
+
+void enqueue_dist_control(const MultiPass& m, const double* qs, const double* qm, cudaStream_t s) {
+  const PassArgs& a = m.args;
+  double* q0 = const_cast<double*>(qs);
+  double* q1 = const_cast<double*>(qm);
+  if (m.solver == DCX_SOLVER_DOCH) {
+    reduce_control<<<a.cfg.R, 256, 0, s>>>(a, nullptr, 0, 0, 1, 2, q0, q1);
+    return;
+  }
+  reduce_control<<<a.cfg.R, 256, 0, s>>>(a, nullptr, 0, 1, 0, 2, q0, q1);
+  if (m.f64) adoch_finalize<double><<<m.fgrid, 256, 0, s>>>(a, m.spart, m.sslots);
+  else adoch_finalize<float><<<m.fgrid, 256, 0, s>>>(a, m.spart, m.sslots);
   advance_pass<<<1, 1, 0, s>>>(a.g);
 }
 

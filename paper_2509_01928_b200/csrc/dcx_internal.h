@@ -27,7 +27,8 @@ struct PassArgs {
   double scale;
   RepCtl* ctl;
   GState* g;
-  void* x[2];      // iterate buffers by pass parity, layout [n][R]
+  void* x[2];      // iterate buffers by pass parity, layout [n][R], at this context's own rows
+  void* gx[2];     // the same buffers at spin 0: the gather source (== x unless row-partitioned)
   void* ax[2];     // ADOCH (J+aI)x_p by parity
   void* ay;        // ADOCH exact (J+aI)y
   int8_t* best;    // best spins [n][R]
@@ -47,6 +48,10 @@ struct MultiPass {
 
 // dcx_csr.cu
 void enqueue_iteration(const MultiPass& m, cudaStream_t s);
+// row-partitioned (multi-GPU) iteration, split around the caller's all-reduce of
+// the per-replica partials: pass + per-rank reduction into qs/qm, then control
+void enqueue_dist_pass(const MultiPass& m, double* qs, double* qm, cudaStream_t s);
+void enqueue_dist_control(const MultiPass& m, const double* qs, const double* qm, cudaStream_t s);
 void enqueue_flush(const MultiPass& m, cudaStream_t s);
 void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
 void enqueue_start_clock(GState* g, cudaStream_t s);

@@ -1,0 +1,238 @@
+"""Row-partitioned DOCH / ADOCH across ranks.
+
+The reference has no distributed solver: one ``doch_solve`` / ``adoch_solve``
+(dc/solvers/doch.py:169-356) runs one scipy ``csr_matvec`` per iteration
+(dc/coupling.py:189-190) in one process. Here the coupling rows are split into
+contiguous, nnz-balanced blocks, one per rank (one process per GPU, NCCL over
+NVLink). Per iteration every rank
+
+  1. runs the fused pass over its rows (``dcx_dist_pass``): (J+aI)x, the cube-root
+     update of its slice of x, and its share of the per-replica sums
+     (sum x^4, sum x.Ax, sum s.Js, max |dx|),
+  2. all-reduces those sums (SUM) and maxima (MAX) -- 8 doubles per replica,
+  3. runs the control on the reduced values (``dcx_dist_control``): identical on
+     every rank, so stop / record / ADOCH-accept decisions agree,
+  4. all-gathers the new x slices (in place) for the next pass.
+
+Blocks are padded to a common row count B so the all-gather is a plain
+``all_gather_into_tensor``; columns are remapped into that padded index space
+(rank q's rows live at [q*B, q*B + rows_q)). The remap is monotone, so each
+row's sum order -- and therefore every iterate -- is bit-identical to the
+single-GPU multipass path; only the order of the H partial sums across blocks
+differs.
+
+With the NCCL backend the collectives run on the context stream directly on
+device buffers; with gloo (CPU transport) they are staged through host memory.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native
+from .solvers import CONVERGENCE_TOL, DESCENT_WARN_TOL, SOLVER_NAMES, assemble_results
+
+
+# ---------------------------------------------------------------- partitioning
+def partition_rows(row_offsets, world: int) -> list:
+    """Contiguous row blocks [(row0, row1)] balancing nnz + rows per block.
+
+    Every block is non-empty when n >= world (a rank with no rows would still
+    take part in every collective, which is allowed but pointless).
+    """
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    n = len(ro) - 1
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if n < world:
+        raise ValueError(f"cannot split {n} rows over {world} ranks")
+    cost = ro + np.arange(n + 1)  # cumulative nnz + rows
+    total = cost[-1]
+    cuts = [0]
+    for q in range(1, world):
+        c = int(np.searchsorted(cost, total * q / world, side="left"))
+        c = min(max(c, cuts[-1] + 1), n - (world - q))  # at least one row per block
+        cuts.append(c)
+    cuts.append(n)
+    return [(cuts[q], cuts[q + 1]) for q in range(world)]
+
+
+@dataclass
+class RowBlocks:
+    """Blocks of a row partition and the padded exchange index space."""
+
+    blocks: list
+    n: int
+
+    @property
+    def world(self) -> int:
+        return len(self.blocks)
+
+    @property
+    def B(self) -> int:
+        return max(r1 - r0 for r0, r1 in self.blocks)
+
+    @property
+    def n_space(self) -> int:
+        return self.world * self.B
+
+    def position(self, j):
+        """Index of spin j in the padded space."""
+        j = np.asarray(j, dtype=np.int64)
+        starts = np.array([r0 for r0, _ in self.blocks], dtype=np.int64)
+        q = np.searchsorted(starts, j, side="right") - 1
+        return q * self.B + (j - starts[q])
+
+    def unpad(self, arr):
+        """[..., n_space] -> [..., n] (drops the padding rows)."""
+        parts = [arr[..., q * self.B: q * self.B + (r1 - r0)] for q, (r0, r1) in enumerate(self.blocks)]
+        return np.concatenate(parts, axis=-1)
+
+
+def local_block(J, rb: RowBlocks, rank: int):
+    """This rank's CSR rows with columns mapped into the padded space."""
+    r0, r1 = rb.blocks[rank]
+    ro = np.asarray(J.row_offsets, dtype=np.int64)
+    lo, hi = int(ro[r0]), int(ro[r1])
+    cols = rb.position(np.asarray(J.col_indices[lo:hi], dtype=np.int64))
+    vals = np.asarray(J.values[lo:hi], dtype=np.float64)
+    return r1 - r0, vals, cols, ro[r0:r1 + 1] - lo
+
+
+# ------------------------------------------------------------------ exchange
+class Exchange:
+    """The three collectives of one iteration on torch.distributed.
+
+    NCCL: in place on the device tensors (issued on the current stream, which
+    the driver sets to the context stream). gloo: staged through host memory.
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.host_staged = dist.get_backend(group) != "nccl"
+
+    def all_gather_rows(self, X, B: int):
+        """X: [world*B, R] tensor whose rows [rank*B, (rank+1)*B) are this rank's."""
+        dist = self.dist
+        mine = X[self.rank * B:(self.rank + 1) * B]
+        if not self.host_staged:
+            dist.all_gather_into_tensor(X, mine, group=self.group)
+            return
+        import torch
+
+        h = mine.cpu()
+        parts = [torch.empty_like(h) for _ in range(self.world)]
+        dist.all_gather(parts, h, group=self.group)
+        X.copy_(torch.cat(parts, 0))
+
+    def all_reduce(self, t, op: str):
+        dist = self.dist
+        rop = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX}[op]
+        if not self.host_staged:
+            dist.all_reduce(t, op=rop, group=self.group)
+            return
+        h = t.cpu()
+        dist.all_reduce(h, op=rop, group=self.group)
+        t.copy_(h)
+
+
+# -------------------------------------------------------------------- driver
+def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max_iters: int = 1000,
+                      lookback_q: int = 5, window_mode: str = "economy", trace_stride: int = 1,
+                      time_budget: Optional[float] = None, precision: str = "f32",
+                      seeds: Optional[Sequence[int]] = None, poll_every: int = 16,
+                      device: Optional[int] = None, _context=None) -> list:
+    """Row-partitioned ``solve_replicas``: the same R replicas, the coupling split by rows over the ranks
+    of ``group`` (every rank passes the same instance and the same full ``x0`` [R][n]).
+
+    Returns one SolveResult per replica on every rank (best spins and final x gathered to all ranks).
+    ``_context`` replaces the libdcx context (tests only).
+    """
+    import torch
+
+    if solver not in SOLVER_NAMES:
+        raise ValueError(f"unknown solver {solver!r}")
+    if window_mode != "economy":
+        raise ValueError("the row-partitioned solver supports window_mode 'economy'")
+    if precision not in ("f64", "f32"):
+        raise ValueError("the row-partitioned solver runs in precision 'f64' or 'f32'")
+    t_entry = time.perf_counter()
+    ex = Exchange(group)
+    J = instance.coupling
+    if not all(hasattr(J, a) for a in ("values", "col_indices", "row_offsets")):
+        raise ValueError("the row-partitioned solver needs a CSR coupling")
+    X0 = np.atleast_2d(np.asarray(x0, dtype=np.float64))
+    R, n = X0.shape
+    if n != J.n:
+        raise ValueError(f"x0 has {n} columns, expected {J.n}")
+    rb = RowBlocks(partition_rows(J.row_offsets, ex.world), J.n)
+    r0, r1 = rb.blocks[ex.rank]
+    n_rows, vals, cols, ro = local_block(J, rb, ex.rank)
+    if _context is None:
+        dev = _native.default_device() if device is None else int(device)
+        ctx = _native.Context(dev)
+        tdev = torch.device("cuda", dev)
+    else:
+        ctx, tdev = _context, torch.device("cpu")
+    ctx.set_csr_block(n_rows, rb.n_space, ex.rank * rb.B, vals, cols, ro)
+    dt = torch.float64 if precision == "f64" else torch.float32
+    X = [torch.zeros(rb.n_space, R, dtype=dt, device=tdev) for _ in range(2)]
+    qs = torch.zeros(R, _native.QSUM, dtype=torch.float64, device=tdev)
+    qm = torch.zeros(R, _native.QMAX, dtype=torch.float64, device=tdev)
+    prm = _native.Params(
+        solver=_native.SOLVER[solver], window_mode=_native.WINDOW[window_mode],
+        precision=_native.PRECISION[precision], lookback_q=int(lookback_q), max_iters=int(max_iters),
+        trace_stride=int(trace_stride), time_budget_s=-1.0 if time_budget is None else float(time_budget),
+        conv_tol=CONVERGENCE_TOL, descent_tol=DESCENT_WARN_TOL, record_states=0,
+        path=_native.PATH["multipass"], chunk=0, reserved=0)
+    stream = (torch.cuda.ExternalStream(ctx.stream(), device=tdev) if tdev.type == "cuda" else None)
+    with (torch.cuda.stream(stream) if stream is not None else _nullcontext()):
+        ctx.dist_begin(prm, alpha, beta, X0[:, r0:r1], X[0].data_ptr(), X[1].data_ptr(), qs.data_ptr(),
+                       qm.data_ptr())
+        offset = time.perf_counter() - t_entry
+        ex.all_gather_rows(X[0], rb.B)
+        p, live = 0, True
+        while live:
+            for _ in range(max(1, int(poll_every))):
+                ctx.dist_pass()
+                ex.all_reduce(qs, "sum")
+                ex.all_reduce(qm, "max")
+                ctx.dist_control()
+                p += 1
+                ex.all_gather_rows(X[p & 1], rb.B)
+            live, _ = ctx.dist_poll()
+        ctx.dist_finish()
+        # gather best spins and final states of every row block (padded space)
+        pad = np.zeros((R, rb.B))
+        pad[:, :n_rows] = ctx.best_spins().astype(np.float64)
+        best_t = torch.from_numpy(pad.T.copy()).to(tdev)
+        full_b = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
+        full_b[ex.rank * rb.B:(ex.rank + 1) * rb.B] = best_t
+        ex.all_gather_rows(full_b, rb.B)
+        pad[:, :n_rows] = ctx.state()
+        full_x = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
+        full_x[ex.rank * rb.B:(ex.rank + 1) * rb.B] = torch.from_numpy(pad.T.copy()).to(tdev)
+        ex.all_gather_rows(full_x, rb.B)
+        if stream is not None:
+            stream.synchronize()
+    best = rb.unpad(full_b.cpu().numpy().T)
+    xs = rb.unpad(full_x.cpu().numpy().T)
+    return assemble_results(ctx, solver, R, best, xs, offset, getattr(instance, "cut_offset", None), seeds,
+                            path="row-partitioned")
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False

@@ -228,8 +228,15 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
         ctx.run()
     best = ctx.best_spins().astype(np.float64)
     xs = ctx.state()
-    dev_s = ctx.device_seconds()
     path_used = _native.PATH_NAME.get(int(ctx.summary(0).path_used))
+    return assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path_used, record_states)
+
+
+def assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path=None, record_states=False):
+    """SolveResults of a finished run from the context's summaries and history
+    (shared by solve_replicas and the row-partitioned driver)."""
+    dev_s = ctx.device_seconds()
+    path_used = path
     # bulk download of every replica's history, then per-replica views (no per-replica FFI calls)
     iters, stops, bests, nh, warn = ctx.summaries()
     K = int(nh.max()) if R else 0
@@ -245,7 +252,7 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
         if warn[r] >= 0 and solver == "doch":
             k = int(warn[r])
             warnings.warn(f"Hamiltonian increased by {h[k] - h[k - 1]:.3e} at iteration {k}",
-                          RuntimeWarning, stacklevel=3)
+                          RuntimeWarning, stacklevel=4)
         accepted = None
         if solver == "adoch":
             accepted = ([True] + ((ev[2:it + 1] & _native.EV_ACCEPTED) != 0).tolist()) if it else []
