@@ -157,6 +157,13 @@ DCX_API int dcx_result_states(dcx_ctx* ctx, int32_t r, double* out /* [(iteratio
  * dcx_solve_begin, launches it `launches` times on the context stream between
  * two CUDA events and returns the mean duration. Consumes the run. */
 DCX_API int dcx_profile_kernel(dcx_ctx* ctx, int32_t launches, double* ms_per_launch, int32_t* kernel_id);
+/* Power iteration of dc/spectral.py:60-111 (_power_core) on M = shift*I - J
+ * (use_shift != 0) or M = -J, entirely on the device (one cooperative kernel;
+ * per iteration one product and fixed-order grid reductions). `restart` is the
+ * normalised seeded restart vector (n entries) the reference would draw.
+ * Outputs (|lambda|, Rayleigh quotient, iterations, converged) as _power_core. */
+DCX_API int dcx_power(dcx_ctx* ctx, int32_t use_shift, double shift, double tol, int64_t max_iters,
+                      const double* restart, double* mag, double* rayleigh, int64_t* iterations, int32_t* converged);
 /* device time of the last dcx_solve_run/step sequence, seconds */
 DCX_API int dcx_result_device_seconds(dcx_ctx* ctx, double* out);
 

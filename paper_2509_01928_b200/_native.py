@@ -37,7 +37,7 @@ EXPORTS = (
     "dcx_solve_run", "dcx_result_summary", "dcx_result_summaries", "dcx_result_history",
     "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states",
     "dcx_result_device_seconds", "dcx_profile_kernel", "dcx_set_csr_block", "dcx_stream", "dcx_dist_begin",
-    "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish",
+    "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish", "dcx_power",
 )
 QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
@@ -116,6 +116,7 @@ def load(path: Path | str | None = None):
         "dcx_dist_control": (C.c_int, [_P]),
         "dcx_dist_poll": (C.c_int, [_P, _PI32, _PI64]),
         "dcx_dist_finish": (C.c_int, [_P]),
+        "dcx_power": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_int64, _PD, _PD, _PD, _PI64, _PI32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -287,6 +288,14 @@ class Context:
         out = C.c_double()
         check(self.lib.dcx_result_device_seconds(self.h, C.byref(out)), self.h)
         return out.value
+
+    def power(self, use_shift: bool, shift: float, tol: float, max_iters: int, restart: np.ndarray):
+        r = np.ascontiguousarray(restart, dtype=np.float64)
+        mag, ray = C.c_double(), C.c_double()
+        it, conv = C.c_int64(), C.c_int32()
+        check(self.lib.dcx_power(self.h, int(bool(use_shift)), float(shift), float(tol), int(max_iters),
+                                 ptr(r, C.c_double), C.byref(mag), C.byref(ray), C.byref(it), C.byref(conv)), self.h)
+        return mag.value, ray.value, int(it.value), bool(conv.value)
 
     # ------------------------------------------------- row-partitioned runs
     def set_csr_block(self, n_rows, n_cols, row_base, values, col_indices, row_offsets):

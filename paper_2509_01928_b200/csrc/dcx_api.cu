@@ -1101,6 +1101,44 @@ int dcx_profile_kernel(dcx_ctx* c, int32_t launches, double* ms_per_launch, int3
   });
 }
 
+int dcx_power(dcx_ctx* c, int32_t use_shift, double shift, double tol, int64_t max_iters, const double* restart,
+              double* mag, double* rayleigh, int64_t* iterations, int32_t* converged) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    require_coupling(c);
+    if (c->row_base != 0 || c->n_cols != c->n) throw InvalidArg("power iteration needs the whole coupling");
+    if (!restart || max_iters < 0) throw InvalidArg("bad power-iteration arguments");
+    if (ensure_csr(c) != DCX_OK) throw CudaError(c->err);
+    const CsrDev J = csr_view(c, true);
+    const int64_t n = c->n;
+    int dev = 0, blocks_per_sm = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    blocks_per_sm = 1;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * blocks_per_sm, (n + 7) / 8));
+    DevBuf v, w, rs, part, part2, bar, out;
+    v.alloc(n * 8);
+    w.alloc(n * 8);
+    rs.alloc(n * 8);
+    part.alloc(size_t(grid) * 16);
+    part2.alloc(size_t(grid) * 8);
+    bar.alloc(8);
+    out.alloc(32);
+    CK(cudaMemcpyAsync(rs.p, restart, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(bar.p, 0, 8, c->stream));
+    launch_power(J, use_shift, shift, tol, max_iters, v.as<double>(), w.as<double>(), rs.as<double>(),
+                 part.as<double>(), part2.as<double>(), bar.as<unsigned>(), out.as<double>(), grid, c->stream);
+    CK(cudaGetLastError());
+    double h[4];
+    CK(cudaMemcpyAsync(h, out.p, 32, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (mag) *mag = h[0];
+    if (rayleigh) *rayleigh = h[1];
+    if (iterations) *iterations = int64_t(h[2]);
+    if (converged) *converged = int32_t(h[3]);
+  });
+}
+
 int dcx_result_device_seconds(dcx_ctx* c, double* out) {
   if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
   *out = c->dev_seconds;

@@ -56,6 +56,10 @@ void enqueue_flush(const MultiPass& m, cudaStream_t s);
 void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
 void enqueue_start_clock(GState* g, cudaStream_t s);
 int replica_vector_width(int R, bool f64);
+// dcx_power.cu
+void launch_power(const CsrDev& J, int use_shift, double shift, double tol, int64_t max_iters, double* v, double* w,
+                  const double* restart, double* part, double* part2, unsigned* bar, double* out, int grid,
+                  cudaStream_t s);
 template <typename T>
 void launch_csr_apply(const CsrDev& J, const T* v, int R, T* jv, double* es_rows, cudaStream_t s);
 

@@ -2,8 +2,8 @@
 
 ``derive_params`` follows dc/spectral.py:224-256: alpha = eta * lambda_max(-J)
 (two-stage shifted power iteration below n = 1e4, Wigner estimate at or
-above), beta = n sqrt(n) (alpha + max_i sum_j |J_ij|). Every power-iteration
-product runs on the device (``dcx_matvec``). ``tune_eta`` runs all eta
+above), beta = n sqrt(n) (alpha + max_i sum_j |J_ij|). The power iteration runs
+entirely on the device (``dcx_power``: one cooperative kernel per stage). ``tune_eta`` runs all eta
 candidates as one batch of replicas (one launch sequence instead of one solve
 per candidate, dc/spectral.py:259-298).
 """
@@ -45,43 +45,6 @@ class SolverParams:
             raise ValueError("lookback_q must be >= 1")
 
 
-def _power(apply_m, n, tol, max_iters, seed=0):
-    """Power iteration with one seeded restart; products on the device."""
-    v = np.full(n, 1.0 / np.sqrt(n))
-    restarted, best_res, stall = False, np.inf, 0
-    mag = ray = 0.0
-    k = 0
-
-    def fresh():
-        r = np.random.default_rng(seed).standard_normal(n)
-        return r / np.linalg.norm(r)
-
-    while k < max_iters:
-        w = apply_m(v)
-        mag = float(np.linalg.norm(w))
-        if mag == 0.0:
-            if restarted:
-                return 0.0, 0.0, k, False
-            v, restarted = fresh(), True
-            k += 1
-            continue
-        ray = float(v @ w)
-        res = float(np.linalg.norm(w - ray * v)) / mag
-        if res <= tol:
-            return mag, ray, k + 1, True
-        if res < 0.999 * best_res:
-            best_res, stall = res, 0
-        else:
-            stall += 1
-            if stall > 50 and not restarted:
-                v, restarted, stall = fresh(), True, 0
-                k += 1
-                continue
-        v = w / mag
-        k += 1
-    return mag, ray, k, False
-
-
 def _moments(J):
     if hasattr(J, "array"):
         a = np.asarray(J.array)
@@ -115,11 +78,13 @@ def estimate_lambda_max_neg(J, method="auto", tol=1e-10, max_iters=20_000) -> fl
         if est > 0:
             return est
     ctx = device_context(J)
-    mv = lambda v: ctx.matvec(v[None, :])[0]  # noqa: E731
-    rho = _power(lambda v: -mv(v), J.n, tol, max_iters)[0]
+    # the reference's seeded restart vector (dc/spectral.py:84-86), drawn once on the host
+    r = np.random.default_rng(0).standard_normal(J.n)
+    r /= np.linalg.norm(r)
+    rho = ctx.power(False, 0.0, tol, max_iters, r)[0]  # whole loop on the device (dcx_power)
     if rho == 0.0:
         raise ValueError("coupling matrix must have at least one nonzero entry")
-    dom, _, _, ok = _power(lambda v: rho * v - mv(v), J.n, tol, max_iters)
+    dom, _, _, ok = ctx.power(True, rho, tol, max_iters, r)
     if not ok:
         warnings.warn("shifted power iteration did not converge; using best estimate", RuntimeWarning)
     return dom - rho

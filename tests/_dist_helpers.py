@@ -214,6 +214,8 @@ def gpu_worker(rank, world, init_file, out_file, solver, precision, R, max_iters
         np.savez(out_file, x=np.stack([r.x for r in res]), spins=np.stack([r.spins for r in res]),
                  energy=np.array([r.energy for r in res]), iterations=np.array([r.iterations for r in res]),
                  stop=np.array([r.stop_reason for r in res]),
-                 h=np.stack([np.asarray(r.h_values)[: r.iterations + 1][:2] for r in res]))
+                 h=np.stack([np.asarray(r.h_values)[: r.iterations + 1][:2] for r in res]),
+                 accepted=np.array([(r.accepted or []) + [False] * (max_iters + 1 - len(r.accepted or []))
+                                    for r in res], dtype=bool))
     dist.barrier()
     dist.destroy_process_group()
