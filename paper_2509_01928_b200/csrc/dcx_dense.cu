@@ -87,7 +87,7 @@ struct Args {
   int n, npad, R, Rpad, tiles_n, p_end;
   float jscale;
   int nodata;  // DCX_DENSE_NODATA timing experiment (wrong results)
-  int fence_mode;  // DCX_DENSE_FENCE=1: single proxy fence per CTA (experiment)
+  int fence_mode;  // DCX_DENSE_FENCE experiments: 1 single proxy fence per CTA, 2 no xh/s8 stores, 3 no fence
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -295,7 +295,7 @@ __device__ __forceinline__ void group_barrier(SyncWords* s, unsigned int members
 }
 
 struct __align__(8) Smem {
-  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2;
+  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2, d1free;
   uint32_t tmem_base;
   int pad;
   float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     }
     mbar_init(smem_u32(&sm.accf1), 1);
     mbar_init(smem_u32(&sm.accf2), 1);
+    mbar_init(smem_u32(&sm.d1free), 8);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -399,8 +400,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   // iteration p; warps 2-11 first finish the control of iteration p, which
   // therefore overlaps the next GEMM. The exit test reads the snapshot taken at
   // the barrier, identical for every thread of every CTA of the group.
+#define TL(k) do { if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 23 + 64 * 256 + p * 8 + (k)] = clock64(); } while (0)
   for (; p < a.p_end; ++p) {
-    if (p > p_start && __ldcg(&grp->running_snap) == 0) break;  // every replica of the group stopped
+    if (p > p_start && __ldcg(&grp->running_snap) == 0) break;
+    TL(0);  // every replica of the group stopped
     const int cur = p & 1;
     const bool trace = a.dbg && blockIdx.x == 0 && threadIdx.x == 64 && p < 4096;
     if (trace) {
@@ -411,7 +414,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       if (warp == 0) {
       // ---------------------------------------------------------- producer
       if (lane == 0) {
+        if (a.dbg && blockIdx.x == 0 && p < 4096) a.dbg[4096 * 31 + 64 * 256 + p * 4 + 1] = clock64();
         fence_async_global();
+        if (a.dbg && blockIdx.x == 0 && p < 4096) a.dbg[4096 * 31 + 64 * 256 + p * 4 + 2] = clock64();
         const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
         if (tr) a.dbg[p * 12 + 5] = clock64();
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
@@ -457,6 +462,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t ph = (kiter / P::STAGES) & 1;
           const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
+          if (kb == KB1 && a.fence_mode == 4) mbar_wait(smem_u32(&sm.d1free), acc_phase);  // experiment
           wait_cyc += clock64() - tw0;
           tc_fence_after();
           const uint32_t s0 = smem_u32(tiles + s * P::STAGE);
@@ -515,6 +521,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       }
       uint64_t curmask = 0;
       mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
+      TL(1);
       tc_fence_after();
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 11] = clock64();
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
@@ -525,41 +532,82 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         tmem_ld32(tmem + (uint32_t(q * 32) << 16) + h * 64 + cc * 32, v1);
         tmem_ld32(xaddr + cc * 32, xv);
         tmem_ld_wait();
-        __align__(16) __half hv[32];
-        __align__(16) int8_t sv[32];
+        __align__(16) __half2 hv[16];
+        __align__(16) uint32_t sv[8];
+        if (lim == 64) {
+          // full tile: branch-free (x is never -0.0, so x < 0 <=> sign bit)
+          uint32_t m = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float x = __uint_as_float(xv[j]);
-          const bool in = cc * 32 + j < lim;
-          const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j]));
-          const float nxt = cbrtf(ax * inv_beta);
-          if (in) {
-            const float x2 = x * x;
-            s4 = fmaf(x2, x2, s4);
-            sxax = fmaf(x, ax, sxax);
-            step = fmaxf(step, fabsf(nxt - x));
-            if (x < 0.f) curmask |= 1ull << (cc * 32 + j);
+          for (int j = 0; j < 32; j += 2) {
+            float nx[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const float x = __uint_as_float(xv[j + u]);
+              const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j + u]));
+              nx[u] = cbrt_fast(ax * inv_beta);
+              const float x2 = x * x;
+              s4 = fmaf(x2, x2, s4);
+              sxax = fmaf(x, ax, sxax);
+              step = fmaxf(step, fabsf(nx[u] - x));
+              m |= (xv[j + u] >> 31) << (j + u);
+              nv[j + u] = running ? __float_as_uint(nx[u]) : xv[j + u];
+            }
+            hv[j / 2] = __floats2half2_rn(nx[0] * inv_lam, nx[1] * inv_lam);
+            if ((j & 3) == 2) {  // 4 spins -> 4 bytes of +-1: 0x01 per byte, 0xff where negative
+              const uint32_t t = (nv[j - 2] >> 31) | ((nv[j - 1] >> 31) << 8) |
+                                 ((__float_as_uint(nx[0]) >> 31) << 16) | ((__float_as_uint(nx[1]) >> 31) << 24);
+              sv[j / 4] = 0x01010101u + t * 0xfeu;
+            }
           }
-          nv[j] = (in && running) ? __float_as_uint(nxt) : xv[j];
-          hv[j] = __float2half_rn(in ? nxt * inv_lam : 0.f);
-          sv[j] = in ? (nxt >= 0.f ? 1 : -1) : 0;
+          curmask |= uint64_t(m) << (cc * 32);
+        } else {
+          __align__(16) __half hh[32];
+          __align__(16) int8_t ss[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = __uint_as_float(xv[j]);
+            const bool in = cc * 32 + j < lim;
+            const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j]));
+            const float nxt = cbrt_fast(ax * inv_beta);
+            if (in) {
+              const float x2 = x * x;
+              s4 = fmaf(x2, x2, s4);
+              sxax = fmaf(x, ax, sxax);
+              step = fmaxf(step, fabsf(nxt - x));
+              if (x < 0.f) curmask |= 1ull << (cc * 32 + j);
+            }
+            nv[j] = (in && running) ? __float_as_uint(nxt) : xv[j];
+            hh[j] = __float2half_rn(in ? nxt * inv_lam : 0.f);
+            ss[j] = in ? (nxt >= 0.f ? 1 : -1) : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) hv[j] = __halves2half2(hh[2 * j], hh[2 * j + 1]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sv[j] = reinterpret_cast<const uint32_t*>(ss)[j];
         }
         tmem_st32(xaddr + cc * 32, nv);
-        if (running && lim > 0) {
+        if (running && lim > 0 && a.fence_mode != 2) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) *reinterpret_cast<uint4*>(hn + cc * 32 + j) = *reinterpret_cast<uint4*>(hv + j);
+          for (int j = 0; j < 16; j += 4) *reinterpret_cast<uint4*>(hn + cc * 32 + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
           if (write_master) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
               *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(xv + j);
           }
           *reinterpret_cast<uint4*>(sn + cc * 32) = *reinterpret_cast<uint4*>(sv);
-          *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 16);
+          *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 4);
         }
       }
       tmem_st_wait();
+      // experiment (DCX_DENSE_FENCE=4): GEMM2 waits for the whole update
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sm.d1free));
+#define TL2(k) do { if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 35 + 64 * 256 + p * 4 + (k)] = clock64(); } while (0)
+      TL2(0);
       // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
+      TL2(1);
       tc_fence_after();
       for (int cc = 0; cc < 2; ++cc) {
         uint32_t v2[32];
@@ -571,11 +619,13 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           if (cc * 32 + j < lim) es += ((curmask >> (cc * 32 + j)) & 1) ? -y2 : y2;
         }
       }
+      TL2(2);
       if (running) prevmask = curmask;
       sm.red[h][rl][0] = s4;
       sm.red[h][rl][1] = sxax;
       sm.red[h][rl][2] = es;
       sm.red[h][rl][3] = step;
+      if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 15 + 64 * 256 + p * 8 + 6] = clock64();
         }
     if (trace) {
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
@@ -583,8 +633,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     }
     acc_phase ^= 1;
     tc_fence_before();
+    TL(2);
     __syncthreads();
+    TL(3);
     if (trace) a.dbg[p * 12 + 2] = clock64();
+    if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 15 + 64 * 256 + p * 8 + 7] = clock64();
     if (threadIdx.x < TM) {
       const int rr = r0 + threadIdx.x;
       if (rr < a.R) {
@@ -599,16 +652,24 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         *reinterpret_cast<double4*>(dst) = v;
       }
     }
-    if (a.fence_mode == 0) {
+    unsigned long long* pr = (a.dbg && blockIdx.x == 0 && p < 4096) ? a.dbg + 4096 * 15 + 64 * 256 + p * 8 : nullptr;
+    if (pr && (threadIdx.x == 64 || threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 128))
+      pr[threadIdx.x == 64 ? 0 : threadIdx.x == 0 ? 1 : threadIdx.x == 32 ? 2 : 3] = clock64();
+    if (a.fence_mode == 0 || a.fence_mode == 2) {
       if (epi) fence_async_global();  // xh / s8 written here are read by TMA next iteration
-    } else {
+    } else if (a.fence_mode == 1) {
       __syncthreads();
       if (threadIdx.x == 0) fence_async_global();  // experiment: one proxy fence per CTA
     }
     if (a.dbg && threadIdx.x == 0 && p < 64) a.dbg[4096 * 14 + p * 256 + blockIdx.x] = globaltimer();  // arrival
+    if (pr && (threadIdx.x == 0 || threadIdx.x == 128)) pr[threadIdx.x == 0 ? 4 : 5] = clock64();
+    TL(4);
     __syncthreads();
+    TL(5);
     if (trace) a.dbg[4096 * 14 + 64 * 256 + p] = clock64();  // every thread done (incl. proxy fences)
     group_barrier(grp, NC * a.tiles_n);
+    TL(6);
+    if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 0) a.dbg[4096 * 31 + 64 * 256 + p * 4 + 0] = clock64();
     if (trace) a.dbg[p * 12 + 3] = clock64();
     if (warp < 2) continue;  // TMA / MMA go on with the next iteration
     // ---------------------------------------------------------- control (warps 4-11)
@@ -666,6 +727,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       asm volatile("bar.sync 1, 256;" ::: "memory");
     }
     if (trace) a.dbg[p * 12 + 4] = clock64();
+    TL(7);
   }
   // ---------------------------------------------------------------- teardown
   if (epi) {
@@ -926,8 +988,8 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) cudaFree(d.dbg);
   d.dbg = nullptr;
   if (std::getenv("DCX_DENSE_TRACE")) {
-    DCK(cudaMalloc(&d.dbg, (4096 * 15 + 64 * 256) * 8));
-    DCK(cudaMemsetAsync(d.dbg, 0, (4096 * 15 + 64 * 256) * 8, s));
+    DCK(cudaMalloc(&d.dbg, (4096 * 39 + 64 * 256) * 8));
+    DCK(cudaMemsetAsync(d.dbg, 0, (4096 * 39 + 64 * 256) * 8, s));
   }
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
@@ -978,7 +1040,7 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.p_end = p_end;
   a.jscale = d.jscale;
   a.nodata = std::getenv("DCX_DENSE_NODATA") ? 1 : 0;
-  a.fence_mode = std::getenv("DCX_DENSE_FENCE") ? 1 : 0;
+  a.fence_mode = std::getenv("DCX_DENSE_FENCE") ? std::atoi(std::getenv("DCX_DENSE_FENCE")) : 0;
   const int grid = (d.Rpad / 128) * a.tiles_n;
   if (d.nc == 1) {
     void* args[] = {&a};
@@ -1068,6 +1130,70 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
       if (c2)
         std::fprintf(stderr, "[dcx dense trace] kcycles: partials+proxy fences %.2f, group barrier %.2f\n",
                      pre / c2 / 1e3, bar / c2 / 1e3);
+      std::vector<unsigned long long> pq(4096 * 8);
+      DCK(cudaMemcpyAsync(pq.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 15 + 64 * 256,
+                          pq.size() * 8, cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int c3 = 0;
+      for (int p = 1; p < 4096 && t[p * 12 + 4] && pq[p * 8 + 6]; ++p, ++c3)
+        for (int k = 0; k < 8; ++k) q[k] += double(pq[p * 8 + k]) - double(t[p * 12 + 2]);
+      if (c3)
+        std::fprintf(stderr,
+                     "[dcx dense trace] after sync1 (kcycles): part-store t64 %.2f t0 %.2f t32 %.2f t128 %.2f | "
+                     "pre-sync2 t0 %.2f t128 %.2f | t128 BEFORE sync1 %.2f | t128 right after sync1 %.2f\n",
+                     q[0] / c3 / 1e3, q[1] / c3 / 1e3, q[2] / c3 / 1e3, q[3] / c3 / 1e3, q[4] / c3 / 1e3,
+                     q[5] / c3 / 1e3, q[6] / c3 / 1e3, q[7] / c3 / 1e3);
+    }
+    {
+      std::vector<unsigned long long> tl(4096 * 8);
+      DCK(cudaMemcpyAsync(tl.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 23 + 64 * 256,
+                          tl.size() * 8, cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int c4 = 0;
+      for (int p = 2; p + 1 < 4096 && tl[(p + 1) * 8] && tl[p * 8 + 7]; ++p, ++c4) {
+        for (int k = 1; k < 8; ++k) q[k] += double(tl[p * 8 + k]) - double(tl[p * 8 + k - 1]);
+        q[0] += double(tl[(p + 1) * 8]) - double(tl[p * 8 + 7]);
+      }
+      if (c4)
+        std::fprintf(stderr,
+                     "[dcx dense trace] epilogue thread timeline (kcycles): top->accf1 %.2f, update+es %.2f, "
+                     "sync1 %.2f, partials/fence %.2f, sync2 %.2f, group barrier %.2f, control %.2f, loop %.2f\n",
+                     q[1] / c4 / 1e3, q[2] / c4 / 1e3, q[3] / c4 / 1e3, q[4] / c4 / 1e3, q[5] / c4 / 1e3,
+                     q[6] / c4 / 1e3, q[7] / c4 / 1e3, q[0] / c4 / 1e3);
+    }
+    {
+      std::vector<unsigned long long> tp(4096 * 4);
+      DCK(cudaMemcpyAsync(tp.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 31 + 64 * 256,
+                          tp.size() * 8, cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      double q[3] = {0, 0, 0};
+      int c5 = 0;
+      for (int p = 2; p + 1 < 4096 && tp[(p + 1) * 4 + 2] && tp[p * 4]; ++p, ++c5) {
+        q[0] += double(tp[(p + 1) * 4 + 1]) - double(tp[p * 4]);      // barrier exit -> next loop top (producer)
+        q[1] += double(tp[(p + 1) * 4 + 2]) - double(tp[(p + 1) * 4 + 1]);  // proxy fence
+      }
+      if (c5)
+        std::fprintf(stderr, "[dcx dense trace] producer: group barrier -> loop top %.2f kcycles, proxy fence %.2f\n",
+                     q[0] / c5 / 1e3, q[1] / c5 / 1e3);
+      std::vector<unsigned long long> tl(4096 * 8), te2(4096 * 4);
+      DCK(cudaMemcpyAsync(tl.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 23 + 64 * 256,
+                          tl.size() * 8, cudaMemcpyDeviceToHost, s));
+      DCK(cudaMemcpyAsync(te2.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 35 + 64 * 256,
+                          te2.size() * 8, cudaMemcpyDeviceToHost, s));
+      DCK(cudaStreamSynchronize(s));
+      double e[4] = {0, 0, 0, 0};
+      int c6 = 0;
+      for (int p = 2; p < 4096 && te2[p * 4 + 2] && tl[p * 8 + 2]; ++p, ++c6) {
+        e[0] += double(te2[p * 4]) - double(tl[p * 8 + 1]);
+        e[1] += double(te2[p * 4 + 1]) - double(te2[p * 4]);
+        e[2] += double(te2[p * 4 + 2]) - double(te2[p * 4 + 1]);
+        e[3] += double(tl[p * 8 + 2]) - double(te2[p * 4 + 2]);
+      }
+      if (c6)
+        std::fprintf(stderr, "[dcx dense trace] epilogue split: update %.2f, wait accf2 %.2f, es %.2f, red %.2f kcycles\n",
+                     e[0] / c6 / 1e3, e[1] / c6 / 1e3, e[2] / c6 / 1e3, e[3] / c6 / 1e3);
     }
     double wsum = 0;
     for (int p = 1; p < 4096 && t[p * 12 + 4]; ++p) wsum += double(tw[p]);
