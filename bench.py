@@ -313,6 +313,11 @@ def main():
     ap.add_argument("--config", default="k2", choices=["k2", "g1", "t6", "e7"],
                     help="k2 is the headline (BASELINE configs[1]); others: see bench_configs.py")
     args = ap.parse_args()
+    # descent-violation RuntimeWarnings are per-replica diagnostics (1024 lines of
+    # stderr per solve at K2 in f16); neither arm prints them while timed
+    import warnings
+
+    warnings.filterwarnings("ignore", category=RuntimeWarning)
     if args.config != "k2" and args.impl == "ours":
         import bench_configs
 

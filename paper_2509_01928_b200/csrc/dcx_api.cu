@@ -82,6 +82,7 @@ struct dcx_ctx {
   int path = DCX_PATH_MULTIPASS;
   int cap = 0, wcap = 0, chunk = 0, p_host = 0;
   DevBuf ctl, g, hist, window, xb0, xb1, ax0, ax1, ay, best, states, part, spart;
+  DevBuf scratch;  // grow-only staging (x0 upload, result gathers): no cudaMalloc / cudaFree per call
   MultiPass mp;
   CsrDev J;
   SmallPlan sp;
@@ -90,7 +91,11 @@ struct dcx_ctx {
   double dev_seconds = 0.0;
   bool dist = false;              // dcx_dist_begin run: external iterate buffers, caller's collectives
   double *qs = nullptr, *qm = nullptr;
-  std::vector<std::vector<HistRec>> hh;
+  std::vector<std::vector<HistRec>> hh;  // drained history (used when the ring can wrap)
+  bool ring_direct = false;              // the ring holds every record: results read it in place
+  std::vector<int64_t> hcnt;             // records per replica (ring_direct)
+  int64_t nhist(int r) const { return ring_direct ? hcnt[r] : (int64_t)hh[r].size(); }
+  const HistRec& rec(int r, int64_t k) const { return ring_direct ? ring[size_t(r) * cap + k] : hh[r][k]; }
   std::vector<RepCtl> hctl;
   HistRec* ring = nullptr;  // pinned host copy of the device history ring
   size_t ring_n = 0;
@@ -221,6 +226,27 @@ __global__ void from_device_layout(const T* src, double* dst, int64_t n, int R) 
     dst[(int64_t)r * n + i] = double(src[idx]);
   }
 }
+// final state of each replica (buffer by the parity of its last iteration),
+// [n][R] -> [R][n] f64, written coalesced for one device-to-host copy
+template <typename T>
+__global__ void gather_final_state(const T* x0, const T* x1, const RepCtl* ctl, int64_t n, int R, double* out) {
+  const int64_t total = n * R;
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(o / n);
+    const int64_t i = o % n;
+    const int k = max(0, ctl[r].k);
+    out[o] = double(((k & 1) ? x1 : x0)[i * R + r]);
+  }
+}
+__global__ void gather_best(const int8_t* best, int64_t n, int R, int8_t* out) {
+  const int64_t total = n * R;
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(o / n);
+    const int64_t i = o % n;
+    out[o] = best[i * R + r];
+  }
+}
+
 // mode 0: tx = cbrt((jv + a v)/b), h = H(v); mode 1: E = -1/2 scale sum s_i es_i
 template <typename T>
 __global__ void rows_epilogue(int mode, const T* v, const T* jv, const double* es, const double* alpha,
@@ -734,8 +760,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     c->mp.spart = c->spart.as<double>();
     // initial state
     {
-      DevBuf src;
-      src.alloc(tot * 8);
+      DevBuf& src = c->scratch;
+      if (src.bytes < size_t(tot) * 8) src.alloc(size_t(tot) * 8);
       CK(cudaMemcpyAsync(src.p, x0, tot * 8, cudaMemcpyHostToDevice, c->stream));
       if (c->f64) to_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<double*>(a.x[0]), n, R);
       else to_device_layout<float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<float*>(a.x[0]), n, R);
@@ -770,8 +796,13 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     c->hg.running = R;
     CK(cudaMemcpyAsync(c->g.p, &c->hg, sizeof(GState), cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    c->hh.assign(R, {});
-    for (auto& v : c->hh) v.reserve(std::min<int64_t>(P->max_iters + 1, 4096));
+    c->ring_direct = cap >= P->max_iters + 1;
+    c->hcnt.assign(R, 0);
+    c->hh.resize(c->ring_direct ? 0 : R);  // keep each replica's capacity across runs
+    for (auto& v : c->hh) {
+      v.clear();
+      v.reserve(std::min<int64_t>(P->max_iters + 1, 4096));
+    }
     c->hctl = h;
     if (c->ring_n < size_t(R) * cap) {
       if (c->ring) cudaFreeHost(c->ring);
@@ -865,7 +896,7 @@ static void drain(dcx_ctx* c) {
   int64_t lo = std::numeric_limits<int64_t>::max(), hi = -1;
   for (int r = 0; r < R; ++r) {
     const int64_t kr = c->hctl[r].k;
-    const int64_t done = (int64_t)c->hh[r].size();
+    const int64_t done = c->nhist(r);
     if (kr >= done) {
       lo = std::min(lo, done);
       hi = std::max(hi, kr);
@@ -887,6 +918,10 @@ static void drain(dcx_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
   for (int r = 0; r < R; ++r) {
     const int64_t kr = c->hctl[r].k;
+    if (c->ring_direct) {
+      c->hcnt[r] = std::max<int64_t>(c->hcnt[r], kr + 1);
+      continue;
+    }
     auto& v = c->hh[r];
     for (int64_t k = (int64_t)v.size(); k <= kr; ++k) v.push_back(c->ring[(size_t)r * c->cap + (k % c->cap)]);
   }
@@ -957,7 +992,7 @@ int dcx_result_summary(dcx_ctx* c, int32_t r, dcx_summary* out) {
   out->stop_reason = q.status;
   out->best_iter = q.best_iter;
   out->best_energy = q.best;
-  out->n_hist = (int64_t)c->hh[r].size();
+  out->n_hist = c->nhist(r);
   out->descent_warn = q.warned;
   out->path_used = c->path;
   return DCX_OK;
@@ -967,10 +1002,9 @@ int dcx_result_history(dcx_ctx* c, int32_t r, int64_t from, int64_t count, doubl
                        int32_t* ev) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   if (!c->begun || r < 0 || r >= c->R) return fail(c, DCX_E_INVALID, "bad replica");
-  const auto& v = c->hh[r];
-  if (from < 0 || count < 0 || from + count > (int64_t)v.size()) return fail(c, DCX_E_INVALID, "history range");
+  if (from < 0 || count < 0 || from + count > c->nhist(r)) return fail(c, DCX_E_INVALID, "history range");
   for (int64_t k = 0; k < count; ++k) {
-    const HistRec& q = v[from + k];
+    const HistRec& q = c->rec(r, from + k);
     if (h) h[k] = q.h;
     if (e) e[k] = q.e;
     if (t) t[k] = q.t;
@@ -988,7 +1022,7 @@ int dcx_result_summaries(dcx_ctx* c, int64_t* iterations, int32_t* stop_reason, 
     if (iterations) iterations[r] = std::max(0, q.k);
     if (stop_reason) stop_reason[r] = q.status;
     if (best_energy) best_energy[r] = q.best;
-    if (n_hist) n_hist[r] = (int64_t)c->hh[r].size();
+    if (n_hist) n_hist[r] = c->nhist(r);
     if (descent_warn) descent_warn[r] = q.warned;
   }
   return DCX_OK;
@@ -998,11 +1032,10 @@ int dcx_result_history_all(dcx_ctx* c, int64_t K, double* h, double* e, double* 
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   if (!c->begun) return fail(c, DCX_E_STATE, "no run");
   for (int r = 0; r < c->R; ++r) {
-    const auto& v = c->hh[r];
-    const int64_t cnt = std::min<int64_t>(K, (int64_t)v.size());
+    const int64_t cnt = std::min<int64_t>(K, c->nhist(r));
     const int64_t base = (int64_t)r * K;
     for (int64_t k = 0; k < cnt; ++k) {
-      const HistRec& q = v[k];
+      const HistRec& q = c->rec(r, k);
       if (h) h[base + k] = q.h;
       if (e) e[base + k] = q.e;
       if (t) t[base + k] = q.t;
@@ -1017,11 +1050,11 @@ int dcx_result_best_spins(dcx_ctx* c, int8_t* out) {
   return guarded(c, [&] {
     if (!c->begun) throw InvalidArg("no run");
     const int64_t n = c->n, R = c->R;
-    std::vector<int8_t> tmp(n * R);
-    CK(cudaMemcpyAsync(tmp.data(), c->best.p, n * R, cudaMemcpyDeviceToHost, c->stream));
+    DevBuf& tmp = c->scratch;
+    if (tmp.bytes < size_t(n * R)) tmp.alloc(size_t(n * R));
+    gather_best<<<grid_for(n * R), 256, 0, c->stream>>>(c->best.as<int8_t>(), n, (int)R, tmp.as<int8_t>());
+    CK(cudaMemcpyAsync(out, tmp.p, n * R, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t r = 0; r < R; ++r) out[r * n + i] = tmp[i * R + r];
   });
 }
 
@@ -1030,19 +1063,18 @@ int dcx_result_state(dcx_ctx* c, double* out) {
   return guarded(c, [&] {
     if (!c->begun) throw InvalidArg("no run");
     const int64_t n = c->n, R = c->R, tot = n * R;
-    const size_t tb = c->f64 ? 8 : 4;
-    std::vector<unsigned char> b0(tot * tb), b1(tot * tb);
-    CK(cudaMemcpyAsync(b0.data(), c->mp.args.x[0], tot * tb, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(b1.data(), c->mp.args.x[1], tot * tb, cudaMemcpyDeviceToHost, c->stream));
+    DevBuf& tmp = c->scratch;
+    if (tmp.bytes < size_t(tot) * 8) tmp.alloc(size_t(tot) * 8);
+    if (c->f64)
+      gather_final_state<double><<<grid_for(tot), 256, 0, c->stream>>>(
+          static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          n, (int)R, tmp.as<double>());
+    else
+      gather_final_state<float><<<grid_for(tot), 256, 0, c->stream>>>(
+          static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          n, (int)R, tmp.as<double>());
+    CK(cudaMemcpyAsync(out, tmp.p, tot * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (int64_t r = 0; r < R; ++r) {
-      const int k = std::max(0, c->hctl[r].k);
-      const unsigned char* src = (k & 1) ? b1.data() : b0.data();
-      for (int64_t i = 0; i < n; ++i) {
-        const int64_t idx = i * R + r;
-        out[r * n + i] = c->f64 ? reinterpret_cast<const double*>(src)[idx] : double(reinterpret_cast<const float*>(src)[idx]);
-      }
-    }
   });
 }
 

@@ -885,20 +885,33 @@ void DenseDev::release() {
   q16 = q8 = nullptr;
   if (tmaps) delete[] reinterpret_cast<CUtensorMap*>(tmaps);
   tmaps = nullptr;
+  if (scratch) cudaFree(scratch);
+  scratch = nullptr;
+  scratch_bytes = 0;
   n = npad = 0;
   exact = false;
 }
 
 void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
-  d.release();
+  // a re-upload of the same size keeps every device buffer (operands, run state,
+  // scratch): no cudaMalloc / cudaFree, which synchronise and cost milliseconds
+  const int64_t npad = (n + 255) / 256 * 256;  // whole int8 stages (2 x 128 of K)
+  if (d.npad != npad) d.release();
   d.n = n;
-  d.npad = (n + 255) / 256 * 256;  // whole int8 stages (2 x 128 of K)
+  d.npad = npad;
+  d.exact = false;
   // exact small-integer form J = jscale * Q (the K2000 instance: jscale = 1/2, Q = -W),
   // found and converted on the device: min |nonzero| gives the candidate scale
-  double* dA = nullptr;
-  unsigned long long* dw = nullptr;  // [0] min |a| bits, [1] failure flag
-  DCK(cudaMalloc(&dA, n * n * 8));
-  DCK(cudaMalloc(&dw, 16));
+  const size_t need = size_t(n * n) * 8 + 16;
+  if (d.scratch_bytes < need) {
+    if (d.scratch) cudaFree(d.scratch);
+    d.scratch = nullptr;
+    d.scratch_bytes = 0;
+    DCK(cudaMalloc(&d.scratch, need));
+    d.scratch_bytes = need;
+  }
+  double* dA = static_cast<double*>(d.scratch);
+  unsigned long long* dw = reinterpret_cast<unsigned long long*>(static_cast<char*>(d.scratch) + size_t(n * n) * 8);
   DCK(cudaMemcpyAsync(dA, A, n * n * 8, cudaMemcpyHostToDevice, s));
   const unsigned long long init[2] = {~0ull, 0ull};
   DCK(cudaMemcpyAsync(dw, init, 16, cudaMemcpyHostToDevice, s));
@@ -910,8 +923,8 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   if (mnbits != ~0ull) {
     double mn;
     std::memcpy(&mn, &mnbits, 8);
-    DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
-    DCK(cudaMalloc(&d.q8, d.npad * d.npad));
+    if (!d.q16) DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
+    if (!d.q8) DCK(cudaMalloc(&d.q8, d.npad * d.npad));
     for (double cand : {mn, 1.0, 0.5}) {
       DCK(cudaMemsetAsync(dw + 1, 0, 8, s));
       tc::q_expand<<<1024, 256, 0, s>>>(dA, cand, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8),
@@ -925,16 +938,10 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
       }
     }
   }
-  cudaFree(dA);
-  cudaFree(dw);
-  if (scale == 0.0) {  // real-valued couplings: no exact int8 / f16 operand, tensor path unavailable
-    d.release();
-    d.n = n;
-    return;
-  }
+  if (scale == 0.0) return;  // real-valued couplings: no exact int8 / f16 operand, tensor path unavailable
   d.jscale = float(scale);
   d.exact = true;
-  d.tmaps = new CUtensorMap[6];
+  if (!d.tmaps) d.tmaps = new CUtensorMap[6];
 }
 
 static size_t dense_smem_bytes(int nc) {

@@ -26,6 +26,8 @@ struct DenseDev {
   void* tmaps = nullptr;             // host-side CUtensorMap storage (3 maps)
   int chunk_hint = 0;
   void* dbg = nullptr;                // phase timestamps (DCX_DENSE_TRACE)
+  void* scratch = nullptr;            // f64 upload staging (grow-only)
+  size_t scratch_bytes = 0;
   void release();
   void release_run();
 };

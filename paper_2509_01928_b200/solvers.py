@@ -138,12 +138,14 @@ class LazyTrace(Sequence):
     (a stride-1 trace of 1024 replicas x 1000 iterations would otherwise be a
     million Python objects)."""
 
-    def __init__(self, solver, iters, elapsed, energy, cut_offset, ev):
+    def __init__(self, solver, iters, elapsed, energy, cut_offset, ev, best=None):
         self.solver = solver
         self.iters = iters
         self.elapsed = elapsed
         self.energy = energy
-        self.best = np.minimum.accumulate(energy) if len(energy) else energy
+        if best is None:
+            best = np.minimum.accumulate(energy) if len(energy) else energy
+        self.best = best
         self.cut_offset = cut_offset
         self.ev = ev
 
@@ -241,13 +243,22 @@ def assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path=N
     iters, stops, bests, nh, warn = ctx.summaries()
     K = int(nh.max()) if R else 0
     H, E, T, EV = ctx.history_all(K)
+    T += offset
     rec = (EV & _native.EV_RECORDED) != 0
+    # rows recorded at every iteration (trace_stride 1) become views of the bulk
+    # arrays, with the running best computed for all of them at once
+    full = rec.sum(axis=1) == nh
+    B = np.minimum.accumulate(np.where(rec, E, np.inf), axis=1) if full.any() else None
+    ar = np.arange(K)
     out = []
     for r in range(R):
         n_r = int(nh[r])
         h, ev = H[r, :n_r], EV[r, :n_r]
-        ks = np.nonzero(rec[r, :n_r])[0]
-        trace = LazyTrace(solver, ks, T[r, ks] + offset, E[r, ks], cut_offset, ev[ks])
+        if full[r]:
+            trace = LazyTrace(solver, ar[:n_r], T[r, :n_r], E[r, :n_r], cut_offset, ev, best=B[r, :n_r])
+        else:
+            ks = np.nonzero(rec[r, :n_r])[0]
+            trace = LazyTrace(solver, ks, T[r, ks], E[r, ks], cut_offset, ev[ks])
         it = int(iters[r])
         if warn[r] >= 0 and solver == "doch":
             k = int(warn[r])
