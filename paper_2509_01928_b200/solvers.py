@@ -143,11 +143,15 @@ class LazyTrace(Sequence):
         self.iters = iters
         self.elapsed = elapsed
         self.energy = energy
-        if best is None:
-            best = np.minimum.accumulate(energy) if len(energy) else energy
-        self.best = best
+        self._best = best
         self.cut_offset = cut_offset
         self.ev = ev
+
+    @property
+    def best(self):
+        if self._best is None:
+            self._best = np.minimum.accumulate(self.energy) if len(self.energy) else self.energy
+        return self._best
 
     def __len__(self):
         return len(self.iters)
@@ -243,39 +247,40 @@ def assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path=N
     iters, stops, bests, nh, warn = ctx.summaries()
     K = int(nh.max()) if R else 0
     H, E, T, EV = ctx.history_all(K)
-    T += offset
+    if offset:
+        T += offset
     rec = (EV & _native.EV_RECORDED) != 0
     # rows recorded at every iteration (trace_stride 1) become views of the bulk
-    # arrays, with the running best computed for all of them at once
-    full = rec.sum(axis=1) == nh
-    B = np.minimum.accumulate(np.where(rec, E, np.inf), axis=1) if full.any() else None
+    # arrays; the running best is computed on first use (LazyTrace.best)
+    full = (rec.sum(axis=1) == nh).tolist()
     ar = np.arange(K)
+    nh_l, it_l, be_l = nh.tolist(), iters.tolist(), bests.tolist()
+    stop_l = [_native.STOP.get(v, "max_iters") for v in stops.tolist()]
+    warned = np.nonzero(warn >= 0)[0] if solver == "doch" else ()
+    for r in warned:
+        k = int(warn[r])
+        warnings.warn(f"Hamiltonian increased by {H[r, k] - H[r, k - 1]:.3e} at iteration {k}",
+                      RuntimeWarning, stacklevel=4)
     out = []
+    append = out.append
     for r in range(R):
-        n_r = int(nh[r])
-        h, ev = H[r, :n_r], EV[r, :n_r]
+        n_r = nh_l[r]
+        hr, evr = H[r, :n_r], EV[r, :n_r]
         if full[r]:
-            trace = LazyTrace(solver, ar[:n_r], T[r, :n_r], E[r, :n_r], cut_offset, ev, best=B[r, :n_r])
+            trace = LazyTrace(solver, ar[:n_r], T[r, :n_r], E[r, :n_r], cut_offset, evr)
         else:
             ks = np.nonzero(rec[r, :n_r])[0]
-            trace = LazyTrace(solver, ks, T[r, ks], E[r, ks], cut_offset, ev[ks])
-        it = int(iters[r])
-        if warn[r] >= 0 and solver == "doch":
-            k = int(warn[r])
-            warnings.warn(f"Hamiltonian increased by {h[k] - h[k - 1]:.3e} at iteration {k}",
-                          RuntimeWarning, stacklevel=4)
+            trace = LazyTrace(solver, ks, T[r, ks], E[r, ks], cut_offset, evr[ks])
+        it = it_l[r]
         accepted = None
         if solver == "adoch":
-            accepted = ([True] + ((ev[2:it + 1] & _native.EV_ACCEPTED) != 0).tolist()) if it else []
+            accepted = ([True] + ((evr[2:it + 1] & _native.EV_ACCEPTED) != 0).tolist()) if it else []
         states = None
         if record_states:
             st = ctx.states(r, it)
             states = [st[k].copy() for k in range(it + 1)]
-        out.append(SolveResult(
-            solver=solver, spins=best[r], energy=float(bests[r]), iterations=it,
-            stop_reason=_native.STOP.get(int(stops[r]), "max_iters"), trace=trace,
-            seed=None if seeds is None else seeds[r], x=xs[r], h_values=h if R > 1 else h.tolist(),
-            accepted=accepted, states=states, device_seconds=dev_s, path=path_used))
+        append(SolveResult(solver, best[r], be_l[r], it, stop_l[r], trace, None if seeds is None else seeds[r],
+                           xs[r], hr if R > 1 else hr.tolist(), accepted, states, dev_s, path_used))
     return out
 
 
