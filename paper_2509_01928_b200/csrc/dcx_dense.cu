@@ -87,6 +87,7 @@ struct Args {
   int n, npad, R, Rpad, tiles_n, p_end;
   float jscale;
   int nodata;  // DCX_DENSE_NODATA timing experiment (wrong results)
+  int mc;          // NC = 2: clusters of two pairs sharing the A tiles by TMA multicast
   int fence_mode;  // DCX_DENSE_FENCE experiments: 1 single proxy fence per CTA, 2 no xh/s8 stores, 3 no fence
 };
 
@@ -118,6 +119,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 // mbarrier polling off the shared-memory pipe the tensor core is reading
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
   uint32_t ok = 0;
+  long long t0 = 0;
   while (true) {
     asm volatile(
         "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
@@ -126,6 +128,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
         : "memory");
     if (ok) break;
     __nanosleep(256);
+    if (t0 == 0) t0 = clock64();
+    else if (clock64() - t0 > (1ll << 35)) __trap();
   }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
@@ -141,6 +145,16 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar & 0xFEFFFFFFu)
+      : "memory");
+}
+// pair TMA multicast to the CTAs in `mask` (same smem offset in each); every
+// destination's pair leader barrier receives that destination's bytes
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar,
+                                                    uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar & 0xFEFFFFFFu), "h"(mask)
       : "memory");
 }
 template <int NC>
@@ -163,13 +177,12 @@ __device__ __forceinline__ void mma_i8_g(uint32_t dtmem, uint64_t ad, uint64_t b
                  "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
   }
 }
-// MMA completion -> mbarrier (both CTAs of a pair receive it)
+// MMA completion -> mbarrier (NC = 2: every CTA of the cluster in `mask` receives it)
 template <int NC>
-__device__ __forceinline__ void mma_commit_g(uint32_t mbar) {
+__device__ __forceinline__ void mma_commit_g(uint32_t mbar, uint16_t mask = 3) {
   if constexpr (NC == 1) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
   } else {
-    const uint16_t mask = 3;
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                      mbar),
                  "h"(mask)
@@ -316,7 +329,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   unsigned char* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Smem& sm = *reinterpret_cast<Smem*>(tiles + P::TILES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta_rank = NC == 2 ? int(blockIdx.x & 1) : 0;  // rank in the CTA pair (cluster)
+  const int cta_rank = NC == 2 ? int(blockIdx.x & 1) : 0;  // rank in the CTA pair
+  // multicast clusters (a.mc): pairs 2k, 2k+1 (same replica group, adjacent spin
+  // tiles) form one 4-CTA cluster; pair 0 loads the A tiles for both
+  const int psub = (NC == 2 && a.mc) ? int((blockIdx.x >> 1) & 1) : 0;
   const int pair = blockIdx.x / NC;
   const int rg = pair / a.tiles_n, nt = pair % a.tiles_n;  // replica group (NC x 128 replicas), spin tile
   const int rt = rg * NC + cta_rank;                        // this CTA's 128-replica tile
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < P::STAGES; ++s) {
       mbar_init(smem_u32(&sm.full[s]), 1);
-      mbar_init(smem_u32(&sm.empty[s]), 1);
+      mbar_init(smem_u32(&sm.empty[s]), (NC == 2 && a.mc && psub == 0) ? 2 : 1);  // A writers wait for both pairs
     }
     mbar_init(smem_u32(&sm.accf1), 1);
     mbar_init(smem_u32(&sm.accf2), 1);
@@ -443,7 +459,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               tma_load_2d(da, ma, kc + q * katom, r0, fb);
               tma_load_2d(db, mb, kc + q * katom, bi, fb);
             } else {
-              tma_load_2d_pair(da, ma, kc + q * katom, r0, fb);
+              if (!a.mc) tma_load_2d_pair(da, ma, kc + q * katom, r0, fb);
+              else if (psub == 0)
+                tma_load_2d_pair_mc(da, ma, kc + q * katom, r0, fb, uint16_t((1u << cta_rank) | (1u << (cta_rank + 2))));
               tma_load_2d_pair(db, mb, kc + q * katom, bi, fb);
             }
           }
@@ -481,16 +499,16 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
                              ((kb - KB1) | q | k) ? 1u : 0u);
             }
           }
-          mma_commit_g<NC>(smem_u32(&sm.empty[s]));
+          mma_commit_g<NC>(smem_u32(&sm.empty[s]), uint16_t(!a.mc ? 0x3 : (psub == 0 ? 0x3 : 0xF)));
           if (tr && kb == 0) a.dbg[p * 12 + 8] = clock64();
           if (kb == KB1 - 1) {
-            mma_commit_g<NC>(smem_u32(&sm.accf1));
+            mma_commit_g<NC>(smem_u32(&sm.accf1), uint16_t(0x3u << (2 * psub)));
             if (tr) a.dbg[p * 12 + 9] = clock64();
           }
         }
         if (tr) a.dbg[p * 12 + 10] = clock64();
         if (tr) a.dbg[4096 * 12 + p] = wait_cyc;
-        mma_commit_g<NC>(smem_u32(&sm.accf2));
+        mma_commit_g<NC>(smem_u32(&sm.accf2), uint16_t(0x3u << (2 * psub)));
       }
       __syncwarp();
       }
@@ -1048,6 +1066,12 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.jscale = d.jscale;
   a.nodata = std::getenv("DCX_DENSE_NODATA") ? 1 : 0;
   a.fence_mode = std::getenv("DCX_DENSE_FENCE") ? std::atoi(std::getenv("DCX_DENSE_FENCE")) : 0;
+  a.mc = 0;
+  if (d.nc == 2 && (d.npad / 128) % 2 == 0) {
+    const char* e = std::getenv("DCX_DENSE_MC");
+    a.mc = (e && std::atoi(e) == 1) ? 1 : 0;
+  }
+  if (d.dbg) std::fprintf(stderr, "[dcx dense trace] launch: nc=%d mc=%d grid=%d\n", d.nc, a.mc, (d.Rpad / 128) * int(d.npad / 128));
   const int grid = (d.Rpad / 128) * a.tiles_n;
   if (d.nc == 1) {
     void* args[] = {&a};
@@ -1062,7 +1086,7 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = a.mc ? 4 : 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeCooperative;
