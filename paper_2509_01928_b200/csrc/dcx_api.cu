@@ -705,7 +705,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
       // two resident 256-thread blocks per SM (the kernel needs up to 128 registers)
       const int vw = replica_vector_width(R, c->f64);
       const int chunks = (R + 32 * vw - 1) / (32 * vw);
-      c->mp.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, std::max(1, 148 * 2 / chunks)));
+      const int per_sm = (vw * (c->f64 ? 8 : 4) >= 16) ? 2 : 3;  // resident blocks (pass_rv launch bounds)
+      c->mp.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, std::max(1, 148 * per_sm / chunks)));
       slots = c->mp.grid;
     }
     c->part.alloc(sizeof(double) * R * NQ * slots);

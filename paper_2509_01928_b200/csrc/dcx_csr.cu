@@ -6,6 +6,8 @@
 // reads the CSR stream once and gathers x once; from the same gather it forms
 // (J+aI)x, the next iterate, and J*sign(x) for the spin energy (exact integer
 // accumulation for integer couplings), plus the H / E / step partials.
+#include <cstdlib>
+
 #include "dcx_internal.h"
 
 namespace dcx {
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
 template <typename T, int VW>
 struct VecT;
 template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<float, 2> { using type = float2; };
 template <> struct VecT<float, 4> { using type = float4; };
 template <> struct VecT<double, 1> { using type = double; };
 template <> struct VecT<double, 2> { using type = double2; };
@@ -224,7 +227,7 @@ template <typename T, int VW, int MODE>
 constexpr size_t rv_smem_bytes() { return size_t(2) * 8 * rv_staged_edges<MODE>() * 32 * VW * sizeof(T); }
 
 template <typename T, int VK, int VW, int MODE>
-__global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
+__global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(PassArgs a) {
   constexpr int UNROLL = 4;
   constexpr int G = rv_staged_edges<MODE>();
   constexpr int CB = VW * int(sizeof(T));  // bytes per lane per spin row
@@ -265,13 +268,15 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
   const T* xp = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
   T* xn_buf = reinterpret_cast<T*>(a.x[(p + 1) & 1]);
   const T scale = T(a.scale);
-  // per-replica partials over this warp's rows; the step max stays in T (exact)
-  double s4[VW], sxax[VW], esum[VW], sy4[VW], syay[VW];
-  T step[VW];
+  // per-replica partials over this warp's rows, in T (f32 mode: a few hundred
+  // rows per lane, summed in double across warps and blocks); the step max is
+  // exact in T; the spin-energy sum stays in double (exact for integer J)
+  T s4[VW], sxax[VW], sy4[VW], syay[VW], step[VW];
+  double esum[VW];
 #pragma unroll
   for (int v = 0; v < VW; ++v) {
-    s4[v] = sxax[v] = esum[v] = sy4[v] = syay[v] = 0.0;
-    step[v] = T(0);
+    s4[v] = sxax[v] = sy4[v] = syay[v] = step[v] = T(0);
+    esum[v] = 0.0;
   }
 
   // Pipeline over this warp's rows A = i, B = i+S, C = i+2S, D = i+3S. While
@@ -447,9 +452,9 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
 #pragma unroll
       for (int v = 0; v < VW; ++v) {
         const T ax = shifted(acc[v], alpha[v], xi[v]);
-        const double x2 = double(mul_rn(xi[v], xi[v]));
+        const T x2 = mul_rn(xi[v], xi[v]);
         s4[v] += x2 * x2;
-        sxax[v] += double(xi[v]) * double(ax);
+        sxax[v] += xi[v] * ax;
         const double e = es[v].value(deg);
         esum[v] += negbit(xi[v]) ? -e : e;
         const T xnew = tmap(ax, beta[v], ibeta[v]);
@@ -464,9 +469,9 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
 #pragma unroll
       for (int v = 0; v < VW; ++v) {
         ax[v] = shifted(acc[v], alpha[v], xi[v]);
-        const double x2 = double(mul_rn(xi[v], xi[v]));
+        const T x2 = mul_rn(xi[v], xi[v]);
         s4[v] += x2 * x2;
-        sxax[v] += double(xi[v]) * double(ax[v]);
+        sxax[v] += xi[v] * ax[v];
         const double e = es[v].value(deg);
         esum[v] += negbit(xi[v]) ? -e : e;
       }
@@ -479,9 +484,9 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
         for (int v = 0; v < VW; ++v) {
           const T yi = extrap(xi[v], xq[v], cm[v]);
           const T ayi = extrap(ax[v], axq[v], cm[v]);
-          const double y2 = double(mul_rn(yi, yi));
+          const T y2 = mul_rn(yi, yi);
           sy4[v] += y2 * y2;
-          syay[v] += double(yi) * double(ayi);
+          syay[v] += yi * ayi;
         }
       }
     } else {  // MODE_ADOCH_Y: acc = J y
@@ -493,9 +498,9 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
       for (int v = 0; v < VW; ++v) {
         const T yi = extrap(xi[v], xq[v], cm[v]);
         ay[v] = shifted(acc[v], alpha[v], yi);
-        const double y2 = double(yi) * double(yi);
+        const T y2 = yi * yi;
         sy4[v] += y2 * y2;
-        syay[v] += double(yi) * double(ay[v]);
+        syay[v] += yi * ay[v];
       }
       vstore<T, VW>(reinterpret_cast<T*>(a.ay) + idx, ay);
     }
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(256, 2) pass_rv(PassArgs a) {
 #pragma unroll
       for (int v = 0; v < VW; ++v) {
         const int c = lane * VW + v;
-        const double q[NQ] = {s4[v], sxax[v], esum[v], double(step[v]), sy4[v], syay[v]};
+        const double q[NQ] = {double(s4[v]), double(sxax[v]), esum[v], double(step[v]), double(sy4[v]), double(syay[v])};
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
           if (w == 0) red[k][c] = q[k];
@@ -821,8 +826,18 @@ static void launch_rv(int mode, const PassArgs& a, dim3 grid, cudaStream_t s) {
 }
 
 // replicas per lane of the R > 1 kernel
+// f32 replica vector width (4, or 2 with DCX_RV_VW=2: fewer registers per lane,
+// three resident blocks per SM)
+static int rv_vw_f32() {
+  static const int w = [] {
+    const char* e = std::getenv("DCX_RV_VW");
+    return (e && std::atoi(e) == 2) ? 2 : 4;
+  }();
+  return w;
+}
+
 int replica_vector_width(int R, bool f64) {
-  const int w = f64 ? 2 : 4;
+  const int w = f64 ? 2 : rv_vw_f32();
   return R % w == 0 ? w : 1;
 }
 
@@ -839,9 +854,15 @@ static void launch_pass_vk(int mode, const PassArgs& a, int V, int grid, cudaStr
     }
   } else {
     const int R = a.cfg.R;
-    constexpr int W = 16 / sizeof(T);
-    if (R % W == 0) launch_rv<T, VK, W>(mode, a, dim3(grid, (R + 32 * W - 1) / (32 * W)), s);
-    else launch_rv<T, VK, 1>(mode, a, dim3(grid, (R + 31) / 32), s);
+    const int W = replica_vector_width(R, sizeof(T) == 8);
+    if constexpr (sizeof(T) == 8) {
+      if (W == 2) launch_rv<T, VK, 2>(mode, a, dim3(grid, (R + 63) / 64), s);
+      else launch_rv<T, VK, 1>(mode, a, dim3(grid, (R + 31) / 32), s);
+    } else {
+      if (W == 4) launch_rv<T, VK, 4>(mode, a, dim3(grid, (R + 127) / 128), s);
+      else if (W == 2) launch_rv<T, VK, 2>(mode, a, dim3(grid, (R + 63) / 64), s);
+      else launch_rv<T, VK, 1>(mode, a, dim3(grid, (R + 31) / 32), s);
+    }
   }
 }
 
