@@ -43,6 +43,16 @@ REF_BEST_CUT = 595.0 + 32898.0  # best DOCH cut of the CPU reference over 32 see
 TTS_FRACTION = 0.99  # dc/bench.py:111
 
 
+def traffic_bytes(config: str, kernel: str, iterations: int):
+    """DRAM bytes of one profiled launch of `kernel` on `config` from the committed ncu
+    capture (profiles/r1_traffic.json: dram__bytes_read + dram__bytes_write per iteration)."""
+    try:
+        with open(ROOT / "profiles" / "r1_traffic.json") as f:
+            return float(json.load(f)[f"{config}:{kernel}"]["dram_bytes_per_iteration"]) * iterations
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -259,7 +269,8 @@ def run_ours(args):
     peak = bf16 if prof["bound"] == "tensor" else hbm
     roof = {"bound": prof["bound"], "achieved": achieved if prof["bound"] == "tensor" else
             prof["bytes_per_launch"] / (prof["ms_per_launch"] * 1e-3) / 1e9,
-            "peak": peak, "unit": "TFLOP/s" if prof["bound"] == "tensor" else "GB/s", "traffic": None,
+            "peak": peak, "unit": "TFLOP/s" if prof["bound"] == "tensor" else "GB/s",
+            "traffic": traffic_bytes("k2", prof["kernel"], 10 if prof["kernel"] == "dense_doch_kernel" else 1),
             "kernel": prof["kernel"], "ms_per_launch": prof["ms_per_launch"], "peak_source": src}
     roof["frac"] = roof["achieved"] / roof["peak"]
     its = max_iters_seen + 1

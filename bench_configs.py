@@ -123,8 +123,11 @@ def run(args):
         prof = dc.profile_dominant_kernel(inst, alpha, beta, X0, precision=cfg["precision"], path="multipass",
                                           launches=10)
         gbs = prof["bytes_per_launch"] / (prof["ms_per_launch"] * 1e-3) / 1e9
+        from bench import traffic_bytes
+
         line["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                            "traffic": None, "kernel": prof["kernel"], "ms_per_launch": prof["ms_per_launch"],
+                            "traffic": traffic_bytes(name, prof["kernel"], 1),
+                            "kernel": prof["kernel"], "ms_per_launch": prof["ms_per_launch"],
                             "bytes_per_launch": prof["bytes_per_launch"], "peak_source": src}
     else:
         line["roofline"] = {"bound": "latency", "achieved": None, "peak": None, "unit": "us/iteration",

@@ -1092,7 +1092,11 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    // DCX_DENSE_COOP=0 drops the cooperative attribute (every CTA is still
+    // resident: one per SM, grid <= SM count); Nsight Compute cannot replay a
+    // cooperative cluster launch, so profiling runs use it
+    const char* coop = std::getenv("DCX_DENSE_COOP");
+    cfg.numAttrs = (coop && std::atoi(coop) == 0) ? 1 : 2;
     DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2>, a));
   }
 }
