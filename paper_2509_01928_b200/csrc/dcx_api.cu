@@ -73,6 +73,7 @@ struct dcx_ctx {
   int vk_int = -1;  // VK_UNIFORM / VK_I8 / VK_I16, or -1 for real values
   double scale = 1.0;
   int V32 = 1;
+  int64_t ell_entries = 0;  // 32-row sliced ELL size of the pattern (n <= 65536)
   DevBuf rp, col, col16, vint, v64, v32;
   DenseDev dn;  // dense tensor-core operands (dcx_dense.cu)
   // ---------------------------------------------------------- run state
@@ -196,6 +197,11 @@ CsrDev csr_view(const dcx_ctx* c, bool f64) {
     J.val = c->v32.p;
   }
   J.V = f64 ? 1 : c->V32;
+  J.ell = c->ell_entries;
+  if (J.vk == VK_UNIFORM && J.scale != 0.0) {
+    int ex = 0;
+    J.pow2_uniform = std::frexp(std::fabs(J.scale), &ex) == 0.5;
+  }
   const int64_t rows_per_warp = 32 / J.V;
   const int64_t warps = (c->n + rows_per_warp - 1) / rows_per_warp;
   J.grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 16));
@@ -497,6 +503,13 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
       CK(cudaMemcpy(c->v32.p, f.data(), nnz * 4, cudaMemcpyHostToDevice));
     }
     c->V32 = lanes_for_degree(double(nnz) / double(n));
+    c->ell_entries = 0;
+    if (n_cols <= 65536 && n == n_cols)
+      for (int64_t s0 = 0; s0 < n; s0 += 32) {
+        int64_t mx = 0;
+        for (int64_t i = s0; i < std::min<int64_t>(n, s0 + 32); ++i) mx = std::max<int64_t>(mx, ro[i + 1] - ro[i]);
+        c->ell_entries += 32 * mx;
+      }
     c->have = true;
   });
 }

@@ -16,6 +16,8 @@ struct CsrDev {
   int vk = VK_F64;
   double scale = 1.0;
   int V = 1;     // lanes per row (R = 1 kernels and the operator seam)
+  int64_t ell = 0;  // entries of the 32-row sliced-ELL form of the pattern (persistent kernel, n <= 65536)
+  bool pow2_uniform = false;  // uniform values with a power-of-two scale (sum x, then scale: exact)
   int grid = 1;  // grid of the R = 1 pass / apply kernels
 };
 
@@ -68,6 +70,7 @@ struct SmallPlan {
   size_t smem = 0;
   int threads = 256;
   bool fits = false;
+  bool ell = false;  // sliced-ELL column layout in shared memory
 };
 SmallPlan plan_small(const CsrDev& J, int solver, int window_mode, bool f64);
 void launch_small(const MultiPass& m, const CsrDev& J, const SmallPlan& sp, int p_end, cudaStream_t s);

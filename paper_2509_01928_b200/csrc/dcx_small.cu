@@ -18,6 +18,8 @@ struct SmallArgs {
   int V;
   int p_end;  // stop after executing pass p_end - 1 (chunk end)
   int col_is16;
+  int ell;    // columns held as 32-row sliced ELL (V == 1): one conflict-free load per 32 rows and entry
+  int pow2;   // uniform values, power-of-two scale: sum x_j, multiply once (bit-identical to sum v x_j)
 };
 
 __host__ __device__ constexpr int val_bytes(int vk) {
@@ -26,11 +28,11 @@ __host__ __device__ constexpr int val_bytes(int vk) {
 
 // Shared-memory carve-up (16-byte aligned regions), identical on host and device.
 struct SmemLayout {
-  uint32_t x0, x1, ax0, ax1, ay, rp, col, val, total;
+  uint32_t x0, x1, ax0, ax1, ay, rp, col, val, sofs, total;
 };
 __host__ __device__ inline uint32_t align16(uint64_t v) { return uint32_t((v + 15) & ~uint64_t(15)); }
 __host__ __device__ inline SmemLayout small_layout(int n, uint32_t nnz, int tb, bool adoch, bool exact, bool col16,
-                                                   int vb) {
+                                                   int vb, uint32_t ell = 0) {
   SmemLayout L;
   uint32_t o = 0;
   const uint32_t vec = align16(uint64_t(n) * tb);
@@ -40,8 +42,9 @@ __host__ __device__ inline SmemLayout small_layout(int n, uint32_t nnz, int tb, 
   L.ax1 = o; if (adoch) o += vec;
   L.ay = o; if (adoch && exact) o += vec;
   L.rp = o; o += align16(uint64_t(n + 1) * 4);
-  L.col = o; o += align16(uint64_t(nnz) * (col16 ? 2 : 4));
+  L.col = o; o += ell ? align16(uint64_t(ell) * 2) : align16(uint64_t(nnz) * (col16 ? 2 : 4));
   L.val = o; o += align16(uint64_t(nnz) * vb);
+  L.sofs = o; if (ell) o += align16(uint64_t((n + 31) / 32 + 1) * 4);
   L.total = o;
   return L;
 }
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
   // ---- carve shared memory
   const uint32_t NNZ = __ldg(a.rp + n);
   constexpr int VB = val_bytes(VK);
-  const SmemLayout L = small_layout(n, NNZ, sizeof(T), adoch, exact, s.col_is16, VB);
+  const SmemLayout L = small_layout(n, NNZ, sizeof(T), adoch, exact, s.col_is16, VB, uint32_t(s.ell));
   T* xb0 = reinterpret_cast<T*>(smem + L.x0);
   T* xb1 = reinterpret_cast<T*>(smem + L.x1);
   T* axb0 = reinterpret_cast<T*>(smem + L.ax0);
@@ -91,7 +94,28 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
   __shared__ int flag_stop;
 
   for (int i = threadIdx.x; i <= n; i += blockDim.x) rp[i] = a.rp[i];
-  if (s.col_is16) {
+  uint32_t* sofs = reinterpret_cast<uint32_t*>(smem + L.sofs);
+  if (s.ell) {
+    // 32-row slices: entry k of row i at sofs[i / 32] + 32 k + i % 32
+    __syncthreads();
+    const int ns = (n + 31) / 32;
+    if (threadIdx.x == 0) {
+      uint32_t o = 0;
+      for (int sl = 0; sl < ns; ++sl) {
+        uint32_t mx = 0;
+        for (int i = sl * 32; i < min(n, sl * 32 + 32); ++i) mx = max(mx, rp[i + 1] - rp[i]);
+        sofs[sl] = o;
+        o += 32 * mx;
+      }
+      sofs[ns] = o;
+    }
+    __syncthreads();
+    uint16_t* ell = reinterpret_cast<uint16_t*>(colp);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t base = sofs[i >> 5] + (i & 31), lo = rp[i], len = rp[i + 1] - lo;
+      for (uint32_t k = 0; k < len; ++k) ell[base + 32 * k] = s.col16[lo + k];
+    }
+  } else if (s.col_is16) {
     uint16_t* c16 = reinterpret_cast<uint16_t*>(colp);
     for (uint32_t e = threadIdx.x; e < NNZ; e += blockDim.x) c16[e] = s.col16[e];
   } else {
@@ -142,6 +166,38 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
                     typename EsAcc<VK>::type& es) {
     acc = T(0);
     es = 0;
+    if (s.ell) {  // V == 1: lane = row % 32, column order as in the CSR row
+      if (i < n) {
+        const uint32_t lo = rp[i], len = rp[i + 1] - lo;
+        const uint16_t* ell = reinterpret_cast<const uint16_t*>(colp) + sofs[i >> 5] + (i & 31);
+        if (VK == VK_UNIFORM && s.pow2 && !ymode) {
+          // unit pattern, power-of-two weight: sum x_j in column order, scale once
+          // (bit-identical to sum v x_j); spin sum = len - 2 #negative (x is never -0.0)
+          uint32_t neg = 0;
+          for (uint32_t k = 0; k < len; ++k) {
+            const T xj = xv[ell[32 * k]];
+            acc = add_rn(acc, xj);
+            neg += negbit(xj);
+          }
+          acc = mul_rn(acc, scale);
+          es = typename EsAcc<VK>::type(int(len) - 2 * int(neg));
+        } else {
+          for (uint32_t k = 0; k < len; ++k) {
+            const int j = ell[32 * k];
+            int q;
+            const T v = load_entry<VK, false, T>(valp, lo + k, scale, q);
+            if (ymode) {
+              acc = madd(acc, v, extrap(xv[j], xpv[j], cmv));
+            } else {
+              const T xj = xv[j];
+              acc = madd(acc, v, xj);
+              es += es_term<VK, T>(q, v, xj);
+            }
+          }
+        }
+      }
+      return;
+    }
     if (i < n) {
       const uint32_t lo = rp[i], hi = rp[i + 1];
       for (uint32_t e = lo + sub; e < hi; e += V) {
@@ -294,8 +350,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
 SmallPlan plan_small(const CsrDev& J, int solver, int window_mode, bool f64) {
   SmallPlan sp;
   const bool adoch = solver == DCX_SOLVER_ADOCH;
+  const bool ell = J.V == 1 && J.col16 != nullptr && J.ell > 0 && J.ell < (1ll << 31);
   const SmemLayout L = small_layout((int)J.n, (uint32_t)J.nnz, f64 ? 8 : 4, adoch,
-                                    window_mode == DCX_WINDOW_EXACT, J.col16 != nullptr, val_bytes(J.vk));
+                                    window_mode == DCX_WINDOW_EXACT, J.col16 != nullptr, val_bytes(J.vk),
+                                    ell ? uint32_t(J.ell) : 0u);
+  sp.ell = ell;
   sp.smem = L.total;
   sp.threads = SMALL_THREADS;
   sp.fits = L.total <= 200 * 1024 && J.n <= (1 << 20) && J.nnz < (1ll << 31);
@@ -316,6 +375,8 @@ void launch_small(const MultiPass& m, const CsrDev& J, const SmallPlan& sp, int 
   s.col_is16 = J.col16 != nullptr;
   s.V = J.V;
   s.p_end = p_end;
+  s.ell = sp.ell ? int(J.ell) : 0;
+  s.pow2 = J.pow2_uniform ? 1 : 0;
   if (m.f64) {
     switch (J.vk) {
       case VK_UNIFORM: launch_small_t<double, VK_UNIFORM>(s, sp, st); break;
