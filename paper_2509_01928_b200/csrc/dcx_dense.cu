@@ -66,7 +66,8 @@ struct __align__(64) SyncWords {
   int running;       // replicas of the group still running
   int running_snap;  // snapshot taken by the last arriver
   int p_exec;        // passes executed by the group (resume point / exit record)
-  int pad[9];
+  unsigned int countB, genB;  // second phase (partials written)
+  int pad[7];
 };
 
 struct Args {
@@ -412,27 +413,56 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   if (nt != 0) cfg.hist = nullptr;  // only the nt == 0 CTA of a replica tile writes history
 
   uint32_t kiter = 0, acc_phase = 0;
-  // Warps 0-1 (TMA / MMA) start iteration p+1 right after the group barrier of
-  // iteration p; warps 2-11 first finish the control of iteration p, which
-  // therefore overlaps the next GEMM. The exit test reads the snapshot taken at
-  // the barrier, identical for every thread of every CTA of the group.
-#define TL(k) do { if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 23 + 64 * 256 + p * 8 + (k)] = clock64(); } while (0)
-  for (; p < a.p_end; ++p) {
-    if (p > p_start && __ldcg(&grp->running_snap) == 0) break;
-    TL(0);  // every replica of the group stopped
-    const int cur = p & 1;
-    const bool trace = a.dbg && blockIdx.x == 0 && threadIdx.x == 64 && p < 4096;
-    if (trace) {
-      a.dbg[p * 12 + 0] = clock64();
-      a.dbg[4096 * 13 + p] = globaltimer();
+  // Group synchronisation without CTA-wide barriers in the loop. Per iteration p:
+  //   A(p): every CTA of the replica group wrote x_{p+1} (xh, s8) -> the producers
+  //         may load iteration p+1's operands; its last arriver snapshots the
+  //         running count (the exit test of iteration p+1);
+  //   B(p): every CTA wrote its per-replica partials of p -> control p may sum them;
+  //         its last arriver stamps the device time (time budget of control p).
+  // Each CTA arrives at A right after its update (while GEMM2 still runs) and at B
+  // after the energy GEMM, so the tensor core goes from GEMM2(p) straight into
+  // GEMM1(p+1); the control of iteration p runs on the epilogue warps while
+  // GEMM1(p+1) executes. Generations count completed phases from the launch base.
+  const unsigned int genA0 = *reinterpret_cast<volatile unsigned int*>(&grp->gen);
+  const unsigned int genB0 = *reinterpret_cast<volatile unsigned int*>(&grp->genB);
+  const unsigned int members = NC * a.tiles_n;
+  const int64_t part_stride = (int64_t)a.Rpad * a.tiles_n * 4;  // partials double-buffered by iteration parity
+  auto wait_gen = [&](const unsigned int* g, unsigned int target) {
+    long long t0 = 0;
+    unsigned int polls = 0;
+    while (int(ld_acquire(g) - target) < 0) {
+      if ((++polls & 1023u) == 0) {
+        if (t0 == 0) t0 = clock64();
+        else if (clock64() - t0 > (1ll << 36)) __trap();  // a lost arrival: fail the launch, do not hang
+      }
     }
-    if (warp < 2) {
-      if (warp == 0) {
-      // ---------------------------------------------------------- producer
-      if (lane == 0) {
-        if (a.dbg && blockIdx.x == 0 && p < 4096) a.dbg[4096 * 31 + 64 * 256 + p * 4 + 1] = clock64();
-        fence_async_global();
-        if (a.dbg && blockIdx.x == 0 && p < 4096) a.dbg[4096 * 31 + 64 * 256 + p * 4 + 2] = clock64();
+  };
+  // one arrival per CTA (release: covers the CTA's writes ordered before it by the named barrier)
+  auto arrive = [&](unsigned int* cnt, unsigned int* gen, unsigned int gen_base_next, bool snapshot) {
+    unsigned int old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    if (old == members - 1) {
+      *cnt = 0;
+      if (snapshot) {
+        int run;
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(run) : "l"(&grp->running) : "memory");
+        grp->running_snap = run;
+      } else {
+        grp->stamp = globaltimer();
+      }
+      st_release(gen, gen_base_next);
+    }
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (; p < a.p_end; ++p) {
+        if (p > p_start) {
+          wait_gen(&grp->gen, genA0 + unsigned(p - p_start));  // operands of p are written
+          if (__ldcg(&grp->running_snap) == 0) break;
+        }
+        fence_async_global();  // generic writes (acquired above) before the async-proxy loads
         const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
         if (tr) a.dbg[p * 12 + 5] = clock64();
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
@@ -440,13 +470,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t ph = (kiter / P::STAGES) & 1;
           mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
           const uint32_t fb = smem_u32(&sm.full[s]);
-          if (a.nodata) {  // timing experiment: MMAs on stale stage data, no TMA
-            mbar_arrive(fb);
-            continue;
-          }
           if (leader) mbar_expect_tx(fb, NC * P::STAGE);  // the leader's barrier counts both CTAs' bytes
           unsigned char* st = tiles + s * P::STAGE;
           const int bi = i0 + cta_rank * (TN / NC);  // this CTA's B rows
+          const int cur = p & 1;
           const CUtensorMap* ma = kb < KB1 ? &a.tmA[cur] : &a.tmS[cur];
           const CUtensorMap* mb = kb < KB1 ? &a.tmB : &a.tmQ8;
           const int katom = kb < KB1 ? TK : 2 * TK;  // elements of K per 128-byte atom
@@ -465,14 +492,18 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               tma_load_2d_pair(db, mb, kc + q * katom, bi, fb);
             }
           }
-          if (tr && kb == KB1 - 1) a.dbg[p * 12 + 6] = clock64();
         }
         if (tr) a.dbg[p * 12 + 7] = clock64();
       }
-      __syncwarp();
-    } else if (warp == 1) {
-      // ---------------------------------------------------------- MMA issuer
-      if (lane == 0 && leader) {  // one thread of the (leader) CTA issues every MMA of the tile
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && leader) {  // one thread of the (leader) CTA issues every MMA of the tile
+      for (; p < a.p_end; ++p) {
+        if (p > p_start) {
+          wait_gen(&grp->gen, genA0 + unsigned(p - p_start));  // same exit test as the producer
+          if (__ldcg(&grp->running_snap) == 0) break;
+        }
         const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
         unsigned long long wait_cyc = 0;
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
@@ -480,7 +511,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t ph = (kiter / P::STAGES) & 1;
           const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
-          if (kb == KB1 && a.fence_mode == 4) mbar_wait(smem_u32(&sm.d1free), acc_phase);  // experiment
+          // D2 of iteration p-1 drained by the epilogue before GEMM2(p) overwrites it
+          if (kb == KB1 && p > p_start) mbar_wait(smem_u32(&sm.d1free), (p - 1 - p_start) & 1);
           wait_cyc += clock64() - tw0;
           tc_fence_after();
           const uint32_t s0 = smem_u32(tiles + s * P::STAGE);
@@ -510,21 +542,89 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         if (tr) a.dbg[4096 * 12 + p] = wait_cyc;
         mma_commit_g<NC>(smem_u32(&sm.accf2), uint16_t(0x3u << (2 * psub)));
       }
-      __syncwarp();
+    }
+  } else if (epi) {
+    // ------------------------------------------------------------ epilogue + control
+    auto epi_sync = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    // control of iteration pc (after B(pc)): per-replica sums of the group's tile
+    // partials in a fixed order, then control_after_pass (dcx_device.cuh)
+    auto control = [&](int pc) {
+      if (threadIdx.x == 128) wait_gen(&grp->genB, genB0 + unsigned(pc - p_start + 1));
+      epi_sync();
+      const int half = (a.tiles_n + 1) / 2;
+      const int t0 = h * half, t1 = min(a.tiles_n, t0 + half);
+      const double2* src = reinterpret_cast<const double2*>(a.part + (pc & 1) * part_stride +
+                                                            ((int64_t)rt * a.tiles_n * TM) * 4);
+      double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      for (int tb = t0; tb < t1; tb += 4) {  // 4 tiles in flight, summed in tile order
+        double2 u[4], w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tb + k < t1) {
+            const int64_t e = ((int64_t)(tb + k) * TM + rl) * 2;
+            u[k] = __ldcg(src + e);
+            w[k] = __ldcg(src + e + 1);
+          }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tb + k < t1) {
+            s0 += u[k].x;
+            s1 += u[k].y;
+            s2 += w[k].x;
+            s3 = fmax(s3, w[k].y);
+          }
       }
-    } else if (epi) {
-      // ---------------------------------------------------------- epilogue
+      sm.red2[h][rl][0] = s0;
+      sm.red2[h][rl][1] = s1;
+      sm.red2[h][rl][2] = s2;
+      sm.red2[h][rl][3] = s3;
+      epi_sync();
+      if (h == 0 && r < a.R) {
+        RepCtl c = sm.ctl[rl];
+        if (c.status == DCX_STOP_RUNNING) {
+          double tot[NQ] = {0, 0, 0, 0, 0, 0};
+          tot[Q_S4] = sm.red2[0][rl][0] + sm.red2[1][rl][0];
+          tot[Q_SXAX] = sm.red2[0][rl][1] + sm.red2[1][rl][1];
+          tot[Q_ES] = sm.red2[0][rl][2] + sm.red2[1][rl][2];
+          tot[Q_STEP] = fmax(sm.red2[0][rl][3], sm.red2[1][rl][3]);
+          const double now = double(__ldcg(&grp->stamp) - a.g->t0) * 1e-9;
+          const bool stopped = control_after_pass(c, cfg, r, tot, pc, now);
+          c.step = tot[Q_STEP];
+          sm.ctl[rl] = c;
+          if (nt == 0) {
+            a.ctl[r] = c;
+            if (stopped) {
+              atomicSub(&grp->running, 1);
+              atomicSub(&a.g->running, 1);
+            }
+          }
+        }
+      }
+      epi_sync();
+    };
+    for (; p < a.p_end; ++p) {
+      if (p > p_start) {
+        control(p - 1);
+        if (threadIdx.x == 128) wait_gen(&grp->gen, genA0 + unsigned(p - p_start));  // (complete: B(p-1) follows A(p-1))
+        if (__ldcg(&grp->running_snap) == 0) break;  // the producer and MMA warps exit here too
+      }
+      const int cur = p & 1;
+      if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) {
+        a.dbg[p * 12 + 0] = clock64();
+        a.dbg[4096 * 13 + p] = globaltimer();
+      }
       const RepCtl& c = sm.ctl[rl];
       // the stop decision of control p is known now unless a time budget is set:
       // converged <=> step(x_p - x_{p-1}) <= tol (computed by control p-1), or p == max_iters.
-      // A replica that stops at p keeps x_p in shared memory (no update).
+      // A replica that stops at p keeps x_p (no update).
       const bool stops_now = p > 0 && (c.step <= a.cfg.conv_tol || p >= a.cfg.max_iters);
       const bool budget = a.cfg.budget >= 0.0;
       const bool running = valid && c.status == DCX_STOP_RUNNING && !stops_now;
       const bool write_master = running && budget;  // a budget stop at p would need x_p
       const bool copy_prev = valid && p > 0 && c.pend == p - 1;
       const float alpha = sm.alpha[rl], inv_beta = sm.inv_beta[rl], jl = sm.jl[rl], inv_lam = sm.inv_lam[rl];
-      float s4 = 0.f, sxax = 0.f, es = 0.f, step = 0.f;
+      float s4 = 0.f, sxax = 0.f, step = 0.f;
+      int es = 0;
       const int gbase = i0 + h * 64;
       const int lim = valid ? max(0, min(64, a.n - gbase)) : 0;
       if (copy_prev && lim > 0) {
@@ -539,7 +639,6 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       }
       uint64_t curmask = 0;
       mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
-      TL(1);
       tc_fence_after();
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 11] = clock64();
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
@@ -617,135 +716,53 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }
       }
       tmem_st_wait();
-      // experiment (DCX_DENSE_FENCE=4): GEMM2 waits for the whole update
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&sm.d1free));
-#define TL2(k) do { if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 35 + 64 * 256 + p * 4 + (k)] = clock64(); } while (0)
-      TL2(0);
-      // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i
+      // x_{p+1} operands of this CTA are written: make them visible to the async
+      // proxy of every CTA, then one release arrival at A(p)
+      fence_async_global();
+      epi_sync();
+      if (threadIdx.x == 128) arrive(&grp->count, &grp->gen, genA0 + unsigned(p - p_start + 1), true);
+      if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 1] = clock64();
+      // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i, exact in int32
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
-      TL2(1);
       tc_fence_after();
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t v2[32];
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * 64 + cc * 32, v2);
+      {
+        uint32_t v2[64];
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * 64, v2);
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * 64 + 32, v2 + 32);
         tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sm.d1free));  // D2 drained: GEMM2(p+1) may overwrite it
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float y2 = float(int(v2[j]));
-          if (cc * 32 + j < lim) es += ((curmask >> (cc * 32 + j)) & 1) ? -y2 : y2;
+        for (int j = 0; j < 64; ++j) {
+          const int m = -int((curmask >> j) & 1);
+          const int v = (j < lim) ? int(v2[j]) : 0;
+          es += (v ^ m) - m;
         }
       }
-      TL2(2);
       if (running) prevmask = curmask;
+      if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 2] = clock64();
       sm.red[h][rl][0] = s4;
       sm.red[h][rl][1] = sxax;
-      sm.red[h][rl][2] = es;
+      sm.red[h][rl][2] = float(es);
       sm.red[h][rl][3] = step;
-      if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 15 + 64 * 256 + p * 8 + 6] = clock64();
-        }
-    if (trace) {
-      mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
-      a.dbg[p * 12 + 1] = clock64();
-    }
-    acc_phase ^= 1;
-    tc_fence_before();
-    TL(2);
-    __syncthreads();
-    TL(3);
-    if (trace) a.dbg[p * 12 + 2] = clock64();
-    if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 128) a.dbg[4096 * 15 + 64 * 256 + p * 8 + 7] = clock64();
-    if (threadIdx.x < TM) {
-      const int rr = r0 + threadIdx.x;
-      if (rr < a.R) {
-        // layout [replica tile][spin tile][replica in tile] x 4
-        double* dst = a.part + (((int64_t)rt * a.tiles_n + nt) * TM + threadIdx.x) * 4;
-        const int t = threadIdx.x;
+      epi_sync();
+      if (h == 0 && r < a.R) {
+        // layout [parity][replica tile][spin tile][replica in tile] x 4
+        double* dst = a.part + (p & 1) * part_stride + (((int64_t)rt * a.tiles_n + nt) * TM + rl) * 4;
         double4 v;
-        v.x = double(sm.red[0][t][0]) + double(sm.red[1][t][0]);
-        v.y = double(sm.red[0][t][1]) + double(sm.red[1][t][1]);
-        v.z = double(sm.red[0][t][2]) + double(sm.red[1][t][2]);
-        v.w = fmax(double(sm.red[0][t][3]), double(sm.red[1][t][3]));
+        v.x = double(sm.red[0][rl][0]) + double(sm.red[1][rl][0]);
+        v.y = double(sm.red[0][rl][1]) + double(sm.red[1][rl][1]);
+        v.z = double(sm.red[0][rl][2]) + double(sm.red[1][rl][2]);
+        v.w = fmax(double(sm.red[0][rl][3]), double(sm.red[1][rl][3]));
         *reinterpret_cast<double4*>(dst) = v;
       }
+      epi_sync();
+      if (threadIdx.x == 128) arrive(&grp->countB, &grp->genB, genB0 + unsigned(p - p_start + 1), false);
+      acc_phase ^= 1;
     }
-    unsigned long long* pr = (a.dbg && blockIdx.x == 0 && p < 4096) ? a.dbg + 4096 * 15 + 64 * 256 + p * 8 : nullptr;
-    if (pr && (threadIdx.x == 64 || threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 128))
-      pr[threadIdx.x == 64 ? 0 : threadIdx.x == 0 ? 1 : threadIdx.x == 32 ? 2 : 3] = clock64();
-    if (a.fence_mode == 0 || a.fence_mode == 2) {
-      if (epi) fence_async_global();  // xh / s8 written here are read by TMA next iteration
-    } else if (a.fence_mode == 1) {
-      __syncthreads();
-      if (threadIdx.x == 0) fence_async_global();  // experiment: one proxy fence per CTA
-    }
-    if (a.dbg && threadIdx.x == 0 && p < 64) a.dbg[4096 * 14 + p * 256 + blockIdx.x] = globaltimer();  // arrival
-    if (pr && (threadIdx.x == 0 || threadIdx.x == 128)) pr[threadIdx.x == 0 ? 4 : 5] = clock64();
-    TL(4);
-    __syncthreads();
-    TL(5);
-    if (trace) a.dbg[4096 * 14 + 64 * 256 + p] = clock64();  // every thread done (incl. proxy fences)
-    group_barrier(grp, NC * a.tiles_n);
-    TL(6);
-    if (a.dbg && blockIdx.x == 0 && p < 4096 && threadIdx.x == 0) a.dbg[4096 * 31 + 64 * 256 + p * 4 + 0] = clock64();
-    if (trace) a.dbg[p * 12 + 3] = clock64();
-    if (warp < 2) continue;  // TMA / MMA go on with the next iteration
-    // ---------------------------------------------------------- control (warps 4-11)
-    if (epi) {
-      // two threads per replica, each summing half of the spin tiles in a fixed
-      // order straight from L2 (written by the other CTAs of the group)
-      const int half = (a.tiles_n + 1) / 2;
-      const int t0 = h * half, t1 = min(a.tiles_n, t0 + half);
-      const double2* src = reinterpret_cast<const double2*>(a.part + ((int64_t)rt * a.tiles_n * TM) * 4);
-      double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-      for (int tb = t0; tb < t1; tb += 4) {  // 4 tiles in flight, summed in tile order
-        double2 u[4], w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (tb + k < t1) {
-            const int64_t e = ((int64_t)(tb + k) * TM + rl) * 2;
-            u[k] = __ldcg(src + e);
-            w[k] = __ldcg(src + e + 1);
-          }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (tb + k < t1) {
-            s0 += u[k].x;
-            s1 += u[k].y;
-            s2 += w[k].x;
-            s3 = fmax(s3, w[k].y);
-          }
-      }
-      sm.red2[h][rl][0] = s0;
-      sm.red2[h][rl][1] = s1;
-      sm.red2[h][rl][2] = s2;
-      sm.red2[h][rl][3] = s3;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (h == 0 && r < a.R) {
-        RepCtl c = sm.ctl[rl];
-        if (c.status == DCX_STOP_RUNNING) {
-          double tot[NQ] = {0, 0, 0, 0, 0, 0};
-          tot[Q_S4] = sm.red2[0][rl][0] + sm.red2[1][rl][0];
-          tot[Q_SXAX] = sm.red2[0][rl][1] + sm.red2[1][rl][1];
-          tot[Q_ES] = sm.red2[0][rl][2] + sm.red2[1][rl][2];
-          tot[Q_STEP] = fmax(sm.red2[0][rl][3], sm.red2[1][rl][3]);
-          const double now = double(__ldcg(&grp->stamp) - a.g->t0) * 1e-9;
-          const bool stopped = control_after_pass(c, cfg, r, tot, p, now);
-          c.step = tot[Q_STEP];
-          sm.ctl[rl] = c;
-          if (nt == 0) {
-            a.ctl[r] = c;
-            if (stopped) {
-              atomicSub(&grp->running, 1);
-              atomicSub(&a.g->running, 1);
-            }
-          }
-        }
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-    }
-    if (trace) a.dbg[p * 12 + 4] = clock64();
-    TL(7);
+    // the control of the last iteration of this launch (the next launch resumes at p)
+    if (p == a.p_end && p > p_start) control(p - 1);
   }
   // ---------------------------------------------------------------- teardown
   if (epi) {
@@ -998,7 +1015,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   }
   if (!reuse) {
     DCK(cudaMalloc(&d.best8, vec));
-    DCK(cudaMalloc(&d.part, sizeof(double) * 4 * (d.npad / 128) * d.Rpad));
+    DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 4 * (d.npad / 128) * d.Rpad));  // by iteration parity
     DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128)));
   }
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
@@ -1013,8 +1030,8 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) cudaFree(d.dbg);
   d.dbg = nullptr;
   if (std::getenv("DCX_DENSE_TRACE")) {
-    DCK(cudaMalloc(&d.dbg, (4096 * 39 + 64 * 256) * 8));
-    DCK(cudaMemsetAsync(d.dbg, 0, (4096 * 39 + 64 * 256) * 8, s));
+    DCK(cudaMalloc(&d.dbg, 4096 * 14 * 8));
+    DCK(cudaMemsetAsync(d.dbg, 0, 4096 * 14 * 8, s));
   }
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
@@ -1112,148 +1129,35 @@ void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s) {
 
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) {  // phase breakdown of CTA 0 (DCX_DENSE_TRACE=1)
-    std::vector<unsigned long long> t(4096 * 12);
+    std::vector<unsigned long long> t(4096 * 14);
     DCK(cudaMemcpyAsync(t.data(), d.dbg, t.size() * 8, cudaMemcpyDeviceToHost, s));
     DCK(cudaStreamSynchronize(s));
-    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const unsigned long long* gt = t.data() + 4096 * 13;
+    int last = 1;
+    while (last + 1 < 4096 && gt[last + 1]) ++last;
+    if (last > 2)
+      std::fprintf(stderr, "[dcx dense trace] SM clock %.0f MHz, %.2f us/iter over %d iterations\n",
+                   double(t[last * 12] - t[12]) / double(gt[last] - gt[1]) * 1e3,
+                   double(gt[last] - gt[1]) / 1e3 / (last - 1), last - 1);
+    double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int cnt = 0;
-    std::vector<unsigned long long> tw(4096);
-    DCK(cudaMemcpyAsync(tw.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 12, 4096 * 8,
-                        cudaMemcpyDeviceToHost, s));
-    DCK(cudaStreamSynchronize(s));
-    std::vector<unsigned long long> gt(4096);
-    DCK(cudaMemcpyAsync(gt.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 13, 4096 * 8,
-                        cudaMemcpyDeviceToHost, s));
-    DCK(cudaStreamSynchronize(s));
-    {
-      int last = 1;
-      while (last + 1 < 4096 && t[(last + 1) * 12]) ++last;
-      if (last > 2)
-        std::fprintf(stderr, "[dcx dense trace] SM clock during the run: %.0f MHz (%d iterations, %.2f us/iter)\n",
-                     double(t[last * 12] - t[12]) / double(gt[last] - gt[1]) * 1e3, last - 1,
-                     double(gt[last] - gt[1]) / 1e3 / (last - 1));
-    }
-    {  // barrier arrival spread across the CTAs of group 0 (first 64 iterations)
-      std::vector<unsigned long long> ar(64 * 256);
-      DCK(cudaMemcpyAsync(ar.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 14, ar.size() * 8,
-                          cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      const int members = d.nc * int(d.npad / 128);
-      double spread = 0;
-      int cntp = 0;
-      for (int p = 2; p < 64; ++p) {
-        unsigned long long lo = ~0ull, hi = 0;
-        for (int b = 0; b < members; ++b) {
-          const unsigned long long v = ar[p * 256 + b];
-          if (!v) continue;
-          lo = std::min(lo, v);
-          hi = std::max(hi, v);
-        }
-        if (hi > lo) { spread += double(hi - lo); ++cntp; }
-      }
-      if (cntp) std::fprintf(stderr, "[dcx dense trace] group-0 barrier arrival spread %.2f us\n", spread / cntp / 1e3);
-      std::vector<unsigned long long> te(4096);
-      DCK(cudaMemcpyAsync(te.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 14 + 64 * 256, 4096 * 8,
-                          cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      double pre = 0, bar = 0;
-      int c2 = 0;
-      for (int p = 1; p < 4096 && t[p * 12 + 4] && te[p]; ++p, ++c2) {
-        pre += double(te[p]) - double(t[p * 12 + 2]);
-        bar += double(t[p * 12 + 3]) - double(te[p]);
-      }
-      if (c2)
-        std::fprintf(stderr, "[dcx dense trace] kcycles: partials+proxy fences %.2f, group barrier %.2f\n",
-                     pre / c2 / 1e3, bar / c2 / 1e3);
-      std::vector<unsigned long long> pq(4096 * 8);
-      DCK(cudaMemcpyAsync(pq.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 15 + 64 * 256,
-                          pq.size() * 8, cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      int c3 = 0;
-      for (int p = 1; p < 4096 && t[p * 12 + 4] && pq[p * 8 + 6]; ++p, ++c3)
-        for (int k = 0; k < 8; ++k) q[k] += double(pq[p * 8 + k]) - double(t[p * 12 + 2]);
-      if (c3)
-        std::fprintf(stderr,
-                     "[dcx dense trace] after sync1 (kcycles): part-store t64 %.2f t0 %.2f t32 %.2f t128 %.2f | "
-                     "pre-sync2 t0 %.2f t128 %.2f | t128 BEFORE sync1 %.2f | t128 right after sync1 %.2f\n",
-                     q[0] / c3 / 1e3, q[1] / c3 / 1e3, q[2] / c3 / 1e3, q[3] / c3 / 1e3, q[4] / c3 / 1e3,
-                     q[5] / c3 / 1e3, q[6] / c3 / 1e3, q[7] / c3 / 1e3);
-    }
-    {
-      std::vector<unsigned long long> tl(4096 * 8);
-      DCK(cudaMemcpyAsync(tl.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 23 + 64 * 256,
-                          tl.size() * 8, cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      int c4 = 0;
-      for (int p = 2; p + 1 < 4096 && tl[(p + 1) * 8] && tl[p * 8 + 7]; ++p, ++c4) {
-        for (int k = 1; k < 8; ++k) q[k] += double(tl[p * 8 + k]) - double(tl[p * 8 + k - 1]);
-        q[0] += double(tl[(p + 1) * 8]) - double(tl[p * 8 + 7]);
-      }
-      if (c4)
-        std::fprintf(stderr,
-                     "[dcx dense trace] epilogue thread timeline (kcycles): top->accf1 %.2f, update+es %.2f, "
-                     "sync1 %.2f, partials/fence %.2f, sync2 %.2f, group barrier %.2f, control %.2f, loop %.2f\n",
-                     q[1] / c4 / 1e3, q[2] / c4 / 1e3, q[3] / c4 / 1e3, q[4] / c4 / 1e3, q[5] / c4 / 1e3,
-                     q[6] / c4 / 1e3, q[7] / c4 / 1e3, q[0] / c4 / 1e3);
-    }
-    {
-      std::vector<unsigned long long> tp(4096 * 4);
-      DCK(cudaMemcpyAsync(tp.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 31 + 64 * 256,
-                          tp.size() * 8, cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      double q[3] = {0, 0, 0};
-      int c5 = 0;
-      for (int p = 2; p + 1 < 4096 && tp[(p + 1) * 4 + 2] && tp[p * 4]; ++p, ++c5) {
-        q[0] += double(tp[(p + 1) * 4 + 1]) - double(tp[p * 4]);      // barrier exit -> next loop top (producer)
-        q[1] += double(tp[(p + 1) * 4 + 2]) - double(tp[(p + 1) * 4 + 1]);  // proxy fence
-      }
-      if (c5)
-        std::fprintf(stderr, "[dcx dense trace] producer: group barrier -> loop top %.2f kcycles, proxy fence %.2f\n",
-                     q[0] / c5 / 1e3, q[1] / c5 / 1e3);
-      std::vector<unsigned long long> tl(4096 * 8), te2(4096 * 4);
-      DCK(cudaMemcpyAsync(tl.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 23 + 64 * 256,
-                          tl.size() * 8, cudaMemcpyDeviceToHost, s));
-      DCK(cudaMemcpyAsync(te2.data(), reinterpret_cast<unsigned long long*>(d.dbg) + 4096 * 35 + 64 * 256,
-                          te2.size() * 8, cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      double e[4] = {0, 0, 0, 0};
-      int c6 = 0;
-      for (int p = 2; p < 4096 && te2[p * 4 + 2] && tl[p * 8 + 2]; ++p, ++c6) {
-        e[0] += double(te2[p * 4]) - double(tl[p * 8 + 1]);
-        e[1] += double(te2[p * 4 + 1]) - double(te2[p * 4]);
-        e[2] += double(te2[p * 4 + 2]) - double(te2[p * 4 + 1]);
-        e[3] += double(tl[p * 8 + 2]) - double(te2[p * 4 + 2]);
-      }
-      if (c6)
-        std::fprintf(stderr, "[dcx dense trace] epilogue split: update %.2f, wait accf2 %.2f, es %.2f, red %.2f kcycles\n",
-                     e[0] / c6 / 1e3, e[1] / c6 / 1e3, e[2] / c6 / 1e3, e[3] / c6 / 1e3);
-    }
-    double wsum = 0;
-    for (int p = 1; p < 4096 && t[p * 12 + 4]; ++p) wsum += double(tw[p]);
-    double m[6] = {0, 0, 0, 0, 0, 0};
-    for (int p = 1; p < 4096 && t[p * 12 + 4]; ++p, ++cnt) {
-      for (int k = 0; k < 4; ++k) acc[k] += double(t[p * 12 + k + 1]) - double(t[p * 12 + k]);
-      const double base = double(t[p * 12 + 5]);
-      m[0] += double(t[p * 12 + 6]) - base;   // producer: last f16 TMA issued
-      m[1] += double(t[p * 12 + 7]) - base;   // producer: last TMA issued
-      m[2] += double(t[p * 12 + 8]) - base;   // MMA: first stage consumed
-      m[3] += double(t[p * 12 + 9]) - base;   // MMA: last f16 MMA issued
-      m[4] += double(t[p * 12 + 10]) - base;  // MMA: last MMA issued
-      m[5] += double(t[p * 12 + 11]) - base;  // epilogue: GEMM1 complete (accf1)
+    for (int p = 2; p < last; ++p, ++cnt) {
+      const double b0 = double(t[p * 12 + 5]);      // producer: first TMA of p
+      m[0] += double(t[p * 12 + 8]) - b0;            // first MMA
+      m[1] += double(t[p * 12 + 9]) - b0;            // last GEMM1 MMA issued
+      m[2] += double(t[p * 12 + 10]) - b0;           // last MMA issued
+      m[3] += double(t[p * 12 + 11]) - b0;           // epilogue: GEMM1 complete
+      m[4] += double(t[p * 12 + 1]) - double(t[p * 12 + 11]);  // update (to the A arrival)
+      m[5] += double(t[p * 12 + 2]) - double(t[p * 12 + 1]);   // wait GEMM2 + energy
+      m[6] += double(t[(p + 1) * 12 + 5]) - b0;      // producer: iteration period
+      m[7] += double(t[4096 * 12 + p]);              // MMA thread waiting on full[]
     }
     if (cnt)
       std::fprintf(stderr,
-                   "[dcx dense trace] mainloop kcycles from first TMA: lastTMA16 %.2f lastTMA %.2f firstMMA %.2f "
-                   "lastMMA16 %.2f lastMMA %.2f gemm1done %.2f | MMA thread waiting on full[] %.2f\n",
+                   "[dcx dense trace] kcycles from the first TMA of p: firstMMA %.2f lastMMA16 %.2f lastMMA %.2f "
+                   "gemm1done %.2f | update %.2f, gemm2+energy %.2f | period %.2f | MMA waiting on full[] %.2f\n",
                    m[0] / cnt / 1e3, m[1] / cnt / 1e3, m[2] / cnt / 1e3, m[3] / cnt / 1e3, m[4] / cnt / 1e3,
-                   m[5] / cnt / 1e3, wsum / cnt / 1e3);
-    if (cnt)
-      std::fprintf(stderr,
-                   "[dcx dense trace] %d iters, kcycles/iter (CTA 0, warp 2 view): gemms+epilogue %.2f drain %.2f "
-                   "barrier %.2f control %.2f\n",
-                   cnt, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3);
+                   m[5] / cnt / 1e3, m[6] / cnt / 1e3, m[7] / cnt / 1e3);
   }
   tc::unpack_results<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(d.xm[0]),
                                            reinterpret_cast<const float*>(d.xm[1]),
