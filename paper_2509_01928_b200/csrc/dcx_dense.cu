@@ -148,6 +148,20 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar & 0xFEFFFFFFu)
       : "memory");
 }
+// Cube root for the dense epilogue, whose arguments are normal floats or zero
+// (t = (J + aI)x / beta ~ x^3 with x ~ sqrt(alpha / beta) >= 1e-10): MUFU
+// log2 / exp2 estimate and one Newton step with the reciprocal of r^2 + 1e-38,
+// so t = 0 gives +0 without a branch or select (<= 1 ulp from cbrtf on normal
+// arguments; denormal arguments would flush to zero).
+__device__ __forceinline__ float cbrt_lean(float t) {
+  const float a = fabsf(t);
+  float l, r, rc;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaf(r, r, 1e-38f)));
+  r = fmaf(fmaf(a, rc, -r), 1.0f / 3.0f, r);
+  return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
+}
 // pair TMA multicast to the CTAs in `mask` (same smem offset in each); every
 // destination's pair leader barrier receives that destination's bytes
 __device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar,
@@ -661,7 +675,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             for (int u = 0; u < 2; ++u) {
               const float x = __uint_as_float(xv[j + u]);
               const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j + u]));
-              nx[u] = cbrt_fast(ax * inv_beta);
+              nx[u] = cbrt_lean(ax * inv_beta);
               const float x2 = x * x;
               s4 = fmaf(x2, x2, s4);
               sxax = fmaf(x, ax, sxax);
@@ -715,11 +729,15 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 4);
         }
       }
+      const bool tr128 = a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096;
+      if (tr128) a.dbg[p * 12 + 3] = clock64();
       tmem_st_wait();
       // x_{p+1} operands of this CTA are written: make them visible to the async
       // proxy of every CTA, then one release arrival at A(p)
       fence_async_global();
+      if (tr128) a.dbg[p * 12 + 4] = clock64();
       epi_sync();
+      if (tr128) a.dbg[p * 12 + 6] = clock64();
       if (threadIdx.x == 128) arrive(&grp->count, &grp->gen, genA0 + unsigned(p - p_start + 1), true);
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 1] = clock64();
       // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i, exact in int32
@@ -1139,7 +1157,7 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
       std::fprintf(stderr, "[dcx dense trace] SM clock %.0f MHz, %.2f us/iter over %d iterations\n",
                    double(t[last * 12] - t[12]) / double(gt[last] - gt[1]) * 1e3,
                    double(gt[last] - gt[1]) / 1e3 / (last - 1), last - 1);
-    double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double m[8] = {0, 0, 0, 0, 0, 0, 0, 0}, u[4] = {0, 0, 0, 0};
     int cnt = 0;
     for (int p = 2; p < last; ++p, ++cnt) {
       const double b0 = double(t[p * 12 + 5]);      // producer: first TMA of p
@@ -1151,7 +1169,14 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
       m[5] += double(t[p * 12 + 2]) - double(t[p * 12 + 1]);   // wait GEMM2 + energy
       m[6] += double(t[(p + 1) * 12 + 5]) - b0;      // producer: iteration period
       m[7] += double(t[4096 * 12 + p]);              // MMA thread waiting on full[]
+      u[0] += double(t[p * 12 + 3]) - double(t[p * 12 + 11]);  // update loop
+      u[1] += double(t[p * 12 + 4]) - double(t[p * 12 + 3]);   // tmem_st wait + proxy fence
+      u[2] += double(t[p * 12 + 6]) - double(t[p * 12 + 4]);   // epilogue barrier
+      u[3] += double(t[p * 12 + 1]) - double(t[p * 12 + 6]);   // arrival
     }
+    if (cnt)
+      std::fprintf(stderr, "[dcx dense trace] update split kcycles: loop %.2f fence %.2f epi-sync %.2f arrive %.2f\n",
+                   u[0] / cnt / 1e3, u[1] / cnt / 1e3, u[2] / cnt / 1e3, u[3] / cnt / 1e3);
     if (cnt)
       std::fprintf(stderr,
                    "[dcx dense trace] kcycles from the first TMA of p: firstMMA %.2f lastMMA16 %.2f lastMMA %.2f "
