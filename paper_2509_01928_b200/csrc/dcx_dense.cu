@@ -11,11 +11,14 @@
 //   D1[r][i] = sum_j Xh[r][j] Q[i][j]   kind::f16, Xh = f16(x / lambda_r), Q = J / jscale (exact)
 //   D2[r][i] = sum_j S8[r][j] Q8[i][j]  kind::i8,  S8 = sign(x) in int8, Q8 = Q in int8 (exact, s32 acc)
 // One persistent cooperative kernel runs all iterations: a 4-stage TMA ->
-// tcgen05.mma pipeline per 128x128 tile (fp32 / s32 accumulators in TMEM),
-// a TMEM -> register epilogue that applies the DC update and
-// produces the per-replica partials, one grid barrier per iteration, and the
+// tcgen05.mma pipeline per 128x128 tile (fp32 / s32 accumulators in TMEM;
+// CTA pairs with cta_group::2 when R % 256 == 0), a TMEM -> register epilogue
+// that applies the DC update and produces the per-replica partials, and the
 // per-replica control (dcx_device.cuh) evaluated redundantly by every CTA of a
-// replica tile so no second barrier is needed.
+// replica tile. The CTAs of a replica group synchronise through two
+// generation counters per iteration (operands ready / partials ready) instead
+// of a grid barrier, so GEMM2 of iteration p overlaps the update and the
+// control of p overlaps GEMM1 of p+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -87,9 +90,7 @@ struct Args {
   RunCfg cfg;
   int n, npad, R, Rpad, tiles_n, p_end;
   float jscale;
-  int nodata;  // DCX_DENSE_NODATA timing experiment (wrong results)
   int mc;          // NC = 2: clusters of two pairs sharing the A tiles by TMA multicast
-  int fence_mode;  // DCX_DENSE_FENCE experiments: 1 single proxy fence per CTA, 2 no xh/s8 stores, 3 no fence
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -296,34 +297,8 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid barrier (all CTAs co-resident: cooperative launch). The last arriver
-// stamps the device clock and snapshots the running-replica count so every
-// CTA takes identical time-budget and exit decisions.
-__device__ __forceinline__ void group_barrier(SyncWords* s, unsigned int members) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int gen = ld_acquire(&s->gen);
-    // arrival with release semantics: cumulative over the CTA's writes ordered
-    // before it by bar.sync (no separate fence round trip)
-    unsigned int old;
-    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&s->count) : "memory");
-    if (old == members - 1) {
-      s->count = 0;
-      s->stamp = globaltimer();
-      int run;
-      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(run) : "l"(&s->running) : "memory");
-      s->running_snap = run;
-      st_release(&s->gen, gen + 1);
-    } else {
-      while (ld_acquire(&s->gen) == gen) {
-      }
-    }
-  }
-  __syncthreads();
-}
-
 struct __align__(8) Smem {
-  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2, d1free;
+  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2, d2free;
   uint32_t tmem_base;
   int pad;
   float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
@@ -333,9 +308,9 @@ struct __align__(8) Smem {
 };
 
 // Warp roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM
-// owner), warps 2-3 = control helpers, warps 4-11 = epilogue. Epilogue warp w
+// owner), warps 2-3 idle, warps 4-11 = epilogue + control. Epilogue warp w
 // reads TMEM lane quadrant (w % 4) and spin-column half (w - 4) / 4; the
-// CTA's 128 x 128 f32 master state lives in shared memory for the whole run.
+// CTA's 128 x 128 f32 master state lives in TMEM columns [XCOL, XCOL + 128).
 template <int NC>
 __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_constant__ Args a) {
   using P = Pipe<NC>;
@@ -364,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     }
     mbar_init(smem_u32(&sm.accf1), 1);
     mbar_init(smem_u32(&sm.accf2), 1);
-    mbar_init(smem_u32(&sm.d1free), 8);  // one arrive per epilogue warp
+    mbar_init(smem_u32(&sm.d2free), 8);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -526,7 +501,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
           // D2 of iteration p-1 drained by the epilogue before GEMM2(p) overwrites it
-          if (kb == KB1 && p > p_start) mbar_wait(smem_u32(&sm.d1free), (p - 1 - p_start) & 1);
+          if (kb == KB1 && p > p_start) mbar_wait(smem_u32(&sm.d2free), (p - 1 - p_start) & 1);
           wait_cyc += clock64() - tw0;
           tc_fence_after();
           const uint32_t s0 = smem_u32(tiles + s * P::STAGE);
@@ -717,7 +692,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           for (int j = 0; j < 8; ++j) sv[j] = reinterpret_cast<const uint32_t*>(ss)[j];
         }
         tmem_st32(xaddr + cc * 32, nv);
-        if (running && lim > 0 && a.fence_mode != 2) {
+        if (running && lim > 0) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) *reinterpret_cast<uint4*>(hn + cc * 32 + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
           if (write_master) {
@@ -750,7 +725,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&sm.d1free));  // D2 drained: GEMM2(p+1) may overwrite it
+        if (lane == 0) mbar_arrive(smem_u32(&sm.d2free));  // D2 drained: GEMM2(p+1) may overwrite it
 #pragma unroll
         for (int j = 0; j < 64; ++j) {
           const int m = -int((curmask >> j) & 1);
@@ -1099,8 +1074,6 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.tiles_n = int(d.npad / 128);
   a.p_end = p_end;
   a.jscale = d.jscale;
-  a.nodata = std::getenv("DCX_DENSE_NODATA") ? 1 : 0;
-  a.fence_mode = std::getenv("DCX_DENSE_FENCE") ? std::atoi(std::getenv("DCX_DENSE_FENCE")) : 0;
   a.mc = 0;
   if (d.nc == 2 && (d.npad / 128) % 2 == 0) {
     const char* e = std::getenv("DCX_DENSE_MC");
