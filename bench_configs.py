@@ -9,6 +9,8 @@ single-GPU configs through the same public API and report the same JSON keys:
       multipass, pass_rn). HBM bound.
   e7  configs[3]: Erdos-Renyi n = 1e7, degree 8, unit MaxCut, 1 replica, DOCH,
       eta = 1 (f32 multipass, pass_r1). HBM / L2-gather bound.
+  r8  configs[4] on one GPU: random 3-regular n = 1e8, unit MaxCut, 1 replica,
+      DOCH, eta = 1, 20 iterations (the 8-GPU row-partitioned run is dist.py).
 
 Algorithmic bytes per iteration (the HBM roofline numerator):
 nnz * (4 + value bytes) + (n + 1) * 4 + R * n * 4 * 2.
@@ -42,11 +44,11 @@ def _instance(name):
         v, c, o = synth.torus(1000, seed=0)
         J = dc.CsrCoupling(10**6, v, c, o, validate=False)
         return dc.ProblemInstance(coupling=J), 4.0, 8.0e9, (v, c, o)
-    if name == "e7":
-        v, c, o, co = synth.erdos_renyi(10**7, 8, seed=0)
-        J = dc.CsrCoupling(10**7, v, c, o, validate=False)
+    if name in ("e7", "r8"):
+        n = 10**7 if name == "e7" else 10**8
+        v, c, o, co = synth.erdos_renyi(n, 8, seed=0) if name == "e7" else synth.random_regular3(n, seed=0)
+        J = dc.CsrCoupling(n, v, c, o, validate=False)
         # Wigner estimate (n >= 1e4) of dc/spectral.py:175-189 at eta = 1
-        n = 10**7
         s1, s2 = float(v.sum()), float((v * v).sum())
         cnt = n * (n - 1)
         mean = s1 / cnt
@@ -63,6 +65,7 @@ CFG = {
     "g1": dict(R=100, max_iters=1000, precision="f64", desc="800-spin G1-shape MaxCut, eta=0.25, DOCH, 100 seeds"),
     "t6": dict(R=256, max_iters=200, precision="f32", desc="1000x1000 +-1 torus, 256 replicas, DOCH, eta=1"),
     "e7": dict(R=1, max_iters=100, precision="f32", desc="Erdos-Renyi n=1e7 deg 8 unit MaxCut, 1 replica, DOCH, eta=1"),
+    "r8": dict(R=1, max_iters=20, precision="f32", desc="random 3-regular n=1e8 unit MaxCut, 1 replica, DOCH, eta=1, 1 GPU"),
 }
 
 
@@ -72,7 +75,7 @@ def cpu_sample(name, inst, alpha, beta, arrays, budget_s=20.0):
 
     op = orc.Operator(arrays)
     n = op.n
-    iters = {"g1": 1000, "t6": 20, "e7": 3}[name]
+    iters = {"g1": 1000, "t6": 20, "e7": 3, "r8": 1}[name]
     upd, t0, r = 0, time.perf_counter(), 0
     while True:
         out = orc.run(op, alpha, beta, solver="doch", max_iters=iters, seed=r, trace_stride=1)
