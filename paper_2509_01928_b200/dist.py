@@ -27,6 +27,7 @@ device buffers; with gloo (CPU transport) they are staged through host memory.
 
 from __future__ import annotations
 
+import contextlib
 import time
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -195,7 +196,7 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         conv_tol=CONVERGENCE_TOL, descent_tol=DESCENT_WARN_TOL, record_states=0,
         path=_native.PATH["multipass"], chunk=0, reserved=0)
     stream = (torch.cuda.ExternalStream(ctx.stream(), device=tdev) if tdev.type == "cuda" else None)
-    with (torch.cuda.stream(stream) if stream is not None else _nullcontext()):
+    with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
         ctx.dist_begin(prm, alpha, beta, X0[:, r0:r1], X[0].data_ptr(), X[1].data_ptr(), qs.data_ptr(),
                        qm.data_ptr())
         offset = time.perf_counter() - t_entry
@@ -228,11 +229,3 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
     xs = rb.unpad(full_x.cpu().numpy().T)
     return assemble_results(ctx, solver, R, best, xs, offset, getattr(instance, "cut_offset", None), seeds,
                             path="row-partitioned")
-
-
-class _nullcontext:
-    def __enter__(self):
-        return None
-
-    def __exit__(self, *a):
-        return False
