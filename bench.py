@@ -172,7 +172,7 @@ def run_reference(args):
     world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
     if rank != 0:
         return
-    n_rep, iters = 64, 1000  # ~10 s of host work per step (replicas converge in ~150-250 iterations)
+    n_rep, iters = 256, 1000  # ~10 s of host work per step (replicas converge in ~150-250 iterations)
     for _ in range(args.warmup):
         cpu_sample(1, 20)
     vals, times = [], []
@@ -282,9 +282,9 @@ def run_ours(args):
         launches_total = args.steps * (-(-its // MAX_ITERS) + 3)
     cpu = None
     if rank == 0:
-        v, dt, _ = cpu_sample(64, 1000)
+        v, dt, _ = cpu_sample(256, 1000)
         cpu = {"value": v, "unit": "spin-updates/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"64 replicas x <= 1000 DOCH iterations (to convergence), sequential, numpy/OpenBLAS dgemv "
+               "sample": f"256 replicas x <= 1000 DOCH iterations (to convergence), sequential, numpy/OpenBLAS dgemv "
                          f"with {os.cpu_count()} BLAS threads ({dt:.1f} s)"}
     if rank == 0:
         mean_tts = float(np.mean(tts)) if tts else None
