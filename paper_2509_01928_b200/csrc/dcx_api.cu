@@ -712,7 +712,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     int slots;
     if (R == 1) {
       c->mp.grid = c->J.grid;
-      slots = c->mp.grid * 8;
+      slots = c->mp.grid;  // one partial slot per block (pass_r1)
     } else {
       // pass_rv: grid.y = replica chunks, grid.x = row blocks, one partial slot per row block;
       // two resident 256-thread blocks per SM (the kernel needs up to 128 registers)

@@ -23,17 +23,35 @@ struct RowOut {
   double s4 = 0, sxax = 0, es = 0, step = 0, sy4 = 0, syay = 0;
 };
 
+// The replica's control values the epilogue needs, in registers.
+template <typename T>
+struct RowCtl {
+  T alpha, beta, ibeta, cm;
+  int pend;
+  bool running;
+};
+template <typename T>
+__device__ __forceinline__ RowCtl<T> row_ctl(const RepCtl& c, int p) {
+  RowCtl<T> k;
+  k.alpha = T(c.alpha);
+  k.beta = T(c.beta);
+  k.ibeta = inv_beta(k.beta);
+  k.cm = T(p & 1 ? c.cm[1] : c.cm[0]);
+  k.pend = c.pend;
+  k.running = c.status == DCX_STOP_RUNNING;
+  return k;
+}
+
 template <typename T, int MODE>
-__device__ __forceinline__ void row_epilogue(const PassArgs& a, const RepCtl& c, int p, int64_t idx, T acc,
+__device__ __forceinline__ void row_epilogue(const PassArgs& a, const RowCtl<T>& c, int p, int64_t idx, T acc,
                                              double esrow, RowOut<T, MODE>& o) {
   const T* xcur = reinterpret_cast<const T*>(a.x[p & 1]);
   T* xnext = reinterpret_cast<T*>(a.x[(p + 1) & 1]);
-  const T alpha = T(c.alpha), beta = T(c.beta);
+  const T alpha = c.alpha;
   if constexpr (MODE == MODE_ADOCH_Y) {
     // acc = J y ; y recomputed identically to the gather
     const T* xprev = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
-    const T cm = T(c.cm[p & 1]);
-    T yi = extrap(xcur[idx], xprev[idx], cm);
+    T yi = extrap(xcur[idx], xprev[idx], c.cm);
     T ayi = shifted(acc, alpha, yi);
     reinterpret_cast<T*>(a.ay)[idx] = ayi;
     double y2 = double(yi) * double(yi);
@@ -50,8 +68,8 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RepCtl& c,
     if constexpr (MODE == MODE_DOCH) {
       // pending best-spin copy of x_{p-1}, still held in the write buffer
       if (c.pend == p - 1 && p > 0) a.best[idx] = xnext[idx] >= T(0) ? 1 : -1;
-      if (c.status == DCX_STOP_RUNNING) {
-        T xn = tmap(ax, beta, inv_beta(beta));
+      if (c.running) {
+        T xn = tmap(ax, c.beta, c.ibeta);
         xnext[idx] = xn;
         if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * a.cfg.n * a.cfg.R + idx] = xn;
         o.step = fmax(o.step, double(fabs(xn - xi)));
@@ -62,9 +80,8 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RepCtl& c,
       if (p > 0 && a.cfg.window_mode == DCX_WINDOW_ECONOMY) {
         const T* xprev = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
         const T* axprev = reinterpret_cast<const T*>(a.ax[(p + 1) & 1]);
-        const T cm = T(c.cm[p & 1]);
-        T yi = extrap(xi, xprev[idx], cm);
-        T ayi = extrap(ax, axprev[idx], cm);
+        T yi = extrap(xi, xprev[idx], c.cm);
+        T ayi = extrap(ax, axprev[idx], c.cm);
         double y2 = double(mul_rn(yi, yi));
         o.sy4 += y2 * y2;
         o.syay += double(yi) * double(ayi);
@@ -92,8 +109,8 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
   if (!a.g->live) return;
   const int p = a.g->p;
   if (MODE == MODE_ADOCH_Y && p == 0) return;  // no extrapolation at k = 0
-  const RepCtl c = a.ctl[0];
-  const bool running = c.status == DCX_STOP_RUNNING;
+  const RowCtl<T> c = row_ctl<T>(a.ctl[0], p);
+  const bool running = c.running;
   if (!running && !(MODE == MODE_DOCH && c.pend == p - 1)) return;
   const int lane = threadIdx.x & 31;
   const int sub = lane % V;
@@ -102,28 +119,75 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
   constexpr int RPW = 32 / V;  // rows per warp step
   const T* xc = reinterpret_cast<const T*>(a.gx[p & 1]);  // gather source (all spins)
   const T* xp = reinterpret_cast<const T*>(a.gx[(p + 1) & 1]);
-  const T cm = T(c.cm[p & 1]);
+  const T cm = c.cm;
   const T scale = T(a.scale);
   RowOut<T, MODE> o;
   const int64_t n = a.cfg.n;
-  for (int64_t base = gw * RPW; base < n; base += nwarps * RPW) {
+  // Software pipeline over this warp's row batches b, b+S, b+2S: while batch b
+  // gathers, the first two column entries of each lane's row in batch b+S and
+  // the row pointers of batch b+2S are in flight, so a row's gathers issue
+  // without waiting for its index loads.
+  const int64_t S = nwarps * RPW;
+  const uint32_t* rp = a.rp;  // locals: a lambda must not take the address of the kernel parameter
+  const int32_t* colp = a.col;
+  auto load_rp = [rp, running, n, lane](int64_t b, uint32_t& lo, uint32_t& hi) {
+    const int64_t i = b + lane / V;
+    lo = hi = 0;
+    if (running && i < n) { lo = __ldg(rp + i); hi = __ldg(rp + i + 1); }
+  };
+  auto load_cols = [colp, sub](uint32_t lo, uint32_t hi, int& c0, int& c1) {
+    c0 = c1 = 0;
+    if (lo + sub < hi) c0 = __ldg(colp + lo + sub);
+    if (lo + sub + V < hi) c1 = __ldg(colp + lo + sub + V);
+  };
+  auto gather = [xc, xp, cm](int j) -> T {
+    if constexpr (MODE == MODE_ADOCH_Y) return extrap(xc[j], xp[j], cm);
+    else return xc[j];
+  };
+  uint32_t c_lo, c_hi, n_lo, n_hi;
+  int c_c0, c_c1;
+  int64_t base = gw * RPW;
+  load_rp(base, c_lo, c_hi);
+  load_cols(c_lo, c_hi, c_c0, c_c1);
+  load_rp(base + S, n_lo, n_hi);
+  for (; base < n; base += S) {
+    int f_c0, f_c1;
+    uint32_t f_lo, f_hi;
+    load_cols(n_lo, n_hi, f_c0, f_c1);  // batch b+S
+    load_rp(base + 2 * S, f_lo, f_hi);  // batch b+2S
     const int64_t i = base + lane / V;
     const bool ok = i < n;
     T acc = T(0);
     typename EsAcc<VK>::type es = 0;
     if (ok && running) {
-      const uint32_t lo = __ldg(a.rp + i), hi = __ldg(a.rp + i + 1);
-      for (uint32_t e = lo + sub; e < hi; e += V) {
+      // the first two entries of this lane (prefetched columns): both gathers in flight together
+      const uint32_t e0 = c_lo + sub, e1 = e0 + V;
+      const bool h0 = e0 < c_hi, h1 = e1 < c_hi;
+      const T x0 = h0 ? gather(c_c0) : T(0);
+      const T x1 = h1 ? gather(c_c1) : T(0);
+      if (h0) {
+        int q;
+        const T v = load_entry<VK, true, T>(a.val, e0, scale, q);
+        acc = madd(acc, v, x0);
+        if constexpr (MODE != MODE_ADOCH_Y) es += es_term<VK, T>(q, v, x0);
+      }
+      if (h1) {
+        int q;
+        const T v = load_entry<VK, true, T>(a.val, e1, scale, q);
+        acc = madd(acc, v, x1);
+        if constexpr (MODE != MODE_ADOCH_Y) es += es_term<VK, T>(q, v, x1);
+      }
+      for (uint32_t e = e1 + V; e < c_hi; e += V) {  // longer rows: the rest in column order
         const int j = __ldg(a.col + e);
-        T xj;
-        if constexpr (MODE == MODE_ADOCH_Y) xj = extrap(xc[j], xp[j], cm);
-        else xj = xc[j];
+        const T xj = gather(j);
         int q;
         const T v = load_entry<VK, true, T>(a.val, e, scale, q);
         acc = madd(acc, v, xj);
         if constexpr (MODE != MODE_ADOCH_Y) es += es_term<VK, T>(q, v, xj);
       }
     }
+    c_lo = n_lo; c_hi = n_hi; c_c0 = f_c0; c_c1 = f_c1;
+    n_lo = f_lo; n_hi = f_hi;
 #pragma unroll
     for (int off = V / 2; off > 0; off >>= 1) {
       acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
@@ -142,7 +206,28 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
   o.step = warp_max(o.step);
   o.sy4 = warp_sum(o.sy4);
   o.syay = warp_sum(o.syay);
-  if (lane == 0) write_partials<T, MODE>(a, 0, (int)gw, o);
+  // one partial slot per block: the 8 warp sums in warp order (deterministic)
+  __shared__ double red[8][NQ];
+  const int warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[warp][Q_S4] = o.s4;
+    red[warp][Q_SXAX] = o.sxax;
+    red[warp][Q_ES] = o.es;
+    red[warp][Q_STEP] = o.step;
+    red[warp][Q_SY4] = o.sy4;
+    red[warp][Q_SYAY] = o.syay;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    RowOut<T, MODE> b;
+    b.s4 = red[0][Q_S4]; b.sxax = red[0][Q_SXAX]; b.es = red[0][Q_ES];
+    b.step = red[0][Q_STEP]; b.sy4 = red[0][Q_SY4]; b.syay = red[0][Q_SYAY];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      b.s4 += red[w][Q_S4]; b.sxax += red[w][Q_SXAX]; b.es += red[w][Q_ES];
+      b.step = fmax(b.step, red[w][Q_STEP]); b.sy4 += red[w][Q_SY4]; b.syay += red[w][Q_SYAY];
+    }
+    write_partials<T, MODE>(a, 0, (int)blockIdx.x, b);
+  }
 }
 
 // ---------------------------------------------------------------------------
