@@ -57,12 +57,11 @@ __device__ __forceinline__ void block_reduce(double* v, double (*sh)[NQ], double
   if (lane == 0)
     for (int q = 0; q < NQ; ++q) sh[w][q] = v[q];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < NQ; ++q) {
-      double acc = sh[0][q];
-      for (int i = 1; i < SMALL_WARPS; ++i) acc = (q == Q_STEP) ? fmax(acc, sh[i][q]) : acc + sh[i][q];
-      out[q] = acc;
-    }
+  if (threadIdx.x < NQ) {  // one thread per quantity, warps summed in order
+    const int q = threadIdx.x;
+    double acc = sh[0][q];
+    for (int i = 1; i < SMALL_WARPS; ++i) acc = (q == Q_STEP) ? fmax(acc, sh[i][q]) : acc + sh[i][q];
+    out[q] = acc;
   }
   __syncthreads();
 }
@@ -230,11 +229,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
     const T alpha = T(c.alpha), beta = T(c.beta), cm = T(c.cm[p & 1]);
     double v[NQ] = {0, 0, 0, 0, 0, 0};
     // ---- pass over x_p
-    for (int base = w * rpw; base < n; base += nwarps * rpw) {
-      const int i = base + lane / V;
-      T acc;
-      typename EsAcc<VK>::type es;
-      rowdot(i, xc, nullptr, T(0), false, acc, es);
+    auto row_done = [&](int i, T acc, typename EsAcc<VK>::type es) {
       if (i < n && sub == 0) {
         const T xi = xc[i];
         const T ax = shifted(acc, alpha, xi);
@@ -258,6 +253,45 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
             v[Q_SYAY] += double(yi) * double(ayi);
           }
         }
+      }
+    };
+    if (VK == VK_UNIFORM && s.pow2 && s.ell) {
+      // sliced ELL, unit weights: each thread owns rows t and t + blockDim (same
+      // lane of two slices) and walks both sums together, two independent
+      // column-order chains in flight
+      const int nb = blockDim.x;
+      const uint16_t* ell = reinterpret_cast<const uint16_t*>(colp);
+      for (int i0 = threadIdx.x; i0 < n; i0 += 2 * nb) {
+        const int i1 = i0 + nb;
+        const uint32_t len0 = rp[i0 + 1] - rp[i0];
+        const uint32_t len1 = i1 < n ? rp[i1 + 1] - rp[i1] : 0u;
+        const uint16_t* e0 = ell + sofs[i0 >> 5] + (i0 & 31);
+        const uint16_t* e1 = ell + (i1 < n ? sofs[i1 >> 5] + (i1 & 31) : 0);
+        T a0 = T(0), a1 = T(0);
+        uint32_t n0 = 0, n1 = 0;
+        const uint32_t m = max(len0, len1);
+        for (uint32_t k = 0; k < m; ++k) {
+          if (k < len0) {
+            const T xj = xc[e0[32 * k]];
+            a0 = add_rn(a0, xj);
+            n0 += negbit(xj);
+          }
+          if (k < len1) {
+            const T xj = xc[e1[32 * k]];
+            a1 = add_rn(a1, xj);
+            n1 += negbit(xj);
+          }
+        }
+        row_done(i0, mul_rn(a0, scale), typename EsAcc<VK>::type(int(len0) - 2 * int(n0)));
+        if (i1 < n) row_done(i1, mul_rn(a1, scale), typename EsAcc<VK>::type(int(len1) - 2 * int(n1)));
+      }
+    } else {
+      for (int base = w * rpw; base < n; base += nwarps * rpw) {
+        const int i = base + lane / V;
+        T acc;
+        typename EsAcc<VK>::type es;
+        rowdot(i, xc, nullptr, T(0), false, acc, es);
+        row_done(i, acc, es);
       }
     }
     block_reduce(v, red, tot);
