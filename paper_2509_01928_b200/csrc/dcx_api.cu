@@ -74,6 +74,7 @@ struct dcx_ctx {
   double scale = 1.0;
   int V32 = 1;
   int64_t ell_entries = 0;  // 32-row sliced ELL size of the pattern (n <= 65536)
+  double es_row_bound = 0;  // max over rows of sum_j |q_ij| (integer kinds; bound)
   DevBuf rp, col, col16, vint, v64, v32;
   DenseDev dn;  // dense tensor-core operands (dcx_dense.cu)
   // ---------------------------------------------------------- run state
@@ -504,6 +505,14 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     }
     c->V32 = lanes_for_degree(double(nnz) / double(n));
     c->ell_entries = 0;
+    {
+      int64_t maxlen = 0;
+      for (int64_t i = 0; i < n; ++i) maxlen = std::max<int64_t>(maxlen, ro[i + 1] - ro[i]);
+      double qmax = vk == VK_UNIFORM ? 1.0 : 0.0;
+      if (vk == VK_I8 || vk == VK_I16)
+        for (int64_t e = 0; e < nnz; ++e) qmax = std::max(qmax, std::fabs(std::nearbyint(v[e] / scale)));
+      c->es_row_bound = double(maxlen) * qmax;
+    }
     if (n_cols <= 65536 && n == n_cols)
       for (int64_t s0 = 0; s0 < n; s0 += 32) {
         int64_t mx = 0;
@@ -755,6 +764,10 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.states = c->states.p;
     a.part = c->part.as<double>();
     a.slots = slots;
+    // pass_rv lanes sum the spin energy of ceil(n / (8 grid)) rows; integer couplings keep that exact in f32
+    a.es_f32 = (R > 1 && c->vk_int >= 0 &&
+                double((n + 8 * int64_t(c->mp.grid) - 1) / (8 * int64_t(c->mp.grid))) * c->es_row_bound < 16777216.0)
+                   ? 1 : 0;
     RunCfg& cfg = a.cfg;
     cfg.n = n;
     cfg.R = R;

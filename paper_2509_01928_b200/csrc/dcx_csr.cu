@@ -69,7 +69,7 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RowCtl<T>&
       // pending best-spin copy of x_{p-1}, still held in the write buffer
       if (c.pend == p - 1 && p > 0) a.best[idx] = xnext[idx] >= T(0) ? 1 : -1;
       if (c.running) {
-        T xn = tmap(ax, c.beta, c.ibeta);
+        T xn = tmap_pass(ax, c.beta, c.ibeta);
         xnext[idx] = xn;
         if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * a.cfg.n * a.cfg.R + idx] = xn;
         o.step = fmax(o.step, double(fabs(xn - xi)));
@@ -358,10 +358,13 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
   // exact in T; the spin-energy sum stays in double (exact for integer J)
   T s4[VW], sxax[VW], sy4[VW], syay[VW], step[VW];
   double esum[VW];
+  float esf[VW];  // exact f32 spin-energy sums (a.es_f32, integer kinds)
+  const bool es32 = (VK == VK_UNIFORM || VK == VK_I8 || VK == VK_I16) && a.es_f32;
 #pragma unroll
   for (int v = 0; v < VW; ++v) {
     s4[v] = sxax[v] = sy4[v] = syay[v] = step[v] = T(0);
     esum[v] = 0.0;
+    esf[v] = 0.0f;
   }
 
   // Pipeline over this warp's rows A = i, B = i+S, C = i+2S, D = i+3S. While
@@ -540,9 +543,13 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
         const T x2 = mul_rn(xi[v], xi[v]);
         s4[v] += x2 * x2;
         sxax[v] += xi[v] * ax;
-        const double e = es[v].value(deg);
-        esum[v] += negbit(xi[v]) ? -e : e;
-        const T xnew = tmap(ax, beta[v], ibeta[v]);
+        if (es32) {
+          esf[v] += __uint_as_float(__float_as_uint(float(es[v].value(deg))) ^ (negbit(xi[v]) << 31));
+        } else {
+          const double e = es[v].value(deg);
+          esum[v] += negbit(xi[v]) ? -e : e;
+        }
+        const T xnew = tmap_pass(ax, beta[v], ibeta[v]);
         step[v] = fmax(step[v], fabs(xnew - xi[v]));
         xn[v] = run[v] ? xnew : xn[v];
       }
@@ -557,8 +564,12 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
         const T x2 = mul_rn(xi[v], xi[v]);
         s4[v] += x2 * x2;
         sxax[v] += xi[v] * ax[v];
-        const double e = es[v].value(deg);
-        esum[v] += negbit(xi[v]) ? -e : e;
+        if (es32) {
+          esf[v] += __uint_as_float(__float_as_uint(float(es[v].value(deg))) ^ (negbit(xi[v]) << 31));
+        } else {
+          const double e = es[v].value(deg);
+          esum[v] += negbit(xi[v]) ? -e : e;
+        }
       }
       vstore<T, VW>(reinterpret_cast<T*>(a.ax[p & 1]) + idx, ax);
       if (p > 0 && a.cfg.window_mode == DCX_WINDOW_ECONOMY) {
@@ -599,7 +610,8 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
 #pragma unroll
       for (int v = 0; v < VW; ++v) {
         const int c = lane * VW + v;
-        const double q[NQ] = {double(s4[v]), double(sxax[v]), esum[v], double(step[v]), double(sy4[v]), double(syay[v])};
+        const double q[NQ] = {double(s4[v]), double(sxax[v]), es32 ? double(esf[v]) : esum[v], double(step[v]),
+                              double(sy4[v]), double(syay[v])};
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
           if (w == 0) red[k][c] = q[k];
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
       } else {
         av = axc[i];
       }
-      const T xn = tmap(av, beta, inv_beta(beta));
+      const T xn = tmap_pass(av, beta, inv_beta(beta));
       xo[i] = xn;
       if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + i] = xn;
       st = fmax(st, double(fabs(xn - xi)));
@@ -682,7 +694,7 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
     } else {
       av = axc[idx];
     }
-    const T xn = tmap(av, beta, inv_beta(beta));
+    const T xn = tmap_pass(av, beta, inv_beta(beta));
     xo[idx] = xn;
     if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + idx] = xn;
     st = fmax(st, double(fabs(xn - xi)));

@@ -149,20 +149,6 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar & 0xFEFFFFFFu)
       : "memory");
 }
-// Cube root for the dense epilogue, whose arguments are normal floats or zero
-// (t = (J + aI)x / beta ~ x^3 with x ~ sqrt(alpha / beta) >= 1e-10): MUFU
-// log2 / exp2 estimate and one Newton step with the reciprocal of r^2 + 1e-38,
-// so t = 0 gives +0 without a branch or select (<= 1 ulp from cbrtf on normal
-// arguments; denormal arguments would flush to zero).
-__device__ __forceinline__ float cbrt_lean(float t) {
-  const float a = fabsf(t);
-  float l, r, rc;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaf(r, r, 1e-38f)));
-  r = fmaf(fmaf(a, rc, -r), 1.0f / 3.0f, r);
-  return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
-}
 // pair TMA multicast to the CTAs in `mask` (same smem offset in each); every
 // destination's pair leader barrier receives that destination's bytes
 __device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar,

@@ -118,10 +118,27 @@ __device__ __forceinline__ float cbrt_fast(float t) {
   r = a == __int_as_float(0x7f800000) ? a : r;  // inf
   return a == 0.0f ? 0.0f : copysignf(r, t);
 }
+// Cube root for the solver iterations, whose arguments are normal floats or zero
+// (t = (J + aI)x / beta ~ x^3 with x ~ sqrt(alpha / beta), far above the denormal range): MUFU
+// log2 / exp2 estimate and one Newton step with the reciprocal of r^2 + 1e-38,
+// so t = 0 gives +0 without a branch or select (<= 1 ulp from cbrtf on normal
+// arguments; denormal arguments would flush to zero).
+__device__ __forceinline__ float cbrt_lean(float t) {
+  const float a = fabsf(t);
+  float l, r, rc;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaf(r, r, 1e-38f)));
+  r = fmaf(fmaf(a, rc, -r), 1.0f / 3.0f, r);
+  return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
+}
 __device__ __forceinline__ double inv_beta(double beta) { return beta; }  // unused in f64
 __device__ __forceinline__ float inv_beta(float beta) { return __frcp_rn(beta); }
 __device__ __forceinline__ double tmap(double ax, double beta, double) { return cbrt(__ddiv_rn(ax, beta)); }
 __device__ __forceinline__ float tmap(float ax, float, float ibeta) { return cbrt_fast(__fmul_rn(ax, ibeta)); }
+// inside the solver iterations (arguments never denormal / infinite): the lean cube root
+__device__ __forceinline__ double tmap_pass(double ax, double beta, double ib) { return tmap(ax, beta, ib); }
+__device__ __forceinline__ float tmap_pass(float ax, float, float ibeta) { return cbrt_lean(__fmul_rn(ax, ibeta)); }
 
 // Sign-bit helpers for the spin-energy accumulation: x < 0 <=> sign bit set,
 // valid because iterates are never -0.0 (see tmap; initial states are

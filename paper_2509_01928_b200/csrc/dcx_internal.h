@@ -37,6 +37,7 @@ struct PassArgs {
   void* states;    // optional [(max_iters+1)][n][R]
   double* part;    // pass partials [R][NQ][slots]
   int32_t slots;
+  int32_t es_f32;  // pass_rv: per-lane spin-energy sums exact in f32 (integer couplings, bounded rows)
   RunCfg cfg;
 };
 

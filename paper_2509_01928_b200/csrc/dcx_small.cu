@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
         v[Q_ES] += xi >= T(0) ? double(es) : -double(es);
         if (!adoch) {
           if (p > 0 && c.pend == p - 1) a.best[(int64_t)i * R + r] = xo[i] >= T(0) ? 1 : -1;
-          const T xn = tmap(ax, beta, inv_beta(beta));
+          const T xn = tmap_pass(ax, beta, inv_beta(beta));
           v[Q_STEP] = fmax(v[Q_STEP], double(fabs(xn - xi)));
           xo[i] = xn;  // own row only: no other thread reads xo in this phase
           if (states) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
         if (c.pend == p) a.best[(int64_t)i * R + r] = xi >= T(0) ? 1 : -1;
         if (flag_stop) continue;
         const T av = acc_y ? (exact ? ayb[i] : extrap(ac[i], ao[i], cm)) : ac[i];
-        const T xn = tmap(av, beta, inv_beta(beta));
+        const T xn = tmap_pass(av, beta, inv_beta(beta));
         st = fmax(st, double(fabs(xn - xi)));
         xo[i] = xn;
         if (states) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
