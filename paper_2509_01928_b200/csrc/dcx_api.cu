@@ -85,6 +85,7 @@ struct dcx_ctx {
   int cap = 0, wcap = 0, chunk = 0, p_host = 0;
   DevBuf ctl, g, hist, window, xb0, xb1, ax0, ax1, ay, best, states, part, spart;
   DevBuf scratch;  // grow-only staging (x0 upload, result gathers): no cudaMalloc / cudaFree per call
+  DevBuf xmaps;    // pass_rv row-gather TMA maps over the two iterate buffers
   MultiPass mp;
   CsrDev J;
   SmallPlan sp;
@@ -764,6 +765,20 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.states = c->states.p;
     a.part = c->part.as<double>();
     a.slots = slots;
+    a.xmap[0] = a.xmap[1] = nullptr;
+    if (R > 1 && replica_vector_width(R, c->f64) > 1) {
+      const char* e = std::getenv("DCX_RV_TMA");
+      if (!(e && std::atoi(e) == 0)) {
+        alignas(64) unsigned char maps[2][128];
+        const int vw = replica_vector_width(R, c->f64);
+        for (int k = 0; k < 2; ++k)
+          encode_row_gather_map(maps[k], a.gx[k], uint64_t(R), uint64_t(c->n_cols), c->f64, uint32_t(32 * vw));
+        c->xmaps.alloc(sizeof(maps));
+        CK(cudaMemcpy(c->xmaps.p, maps, sizeof(maps), cudaMemcpyHostToDevice));
+        a.xmap[0] = c->xmaps.p;
+        a.xmap[1] = static_cast<char*>(c->xmaps.p) + 128;
+      }
+    }
     // pass_rv lanes sum the spin energy of ceil(n / (8 grid)) rows; integer couplings keep that exact in f32
     a.es_f32 = (R > 1 && c->vk_int >= 0 &&
                 double((n + 8 * int64_t(c->mp.grid) - 1) / (8 * int64_t(c->mp.grid))) * c->es_row_bound < 16777216.0)

@@ -390,9 +390,45 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
       v = load_entry<VK, true, T>(a.val, base + lane, scale, q);
     }
   };
+  // TMA staging (a.xmap set): one tile::gather4 per four staged edges, issued by
+  // lane 0 with the columns the batch registers hold, completion on an mbarrier
+  const bool tma = G > 0 && a.xmap[0] != nullptr;
+  const void* xmap = a.xmap[p & 1];
+  const int cb = int(blockIdx.y) * 32 * VW;  // first replica of this block's chunk
+  constexpr uint32_t CHUNK = 32u * CB;
+  __shared__ __align__(8) uint64_t stage_bar[8][2];
+  const uint32_t mb0 = smem_u32(&stage_bar[warp][0]);
+  uint32_t bar_par = 0;
   auto stage_row = [&](int s, uint32_t lo, uint32_t hi, int col) {
     if constexpr (G > 0) {
       const uint32_t deg = hi - lo;
+      if (tma) {
+        const uint32_t ne = min(deg, uint32_t(G));
+        if (ne == 0) return;
+        int jj[G];
+#pragma unroll
+        for (int e = 0; e < G; ++e) jj[e] = __shfl_sync(0xffffffffu, col, e);
+        if (lane == 0) {
+#pragma unroll
+          for (int e = 1; e < G; ++e)
+            if (uint32_t(e) >= ne) jj[e] = jj[0];  // padding rows: any valid row (weight 0)
+          const uint32_t nq = (ne + 3) / 4;
+          const uint32_t mb = mb0 + 8u * s;
+          const uint32_t dst = smem_u32(stage_mem) + uint32_t((s * 8 + warp) * G) * CHUNK;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(nq * 4 * CHUNK)
+                       : "memory");
+#pragma unroll
+          for (uint32_t g = 0; g < uint32_t(G) / 4; ++g)
+            if (g < nq)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+                  "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst + g * 4 * CHUNK),
+                  "l"(reinterpret_cast<uint64_t>(xmap)), "r"(cb), "r"(jj[4 * g]), "r"(jj[4 * g + 1]),
+                  "r"(jj[4 * g + 2]), "r"(jj[4 * g + 3]), "r"(mb)
+                  : "memory");
+        }
+        return;
+      }
 #pragma unroll
       for (int e = 0; e < G; ++e) {
         if (e >= deg) break;  // warp-uniform
@@ -408,6 +444,11 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
     const T z[VW] = {};
     for (int e = 0; e < 2 * G; ++e)
       vstore<T, VW>(reinterpret_cast<T*>(stage_mem + ((e / G) * ST_STRIDE + (warp * G + e % G) * 32 * CB + lane * CB)), z);
+    if (tma && lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8) : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero fill / inits before async-proxy writes
     __syncwarp();
   }
   // one edge's value / integer weight from the lane-distributed batch registers
@@ -449,7 +490,16 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
     for (int v = 0; v < VW; ++v) acc[v] = T(0);
     const uint32_t deg = a_hi - a_lo;
     if constexpr (G > 0) {
-      cp_async_wait1();  // row A's stage has landed (row B's may still be in flight)
+      if (!tma) {
+        cp_async_wait1();  // row A's stage has landed (row B's may still be in flight)
+      } else if (deg > 0) {
+        const uint32_t mb = mb0 + 8u * s, par = (bar_par >> s) & 1u;
+        asm volatile(
+            "{\n.reg .pred P1;\nRVW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra RVW;\n}\n" ::"r"(mb),
+            "r"(par)
+            : "memory");
+        bar_par ^= 1u << s;
+      }
       const uint32_t sa = st_base + s * ST_STRIDE;
 #pragma unroll
       for (int k = 0; k < G; k += UNROLL) {

@@ -870,6 +870,21 @@ static void make_map(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, b
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
 
+// Row-gather map over an iterate buffer [rows][cols] (f32 or f64): box = one row
+// of box_cols elements, no swizzle, zero fill past the last column; used by
+// pass_rv's tile::gather4 staging (four neighbour rows per TMA instruction).
+void encode_row_gather_map(void* map_out, void* base, uint64_t cols, uint64_t rows, bool f64, uint32_t box_cols) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * (f64 ? 8 : 4)};
+  const cuuint32_t box[2] = {box_cols, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(map_out),
+                            f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (row gather) failed: " + std::to_string(int(r)));
+}
+
 #define DCK(call)                                                                                          \
   do {                                                                                                     \
     cudaError_t e_ = (call);                                                                               \

@@ -38,6 +38,7 @@ struct PassArgs {
   double* part;    // pass partials [R][NQ][slots]
   int32_t slots;
   int32_t es_f32;  // pass_rv: per-lane spin-energy sums exact in f32 (integer couplings, bounded rows)
+  const void* xmap[2];  // pass_rv: tile::gather4 maps over gx[0] / gx[1] (device copies), or null (cp.async staging)
   RunCfg cfg;
 };
 
@@ -59,6 +60,8 @@ void enqueue_flush(const MultiPass& m, cudaStream_t s);
 void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
 void enqueue_start_clock(GState* g, cudaStream_t s);
 int replica_vector_width(int R, bool f64);
+// dcx_dense.cu: row-gather TMA map ([rows][cols], box = one row of box_cols elements)
+void encode_row_gather_map(void* map_out, void* base, uint64_t cols, uint64_t rows, bool f64, uint32_t box_cols);
 // dcx_power.cu
 void launch_power(const CsrDev& J, int use_shift, double shift, double tol, int64_t max_iters, double* v, double* w,
                   const double* restart, double* part, double* part2, unsigned* bar, double* out, int grid,
