@@ -106,3 +106,36 @@ def test_tc_k2000_quality_vs_reference(gold):
     # the reference's own best over 32 seeds sits 2.4 sigma out; 1024 replicas reach 2 sigma
     assert e.min() <= ref.mean() - 2.0 * ref.std()
     assert np.quantile(e, 0.1) <= np.quantile(ref, 0.1) + 3 * se
+
+
+def _run_with_env(env, fn):
+    import os
+
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_tc_operand_multicast_and_pair_variants_agree(gold):
+    """The data-movement variants of the dense kernel (A tiles by pair TMA multicast
+    in 4-CTA clusters, DCX_DENSE_MC=1; single-CTA tiles, DCX_DENSE_NC=1) compute
+    the same products in the same order: identical results."""
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(256))
+    run = lambda: dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=40,  # noqa: E731
+                                    precision="f16tc")
+    base = run()
+    mc = _run_with_env({"DCX_DENSE_MC": "1"}, run)
+    nc1 = _run_with_env({"DCX_DENSE_NC": "1"}, run)
+    for other in (mc, nc1):
+        for a, b in zip(base, other):
+            assert a.energy == b.energy and a.iterations == b.iterations
+            assert np.array_equal(a.x, b.x)

@@ -291,3 +291,25 @@ def test_k2000_f64_seed0(gold):
     r = dc.doch_solve(inst, dc.SolverParams(alpha=g["alpha"], beta=g["beta"], eta=0.1, max_iters=1000, seed=0))
     ref = g["doch_s0"]
     assert r.energy == ref["energy"] and r.iterations == ref["iterations"] and r.stop_reason == ref["stop_reason"]
+
+
+def test_replica_pass_staging_paths_agree():
+    """pass_rv stages neighbour rows by TMA tile::gather4 (default) or per-lane
+    cp.async (DCX_RV_TMA=0): the same values reach the same sums, results are
+    bit-identical (f32, 256 replicas on a +-1 torus)."""
+    import os
+
+    v, c, o = synth.torus(32, seed=0)
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(1024, v, c, o, validate=False))
+    X0 = np.stack([dc.initial_state(1024, 4.0, 8.0e4, np.random.default_rng(s)) for s in range(256)])
+    run = lambda: dc.solve_replicas(inst, "doch", 4.0, 8.0e4, X0, max_iters=50, precision="f32",  # noqa: E731
+                                    path="multipass")
+    a = run()
+    os.environ["DCX_RV_TMA"] = "0"
+    try:
+        b = run()
+    finally:
+        os.environ.pop("DCX_RV_TMA", None)
+    for ra, rb in zip(a, b):
+        assert ra.energy == rb.energy and ra.iterations == rb.iterations
+        assert np.array_equal(ra.x, rb.x)
