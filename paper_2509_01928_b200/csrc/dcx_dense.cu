@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -63,15 +64,18 @@ constexpr uint32_t XCOL = 256;
 // the only ones that depend on each other (replicas are independent), so each
 // group synchronises on its own words and runs its own number of iterations.
 struct __align__(64) SyncWords {
-  unsigned int count;
-  unsigned int gen;
-  unsigned long long stamp;
-  int running;       // replicas of the group still running
-  int running_snap;  // snapshot taken by the last arriver
-  int p_exec;        // passes executed by the group (resume point / exit record)
-  unsigned int countB, genB;  // second phase (partials written)
-  int pad[7];
+  unsigned long long stamp;   // device time of the last B arrival (time budget)
+  int running;                // replicas of the group still running
+  int p_exec;                 // passes executed by the group (resume point / exit record)
+  unsigned int countB, genB;  // B phase (partials written): arrivals, generation
+  int snapB[2];               // running count snapshot at B(k), slot k & 1
 };
+static_assert(sizeof(SyncWords) == 64, "one line per group");
+// Operand-ready flags: flags[(rt * tiles_n + t) * FLAG_STRIDE] = v <=> the CTA of
+// replica tile rt and spin tile t has written its part of x_v (f16 and sign
+// operands). Own 64-byte line each; stored after the SyncWords array.
+constexpr int FLAG_STRIDE = 16;
+constexpr int MAX_FLAGS = 256;
 
 struct Args {
   CUtensorMap tmA[2];   // Xh by parity (f16)
@@ -86,6 +90,7 @@ struct Args {
   RepCtl* ctl;
   GState* g;
   SyncWords* sync;
+  unsigned int* flags;
   unsigned long long* dbg;  // optional phase timestamps of CTA 0 (DCX_DENSE_TRACE)
   RunCfg cfg;
   int n, npad, R, Rpad, tiles_n, p_end;
@@ -284,9 +289,10 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
 }
 
 struct __align__(8) Smem {
-  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2, d2free;
+  uint64_t full[MAX_STAGES], empty[MAX_STAGES], accf1, accf2, d1free, d2free;
   uint32_t tmem_base;
   int pad;
+  unsigned tdbg[8];  // epilogue phase stamps / sums (DCX_DENSE_TRACE)
   float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
   float red[2][TM][4];
   double red2[2][TM][4];
@@ -316,6 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const bool leader = cta_rank == 0;
   const int KB1 = a.npad / (TK * P::KA);      // f16 stages (KA x 64 of K each)
   const int KB2 = a.npad / (2 * TK * P::KA);  // int8 stages (KA x 128 of K each)
+  static_assert(P::KA * TK == TN, "one GEMM1 stage = one spin tile (operand flags are per tile)");
   SyncWords* grp = a.sync + rg;
 
   if (threadIdx.x == 0) {
@@ -325,7 +332,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     }
     mbar_init(smem_u32(&sm.accf1), 1);
     mbar_init(smem_u32(&sm.accf2), 1);
-    mbar_init(smem_u32(&sm.d2free), 8);  // one arrive per epilogue warp
+    mbar_init(smem_u32(&sm.d1free), 8);  // one arrive per epilogue warp
+    mbar_init(smem_u32(&sm.d2free), 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -388,20 +396,28 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   if (nt != 0) cfg.hist = nullptr;  // only the nt == 0 CTA of a replica tile writes history
 
   uint32_t kiter = 0, acc_phase = 0;
-  // Group synchronisation without CTA-wide barriers in the loop. Per iteration p:
-  //   A(p): every CTA of the replica group wrote x_{p+1} (xh, s8) -> the producers
-  //         may load iteration p+1's operands; its last arriver snapshots the
-  //         running count (the exit test of iteration p+1);
-  //   B(p): every CTA wrote its per-replica partials of p -> control p may sum them;
-  //         its last arriver stamps the device time (time budget of control p).
-  // Each CTA arrives at A right after its update (while GEMM2 still runs) and at B
-  // after the energy GEMM, so the tensor core goes from GEMM2(p) straight into
-  // GEMM1(p+1); the control of iteration p runs on the epilogue warps while
-  // GEMM1(p+1) executes. Generations count completed phases from the launch base.
-  const unsigned int genA0 = *reinterpret_cast<volatile unsigned int*>(&grp->gen);
+  // Synchronisation without CTA-wide barriers in the loop. Per iteration p:
+  //   operands: each CTA publishes x_{p+1} of its tile by a release store of p+1
+  //         to its flag right after its update (while GEMM2(p) still runs). The
+  //         producers wait per K stage for the flag of the spin tile that stage
+  //         loads, walking the K tiles in a rotated order (from tile nt & ~1), so
+  //         a late tile only stalls the consumers that reach it before it lands
+  //         instead of the whole group;
+  //   B(p): every CTA of the replica group wrote its per-replica partials of p ->
+  //         control p may sum them; its last arriver stamps the device time (time
+  //         budget of control p) and snapshots the running count into snapB[p&1].
+  // Exit test at the top of iteration p (p >= p_start + 2): snapB of B(p-2) == 0,
+  // read by the producer, the MMA issuer and the epilogue of every CTA alike.
+  // B(p-1) is waited by control p-1 before update p, which also orders every
+  // CTA's GEMM2(p-1) reads of the sign operands before they are overwritten.
   const unsigned int genB0 = *reinterpret_cast<volatile unsigned int*>(&grp->genB);
   const unsigned int members = NC * a.tiles_n;
   const int64_t part_stride = (int64_t)a.Rpad * a.tiles_n * 4;  // partials double-buffered by iteration parity
+  // per-CTA phase sums (DCX_DENSE_TRACE): [0] MMA wait on full[], [1] GEMM1 issue span,
+  // [2] update, [3] epilogue wait for GEMM1, [4] producer flag wait, [5] iterations, [6] control
+  const int kbase = nt & ~1;  // rotation of the K order (common to both pairs of a multicast cluster)
+  unsigned int* const my_flag = a.flags + ((int64_t)rt * a.tiles_n + nt) * FLAG_STRIDE;
+  const unsigned int* const tile_flags = a.flags + (int64_t)rt * a.tiles_n * FLAG_STRIDE;
   auto wait_gen = [&](const unsigned int* g, unsigned int target) {
     long long t0 = 0;
     unsigned int polls = 0;
@@ -412,38 +428,46 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       }
     }
   };
-  // one arrival per CTA (release: covers the CTA's writes ordered before it by the named barrier)
-  auto arrive = [&](unsigned int* cnt, unsigned int* gen, unsigned int gen_base_next, bool snapshot) {
+  // one arrival per CTA at B (acq_rel: the last arriver sees every CTA's running decrements)
+  auto arriveB = [&](int pk) {
     unsigned int old;
-    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&grp->countB) : "memory");
     if (old == members - 1) {
-      *cnt = 0;
-      if (snapshot) {
-        int run;
-        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(run) : "l"(&grp->running) : "memory");
-        grp->running_snap = run;
-      } else {
-        grp->stamp = globaltimer();
-      }
-      st_release(gen, gen_base_next);
+      grp->countB = 0;
+      int run;
+      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(run) : "l"(&grp->running) : "memory");
+      grp->snapB[pk & 1] = run;
+      grp->stamp = globaltimer();
+      st_release(&grp->genB, genB0 + unsigned(pk - p_start + 1));
     }
+  };
+  // exit test of iteration p (producer / MMA issuer; the epilogue has waited B(p-1) in control)
+  auto group_done = [&](int pk) {
+    if (pk < p_start + 2) return false;
+    wait_gen(&grp->genB, genB0 + unsigned(pk - p_start - 1));  // B(pk-2)
+    return __ldcg(&grp->snapB[pk & 1]) == 0;
   };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      unsigned d_flag = 0;
       for (; p < a.p_end; ++p) {
-        if (p > p_start) {
-          wait_gen(&grp->gen, genA0 + unsigned(p - p_start));  // operands of p are written
-          if (__ldcg(&grp->running_snap) == 0) break;
-        }
-        fence_async_global();  // generic writes (acquired above) before the async-proxy loads
+        if (group_done(p)) break;
         const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
         if (tr) a.dbg[p * 12 + 5] = clock64();
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
           const int s = kiter % P::STAGES;
           const uint32_t ph = (kiter / P::STAGES) & 1;
           mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
+          // K tile of this stage (GEMM1: one spin tile; GEMM2: two, both already waited in GEMM1)
+          const int kt = kb < KB1 ? (kb + kbase) % KB1 : (kb - KB1 + kbase / 2) % KB2;
+          if (kb < KB1) {
+            const unsigned tf0 = a.dbg ? clock() : 0u;
+            wait_gen(tile_flags + kt * FLAG_STRIDE, unsigned(p));  // x_p of spin tile kt is written
+            if (a.dbg) d_flag += clock() - tf0;
+            fence_async_global();  // generic writes (acquired above) before the async-proxy loads
+          }
           const uint32_t fb = smem_u32(&sm.full[s]);
           if (leader) mbar_expect_tx(fb, NC * P::STAGE);  // the leader's barrier counts both CTAs' bytes
           unsigned char* st = tiles + s * P::STAGE;
@@ -452,7 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const CUtensorMap* ma = kb < KB1 ? &a.tmA[cur] : &a.tmS[cur];
           const CUtensorMap* mb = kb < KB1 ? &a.tmB : &a.tmQ8;
           const int katom = kb < KB1 ? TK : 2 * TK;  // elements of K per 128-byte atom
-          const int kc = (kb < KB1 ? kb : kb - KB1) * P::KA * katom;
+          const int kc = kt * P::KA * katom;
 #pragma unroll
           for (int q = 0; q < P::KA; ++q) {
             const uint32_t da = smem_u32(st + q * TILE_BYTES);
@@ -470,15 +494,14 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }
         if (tr) a.dbg[p * 12 + 7] = clock64();
       }
+      if (a.dbg) a.dbg[4096 * 14 + blockIdx.x * 8 + 4] = d_flag;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && leader) {  // one thread of the (leader) CTA issues every MMA of the tile
+      unsigned d_mw = 0, d_g1 = 0;
       for (; p < a.p_end; ++p) {
-        if (p > p_start) {
-          wait_gen(&grp->gen, genA0 + unsigned(p - p_start));  // same exit test as the producer
-          if (__ldcg(&grp->running_snap) == 0) break;
-        }
+        if (group_done(p)) break;  // same exit test as the producer
         const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
         unsigned long long wait_cyc = 0;
         for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
@@ -486,6 +509,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t ph = (kiter / P::STAGES) & 1;
           const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
+          // D1 of iteration p-1 read by the epilogue before GEMM1(p) overwrites it
+          if (kb == 0 && p > p_start) mbar_wait(smem_u32(&sm.d1free), (p - 1 - p_start) & 1);
           // D2 of iteration p-1 drained by the epilogue before GEMM2(p) overwrites it
           if (kb == KB1 && p > p_start) mbar_wait(smem_u32(&sm.d2free), (p - 1 - p_start) & 1);
           wait_cyc += clock64() - tw0;
@@ -508,14 +533,21 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           }
           mma_commit_g<NC>(smem_u32(&sm.empty[s]), uint16_t(!a.mc ? 0x3 : (psub == 0 ? 0x3 : 0xF)));
           if (tr && kb == 0) a.dbg[p * 12 + 8] = clock64();
+          if (a.dbg && kb == 0) d_g1 -= clock();
           if (kb == KB1 - 1) {
+            if (a.dbg) d_g1 += clock();
             mma_commit_g<NC>(smem_u32(&sm.accf1), uint16_t(0x3u << (2 * psub)));
             if (tr) a.dbg[p * 12 + 9] = clock64();
           }
         }
         if (tr) a.dbg[p * 12 + 10] = clock64();
         if (tr) a.dbg[4096 * 12 + p] = wait_cyc;
+        if (a.dbg) d_mw += unsigned(wait_cyc);
         mma_commit_g<NC>(smem_u32(&sm.accf2), uint16_t(0x3u << (2 * psub)));
+      }
+      if (a.dbg) {
+        a.dbg[4096 * 14 + blockIdx.x * 8 + 0] = d_mw;
+        a.dbg[4096 * 14 + blockIdx.x * 8 + 1] = d_g1;
       }
     }
   } else if (epi) {
@@ -577,11 +609,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       }
       epi_sync();
     };
+    if (threadIdx.x == 128) sm.tdbg[4] = sm.tdbg[5] = sm.tdbg[6] = sm.tdbg[7] = 0;
     for (; p < a.p_end; ++p) {
+      if (a.dbg && threadIdx.x == 128) sm.tdbg[0] = clock();
       if (p > p_start) {
-        control(p - 1);
-        if (threadIdx.x == 128) wait_gen(&grp->gen, genA0 + unsigned(p - p_start));  // (complete: B(p-1) follows A(p-1))
-        if (__ldcg(&grp->running_snap) == 0) break;  // the producer and MMA warps exit here too
+        control(p - 1);  // waits B(p-1), hence B(p-2)
+        if (p >= p_start + 2 && __ldcg(&grp->snapB[p & 1]) == 0) break;  // the producer and MMA warps exit here too
       }
       const int cur = p & 1;
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) {
@@ -613,21 +646,31 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }
       }
       uint64_t curmask = 0;
+      if (a.dbg && threadIdx.x == 128) sm.tdbg[1] = clock();
       mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
       tc_fence_after();
+      if (a.dbg && threadIdx.x == 128) sm.tdbg[2] = clock();
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 11] = clock64();
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
       float* xg = a.xm[cur] + (int64_t)r * a.npad + gbase;  // x_p (time-budget runs only)
       for (int cc = 0; cc < 2; ++cc) {
-        uint32_t v1[32], xv[32], nv[32];
+        uint32_t v1[32], xv[32];  // xv: x_p, updated in place to the next master state
         tmem_ld32(tmem + (uint32_t(q * 32) << 16) + h * 64 + cc * 32, v1);
         tmem_ld32(xaddr + cc * 32, xv);
         tmem_ld_wait();
+        if (write_master && lim > 0) {  // x_p persisted (a budget stop at p keeps it)
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(xv + j);
+        }
         __align__(16) __half2 hv[16];
         __align__(16) uint32_t sv[8];
-        if (lim == 64) {
-          // full tile: branch-free (x is never -0.0, so x < 0 <=> sign bit)
+        if (lim > 0) {
+          // branch-free over all 64 columns (x is never -0.0, so x < 0 <=> sign bit). Padding
+          // columns (i >= n) hold x = +0 and D1 = 0 (zero rows/columns of Q), so they
+          // update to +0, add nothing to the sums and read as spin +1 (a zero term of
+          // the energy GEMM: the padded rows and columns of Q are zero)
           uint32_t m = 0;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -642,64 +685,44 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               sxax = fmaf(x, ax, sxax);
               step = fmaxf(step, fabsf(nx[u] - x));
               m |= (xv[j + u] >> 31) << (j + u);
-              nv[j + u] = running ? __float_as_uint(nx[u]) : xv[j + u];
+              xv[j + u] = running ? __float_as_uint(nx[u]) : xv[j + u];
             }
             hv[j / 2] = __floats2half2_rn(nx[0] * inv_lam, nx[1] * inv_lam);
             if ((j & 3) == 2) {  // 4 spins -> 4 bytes of +-1: 0x01 per byte, 0xff where negative
-              const uint32_t t = (nv[j - 2] >> 31) | ((nv[j - 1] >> 31) << 8) |
+              const uint32_t t = (xv[j - 2] >> 31) | ((xv[j - 1] >> 31) << 8) |
                                  ((__float_as_uint(nx[0]) >> 31) << 16) | ((__float_as_uint(nx[1]) >> 31) << 24);
               sv[j / 4] = 0x01010101u + t * 0xfeu;
             }
           }
           curmask |= uint64_t(m) << (cc * 32);
-        } else {
-          __align__(16) __half hh[32];
-          __align__(16) int8_t ss[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = __uint_as_float(xv[j]);
-            const bool in = cc * 32 + j < lim;
-            const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j]));
-            const float nxt = cbrt_fast(ax * inv_beta);
-            if (in) {
-              const float x2 = x * x;
-              s4 = fmaf(x2, x2, s4);
-              sxax = fmaf(x, ax, sxax);
-              step = fmaxf(step, fabsf(nxt - x));
-              if (x < 0.f) curmask |= 1ull << (cc * 32 + j);
-            }
-            nv[j] = (in && running) ? __float_as_uint(nxt) : xv[j];
-            hh[j] = __float2half_rn(in ? nxt * inv_lam : 0.f);
-            ss[j] = in ? (nxt >= 0.f ? 1 : -1) : 0;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) hv[j] = __halves2half2(hh[2 * j], hh[2 * j + 1]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) sv[j] = reinterpret_cast<const uint32_t*>(ss)[j];
-        }
-        tmem_st32(xaddr + cc * 32, nv);
+        }  // (lim == 0: padding replica or columns, the master state stays)
+        tmem_st32(xaddr + cc * 32, xv);
         if (running && lim > 0) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) *reinterpret_cast<uint4*>(hn + cc * 32 + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
-          if (write_master) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(xv + j);
-          }
           *reinterpret_cast<uint4*>(sn + cc * 32) = *reinterpret_cast<uint4*>(sv);
           *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 4);
         }
       }
       const bool tr128 = a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096;
       if (tr128) a.dbg[p * 12 + 3] = clock64();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sm.d1free));  // D1 read: GEMM1(p+1) may overwrite it
       tmem_st_wait();
       // x_{p+1} operands of this CTA are written: make them visible to the async
-      // proxy of every CTA, then one release arrival at A(p)
+      // proxy of every CTA, then publish them with one release store of the flag
       fence_async_global();
       if (tr128) a.dbg[p * 12 + 4] = clock64();
       epi_sync();
       if (tr128) a.dbg[p * 12 + 6] = clock64();
-      if (threadIdx.x == 128) arrive(&grp->count, &grp->gen, genA0 + unsigned(p - p_start + 1), true);
+      if (threadIdx.x == 128) st_release(my_flag, unsigned(p + 1));
+      if (a.dbg && threadIdx.x == 128) {
+        sm.tdbg[4] += clock() - sm.tdbg[2];
+        sm.tdbg[5] += sm.tdbg[2] - sm.tdbg[1];
+        sm.tdbg[6] += 1;
+        sm.tdbg[7] += sm.tdbg[1] - sm.tdbg[0];
+      }
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 1] = clock64();
       // energy GEMM (overlapped with the update above): Es = sum_i s_i (Q s)_i, exact in int32
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
@@ -737,11 +760,17 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         *reinterpret_cast<double4*>(dst) = v;
       }
       epi_sync();
-      if (threadIdx.x == 128) arrive(&grp->countB, &grp->genB, genB0 + unsigned(p - p_start + 1), false);
+      if (threadIdx.x == 128) arriveB(p);
       acc_phase ^= 1;
     }
     // the control of the last iteration of this launch (the next launch resumes at p)
     if (p == a.p_end && p > p_start) control(p - 1);
+    if (a.dbg && threadIdx.x == 128) {
+      a.dbg[4096 * 14 + blockIdx.x * 8 + 2] = sm.tdbg[4];
+      a.dbg[4096 * 14 + blockIdx.x * 8 + 3] = sm.tdbg[5];
+      a.dbg[4096 * 14 + blockIdx.x * 8 + 5] = sm.tdbg[6];
+      a.dbg[4096 * 14 + blockIdx.x * 8 + 6] = sm.tdbg[7];
+    }
   }
   // ---------------------------------------------------------------- teardown
   if (epi) {
@@ -990,7 +1019,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   DCK(cudaGetDevice(&dev));
   DCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const int tiles = (d.Rpad / 128) * int(d.npad / 128);
-  if (tiles > nsm)
+  if (tiles > nsm || tiles > tc::MAX_FLAGS)
     throw std::invalid_argument("tensor-core path: (R/128)*(n/128) tiles must fit the SM count (" +
                                 std::to_string(tiles) + " > " + std::to_string(nsm) + ")");
   // CTA pairs (cta_group::2) when the replica count allows 256-replica groups
@@ -1010,7 +1039,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (!reuse) {
     DCK(cudaMalloc(&d.best8, vec));
     DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 4 * (d.npad / 128) * d.Rpad));  // by iteration parity
-    DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128)));
+    DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128) + sizeof(unsigned int) * tc::FLAG_STRIDE * tc::MAX_FLAGS));
   }
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
   {
@@ -1020,12 +1049,15 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
     std::memset(sw.data(), 0, sizeof(tc::SyncWords) * ngroups);
     for (int gI = 0; gI < ngroups; ++gI) sw[gI].running = std::max(0, std::min(gsz, d.R - gI * gsz));
     DCK(cudaMemcpyAsync(d.sync, sw.data(), sizeof(tc::SyncWords) * ngroups, cudaMemcpyHostToDevice, s));
+    // operand flags: x_0 of every tile is written by pack_state below (flag value 0)
+    DCK(cudaMemsetAsync(reinterpret_cast<tc::SyncWords*>(d.sync) + d.Rpad / 128, 0,
+                        sizeof(unsigned int) * tc::FLAG_STRIDE * tc::MAX_FLAGS, s));
   }
   if (d.dbg) cudaFree(d.dbg);
   d.dbg = nullptr;
   if (std::getenv("DCX_DENSE_TRACE")) {
-    DCK(cudaMalloc(&d.dbg, 4096 * 14 * 8));
-    DCK(cudaMemsetAsync(d.dbg, 0, 4096 * 14 * 8, s));
+    DCK(cudaMalloc(&d.dbg, (4096 * 14 + 256 * 8) * 8));
+    DCK(cudaMemsetAsync(d.dbg, 0, (4096 * 14 + 256 * 8) * 8, s));
   }
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
@@ -1066,6 +1098,7 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.ctl = m.args.ctl;
   a.g = m.args.g;
   a.sync = reinterpret_cast<tc::SyncWords*>(d.sync);
+  a.flags = reinterpret_cast<unsigned int*>(a.sync + d.Rpad / 128);
   a.dbg = reinterpret_cast<unsigned long long*>(d.dbg);
   a.cfg = m.args.cfg;
   a.n = int(d.n);
@@ -1121,7 +1154,7 @@ void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s) {
 
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) {  // phase breakdown of CTA 0 (DCX_DENSE_TRACE=1)
-    std::vector<unsigned long long> t(4096 * 14);
+    std::vector<unsigned long long> t(4096 * 14 + 256 * 8);
     DCK(cudaMemcpyAsync(t.data(), d.dbg, t.size() * 8, cudaMemcpyDeviceToHost, s));
     DCK(cudaStreamSynchronize(s));
     const unsigned long long* gt = t.data() + 4096 * 13;
@@ -1157,6 +1190,21 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
                    "gemm1done %.2f | update %.2f, gemm2+energy %.2f | period %.2f | MMA waiting on full[] %.2f\n",
                    m[0] / cnt / 1e3, m[1] / cnt / 1e3, m[2] / cnt / 1e3, m[3] / cnt / 1e3, m[4] / cnt / 1e3,
                    m[5] / cnt / 1e3, m[6] / cnt / 1e3, m[7] / cnt / 1e3);
+    // per-CTA distribution (kcycles per iteration): min / median / max over the grid
+    const int grid = (d.Rpad / 128) * int(d.npad / 128);
+    const char* names[7] = {"mma-wait", "gemm1-issue", "update", "epi-wait-gemm1", "flag-wait", "", "control"};
+    for (int k : {0, 1, 2, 3, 4, 6}) {
+      std::vector<double> v;
+      for (int c = 0; c < grid; ++c) {
+        const unsigned long long* cd = t.data() + 4096 * 14 + c * 8;
+        if (cd[5] > 0 && (k > 1 || (c % d.nc) == 0))  // MMA sums: pair leaders only
+          v.push_back(double(cd[k]) / double(cd[5]) / 1e3);
+      }
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      std::fprintf(stderr, "[dcx dense trace] per-CTA %-15s min %.2f med %.2f max %.2f (%zu CTAs)\n", names[k], v[0],
+                   v[v.size() / 2], v.back(), v.size());
+    }
   }
   tc::unpack_results<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(d.xm[0]),
                                            reinterpret_cast<const float*>(d.xm[1]),

@@ -120,15 +120,17 @@ __device__ __forceinline__ float cbrt_fast(float t) {
 }
 // Cube root for the solver iterations, whose arguments are normal floats or zero
 // (t = (J + aI)x / beta ~ x^3 with x ~ sqrt(alpha / beta), far above the denormal range): MUFU
-// log2 / exp2 estimate and one Newton step with the reciprocal of r^2 + 1e-38,
-// so t = 0 gives +0 without a branch or select (<= 1 ulp from cbrtf on normal
+// log2 / exp2 estimate and one Newton step with the reciprocal of r^2 + 1e-37,
+// so t = 0 gives +0 without a branch or select (the offset is a normal float: a
+// denormal one would be flushed by rcp.approx.ftz and turn t = 0 into NaN; it is
+// below 2e-12 of r^2 for every normal t, so <= 1 ulp from cbrtf on normal
 // arguments; denormal arguments would flush to zero).
 __device__ __forceinline__ float cbrt_lean(float t) {
   const float a = fabsf(t);
   float l, r, rc;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a));
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaf(r, r, 1e-38f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaf(r, r, 1e-37f)));
   r = fmaf(fmaf(a, rc, -r), 1.0f / 3.0f, r);
   return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
 }
