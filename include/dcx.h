@@ -43,6 +43,8 @@ enum { DCX_SOLVER_DOCH = 0, DCX_SOLVER_ADOCH = 1 };
 enum { DCX_WINDOW_ECONOMY = 0, DCX_WINDOW_EXACT = 1 };
 enum { DCX_PREC_F64 = 0, DCX_PREC_F32 = 1, DCX_PREC_F16TC = 2 };
 enum { DCX_PATH_AUTO = 0, DCX_PATH_MULTIPASS = 1, DCX_PATH_PERSISTENT = 2, DCX_PATH_DENSE_TC = 3 };
+/* procedural coupling formulas (dc/coupling.py:293-298 _PROCEDURAL_FORMULAS) */
+enum { DCX_FORMULA_SIN_PRODUCT = 0 };
 enum {
   DCX_STOP_RUNNING = 0,
   DCX_STOP_CONVERGED = 1,
@@ -90,7 +92,7 @@ typedef struct {
 
 typedef struct {
   int64_t n, nnz;
-  int32_t value_kind; /* 0 uniform, 1 int8, 2 int16, 3 f32, 4 f64 */
+  int32_t value_kind; /* 0 uniform, 1 int8, 2 int16, 3 f32, 4 f64, 5 procedural */
   int32_t lanes;      /* lanes per row of the R=1 kernels */
   double scale;       /* value = scale * stored integer (integer kinds) */
   int32_t dense;      /* set through dcx_set_dense */
@@ -115,6 +117,17 @@ DCX_API int dcx_set_csr(dcx_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row
                 const double* values);
 DCX_API int dcx_set_dense(dcx_ctx* ctx, int64_t n, const double* J_rowmajor);
 DCX_API int dcx_coupling(const dcx_ctx* ctx, dcx_coupling_info* out);
+/* dcx_set_procedural replaces ProceduralCoupling(n, seed, formula)
+ * (dc/coupling.py:209-229; gen_procedural_sin dc/generate.py:115-123):
+ * J_ij = sin(i*j + seed) for i != j, 0 on the diagonal, never stored: every
+ * product regenerates it on the device (the reference materialises b x b tiles,
+ * dc/matvec.py:117-155). Solves run on the multipass path; dcx_power is not
+ * available (the reference's auto method is the Wigner estimate for
+ * procedural matrices, dc/spectral.py:203-216).
+ * dcx_proc_row_stats: out[3i..3i+2] = (sum_j J_ij, sum_j J_ij^2, sum_j |J_ij|)
+ * over j != i, f64 -- offdiag_moments and abs_row_sums (dc/coupling.py:248-268). */
+DCX_API int dcx_set_procedural(dcx_ctx* ctx, int64_t n, int64_t seed, int32_t formula);
+DCX_API int dcx_proc_row_stats(dcx_ctx* ctx, double* out /* [n][3] */);
 
 /* Operator seam (dc/matvec.py:99-114 matvec; :181-190 operator_energy;
  * dc/model.py:79-87 energy; dc/solvers/doch.py:76-103 hamiltonian/apply_T).

@@ -6,7 +6,7 @@ arithmetic of the solver path runs in libdcx.so (hand-written sm_100a CUDA);
 there is no CPU fallback.
 """
 
-from .coupling import CouplingError, CouplingMatrix, CsrCoupling, DenseCoupling
+from .coupling import CouplingError, CouplingMatrix, CsrCoupling, DenseCoupling, ProceduralCoupling, gen_procedural_sin
 from .model import (
     ProblemInstance,
     cut_value,

@@ -26,6 +26,7 @@ SOLVER = {"doch": 0, "adoch": 1}
 WINDOW = {"economy": 0, "exact": 1}
 PRECISION = {"f64": 0, "f32": 1, "f16tc": 2}
 PATH = {"auto": 0, "multipass": 1, "persistent": 2, "dense_tc": 3}
+FORMULA = {"sin_product": 0}  # DCX_FORMULA_* (dc/coupling.py:297-299 _PROCEDURAL_FORMULAS)
 PATH_NAME = {v: k for k, v in PATH.items()}
 STOP = {1: "converged", 2: "max_iters", 3: "time_budget"}
 EV_RECORDED, EV_DESCENT, EV_ACCEPTED, EV_REJECTED = 1, 2, 4, 8
@@ -38,6 +39,7 @@ EXPORTS = (
     "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states",
     "dcx_result_device_seconds", "dcx_profile_kernel", "dcx_set_csr_block", "dcx_stream", "dcx_dist_begin",
     "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish", "dcx_power",
+    "dcx_set_procedural", "dcx_proc_row_stats",
 )
 QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
@@ -93,6 +95,8 @@ def load(path: Path | str | None = None):
         "dcx_destroy": (None, [_P]),
         "dcx_set_csr": (C.c_int, [_P, C.c_int64, C.c_int64, _PI64, _PI64, _PD]),
         "dcx_set_dense": (C.c_int, [_P, C.c_int64, _PD]),
+        "dcx_set_procedural": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32]),
+        "dcx_proc_row_stats": (C.c_int, [_P, _PD]),
         "dcx_coupling": (C.c_int, [_P, C.POINTER(CouplingInfo)]),
         "dcx_matvec": (C.c_int, [_P, C.c_int32, _PD, _PD, C.c_int32]),
         "dcx_apply": (C.c_int, [_P, C.c_int32, _PD, _PD, _PD, _PD, _PD, C.c_int32]),
@@ -178,6 +182,16 @@ class Context:
         a = np.ascontiguousarray(array, dtype=np.float64)
         check(self.lib.dcx_set_dense(self.h, int(a.shape[0]), ptr(a, C.c_double)), self.h)
         self.n = int(a.shape[0])
+
+    def set_procedural(self, n, seed, formula="sin_product"):
+        check(self.lib.dcx_set_procedural(self.h, int(n), int(seed), FORMULA[formula]), self.h)
+        self.n = int(n)
+
+    def proc_row_stats(self) -> np.ndarray:
+        """[n][3]: per-row sum, sum of squares and sum of |J_ij| over j != i."""
+        out = np.empty((self.n, 3))
+        check(self.lib.dcx_proc_row_stats(self.h, ptr(out, C.c_double)), self.h)
+        return out
 
     def info(self) -> CouplingInfo:
         out = CouplingInfo()

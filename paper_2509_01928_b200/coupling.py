@@ -6,7 +6,8 @@ construct them unchanged; reference objects themselves are also accepted
 anywhere a coupling is expected (duck typing on ``array`` or on
 ``values / col_indices / row_offsets``). The device copy lives in a
 :class:`~paper_2509_01928_b200._native.Context` cached per coupling object
-and uploaded once (``dcx_set_csr`` / ``dcx_set_dense``).
+and uploaded once (``dcx_set_csr`` / ``dcx_set_dense``); a
+:class:`ProceduralCoupling` uploads only (n, seed) (``dcx_set_procedural``).
 """
 
 from __future__ import annotations
@@ -130,6 +131,82 @@ class CsrCoupling(CouplingMatrix):
         return float(self.values.sum()), float((self.values * self.values).sum())
 
 
+_PROCEDURAL_FORMULAS = ("sin_product",)  # dc/coupling.py:297-299
+
+
+class ProceduralCoupling(CouplingMatrix):
+    """Coupling defined by a formula, never stored (dc/coupling.py:209-290).
+
+    ``sin_product``: ``J_ij = sin(i*j + seed)`` on 0-based indices, zero on the
+    diagonal (dc/coupling.py:293-294). Every product, energy and moment runs on
+    the device, where the kernels regenerate the entries (libdcx
+    ``dcx_set_procedural``); :meth:`block` and :meth:`entry` materialise tiles
+    on the host for inspection, as the reference's do.
+    """
+
+    def __init__(self, n: int, seed: int = 100, formula: str = "sin_product", block_size: int = 1024):
+        if n < 2:
+            raise CouplingError("procedural matrices need n >= 2")
+        self.n = int(n)
+        self.seed = int(seed)
+        self.formula = formula
+        self.block_size = int(block_size)
+        self.value_kind = "real"
+        if formula not in _PROCEDURAL_FORMULAS:
+            raise CouplingError(f"unknown procedural formula {formula!r}")
+
+    @staticmethod
+    def _sin_product(i, j, seed):
+        return np.sin(i * j + float(seed))
+
+    def entry(self, i: int, j: int) -> float:
+        if i == j:
+            return 0.0
+        return float(self._sin_product(np.asarray(i), np.asarray(j), self.seed))
+
+    def block(self, r0: int, r1: int, c0: int, c1: int) -> np.ndarray:
+        for lo, hi in ((r0, r1), (c0, c1)):
+            if not (0 <= lo <= hi <= self.n):
+                raise ValueError(f"invalid index range [{lo}, {hi}) for n={self.n}")
+        rows = np.arange(r0, r1)[:, None]
+        cols = np.arange(c0, c1)[None, :]
+        out = self._sin_product(rows, cols, self.seed)
+        diag = rows == cols
+        return np.where(diag, 0.0, out) if diag.any() else out
+
+    def to_dense(self):
+        return self.block(0, self.n, 0, self.n)
+
+    def _row_stats(self) -> np.ndarray:
+        return device_context(self).proc_row_stats()
+
+    def abs_row_sums(self):
+        return self._row_stats()[:, 2].copy()
+
+    def offdiag_moments(self):
+        st = self._row_stats()
+        return float(st[:, 0].sum()), float(st[:, 1].sum())
+
+    def nnz_offdiag(self) -> int:
+        return self.n * (self.n - 1)
+
+    def validate(self, samples: int = 64, seed: int = 0) -> None:
+        """Spot-check symmetry and the zero diagonal on random index pairs (dc/coupling.py:276-290)."""
+        rng = np.random.default_rng(seed)
+        ii = rng.integers(0, self.n, size=samples)
+        jj = rng.integers(0, self.n, size=samples)
+        for i, j in zip(ii, jj):
+            if self.entry(int(i), int(j)) != self.entry(int(j), int(i)):
+                raise CouplingError(f"asymmetric procedural entry at ({i}, {j})")
+        if any(self.entry(int(i), int(i)) != 0.0 for i in ii):
+            raise CouplingError("procedural diagonal must be zero")
+
+
+def gen_procedural_sin(n: int, seed: int = 100) -> ProceduralCoupling:
+    """``entry(i, j) = sin(i * j + seed)`` for i != j (dc/generate.py:115-123)."""
+    return ProceduralCoupling(n, seed=seed, formula="sin_product")
+
+
 # ------------------------------------------------------------ device cache
 
 _ctx_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
@@ -144,6 +221,21 @@ def is_csr(J) -> bool:
     return all(hasattr(J, a) for a in ("values", "col_indices", "row_offsets"))
 
 
+def is_procedural(J) -> bool:
+    return hasattr(J, "formula") and hasattr(J, "seed") and not is_dense(J) and not is_csr(J)
+
+
+def _upload(ctx, J):
+    if is_dense(J):
+        ctx.set_dense(J.array)
+    elif is_csr(J):
+        ctx.set_csr(J.n, J.values, J.col_indices, J.row_offsets)
+    elif is_procedural(J):
+        ctx.set_procedural(J.n, J.seed, J.formula)
+    else:
+        raise CouplingError(f"unsupported coupling storage {type(J).__name__} (dense, CSR or procedural)")
+
+
 def device_context(J, device: int | None = None, reload: bool = False) -> _native.Context:
     """The device copy of coupling ``J`` (uploaded on first use; ``reload``
     copies the host arrays again into the existing device buffers)."""
@@ -153,19 +245,11 @@ def device_context(J, device: int | None = None, reload: bool = False) -> _nativ
         ctx = _ctx_by_id.get(id(J))
     if ctx is not None and (device is None or ctx.device == device):
         if reload:
-            if is_dense(J):
-                ctx.set_dense(J.array)
-            else:
-                ctx.set_csr(J.n, J.values, J.col_indices, J.row_offsets)
+            _upload(ctx, J)
         return ctx
     ctx = _native.Context(device)
     ctx.device = device
-    if is_dense(J):
-        ctx.set_dense(J.array)
-    elif is_csr(J):
-        ctx.set_csr(J.n, J.values, J.col_indices, J.row_offsets)
-    else:
-        raise CouplingError(f"unsupported coupling storage {type(J).__name__} (dense or CSR only)")
+    _upload(ctx, J)
     try:
         _ctx_cache[J] = ctx
     except TypeError:

@@ -67,6 +67,8 @@ struct dcx_ctx {
   std::string err;
   // ---------------------------------------------------------- coupling
   bool have = false, dense = false, csr_ready = false;
+  bool proc = false;         // procedural J_ij = sin(i*j + proc_seed) (dcx_set_procedural)
+  long long proc_seed = 0;
   std::vector<double> dense_host;  // dense couplings: host copy for the lazily built CSR form
   int64_t n = 0, nnz = 0;
   int64_t n_cols = 0, row_base = 0;  // row block of a row-partitioned coupling (n_cols == n, 0 otherwise)
@@ -184,6 +186,13 @@ CsrDev csr_view(const dcx_ctx* c, bool f64) {
   CsrDev J;
   J.n = c->n;
   J.nnz = c->nnz;
+  if (c->proc) {  // nothing stored: the procedural kernels generate every entry
+    J.vk = VK_PROC;
+    J.proc_seed = c->proc_seed;
+    J.V = 1;
+    J.grid = proc_pass_grid(c->n);
+    return J;
+  }
   J.rp = c->rp.as<uint32_t>();
   J.col = c->col.as<int32_t>();
   J.col16 = c->col16.as<uint16_t>();
@@ -416,6 +425,7 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
 int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   c->dense = false;
+  c->proc = false;
   c->csr_ready = false;
   c->dense_host.clear();
   c->dn.release();
@@ -428,6 +438,7 @@ int dcx_set_csr_block(dcx_ctx* c, int64_t n_rows, int64_t n_cols, int64_t row_ba
   if (n_rows < 1 || n_cols < n_rows || row_base < 0 || row_base + n_rows > n_cols)
     return fail(c, DCX_E_INVALID, "row block outside the spin index space");
   c->dense = false;
+  c->proc = false;
   c->csr_ready = false;
   c->dense_host.clear();
   c->dn.release();
@@ -558,6 +569,7 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
     if (A[i * n + i] != 0.0) return fail(c, DCX_E_INVALID, "diagonal must be zero");
   return guarded(c, [&] {
     c->have = false;
+    c->proc = false;
     c->csr_ready = false;
     c->dense_host.assign(A, A + n * n);
     c->n = n;
@@ -570,12 +582,61 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
   });
 }
 
+int dcx_set_procedural(dcx_ctx* c, int64_t n, int64_t seed, int32_t formula) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (n < 2) return fail(c, DCX_E_INVALID, "procedural matrices need n >= 2");
+  if (n >= (int64_t(1) << 31)) return fail(c, DCX_E_INVALID, "n >= 2^31 is not supported");
+  if (formula != DCX_FORMULA_SIN_PRODUCT) return fail(c, DCX_E_INVALID, "unknown procedural formula");
+  const double top = double(n - 1) * double(n - 1) + std::fabs(double(seed));
+  if (top >= 9.2e18) return fail(c, DCX_E_INVALID, "i*j + seed must fit in int64");
+  return guarded(c, [&] {
+    c->have = false;
+    c->dense = false;
+    c->csr_ready = false;
+    c->dense_host.clear();
+    c->dn.release();
+    c->rp.release();
+    c->col.release();
+    c->col16.release();
+    c->vint.release();
+    c->v64.release();
+    c->v32.release();
+    c->n = n;
+    c->n_cols = n;
+    c->row_base = 0;
+    c->nnz = n * (n - 1);
+    c->vk_int = -1;
+    c->scale = 1.0;
+    c->V32 = 1;
+    c->ell_entries = 0;
+    c->es_row_bound = 0;
+    c->proc = true;
+    c->proc_seed = seed;
+    c->have = true;
+  });
+}
+
+int dcx_proc_row_stats(dcx_ctx* c, double* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    require_coupling(c);
+    if (!c->proc) throw InvalidArg("the coupling is not procedural");
+    const int64_t n = c->n;
+    DevBuf& tmp = c->scratch;
+    if (tmp.bytes < size_t(n) * 24) tmp.alloc(size_t(n) * 24);
+    launch_proc_row_stats(n, c->proc_seed, tmp.as<double>(), c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp.p, size_t(n) * 24, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int dcx_coupling(const dcx_ctx* c, dcx_coupling_info* out) {
   if (!c || !out) return fail(nullptr, DCX_E_INVALID, "null argument");
   if (!c->have) return fail(const_cast<dcx_ctx*>(c), DCX_E_STATE, "no coupling set");
   out->n = c->n;
   out->nnz = c->nnz;
-  out->value_kind = c->vk_int >= 0 ? c->vk_int : VK_F64;
+  out->value_kind = c->proc ? VK_PROC : (c->vk_int >= 0 ? c->vk_int : VK_F64);
   out->lanes = c->V32;
   out->scale = c->scale;
   out->dense = c->dense ? 1 : 0;
@@ -668,6 +729,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     const bool use_tc = P->precision == DCX_PREC_F16TC;
     if (!use_tc && ensure_csr(c) != DCX_OK) throw CudaError(c->err);
     if (use_tc && !c->dense) throw InvalidArg("the tensor-core path needs a dense coupling");
+    if (c->proc && P->path == DCX_PATH_PERSISTENT) throw InvalidArg("procedural couplings run on the multipass path");
     c->f64 = P->precision == DCX_PREC_F64;
     const size_t tb = c->f64 ? 8 : 4;
     c->J = csr_view(c, c->f64);
@@ -720,7 +782,10 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     c->mp.vk = c->J.vk;
     c->mp.V = c->J.V;
     int slots;
-    if (R == 1) {
+    if (c->proc) {
+      c->mp.grid = proc_pass_grid(n);  // pass_proc: grid.x row blocks, grid.y replica chunks
+      slots = c->mp.grid;
+    } else if (R == 1) {
       c->mp.grid = c->J.grid;
       slots = c->mp.grid;  // one partial slot per block (pass_r1)
     } else {
@@ -766,7 +831,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.part = c->part.as<double>();
     a.slots = slots;
     a.xmap[0] = a.xmap[1] = nullptr;
-    if (R > 1 && replica_vector_width(R, c->f64) > 1) {
+    a.proc_seed = c->J.proc_seed;
+    if (R > 1 && !c->proc && replica_vector_width(R, c->f64) > 1) {
       const char* e = std::getenv("DCX_RV_TMA");
       if (!(e && std::atoi(e) == 0)) {
         alignas(64) unsigned char maps[2][128];
@@ -1181,6 +1247,7 @@ int dcx_power(dcx_ctx* c, int32_t use_shift, double shift, double tol, int64_t m
   return guarded(c, [&] {
     require_coupling(c);
     if (c->row_base != 0 || c->n_cols != c->n) throw InvalidArg("power iteration needs the whole coupling");
+    if (c->proc) throw InvalidArg("device power iteration needs a stored coupling (procedural: dcx_matvec)");
     if (!restart || max_iters < 0) throw InvalidArg("bad power-iteration arguments");
     if (ensure_csr(c) != DCX_OK) throw CudaError(c->err);
     const CsrDev J = csr_view(c, true);

@@ -14,7 +14,8 @@ namespace dcx {
 
 // ---------------------------------------------------------------- value kinds
 // Coupling values are stored in the narrowest exact form.
-enum ValueKind : int { VK_UNIFORM = 0, VK_I8 = 1, VK_I16 = 2, VK_F32 = 3, VK_F64 = 4 };
+// VK_PROC: procedural J_ij = sin(i*j + seed), generated on the fly (dcx_proc.cu)
+enum ValueKind : int { VK_UNIFORM = 0, VK_I8 = 1, VK_I16 = 2, VK_F32 = 3, VK_F64 = 4, VK_PROC = 5 };
 
 // partial-sum slots (per warp slot, per replica)
 enum : int { Q_S4 = 0, Q_SXAX = 1, Q_ES = 2, Q_STEP = 3, Q_SY4 = 4, Q_SYAY = 5, NQ = 6 };

@@ -19,6 +19,7 @@ struct CsrDev {
   int64_t ell = 0;  // entries of the 32-row sliced-ELL form of the pattern (persistent kernel, n <= 65536)
   bool pow2_uniform = false;  // uniform values with a power-of-two scale (sum x, then scale: exact)
   int grid = 1;  // grid of the R = 1 pass / apply kernels
+  long long proc_seed = 0;  // VK_PROC: seed of sin(i*j + seed)
 };
 
 // Kernel argument block of one multi-pass iteration (passed by value).
@@ -39,6 +40,7 @@ struct PassArgs {
   int32_t slots;
   int32_t es_f32;  // pass_rv: per-lane spin-energy sums exact in f32 (integer couplings, bounded rows)
   const void* xmap[2];  // pass_rv: tile::gather4 maps over gx[0] / gx[1] (device copies), or null (cp.async staging)
+  long long proc_seed;  // procedural coupling (vk == VK_PROC): seed of sin(i*j + seed)
   RunCfg cfg;
 };
 
@@ -68,6 +70,15 @@ void launch_power(const CsrDev& J, int use_shift, double shift, double tol, int6
                   cudaStream_t s);
 template <typename T>
 void launch_csr_apply(const CsrDev& J, const T* v, int R, T* jv, double* es_rows, cudaStream_t s);
+
+// dcx_proc.cu: procedural couplings (VK_PROC)
+template <typename T>
+void launch_proc_pass(int mode, const PassArgs& a, int grid, cudaStream_t s);
+int proc_pass_grid(int64_t n);
+int proc_replica_chunk(int R);
+template <typename T>
+void launch_proc_apply(int64_t n, long long seed, const T* v, int R, T* jv, double* es_rows, cudaStream_t s);
+void launch_proc_row_stats(int64_t n, long long seed, double* out, cudaStream_t s);
 
 // dcx_small.cu: persistent one-CTA-per-replica kernel (whole CSR in smem)
 struct SmallPlan {

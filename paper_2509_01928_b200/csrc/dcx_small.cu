@@ -392,6 +392,7 @@ SmallPlan plan_small(const CsrDev& J, int solver, int window_mode, bool f64) {
   sp.smem = L.total;
   sp.threads = SMALL_THREADS;
   sp.fits = L.total <= 200 * 1024 && J.n <= (1 << 20) && J.nnz < (1ll << 31);
+  if (J.vk == VK_PROC) sp.fits = false;  // no stored pattern: the procedural pass generates J
   return sp;
 }
 

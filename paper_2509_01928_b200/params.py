@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .coupling import device_context
+from .coupling import device_context, is_procedural
 
 WIGNER_SIZE_THRESHOLD = 10_000
 DEFAULT_ETA_GRID = (0.25, 0.5, 0.75, 1.0, 1.25, 1.5, 2.0)
@@ -46,6 +46,8 @@ class SolverParams:
 
 
 def _moments(J):
+    if is_procedural(J):
+        return J.offdiag_moments()  # device row statistics (dcx_proc_row_stats)
     if hasattr(J, "array"):
         a = np.asarray(J.array)
         return float(a.sum()), float((a * a).sum())
@@ -54,6 +56,8 @@ def _moments(J):
 
 
 def _abs_row_max(J) -> float:
+    if is_procedural(J):
+        return float(J.abs_row_sums().max())
     if hasattr(J, "array"):
         return float(np.abs(np.asarray(J.array)).sum(axis=1).max())
     ro = np.asarray(J.row_offsets)
@@ -66,7 +70,12 @@ def estimate_lambda_max_neg(J, method="auto", tol=1e-10, max_iters=20_000) -> fl
     if method not in ("auto", "power_iteration", "wigner"):
         raise ValueError(f"unknown spectral method {method!r}")
     if method == "auto":
-        method = "power_iteration" if J.n < WIGNER_SIZE_THRESHOLD else "wigner"
+        # procedural matrices: the moments cost one generation pass, a power step
+        # regenerates the whole matrix (dc/spectral.py:203-216)
+        if is_procedural(J):
+            method = "wigner"
+        else:
+            method = "power_iteration" if J.n < WIGNER_SIZE_THRESHOLD else "wigner"
     if method == "wigner":
         s1, s2 = _moments(J)
         if s2 == 0.0:
@@ -78,6 +87,8 @@ def estimate_lambda_max_neg(J, method="auto", tol=1e-10, max_iters=20_000) -> fl
         if est > 0:
             return est
     ctx = device_context(J)
+    if is_procedural(J):
+        return _power_procedural(ctx, J.n, tol, max_iters)
     # the reference's seeded restart vector (dc/spectral.py:84-86), drawn once on the host
     r = np.random.default_rng(0).standard_normal(J.n)
     r /= np.linalg.norm(r)
@@ -85,6 +96,54 @@ def estimate_lambda_max_neg(J, method="auto", tol=1e-10, max_iters=20_000) -> fl
     if rho == 0.0:
         raise ValueError("coupling matrix must have at least one nonzero entry")
     dom, _, _, ok = ctx.power(True, rho, tol, max_iters, r)
+    if not ok:
+        warnings.warn("shifted power iteration did not converge; using best estimate", RuntimeWarning)
+    return dom - rho
+
+
+def _power_core(apply_m, n, tol, max_iters, seed=0):
+    """dc/spectral.py:60-111 with the products on the device (procedural couplings,
+    which dcx_power does not cover): the loop and its n-vector norms stay on the host."""
+    v = np.full(n, 1.0 / np.sqrt(n))
+    restarted, best_resid, since_improve = False, np.inf, 0
+    mag = rayleigh = 0.0
+    k = 0
+    while k < max_iters:
+        w = apply_m(v)
+        mag = float(np.linalg.norm(w))
+        if mag == 0.0:
+            if restarted:
+                return 0.0, 0.0, k, False
+            v = np.random.default_rng(seed).standard_normal(n)
+            v /= np.linalg.norm(v)
+            restarted = True
+            k += 1
+            continue
+        rayleigh = float(v @ w)
+        resid = float(np.linalg.norm(w - rayleigh * v)) / mag
+        if resid <= tol:
+            return mag, rayleigh, k + 1, True
+        if resid < 0.999 * best_resid:
+            best_resid, since_improve = resid, 0
+        else:
+            since_improve += 1
+            if since_improve > 50 and not restarted:
+                v = np.random.default_rng(seed).standard_normal(n)
+                v /= np.linalg.norm(v)
+                restarted, since_improve = True, 0
+                k += 1
+                continue
+        v = w / mag
+        k += 1
+    return mag, rayleigh, k, False
+
+
+def _power_procedural(ctx, n, tol, max_iters):
+    """Two-stage shifted power iteration (dc/spectral.py:143-171) over device products."""
+    rho = _power_core(lambda v: -ctx.matvec(v[None, :])[0], n, tol, max_iters)[0]
+    if rho == 0.0:
+        raise ValueError("coupling matrix must have at least one nonzero entry")
+    dom, _, _, ok = _power_core(lambda v: rho * v - ctx.matvec(v[None, :])[0], n, tol, max_iters)
     if not ok:
         warnings.warn("shifted power iteration did not converge; using best estimate", RuntimeWarning)
     return dom - rho

@@ -37,6 +37,15 @@ def garr():
     return golden_arrays()
 
 
+@pytest.fixture(scope="session")
+def pgold():
+    """Procedural-coupling fixtures (tests/golden/make_golden_procedural.py)."""
+    with open(GOLDEN / "golden_procedural.json") as f:
+        g = json.load(f)
+    g["arrays"] = dict(np.load(GOLDEN / "golden_procedural.npz"))
+    return g
+
+
 @lru_cache(maxsize=None)
 def g1_csr():
     from paper_2509_01928_b200 import synth
