@@ -10,7 +10,13 @@ single-GPU configs through the same public API and report the same JSON keys:
   e7  configs[3]: Erdos-Renyi n = 1e7, degree 8, unit MaxCut, 1 replica, DOCH,
       eta = 1 (f32 multipass, pass_r1). HBM / L2-gather bound.
   r8  configs[4] on one GPU: random 3-regular n = 1e8, unit MaxCut, 1 replica,
-      DOCH, eta = 1, 20 iterations (the 8-GPU row-partitioned run is dist.py).
+      DOCH, eta = 1, 20 iterations.
+
+Under torchrun (WORLD_SIZE > 1), or with --rowpart at one GPU, t6 / e7 / r8
+run the row-partitioned solver of dist.py instead (each rank owns a row block,
+x exchanged per iteration by all-gather or the neighbour-only halo, --exchange);
+`value` is then the whole problem's spin-updates over the maximum device time
+over ranks ("scaling": "strong": the instance is fixed, the ranks split it).
 
 Algorithmic bytes per iteration (the HBM roofline numerator):
 nnz * (4 + value bytes) + (n + 1) * 4 + R * n * 4 * 2.
@@ -87,6 +93,61 @@ def cpu_sample(name, inst, alpha, beta, arrays, budget_s=20.0):
     return upd / dt, dt, f"{r} replicas x <= {iters} DOCH iterations, numpy/scipy csr_matvec ({dt:.1f} s)"
 
 
+def run_rowpart(args, name, cfg, inst, alpha, beta, X0, t_build):
+    """Row-partitioned t6 / e7 / r8 (dist.py) on WORLD_SIZE ranks, one GPU each."""
+    import torch
+    import torch.distributed as dist
+
+    from bench import ClockSampler, allreduce, barrier, dist_setup
+    from paper_2509_01928_b200 import dist as dd
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():  # --rowpart at one GPU: NCCL world of one
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    n, R = inst.coupling.n, X0.shape[0]
+    kw = dict(max_iters=cfg["max_iters"], trace_stride=1, precision=cfg["precision"], device=local,
+              exchange=args.exchange, poll_every=16)
+    for _ in range(args.warmup):
+        dd.solve_distributed(inst, "doch", alpha, beta, X0, **kw)
+    dev, wall, upd = 0.0, 0.0, 0
+    barrier(dist.get_world_size())
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = dd.solve_distributed(inst, "doch", alpha, beta, X0, **kw)
+            wall += time.perf_counter() - t0
+            dev += res[0].device_seconds
+            upd += n * sum(r.iterations for r in res)
+    torch.cuda.synchronize()
+    ws = dist.get_world_size()
+    dev_max, = allreduce([dev], "max", ws)
+    wall_max, = allreduce([wall], "max", ws)
+    if rank == 0:
+        e = np.array([r.energy for r in res])
+        line = {
+            "metric": "spin-updates/s", "value": upd / dev_max, "unit": "spin-updates/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg["precision"],
+            "data": "synthetic",
+            "config": {"workload": cfg["desc"].replace(", 1 GPU", "") + f", row-partitioned over {ws} GPU(s)",
+                       "n": n, "replicas": R, "max_iters": cfg["max_iters"], "path": res[0].path,
+                       "parallelism": f"rows x{ws}", "host_instance_build_s": round(t_build, 1),
+                       "l2": "state + CSR stream exceed L2"},
+            # the public entry point re-uploads the row block and x0 every solve (host buffers in,
+            # best spins and final x gathered back to every rank)
+            "e2e": {"value": upd / wall_max, "unit": "spin-updates/s", "h2d_bytes_per_step": int(X0.nbytes),
+                    "d2h_bytes_per_step": int(X0.nbytes + R * n)},
+            "clocks": clk.summary(),
+            "quality": {"best_energy": float(e.min()), "mean_energy": float(e.mean())},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run(args):
     import paper_2509_01928_b200 as dc
 
@@ -98,6 +159,9 @@ def run(args):
     n = inst.coupling.n
     R = cfg["R"]
     X0 = np.stack([dc.initial_state(n, alpha, beta, np.random.default_rng(s)) for s in range(R)])
+    if name != "g1" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or getattr(args, "rowpart", False)):
+        run_rowpart(args, name, cfg, inst, alpha, beta, X0, t_build)
+        return
     kw = dict(max_iters=cfg["max_iters"], trace_stride=1, precision=cfg["precision"])
     for _ in range(args.warmup):
         dc.solve_replicas(inst, "doch", alpha, beta, X0, **kw)

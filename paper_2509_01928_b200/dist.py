@@ -12,7 +12,12 @@ NVLink). Per iteration every rank
   2. all-reduces those sums (SUM) and maxima (MAX) -- 8 doubles per replica,
   3. runs the control on the reduced values (``dcx_dist_control``): identical on
      every rank, so stop / record / ADOCH-accept decisions agree,
-  4. all-gathers the new x slices (in place) for the next pass.
+  4. exchanges the new x slices for the next pass: either an all-gather of every
+     slice (in place), or a neighbour-only exchange ("halo") that sends each rank
+     exactly the x rows its coupling rows reference (a lattice
+     strip needs its two boundary rows; a random 3-regular graph at 8 ranks needs
+     about a third of the remote rows). ``exchange="auto"`` takes the halo when it
+     moves less than 3/4 of the all-gather volume.
 
 Blocks are padded to a common row count B so the all-gather is a plain
 ``all_gather_into_tensor``; columns are remapped into that padded index space
@@ -135,6 +140,48 @@ class Exchange:
         dist.all_gather(parts, h, group=self.group)
         X.copy_(torch.cat(parts, 0))
 
+    def all_to_all_counts(self, counts):
+        """counts[p] = rows this rank receives from p -> rows this rank sends to each p."""
+        import torch
+
+        t = torch.tensor(counts, dtype=torch.int64)
+        out = torch.empty_like(t)
+        if self.host_staged:
+            self.dist.all_to_all_single(out, t, group=self.group)
+        else:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            o = out.to(dev)
+            self.dist.all_to_all_single(o, t.to(dev), group=self.group)
+            out = o.cpu()
+        return [int(v) for v in out]
+
+    def all_to_all_rows_int(self, pos, out_counts, in_counts):
+        """Ragged all-to-all of int64 positions (setup of the halo plan)."""
+        import torch
+
+        t = torch.from_numpy(np.ascontiguousarray(pos, dtype=np.int64))
+        out = torch.empty(sum(in_counts), dtype=torch.int64)
+        if self.host_staged:
+            self.dist.all_to_all_single(out, t, in_counts, out_counts, group=self.group)
+        else:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            o = out.to(dev)
+            self.dist.all_to_all_single(o, t.to(dev), in_counts, out_counts, group=self.group)
+            out = o.cpu()
+        return out.numpy()
+
+    def halo(self, X, plan: HaloPlan, send_idx, recv_idx, recv_buf):
+        """Neighbour-only exchange into X [world*B, R]: rows send_idx go out, rows recv_idx come in."""
+        dist = self.dist
+        send = X.index_select(0, send_idx)
+        if not self.host_staged:
+            dist.all_to_all_single(recv_buf, send, plan.recv_counts, plan.send_counts, group=self.group)
+            X.index_copy_(0, recv_idx, recv_buf)
+            return
+        h = recv_buf.cpu() if recv_buf.device.type != "cpu" else recv_buf
+        dist.all_to_all_single(h, send.cpu(), plan.recv_counts, plan.send_counts, group=self.group)
+        X.index_copy_(0, recv_idx, h.to(X.device))
+
     def all_reduce(self, t, op: str):
         dist = self.dist
         rop = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX}[op]
@@ -146,16 +193,59 @@ class Exchange:
         t.copy_(h)
 
 
+@dataclass
+class HaloPlan:
+    """Neighbour-only exchange of one rank (positions in the padded space).
+
+    ``send_pos`` lists rows of this rank's block, grouped by destination rank
+    (ascending rank, ascending position); ``recv_pos`` lists rows of other
+    blocks this rank's coupling rows reference, grouped by source rank.
+    """
+
+    send_pos: np.ndarray
+    send_counts: list
+    recv_pos: np.ndarray
+    recv_counts: list
+
+    @property
+    def volume(self) -> int:
+        """Rows received per exchange."""
+        return int(self.recv_pos.size)
+
+
+def halo_needs(cols_padded, rb: RowBlocks, rank: int):
+    """Remote rows referenced by this rank's columns: (sorted positions, per-owner counts)."""
+    c = np.unique(np.asarray(cols_padded, dtype=np.int64))
+    lo, hi = rank * rb.B, (rank + 1) * rb.B
+    remote = c[(c < lo) | (c >= hi)]
+    counts = np.bincount(remote // rb.B, minlength=rb.world).astype(np.int64)
+    return remote, [int(k) for k in counts]
+
+
+def halo_plan(ex: "Exchange", cols_padded, rb: RowBlocks) -> HaloPlan:
+    """Every rank states what it needs; two all-to-alls (counts, then positions) turn
+    the needs into send lists. Setup only (once per solve)."""
+    recv_pos, recv_counts = halo_needs(cols_padded, rb, ex.rank)
+    send_counts = ex.all_to_all_counts(recv_counts)
+    send_pos = ex.all_to_all_rows_int(recv_pos, recv_counts, send_counts)
+    lo = ex.rank * rb.B
+    if send_pos.size and (send_pos.min() < lo or send_pos.max() >= lo + rb.B):
+        raise RuntimeError("halo plan: a peer asked for rows this rank does not own")
+    return HaloPlan(send_pos, send_counts, recv_pos, recv_counts)
+
+
 # -------------------------------------------------------------------- driver
 def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max_iters: int = 1000,
                       lookback_q: int = 5, window_mode: str = "economy", trace_stride: int = 1,
                       time_budget: Optional[float] = None, precision: str = "f32",
                       seeds: Optional[Sequence[int]] = None, poll_every: int = 16,
-                      device: Optional[int] = None, _context=None) -> list:
+                      device: Optional[int] = None, exchange: str = "auto", _context=None) -> list:
     """Row-partitioned ``solve_replicas``: the same R replicas, the coupling split by rows over the ranks
     of ``group`` (every rank passes the same instance and the same full ``x0`` [R][n]).
 
     Returns one SolveResult per replica on every rank (best spins and final x gathered to all ranks).
+    ``exchange``: "allgather", "halo" (neighbour-only) or "auto" (halo when it moves < 3/4 of the
+    all-gather rows summed over ranks). Both give bit-identical iterates.
     ``_context`` replaces the libdcx context (tests only).
     """
     import torch
@@ -166,6 +256,8 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         raise ValueError("the row-partitioned solver supports window_mode 'economy'")
     if precision not in ("f64", "f32"):
         raise ValueError("the row-partitioned solver runs in precision 'f64' or 'f32'")
+    if exchange not in ("auto", "allgather", "halo"):
+        raise ValueError(f"unknown exchange {exchange!r}")
     t_entry = time.perf_counter()
     ex = Exchange(group)
     J = instance.coupling
@@ -197,10 +289,26 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         path=_native.PATH["multipass"], chunk=0, reserved=0)
     stream = (torch.cuda.ExternalStream(ctx.stream(), device=tdev) if tdev.type == "cuda" else None)
     with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
+        use_halo = exchange == "halo"
+        if exchange != "allgather" and ex.world > 1:
+            plan = halo_plan(ex, cols, rb)
+            if exchange == "auto":
+                vol = torch.tensor([float(plan.volume), float(rb.n_space - rb.B)], dtype=torch.float64,
+                                   device=tdev)
+                ex.all_reduce(vol, "sum")
+                use_halo = bool(vol[0] < 0.75 * vol[1])
+        if use_halo and ex.world > 1:
+            send_idx = torch.from_numpy(plan.send_pos).to(tdev)
+            recv_idx = torch.from_numpy(plan.recv_pos).to(tdev)
+            recv_buf = torch.empty(plan.volume, R, dtype=dt, device=tdev)
+            step = lambda Xp: ex.halo(Xp, plan, send_idx, recv_idx, recv_buf)  # noqa: E731
+        else:
+            use_halo = False
+            step = lambda Xp: ex.all_gather_rows(Xp, rb.B)  # noqa: E731
         ctx.dist_begin(prm, alpha, beta, X0[:, r0:r1], X[0].data_ptr(), X[1].data_ptr(), qs.data_ptr(),
                        qm.data_ptr())
         offset = time.perf_counter() - t_entry
-        ex.all_gather_rows(X[0], rb.B)
+        step(X[0])
         p, live = 0, True
         while live:
             for _ in range(max(1, int(poll_every))):
@@ -209,7 +317,7 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
                 ex.all_reduce(qm, "max")
                 ctx.dist_control()
                 p += 1
-                ex.all_gather_rows(X[p & 1], rb.B)
+                step(X[p & 1])
             live, _ = ctx.dist_poll()
         ctx.dist_finish()
         # gather best spins and final states of every row block (padded space)
@@ -228,4 +336,4 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
     best = rb.unpad(full_b.cpu().numpy().T)
     xs = rb.unpad(full_x.cpu().numpy().T)
     return assemble_results(ctx, solver, R, best, xs, offset, getattr(instance, "cut_offset", None), seeds,
-                            path="row-partitioned")
+                            path="row-partitioned/" + ("halo" if use_halo else "allgather"))

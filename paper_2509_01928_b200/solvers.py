@@ -370,10 +370,11 @@ def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", 
     dense = bool(info.dense)
     tb = 8 if precision == "f64" else (2 if precision == "f16tc" else 4)
     if kid == 3:
-        # one launch = DENSE_PROFILE_ITERS iterations of the persistent kernel; per
-        # iteration two n x n x R products: J x (f16 -> f32) and J sign(x) (int8 -> s32)
+        # one launch = 100 iterations of the persistent kernel (dense_iters_per_profile_launch,
+        # csrc/dcx_dense.cu; launches resume the run, so launches <= max_iters/100 - 1);
+        # per iteration two n x n x R products: J x (f16 -> f32) and J sign(x) (int8 -> s32)
         name = "dense_doch_kernel"
-        iters = 10
+        iters = 100
         flops = iters * 2 * (2.0 * n * n * R)
         byts = float(iters * R * n * (2 + 1))  # f16 + int8 operands of the next iteration
     else:
@@ -383,5 +384,5 @@ def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", 
             vbytes = tb
         flops = 2.0 * info.nnz * R
         byts = float(info.nnz * (4 + vbytes) + (n + 1) * 4 + R * n * tb * 2)
-    return {"kernel": name, "ms_per_launch": ms, "flops_per_launch": flops, "bytes_per_launch": byts,
+    return {"kernel": name, "ms_per_launch": ms, "iterations_per_launch": iters if kid == 3 else 1, "flops_per_launch": flops, "bytes_per_launch": byts,
             "bound": "tensor" if dense else "hbm", "kernel_id": kid}

@@ -153,21 +153,32 @@ def init_group(rank, world, init_file, backend="gloo"):
     return dist
 
 
-def fake_worker(rank, world, init_file, out_file, n, seed_graph, R, max_iters):
-    """One rank of the CPU test: ER graph, DOCH f64 through the row-partitioned driver."""
+def graph_of(kind, n, seed_graph):
+    from paper_2509_01928_b200 import synth
+
+    if kind == "torus":
+        L = int(round(n ** 0.5))
+        return synth.torus(L, seed=seed_graph) + (None,)
+    if kind == "reg3":
+        return synth.random_regular3(n, seed=seed_graph)
+    return synth.erdos_renyi(n, 6, seed=seed_graph)
+
+
+def fake_worker(rank, world, init_file, out_file, n, seed_graph, R, max_iters, exchange="allgather", kind="er"):
+    """One rank of the CPU test: DOCH f64 through the row-partitioned driver."""
     import paper_2509_01928_b200 as dc
-    from paper_2509_01928_b200 import dist as dd, synth
+    from paper_2509_01928_b200 import dist as dd
 
     dist = init_group(rank, world, init_file)
-    v, c, o, co = synth.erdos_renyi(n, 6, seed=seed_graph)
+    v, c, o, co = graph_of(kind, n, seed_graph)
     J = dc.CsrCoupling(n, v, c, o, validate=False)
     inst = dc.ProblemInstance(coupling=J, cut_offset=co)
     alpha, beta = 3.0, float(n) ** 1.5 * 10.0
     X0 = np.stack([dc.initial_state(n, alpha, beta, np.random.default_rng(s)) for s in range(R)])
     res = dd.solve_distributed(inst, "doch", alpha, beta, X0, max_iters=max_iters, precision="f64",
-                               poll_every=4, _context=FakeRowContext())
+                               poll_every=4, exchange=exchange, _context=FakeRowContext())
     if rank == 0:
-        np.savez(out_file, x=np.stack([r.x for r in res]), spins=np.stack([r.spins for r in res]),
+        np.savez(out_file, path=res[0].path, x=np.stack([r.x for r in res]), spins=np.stack([r.spins for r in res]),
                  energy=np.array([r.energy for r in res]), iterations=np.array([r.iterations for r in res]),
                  stop=np.array([r.stop_reason for r in res]),
                  h=np.stack([np.asarray(r.h_values)[: max_iters + 1] for r in res]) if R > 1 else
@@ -197,7 +208,39 @@ def exchange_worker(rank, world, init_file, out_file):
     dist.destroy_process_group()
 
 
-def gpu_worker(rank, world, init_file, out_file, solver, precision, R, max_iters):
+def halo_plan_worker(rank, world, init_file, out_file, kind, n):
+    """Build the halo plan on every rank; rank 0 saves every rank's lists."""
+    import torch
+
+    import paper_2509_01928_b200 as dc
+    from paper_2509_01928_b200 import dist as dd
+
+    dist = init_group(rank, world, init_file)
+    v, c, o, _ = graph_of(kind, n, 0)
+    J = dc.CsrCoupling(n, v, c, o, validate=False)
+    rb = dd.RowBlocks(dd.partition_rows(o, world), n)
+    _, _, cols, _ = dd.local_block(J, rb, rank)
+    ex = dd.Exchange()
+    plan = dd.halo_plan(ex, cols, rb)
+    # exchange position-valued rows: afterwards every referenced row holds its own index
+    X = torch.full((rb.n_space, 2), -1.0, dtype=torch.float64)
+    lo = rank * rb.B
+    X[lo:lo + rb.B, 0] = torch.arange(lo, lo + rb.B, dtype=torch.float64)
+    X[lo:lo + rb.B, 1] = -torch.arange(lo, lo + rb.B, dtype=torch.float64)
+    ex.halo(X, plan, torch.from_numpy(plan.send_pos), torch.from_numpy(plan.recv_pos),
+            torch.empty(plan.volume, 2, dtype=torch.float64))
+    ok = bool(np.all(X[np.unique(cols), 0].numpy() == np.unique(cols)))
+    ok &= bool(np.all(X[np.unique(cols), 1].numpy() == -np.unique(cols)))
+    info = torch.tensor([plan.volume, int(plan.send_pos.size), int(ok), rb.B], dtype=torch.int64)
+    allinfo = [torch.zeros_like(info) for _ in range(world)]
+    dist.all_gather(allinfo, info)
+    if rank == 0:
+        np.savez(out_file, info=torch.stack(allinfo).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def gpu_worker(rank, world, init_file, out_file, solver, precision, R, max_iters, exchange="allgather"):
     """One rank of the GPU test (every rank on cuda:0, gloo host-staged exchange)."""
     import paper_2509_01928_b200 as dc
     from paper_2509_01928_b200 import dist as dd, synth
@@ -209,7 +252,7 @@ def gpu_worker(rank, world, init_file, out_file, solver, precision, R, max_iters
     alpha, beta = 3.0, 1e4 ** 1.5 * 10.0
     X0 = np.stack([dc.initial_state(10_000, alpha, beta, np.random.default_rng(s)) for s in range(R)])
     res = dd.solve_distributed(inst, solver, alpha, beta, X0, max_iters=max_iters, precision=precision,
-                               device=0, poll_every=8)
+                               device=0, poll_every=8, exchange=exchange)
     if rank == 0:
         np.savez(out_file, x=np.stack([r.x for r in res]), spins=np.stack([r.spins for r in res]),
                  energy=np.array([r.energy for r in res]), iterations=np.array([r.iterations for r in res]),

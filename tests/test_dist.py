@@ -19,7 +19,7 @@ import scipy.sparse as sp
 import paper_2509_01928_b200 as dc
 from paper_2509_01928_b200 import dist as dd, synth
 
-from _dist_helpers import exchange_worker, fake_worker, gpu_worker
+from _dist_helpers import exchange_worker, fake_worker, gpu_worker, halo_plan_worker
 
 
 def _spawn(fn, world, *args):
@@ -80,13 +80,38 @@ def test_exchange_gloo_world2():
     assert np.all(out["m"] == 1.0)
 
 
-# ---------------------------------------------------- driver (CPU, gloo, fake)
-def test_row_partitioned_doch_matches_oracle_gloo_world2():
-    from oracle import dcising_oracle as orc
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_plan_lattice_strips_exchange_boundary_rows_only(world):
+    """A torus split into contiguous row strips: each rank receives exactly the two
+    lattice rows bordering its strip (2 L spins), not the whole of x."""
+    L = 24
+    out = _spawn(halo_plan_worker, world, "torus", L * L)["info"]
+    for q in range(world):
+        recv, sent, ok, B = out[q]
+        assert ok == 1
+        assert recv <= 2 * L + 2 * world  # strips need not start on a lattice row boundary
+        assert recv >= 2 * L - 2
+    assert out[:, 0].sum() == out[:, 1].sum()  # everything received was sent
 
-    n, R, max_iters = 2000, 3, 60
-    out = _spawn(fake_worker, 2, n, 5, R, max_iters)
-    v, c, o, co = synth.erdos_renyi(n, 6, seed=5)
+
+def test_halo_plan_random_3_regular_is_a_fraction_of_allgather():
+    out = _spawn(halo_plan_worker, 3, "reg3", 30_000)["info"]
+    assert np.all(out[:, 2] == 1)
+    B = out[0, 3]
+    # each rank references ~ (1 - exp(-3 x rows/remote rows)) of the remote rows
+    assert np.all(out[:, 0] < 2 * B * 0.85)
+
+
+# ---------------------------------------------------- driver (CPU, gloo, fake)
+@pytest.mark.parametrize("kind,exchange", [("er", "allgather"), ("er", "halo"), ("torus", "auto")])
+def test_row_partitioned_doch_matches_oracle_gloo_world2(kind, exchange):
+    from oracle import dcising_oracle as orc
+    from _dist_helpers import graph_of
+
+    n, R, max_iters = (2000, 3, 60) if kind == "er" else (1600, 2, 60)
+    out = _spawn(fake_worker, 2, n, 5, R, max_iters, exchange, kind)
+    assert str(out["path"]) == "row-partitioned/" + ("allgather" if exchange == "allgather" else "halo")
+    v, c, o, co = graph_of(kind, n, 5)
     alpha, beta = 3.0, float(n) ** 1.5 * 10.0
     op = orc.Operator((v, c, o))
     for r in range(R):
@@ -137,11 +162,12 @@ def test_row_partitioned_world1_nccl_equals_multipass(solver, precision):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("solver", ["doch", "adoch"])
-def test_row_partitioned_two_ranks_one_gpu_gloo(solver):
+@pytest.mark.parametrize("solver,exchange", [("doch", "allgather"), ("adoch", "allgather"), ("doch", "halo"),
+                                             ("adoch", "halo")])
+def test_row_partitioned_two_ranks_one_gpu_gloo(solver, exchange):
     R, max_iters = 4, 120
     _, _, _, _, ref = _single_context(solver, "f64", R, max_iters)
-    out = _spawn(gpu_worker, 2, solver, "f64", R, max_iters)
+    out = _spawn(gpu_worker, 2, solver, "f64", R, max_iters, exchange)
     agree = 0
     for r in range(R):
         assert out["iterations"][r] == ref[r].iterations
