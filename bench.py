@@ -324,6 +324,10 @@ def main():
     ap.add_argument("--path", default=os.environ.get("DCX_BENCH_PATH", "auto"))
     ap.add_argument("--config", default="k2", choices=["k2", "g1", "t6", "e7", "r8"],
                     help="k2 is the headline (BASELINE configs[1]); others: see bench_configs.py")
+    ap.add_argument("--rowpart", action="store_true",
+                    help="t6/e7/r8: row-partitioned solver (dist.py) even at one GPU")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
+                    help="row-partitioned x exchange")
     args = ap.parse_args()
     # descent-violation RuntimeWarnings are per-replica diagnostics (1024 lines of
     # stderr per solve at K2 in f16); neither arm prints them while timed
