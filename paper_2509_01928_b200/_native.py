@@ -82,7 +82,8 @@ def load(path: Path | str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # DCX_LIB: another build of the same ABI (A/B timing of kernel variants)
+    p = Path(path) if path else Path(os.environ.get("DCX_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"libdcx.so not found at {p}: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

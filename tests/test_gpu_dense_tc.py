@@ -105,7 +105,11 @@ def test_tc_k2000_quality_vs_reference(gold):
     assert e.mean() <= ref.mean() + 3 * se
     # the reference's own best over 32 seeds sits 2.4 sigma out; 1024 replicas reach 2 sigma
     assert e.min() <= ref.mean() - 2.0 * ref.std()
-    assert np.quantile(e, 0.1) <= np.quantile(ref, 0.1) + 3 * se
+    # lower decile: the reference's is an order statistic of 32 samples, whose standard
+    # error is sqrt(q (1 - q) / m) / pdf(z_q) sigma = 0.30 sigma for q = 0.1, m = 32 under a
+    # normal fit (3 x that, not 3 x the standard error of the mean)
+    se_q = np.sqrt(0.1 * 0.9 / len(ref)) / (np.exp(-0.5 * 1.2816 ** 2) / np.sqrt(2 * np.pi)) * ref.std()
+    assert np.quantile(e, 0.1) <= np.quantile(ref, 0.1) + 3 * se_q
 
 
 def _run_with_env(env, fn):
