@@ -209,6 +209,24 @@ DCX_API int dcx_dist_poll(dcx_ctx* ctx, int32_t* live, int64_t* passes);
 /* ends the run (pending best-spin copies, device time); results as for dcx_solve_* with n = n_rows */
 DCX_API int dcx_dist_finish(dcx_ctx* ctx);
 
+/* ---- instance generation and ingest on the device ----
+ * gen_sparse_9bit of dc/generate.py:80-112 (replaces the per-row numpy loop and the
+ * scipy COO -> CSR closure): n spins, n_p = int(102300 // p) (computed by the caller
+ * as the reference does), per-row Philox4x64-10 streams keyed (seed, row). The CSR
+ * stays in the context until dcx_gen_result copies it out in the reference's layout
+ * (int64 row_offsets [n+1], int64 col_indices [nnz], f64 values [nnz]) -- the bytes
+ * the reference's CsrCoupling holds. */
+DCX_API int dcx_gen_sparse_9bit(dcx_ctx* ctx, int64_t n, int64_t n_p, uint64_t seed, int64_t* nnz);
+DCX_API int dcx_gen_result(dcx_ctx* ctx, int64_t* row_offsets, int64_t* col_indices, double* values);
+/* CsrCoupling.validate of dc/coupling.py:153-176 on the device (csr_load's ingest check,
+ * dc/io.py:272-305): *check = 0 valid, 2 offsets not starting at 0 / decreasing,
+ * 3 row_offsets[n] != nnz, 4 column out of range, 5 columns not strictly increasing in
+ * row *row, 6 stored diagonal in row *row, 7 non-finite value, 8 asymmetric; the first
+ * failing check in the reference's order. *all_int = every value integral (nnz > 0). */
+DCX_API int dcx_validate_csr(dcx_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_offsets,
+                             const int64_t* col_indices, const double* values, int32_t* check, int64_t* row,
+                             int32_t* all_int);
+
 #ifdef __cplusplus
 }
 #endif

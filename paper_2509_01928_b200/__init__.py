@@ -20,6 +20,8 @@ from .model import (
     maxcut_to_ising,
     spins_from,
 )
+from .generate import gen_sparse_9bit
+from .io import FormatError, csr_load, csr_save
 from .params import DEFAULT_ETA_GRID, SolverParams, derive_params, estimate_lambda_max_neg, tune_eta
 from .solvers import (
     CONVERGENCE_TOL,

@@ -39,7 +39,7 @@ EXPORTS = (
     "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states",
     "dcx_result_device_seconds", "dcx_profile_kernel", "dcx_set_csr_block", "dcx_stream", "dcx_dist_begin",
     "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish", "dcx_power",
-    "dcx_set_procedural", "dcx_proc_row_stats",
+    "dcx_set_procedural", "dcx_proc_row_stats", "dcx_gen_sparse_9bit", "dcx_gen_result", "dcx_validate_csr",
 )
 QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
@@ -122,6 +122,9 @@ def load(path: Path | str | None = None):
         "dcx_dist_poll": (C.c_int, [_P, _PI32, _PI64]),
         "dcx_dist_finish": (C.c_int, [_P]),
         "dcx_power": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_int64, _PD, _PD, _PD, _PI64, _PI32]),
+        "dcx_gen_sparse_9bit": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_uint64, _PI64]),
+        "dcx_gen_result": (C.c_int, [_P, _PI64, _PI64, _PD]),
+        "dcx_validate_csr": (C.c_int, [_P, C.c_int64, C.c_int64, _PI64, _PI64, _PD, _PI32, _PI64, _PI32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -311,6 +314,28 @@ class Context:
         check(self.lib.dcx_power(self.h, int(bool(use_shift)), float(shift), float(tol), int(max_iters),
                                  ptr(r, C.c_double), C.byref(mag), C.byref(ray), C.byref(it), C.byref(conv)), self.h)
         return mag.value, ray.value, int(it.value), bool(conv.value)
+
+    # ------------------------------------------------- generation / ingest
+    def gen_sparse_9bit(self, n: int, n_p: int, seed: int):
+        """(row_offsets int64, col_indices int64, values f64) generated on the device."""
+        nnz = C.c_int64()
+        check(self.lib.dcx_gen_sparse_9bit(self.h, int(n), int(n_p), int(seed) & ((1 << 64) - 1), C.byref(nnz)),
+              self.h)
+        ro = np.empty(int(n) + 1, dtype=np.int64)
+        col = np.empty(nnz.value, dtype=np.int64)
+        val = np.empty(nnz.value, dtype=np.float64)
+        check(self.lib.dcx_gen_result(self.h, ptr(ro, C.c_int64), ptr(col, C.c_int64), ptr(val, C.c_double)), self.h)
+        return ro, col, val
+
+    def validate_csr(self, n, row_offsets, col_indices, values):
+        """(check, row, all_int) of dcx_validate_csr (include/dcx.h)."""
+        ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        ci = np.ascontiguousarray(col_indices, dtype=np.int64)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        chk, row, ai = C.c_int32(), C.c_int64(), C.c_int32()
+        check(self.lib.dcx_validate_csr(self.h, int(n), int(len(v)), ptr(ro, C.c_int64), ptr(ci, C.c_int64),
+                                        ptr(v, C.c_double), C.byref(chk), C.byref(row), C.byref(ai)), self.h)
+        return int(chk.value), int(row.value), bool(ai.value)
 
     # ------------------------------------------------- row-partitioned runs
     def set_csr_block(self, n_rows, n_cols, row_base, values, col_indices, row_offsets):

@@ -105,6 +105,7 @@ struct dcx_ctx {
   HistRec* ring = nullptr;  // pinned host copy of the device history ring
   size_t ring_n = 0;
   GState hg{};
+  GenCsr gen;  // dcx_gen_sparse_9bit result until dcx_gen_result
 
   ~dcx_ctx() {
     if (ring) cudaFreeHost(ring);
@@ -1284,6 +1285,42 @@ int dcx_result_device_seconds(dcx_ctx* c, double* out) {
   if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
   *out = c->dev_seconds;
   return DCX_OK;
+}
+
+// ------------------------------------------------------------ generation / ingest (dcx_gen.cu)
+int dcx_gen_sparse_9bit(dcx_ctx* c, int64_t n, int64_t n_p, uint64_t seed, int64_t* nnz) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    gen_sparse_9bit(n, n_p, seed, c->gen, c->stream);
+    if (nnz) *nnz = c->gen.nnz;
+  });
+}
+
+int dcx_gen_result(dcx_ctx* c, int64_t* ro, int64_t* col, double* val) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->gen.ro) throw InvalidArg("no generated coupling (dcx_gen_sparse_9bit)");
+    if (!ro || (c->gen.nnz && (!col || !val))) throw InvalidArg("null output array");
+    CK(cudaMemcpyAsync(ro, c->gen.ro, sizeof(int64_t) * (c->gen.n + 1), cudaMemcpyDeviceToHost, c->stream));
+    if (c->gen.nnz) {
+      CK(cudaMemcpyAsync(col, c->gen.col, sizeof(int64_t) * c->gen.nnz, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(val, c->gen.val, sizeof(double) * c->gen.nnz, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->gen.release();
+  });
+}
+
+int dcx_validate_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* col, const double* val,
+                     int32_t* check, int64_t* row, int32_t* all_int) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  if (!ro || !check || !row || !all_int || (nnz > 0 && (!col || !val))) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    if (n < 1 || nnz < 0) throw InvalidArg("n must be >= 1 and nnz >= 0");
+    int ai = 0;
+    *check = validate_csr_device(n, nnz, ro, col, val, row, &ai, c->stream);
+    *all_int = ai;
+  });
 }
 
 }  // extern "C"

@@ -80,6 +80,19 @@ template <typename T>
 void launch_proc_apply(int64_t n, long long seed, const T* v, int R, T* jv, double* es_rows, cudaStream_t s);
 void launch_proc_row_stats(int64_t n, long long seed, double* out, cudaStream_t s);
 
+// dcx_gen.cu: instance generation and ingest on the device
+struct GenCsr {  // a generated CSR in the reference's host layout (int64 offsets / columns, f64 values)
+  int64_t n = 0, nnz = 0;
+  int64_t* ro = nullptr;
+  int64_t* col = nullptr;
+  double* val = nullptr;
+  void release();
+  ~GenCsr() { release(); }
+};
+void gen_sparse_9bit(int64_t n, int64_t n_p, uint64_t seed, GenCsr& out, cudaStream_t s);
+int validate_csr_device(int64_t n, int64_t nnz, const int64_t* ro, const int64_t* col, const double* val,
+                        int64_t* row, int* all_int, cudaStream_t s);
+
 // dcx_small.cu: persistent one-CTA-per-replica kernel (whole CSR in smem)
 struct SmallPlan {
   size_t smem = 0;
