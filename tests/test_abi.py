@@ -12,7 +12,7 @@ from paper_2509_01928_b200 import _native
 
 def header_symbols():
     text = (ROOT / "include" / "dcx.h").read_text()
-    return sorted(set(re.findall(r"\b(dcx_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(dcx_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_and_binding_agree():
