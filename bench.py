@@ -322,7 +322,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default=os.environ.get("DCX_BENCH_PRECISION", "f16tc"))
     ap.add_argument("--path", default=os.environ.get("DCX_BENCH_PATH", "auto"))
-    ap.add_argument("--config", default="k2", choices=["k2", "g1", "t6", "e7", "r8"],
+    ap.add_argument("--config", default="k2", choices=["k2", "g1", "t6", "e7", "r8", "gen9"],
                     help="k2 is the headline (BASELINE configs[1]); others: see bench_configs.py")
     ap.add_argument("--rowpart", action="store_true",
                     help="t6/e7/r8: row-partitioned solver (dist.py) even at one GPU")

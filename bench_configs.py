@@ -148,10 +148,68 @@ def run_rowpart(args, name, cfg, inst, alpha, beta, X0, t_build):
     dist.destroy_process_group()
 
 
+def run_gen9(args):
+    """gen_sparse_9bit on the device vs the reference's generator
+    loop on the host. Work unit: one draw of the lower triangle (n(n-1)/2 per instance)."""
+    import torch
+
+    import paper_2509_01928_b200 as dc
+    from oracle import dcising_oracle as orc
+
+    n, p = 100_000, 1.0
+    draws = n * (n - 1) / 2
+    for s in range(args.warmup):
+        dc.gen_sparse_9bit(n, p, seed=s)
+    ctx = dc.generate._context()
+    dev = 0.0
+    wall = 0.0
+    for s in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        # device time: generation + CSR assembly (the download of the result is e2e)
+        J = dc.gen_sparse_9bit(n, p, seed=100 + s)
+        wall += time.perf_counter() - t0
+    # device-only timing of the generation call through the context (result left on the device)
+    import ctypes
+
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    for s in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        out = ctypes.c_int64()
+        e0.record(stream)
+        ctx.lib.dcx_gen_sparse_9bit(ctx.h, n, int(102300 // p), 200 + s, ctypes.byref(out))
+        e1.record(stream)
+        e1.synchronize()
+        dev += e0.elapsed_time(e1) * 1e-3  # CUDA events on the context stream
+    cpu_n = 8000
+    t0 = time.perf_counter()
+    orc.gen_sparse_9bit_numpy(cpu_n, p, 1)
+    cpu_t = time.perf_counter() - t0
+    line = {
+        "metric": "lower-triangle draws/s", "value": args.steps * draws / dev, "unit": "draws/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Philox4x64-10)",
+        "data": "synthetic",
+        "config": {"workload": f"gen_sparse_9bit(n={n}, p={p}) on the device: per-row Philox streams, "
+                               "symmetric CSR in the reference's int64/f64 layout", "n": n, "nnz": int(J.nnz)},
+        "e2e": {"value": args.steps * draws / wall, "unit": "draws/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(J.nnz * 16 + (n + 1) * 8)},
+        "roofline": {"bound": "int pipe (64-bit multiply-high)", "achieved": None, "peak": None, "unit": None,
+                     "frac": None, "traffic": None, "kernel": "rows_9bit"},
+        "cpu_baseline": {"value": cpu_n * (cpu_n - 1) / 2 / cpu_t, "unit": "draws/s", "cores": 1, "kind": "port",
+                         "sample": f"the reference's generator loop (numpy Philox per row, scipy COO->CSR) at "
+                                   f"n={cpu_n}, p={p} ({cpu_t:.2f} s)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run(args):
     import paper_2509_01928_b200 as dc
 
     name = args.config
+    if name == "gen9":
+        run_gen9(args)
+        return
     cfg = CFG[name]
     t_build = time.perf_counter()
     inst, alpha, beta, arrays = _instance(name)
