@@ -69,7 +69,8 @@ struct dcx_ctx {
   bool have = false, dense = false, csr_ready = false;
   bool proc = false;         // procedural J_ij = sin(i*j + proc_seed) (dcx_set_procedural)
   long long proc_seed = 0;
-  std::vector<double> dense_host;  // dense couplings: host copy for the lazily built CSR form
+  std::vector<double> dense_host;  // dense couplings: host copy for the lazily built CSR form (filled on first use
+                                   // from the device copy the dense upload keeps, dn.scratch)
   int64_t n = 0, nnz = 0;
   int64_t n_cols = 0, row_base = 0;  // row block of a row-partitioned coupling (n_cols == n, 0 otherwise)
   int vk_int = -1;  // VK_UNIFORM / VK_I8 / VK_I16, or -1 for real values
@@ -541,6 +542,17 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
 static int ensure_csr(dcx_ctx* c) {
   if (!c->dense || c->csr_ready) return DCX_OK;
   const int64_t n = c->n;
+  if (c->dense_host.size() != size_t(n * n)) {
+    // the f64 coupling as uploaded (dense_upload keeps it in dn.scratch)
+    try {
+      c->dense_host.resize(size_t(n * n));
+    } catch (const std::bad_alloc&) {
+      return fail(c, DCX_E_OOM, "host allocation failed");
+    }
+    if (!c->dn.scratch || c->dn.scratch_bytes < size_t(n * n) * 8) return fail(c, DCX_E_STATE, "dense coupling not on the device");
+    const cudaError_t e = cudaMemcpy(c->dense_host.data(), c->dn.scratch, size_t(n * n) * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(c, DCX_E_CUDA, cudaGetErrorString(e));
+  }
   const double* A = c->dense_host.data();
   std::vector<int64_t> ro(n + 1, 0), ci;
   std::vector<double> vv;
@@ -572,7 +584,7 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
     c->have = false;
     c->proc = false;
     c->csr_ready = false;
-    c->dense_host.assign(A, A + n * n);
+    c->dense_host.clear();  // no 8 n^2-byte host copy per upload: ensure_csr reads the device copy
     c->n = n;
     c->n_cols = n;
     c->row_base = 0;
@@ -1143,6 +1155,18 @@ int dcx_result_history_all(dcx_ctx* c, int64_t K, double* h, double* e, double* 
   for (int r = 0; r < c->R; ++r) {
     const int64_t cnt = std::min<int64_t>(K, c->nhist(r));
     const int64_t base = (int64_t)r * K;
+    if (c->ring_direct && h && e && t && ev) {  // records in place in the pinned ring: one tight de-interleave
+      const HistRec* q = c->ring + size_t(r) * c->cap;
+      double *hp = h + base, *ep = e + base, *tp = t + base;
+      int32_t* vp = ev + base;
+      for (int64_t k = 0; k < cnt; ++k) {
+        hp[k] = q[k].h;
+        ep[k] = q[k].e;
+        tp[k] = q[k].t;
+        vp[k] = q[k].ev;
+      }
+      continue;
+    }
     for (int64_t k = 0; k < cnt; ++k) {
       const HistRec& q = c->rec(r, k);
       if (h) h[base + k] = q.h;
