@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dcx_dense.h"
@@ -39,7 +40,9 @@ namespace dcx {
 namespace tc {
 
 constexpr int TM = 128;  // replicas per tile (UMMA M)
-constexpr int TN = 128;  // spins per tile (UMMA N)
+// spins per tile (UMMA N) is the kernel's template parameter TN: 128, or 112 so that
+// n = 2000 splits into 18 tiles and (R / 128) x 18 = 144 CTAs use 144 of the 148 SMs
+// (16 tiles of 128 leave 20 idle)
 constexpr int TK = 64;   // K per stage: 64 f16 = one 128-byte swizzle row
 constexpr int UK = 16;   // UMMA K for kind::f16
 constexpr int THREADS = 384;
@@ -47,14 +50,15 @@ constexpr int MAX_STAGES = 8;
 constexpr uint32_t TILE_BYTES = TM * TK * 2;   // 16 KB: 128 rows x 128 B (SW128): 64 f16 or 128 int8 of K
 // NC = CTAs per MMA (1: cta_group::1, 128 x 128 tiles; 2: cta_group::2, a CTA pair
 // computes 256 replicas x 128 spins, each CTA holding its 128 A rows and 64 of the B rows)
-template <int NC>
+template <int NC, int TN>
 struct Pipe {
-  static constexpr uint32_t B_BYTES = TILE_BYTES / NC;          // B rows held by this CTA (one K atom)
+  static constexpr uint32_t B_BYTES = (TN / NC) * 128;          // B rows held by this CTA (one K atom)
+  static_assert(B_BYTES % 1024 == 0, "SW128 tiles: whole 8-row groups");
   // KA K-atoms (128 bytes of K each) per stage: fewer mbarrier round trips per MMA,
   // which is what paces tcgen05 at N = 128 (measured: 4 MMAs/stage 124 cyc/MMA, 8: 101)
   static constexpr int KA = 2;
   static constexpr uint32_t STAGE = KA * (TILE_BYTES + B_BYTES);  // A atoms then B atoms
-  static constexpr int STAGES = int(196608 / STAGE);  // 192 KB of stages
+  static constexpr int STAGES = int(196608 / STAGE) < MAX_STAGES ? int(196608 / STAGE) : MAX_STAGES;  // 192 KB
   static constexpr uint32_t TILES = STAGES * STAGE;
 };
 constexpr uint32_t TMEM_COLS = 512;            // D1 [0,128) f32, D2 [128,256) s32, master x [256,384) f32
@@ -266,6 +270,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+// W = 32 or 24 consecutive TMEM columns of this warp's lane quadrant
+template <int W>
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t* v) {
+  if constexpr (W == 32) {
+    tmem_ld32(taddr, v);
+  } else {
+    static_assert(W == 24, "chunks of 32 or 24 columns");
+    tmem_ld16(taddr, v);
+    tmem_ld8(taddr + 16, v + 16);
+  }
+}
+template <int W>
+__device__ __forceinline__ void tmem_stw(uint32_t taddr, const uint32_t* v);
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -276,6 +317,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
       "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
       "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
+}
+template <int W>
+__device__ __forceinline__ void tmem_stw(uint32_t taddr, const uint32_t* v) {
+  if constexpr (W == 32) {
+    tmem_st32(taddr, v);
+  } else {
+    tmem_st16(taddr, v);
+    tmem_st8(taddr + 16, v + 16);
+  }
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -303,9 +353,12 @@ struct __align__(8) Smem {
 // owner), warps 2-3 idle, warps 4-11 = epilogue + control. Epilogue warp w
 // reads TMEM lane quadrant (w % 4) and spin-column half (w - 4) / 4; the
 // CTA's 128 x 128 f32 master state lives in TMEM columns [XCOL, XCOL + 128).
-template <int NC>
+template <int NC, int TN>
 __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_constant__ Args a) {
-  using P = Pipe<NC>;
+  using P = Pipe<NC, TN>;
+  constexpr int HW = TN / 2;   // spin columns of one epilogue warp (its half of the tile)
+  constexpr int W1 = HW - 32;  // width of its second chunk (32 or 24)
+  static_assert(W1 == 32 || W1 == 24, "tile widths 128 or 112");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment (SW128) by offset so the compiler keeps the shared address space
   unsigned char* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -322,7 +375,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const bool leader = cta_rank == 0;
   const int KB1 = a.npad / (TK * P::KA);      // f16 stages (KA x 64 of K each)
   const int KB2 = a.npad / (2 * TK * P::KA);  // int8 stages (KA x 128 of K each)
-  static_assert(P::KA * TK == TN, "one GEMM1 stage = one spin tile (operand flags are per tile)");
+  constexpr int KS = P::KA * TK;  // K columns per GEMM1 stage (128); flags are per spin tile of TN
   SyncWords* grp = a.sync + rg;
 
   if (threadIdx.x == 0) {
@@ -368,10 +421,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const int rl = q * 32 + lane;
   const int r = r0 + rl;
   const bool valid = epi && r < a.R;
-  uint64_t prevmask = 0;  // sign bits of x_{p-1} for this thread's 64 columns
+  uint64_t prevmask = 0;  // sign bits of x_{p-1} for this thread's HW columns
   if (epi) {
-    const int8_t* sp = a.s8[(p + 1) & 1] + (int64_t)r * a.npad + i0 + h * 64;
-    for (int c = 0; c < 64; ++c)
+    const int8_t* sp = a.s8[(p + 1) & 1] + (int64_t)r * a.npad + i0 + h * HW;
+#pragma unroll 1
+    for (int c = 0; c < HW; ++c)
       if (valid && p > 0 && sp[c] < 0) prevmask |= 1ull << c;
   }
   tc_fence_before();
@@ -381,15 +435,16 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const uint32_t tmem = sm.tmem_base;
   const uint32_t idesc = idesc_f16(NC * TM, TN), idesc8 = idesc_i8(NC * TM, TN);
   // the CTA's f32 master states live in TMEM columns [XCOL, XCOL + 128) for the whole run
-  const uint32_t xaddr = tmem + (uint32_t(q * 32) << 16) + XCOL + h * 64;
+  const uint32_t xaddr = tmem + (uint32_t(q * 32) << 16) + XCOL + h * HW;
   if (epi) {
-    const float* src = a.xm[p & 1] + (int64_t)r * a.npad + i0 + h * 64;
-    for (int cc = 0; cc < 2; ++cc) {
-      uint32_t v[32];
+    const float* src = a.xm[p & 1] + (int64_t)r * a.npad + i0 + h * HW;
+    uint32_t v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(valid ? src[cc * 32 + j] : 0.f);
-      tmem_st32(xaddr + cc * 32, v);
-    }
+    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(valid ? src[j] : 0.f);
+    tmem_st32(xaddr, v);
+#pragma unroll
+    for (int j = 0; j < W1; ++j) v[j] = __float_as_uint(valid ? src[32 + j] : 0.f);
+    tmem_stw<W1>(xaddr + 32, v);
     tmem_st_wait();
   }
   RunCfg cfg = a.cfg;
@@ -415,7 +470,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const int64_t part_stride = (int64_t)a.Rpad * a.tiles_n * 4;  // partials double-buffered by iteration parity
   // per-CTA phase sums (DCX_DENSE_TRACE): [0] MMA wait on full[], [1] GEMM1 issue span,
   // [2] update, [3] epilogue wait for GEMM1, [4] producer flag wait, [5] iterations, [6] control
-  const int kbase = nt & ~1;  // rotation of the K order (common to both pairs of a multicast cluster)
+  // rotation of the K order: start at the stage holding the first spin of tile (nt & ~1)
+  // (common to both pairs of a multicast cluster)
+  const int kstart = ((nt & ~1) * TN) / KS;
   unsigned int* const my_flag = a.flags + ((int64_t)rt * a.tiles_n + nt) * FLAG_STRIDE;
   const unsigned int* const tile_flags = a.flags + (int64_t)rt * a.tiles_n * FLAG_STRIDE;
   auto wait_gen = [&](const unsigned int* g, unsigned int target) {
@@ -455,36 +512,34 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     // tile is ready); lane 0 issues the TMA loads. One serial acquire per stage put 16
     // L2 round trips per iteration on the GEMM1 critical path (19.9 -> 18.4 ms / solve).
     unsigned d_flag = 0;
-    const int nflags = KB1;
     for (; p < a.p_end; ++p) {
       if (group_done(p)) break;
       const bool tr = a.dbg && blockIdx.x == 0 && p < 4096 && lane == 0;
       if (tr) a.dbg[p * 12 + 5] = clock64();
-      uint32_t ready = 0;
-      int rbatch = -1;
+      uint32_t ready = 0;  // bit t: spin tile t of x_p is written (lane t polls tile t)
       for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
         const int s = kiter % P::STAGES;
         const uint32_t ph = (kiter / P::STAGES) & 1;
         if (lane == 0) mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
-        const int kt = kb < KB1 ? (kb + kbase) % KB1 : (kb - KB1 + kbase / 2) % KB2;
+        // GEMM1 stage kt: K columns [KS kt, KS kt + KS), written by the spin tiles they
+        // overlap; GEMM2 stages (two int8 atoms of 128) were all waited in GEMM1
+        const int kt = kb < KB1 ? (kb + kstart) % KB1 : (kb - KB1 + kstart / 2) % KB2;
         if (kb < KB1) {
-          const int idx = kb;
-          if ((idx >> 5) != rbatch) {
-            rbatch = idx >> 5;
-            ready = 0;
-          }
+          const unsigned tf0 = a.dbg ? clock() : 0u;
+          const int t_lo = (kt * KS) / TN, t_hi = min(a.tiles_n - 1, (kt * KS + KS - 1) / TN);
+          const uint32_t need = t_lo > t_hi ? 0u : (((2u << t_hi) - 1u) & ~((1u << t_lo) - 1u));
           long long t0 = 0;
           unsigned int polls = 0;
-          while (!((ready >> (idx & 31)) & 1u)) {
-            const int my = rbatch * 32 + lane;
+          while ((ready & need) != need) {
             bool ok = true;
-            if (my < nflags) ok = int(ld_acquire(tile_flags + ((my + kbase) % KB1) * FLAG_STRIDE) - unsigned(p)) >= 0;
+            if (lane < a.tiles_n) ok = int(ld_acquire(tile_flags + lane * FLAG_STRIDE) - unsigned(p)) >= 0;
             ready = __ballot_sync(0xffffffffu, ok);
             if ((++polls & 1023u) == 0) {
               if (t0 == 0) t0 = clock64();
               else if (clock64() - t0 > (1ll << 36)) __trap();  // a lost flag: fail the launch, do not hang
             }
           }
+          if (a.dbg) d_flag += clock() - tf0;
           __syncwarp();  // the lanes' acquires before lane 0's loads
         }
         if (lane == 0) {
@@ -655,17 +710,27 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       const float alpha = sm.alpha[rl], inv_beta = sm.inv_beta[rl], jl = sm.jl[rl], inv_lam = sm.inv_lam[rl];
       float s4 = 0.f, sxax = 0.f, step = 0.f;
       int es = 0;
-      const int gbase = i0 + h * 64;
-      const int lim = valid ? max(0, min(64, a.n - gbase)) : 0;
+      const int gbase = i0 + h * HW;
+      const int lim = valid ? max(0, min(HW, a.n - gbase)) : 0;
+      // int8 stores: 16-byte vectors when this warp's columns start 16-byte aligned (TN = 128),
+      // else 8-byte ones (TN = 112: h * 56 is 8 mod 16)
+      auto store_pm1 = [](int8_t* dst, const uint32_t* w, int words) {
+        if constexpr (HW % 16 == 0) {
+          for (int k = 0; k < words; k += 4) *reinterpret_cast<uint4*>(dst + 4 * k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+        } else {
+          for (int k = 0; k < words; k += 2) *reinterpret_cast<uint2*>(dst + 4 * k) = make_uint2(w[k], w[k + 1]);
+        }
+      };
       if (copy_prev && lim > 0) {
         int8_t* bd = a.best8 + (int64_t)r * a.npad + gbase;
-        for (int cc = 0; cc < 2; ++cc) {
-          __align__(16) int8_t b[32];
+        uint32_t w[HW / 4];  // 4 spins per word: 0x01 per byte, 0xff where negative
 #pragma unroll
-          for (int j = 0; j < 32; ++j) b[j] = (prevmask >> (cc * 32 + j)) & 1 ? -1 : 1;
-          *reinterpret_cast<uint4*>(bd + cc * 32) = *reinterpret_cast<uint4*>(b);
-          *reinterpret_cast<uint4*>(bd + cc * 32 + 16) = *reinterpret_cast<uint4*>(b + 16);
+        for (int k = 0; k < HW / 4; ++k) {
+          const uint32_t nib = uint32_t(prevmask >> (4 * k)) & 0xFu;
+          const uint32_t t = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+          w[k] = 0x01010101u + t * 0xfeu;
         }
+        store_pm1(bd, w, HW / 4);
       }
       uint64_t curmask = 0;
       if (a.dbg && threadIdx.x == 128) sm.tdbg[1] = clock();
@@ -676,26 +741,28 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
       float* xg = a.xm[cur] + (int64_t)r * a.npad + gbase;  // x_p (time-budget runs only)
-      for (int cc = 0; cc < 2; ++cc) {
+      // one chunk of W columns starting at column `off` of this warp's half (bits off.. of the masks)
+      auto chunk = [&](auto wc, const int off) {
+        constexpr int W = decltype(wc)::value;
         uint32_t v1[32], xv[32];  // xv: x_p, updated in place to the next master state
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + h * 64 + cc * 32, v1);
-        tmem_ld32(xaddr + cc * 32, xv);
+        tmem_ldw<W>(tmem + (uint32_t(q * 32) << 16) + h * HW + off, v1);
+        tmem_ldw<W>(xaddr + off, xv);
         tmem_ld_wait();
         if (write_master && lim > 0) {  // x_p persisted (a budget stop at p keeps it)
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(xg + cc * 32 + j) = *reinterpret_cast<float4*>(xv + j);
+          for (int j = 0; j < W; j += 4)
+            *reinterpret_cast<float4*>(xg + off + j) = *reinterpret_cast<float4*>(xv + j);
         }
         __align__(16) __half2 hv[16];
         __align__(16) uint32_t sv[8];
         if (lim > 0) {
-          // branch-free over all 64 columns (x is never -0.0, so x < 0 <=> sign bit). Padding
+          // branch-free over all W columns (x is never -0.0, so x < 0 <=> sign bit). Padding
           // columns (i >= n) hold x = +0 and D1 = 0 (zero rows/columns of Q), so they
           // update to +0, add nothing to the sums and read as spin +1 (a zero term of
           // the energy GEMM: the padded rows and columns of Q are zero)
           uint32_t m = 0;
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
+          for (int j = 0; j < W; j += 2) {
             float nx[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -716,16 +783,17 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               sv[j / 4] = 0x01010101u + t * 0xfeu;
             }
           }
-          curmask |= uint64_t(m) << (cc * 32);
+          curmask |= uint64_t(m) << off;
         }  // (lim == 0: padding replica or columns, the master state stays)
-        tmem_st32(xaddr + cc * 32, xv);
+        tmem_stw<W>(xaddr + off, xv);
         if (running && lim > 0) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) *reinterpret_cast<uint4*>(hn + cc * 32 + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
-          *reinterpret_cast<uint4*>(sn + cc * 32) = *reinterpret_cast<uint4*>(sv);
-          *reinterpret_cast<uint4*>(sn + cc * 32 + 16) = *reinterpret_cast<uint4*>(sv + 4);
+          for (int j = 0; j < W / 2; j += 4) *reinterpret_cast<uint4*>(hn + off + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
+          store_pm1(sn + off, sv, W / 4);
         }
-      }
+      };
+      chunk(std::integral_constant<int, 32>{}, 0);
+      chunk(std::integral_constant<int, W1>{}, 32);
       const bool tr128 = a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096;
       if (tr128) a.dbg[p * 12 + 3] = clock64();
       tc_fence_before();
@@ -751,14 +819,14 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       tc_fence_after();
       {
         uint32_t v2[64];
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * 64, v2);
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * 64 + 32, v2 + 32);
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * HW, v2);
+        tmem_ldw<W1>(tmem + (uint32_t(q * 32) << 16) + TN + h * HW + 32, v2 + 32);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sm.d2free));  // D2 drained: GEMM2(p+1) may overwrite it
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
+        for (int j = 0; j < HW; ++j) {
           const int m = -int((curmask >> j) & 1);
           const int v = (j < lim) ? int(v2[j]) : 0;
           es += (v ^ m) - m;
@@ -798,21 +866,20 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   if (epi) {
     // the run's final (or frozen) states; a time-budget stop at p was persisted above
     const bool budget_stop = sm.ctl[rl].status == DCX_STOP_TIME_BUDGET;
-    float* d0 = a.xm[0] + (int64_t)r * a.npad + i0 + h * 64;
-    float* d1 = a.xm[1] + (int64_t)r * a.npad + i0 + h * 64;
-    const int lim = max(0, min(64, a.n - (i0 + h * 64)));
-    for (int cc = 0; cc < 2; ++cc) {
-      uint32_t v[32];
-      tmem_ld32(xaddr + cc * 32, v);
-      tmem_ld_wait();
-      if (valid && !budget_stop)
+    float* d0 = a.xm[0] + (int64_t)r * a.npad + i0 + h * HW;
+    float* d1 = a.xm[1] + (int64_t)r * a.npad + i0 + h * HW;
+    const int lim = max(0, min(HW, a.n - (i0 + h * HW)));
+    uint32_t v[64];
+    tmem_ld32(xaddr, v);
+    tmem_ldw<W1>(xaddr + 32, v + 32);
+    tmem_ld_wait();
+    if (valid && !budget_stop)
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cc * 32 + j < lim) {
-            d0[cc * 32 + j] = __uint_as_float(v[j]);
-            d1[cc * 32 + j] = __uint_as_float(v[j]);
-          }
-    }
+      for (int j = 0; j < HW; ++j)
+        if (j < lim) {
+          d0[j] = __uint_as_float(v[j]);
+          d1[j] = __uint_as_float(v[j]);
+        }
   }
   // all CTAs of the group read p_exec before the first barrier and exit at the same p
   if (nt == 0 && threadIdx.x == 0) {
@@ -1024,8 +1091,16 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   if (!d.tmaps) d.tmaps = new CUtensorMap[6];
 }
 
-static size_t dense_smem_bytes(int nc) {
-  return 1024 + (nc == 1 ? tc::Pipe<1>::TILES : tc::Pipe<2>::TILES) + sizeof(tc::Smem);
+static size_t dense_smem_bytes(int nc, int tn) {
+  const size_t tiles = nc == 1 ? (tn == 112 ? tc::Pipe<1, 112>::TILES : tc::Pipe<1, 128>::TILES)
+                               : (tn == 112 ? tc::Pipe<2, 112>::TILES : tc::Pipe<2, 128>::TILES);
+  return 1024 + tiles + sizeof(tc::Smem);
+}
+
+template <int NC, int TN>
+static void dense_set_smem() {
+  DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<NC, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)dense_smem_bytes(NC, TN)));
 }
 
 void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
@@ -1040,8 +1115,18 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   int dev = 0, nsm = 0;
   DCK(cudaGetDevice(&dev));
   DCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int tiles = (d.Rpad / 128) * int(d.npad / 128);
-  if (tiles > nsm || tiles > tc::MAX_FLAGS)
+  // spin tile width: 128, or 112 with DCX_DENSE_TN=112 (18 x 8 = 144 CTAs for K2000 x 1024
+  // instead of 16 x 8 = 128). Measured: 18.14 vs 18.05 ms per solve -- an N = 112 MMA
+  // issues no faster than an N = 128 one, so the extra SMs do not shorten the GEMMs
+  const int t112 = int((d.n + 111) / 112), t128 = int(d.npad / 128);
+  d.tn = 128;
+  if (const char* e = std::getenv("DCX_DENSE_TN")) {
+    const int want = std::atoi(e);
+    if (want == 128 || (want == 112 && t112 * 112 <= d.npad && t112 <= 32)) d.tn = want;
+  }
+  d.tiles_n = d.tn == 112 ? t112 : t128;
+  const int tiles = (d.Rpad / 128) * d.tiles_n;
+  if (tiles > nsm || tiles > tc::MAX_FLAGS || d.tiles_n > 32)
     throw std::invalid_argument("tensor-core path: (R/128)*(n/128) tiles must fit the SM count (" +
                                 std::to_string(tiles) + " > " + std::to_string(nsm) + ")");
   // CTA pairs (cta_group::2) when the replica count allows 256-replica groups
@@ -1060,7 +1145,8 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   }
   if (!reuse) {
     DCK(cudaMalloc(&d.best8, vec));
-    DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 4 * (d.npad / 128) * d.Rpad));  // by iteration parity
+    // by iteration parity, for the larger tile count of either width
+    DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 4 * ((d.npad + 111) / 112) * d.Rpad));
     DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128) + sizeof(unsigned int) * tc::FLAG_STRIDE * tc::MAX_FLAGS));
   }
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
@@ -1088,16 +1174,17 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(d.tmaps);
   make_map(&maps[0], d.xh[0], d.npad, d.Rpad, true);
   make_map(&maps[1], d.xh[1], d.npad, d.Rpad, true);
-  make_map(&maps[2], d.q16, d.npad, d.npad, true, 128 / d.nc);
+  make_map(&maps[2], d.q16, d.npad, d.npad, true, uint32_t(d.tn / d.nc));
   make_map(&maps[3], d.s8[0], d.npad, d.Rpad, false);
   make_map(&maps[4], d.s8[1], d.npad, d.Rpad, false);
-  make_map(&maps[5], d.q8, d.npad, d.npad, false, 128 / d.nc);
-  if (d.nc == 1)
-    DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)dense_smem_bytes(1)));
-  else
-    DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)dense_smem_bytes(2)));
+  make_map(&maps[5], d.q8, d.npad, d.npad, false, uint32_t(d.tn / d.nc));
+  if (d.nc == 1) {
+    if (d.tn == 112) dense_set_smem<1, 112>();
+    else dense_set_smem<1, 128>();
+  } else {
+    if (d.tn == 112) dense_set_smem<2, 112>();
+    else dense_set_smem<2, 128>();
+  }
 }
 
 static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
@@ -1127,26 +1214,26 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.npad = int(d.npad);
   a.R = d.R;
   a.Rpad = d.Rpad;
-  a.tiles_n = int(d.npad / 128);
+  a.tiles_n = d.tiles_n;
   a.p_end = p_end;
   a.jscale = d.jscale;
   a.mc = 0;
-  if (d.nc == 2 && (d.npad / 128) % 2 == 0) {
+  if (d.nc == 2 && d.tiles_n % 2 == 0) {
     const char* e = std::getenv("DCX_DENSE_MC");
     a.mc = (e && std::atoi(e) == 1) ? 1 : 0;
   }
-  if (d.dbg) std::fprintf(stderr, "[dcx dense trace] launch: nc=%d mc=%d grid=%d\n", d.nc, a.mc, (d.Rpad / 128) * int(d.npad / 128));
+  if (d.dbg) std::fprintf(stderr, "[dcx dense trace] launch: nc=%d mc=%d tn=%d grid=%d\n", d.nc, a.mc, d.tn, (d.Rpad / 128) * d.tiles_n);
   const int grid = (d.Rpad / 128) * a.tiles_n;
   if (d.nc == 1) {
     void* args[] = {&a};
-    DCK(cudaLaunchCooperativeKernel((const void*)tc::dense_doch_kernel<1>, dim3(grid), dim3(tc::THREADS), args,
-                                    dense_smem_bytes(1), s));
+    const void* fn = d.tn == 112 ? (const void*)tc::dense_doch_kernel<1, 112> : (const void*)tc::dense_doch_kernel<1, 128>;
+    DCK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(tc::THREADS), args, dense_smem_bytes(1, d.tn), s));
   } else {
     // CTA pairs: cluster of 2, every CTA co-resident (group barriers spin across CTAs)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(tc::THREADS);
-    cfg.dynamicSmemBytes = dense_smem_bytes(2);
+    cfg.dynamicSmemBytes = dense_smem_bytes(2, d.tn);
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1161,7 +1248,8 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     // cooperative cluster launch, so profiling runs use it
     const char* coop = std::getenv("DCX_DENSE_COOP");
     cfg.numAttrs = (coop && std::atoi(coop) == 0) ? 1 : 2;
-    DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2>, a));
+    if (d.tn == 112) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 112>, a));
+    else DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 128>, a));
   }
 }
 
@@ -1213,7 +1301,7 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
                    m[0] / cnt / 1e3, m[1] / cnt / 1e3, m[2] / cnt / 1e3, m[3] / cnt / 1e3, m[4] / cnt / 1e3,
                    m[5] / cnt / 1e3, m[6] / cnt / 1e3, m[7] / cnt / 1e3);
     // per-CTA distribution (kcycles per iteration): min / median / max over the grid
-    const int grid = (d.Rpad / 128) * int(d.npad / 128);
+    const int grid = (d.Rpad / 128) * d.tiles_n;
     const char* names[7] = {"mma-wait", "gemm1-issue", "update", "epi-wait-gemm1", "flag-wait", "", "control"};
     for (int k : {0, 1, 2, 3, 4, 6}) {
       std::vector<double> v;

@@ -143,3 +143,25 @@ def test_tc_operand_multicast_and_pair_variants_agree(gold):
         for a, b in zip(base, other):
             assert a.energy == b.energy and a.iterations == b.iterations
             assert np.array_equal(a.x, b.x)
+
+
+def test_tc_112_wide_spin_tiles(gold):
+    """DCX_DENSE_TN=112 (18 spin tiles of 112 for n = 2000, stages straddling two tiles'
+    operand flags): the first iterate matches the f16-operand emulation and returned
+    spins carry their exact energies."""
+    g = gold["k2"]
+    inst = k2_instance()
+    a, b = g["alpha"], g["beta"]
+    lam = np.sqrt(a / b)
+    X0 = x0s(2000, a, b, range(256))
+    J = -0.5 * k2_W()
+    one = _run_with_env({"DCX_DENSE_TN": "112"},
+                        lambda: dc.solve_replicas(inst, "doch", a, b, X0, max_iters=1, precision="f16tc"))
+    for x0, r in zip(X0, one):
+        xq = (x0 / lam).astype(np.float16).astype(np.float64) * lam
+        assert rel2(r.x, np.cbrt((J @ xq + a * x0) / b)) <= EMU_TOL
+    res = _run_with_env({"DCX_DENSE_TN": "112"},
+                        lambda: dc.solve_replicas(inst, "doch", a, b, X0, max_iters=60, precision="f16tc"))
+    assert res[0].path == "dense_tc"
+    for r in res[:32]:
+        assert dc.energy(inst.coupling, r.spins) == r.energy
