@@ -61,8 +61,11 @@ struct Pipe {
   static constexpr int STAGES = int(196608 / STAGE) < MAX_STAGES ? int(196608 / STAGE) : MAX_STAGES;  // 192 KB
   static constexpr uint32_t TILES = STAGES * STAGE;
 };
-constexpr uint32_t TMEM_COLS = 512;            // D1 [0,128) f32, D2 [128,256) s32, master x [256,384) f32
+// D1 [0,128) f32, D2 [128,256) s32, master x [256,384) f32; the ADOCH kernel double-buffers
+// D1 by iteration parity ([0,128) / [384,512)) and parks Ay_p in the D2 columns
+constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t XCOL = 256;
+__host__ __device__ constexpr uint32_t d1col(int p) { return (p & 1) ? 384u : 0u; }
 
 // Per replica-tile group: the tiles_n CTAs that share one replica tile are
 // the only ones that depend on each other (replicas are independent), so each
@@ -87,6 +90,7 @@ struct Args {
   CUtensorMap tmS[2];   // S8 by parity (int8)
   CUtensorMap tmQ8;     // Q (int8)
   float* xm[2];
+  float* axm;  // ADOCH: (J + aI) x of the last iteration of a launch, for the next launch's extrapolation
   __half* xh[2];
   int8_t* s8[2];
   int8_t* best8;
@@ -344,7 +348,7 @@ struct __align__(8) Smem {
   int pad;
   unsigned tdbg[8];  // epilogue phase stamps / sums (DCX_DENSE_TRACE)
   float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
-  float red[2][TM][4];
+  float red[2][TM][8];  // [4, 8): the ADOCH kernel's H(y) partials
   double red2[2][TM][4];
   RepCtl ctl[TM];
 };
@@ -353,7 +357,8 @@ struct __align__(8) Smem {
 // owner), warps 2-3 idle, warps 4-11 = epilogue + control. Epilogue warp w
 // reads TMEM lane quadrant (w % 4) and spin-column half (w - 4) / 4; the
 // CTA's 128 x 128 f32 master state lives in TMEM columns [XCOL, XCOL + 128).
-template <int NC, int TN>
+// AD: ADOCH with the economy window (dc/solvers/doch.py:248-356) instead of DOCH
+template <int NC, int TN, bool AD>
 __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_constant__ Args a) {
   using P = Pipe<NC, TN>;
   constexpr int HW = TN / 2;   // spin columns of one epilogue warp (its half of the tile)
@@ -467,7 +472,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   // CTA's GEMM2(p-1) reads of the sign operands before they are overwritten.
   const unsigned int genB0 = *reinterpret_cast<volatile unsigned int*>(&grp->genB);
   const unsigned int members = NC * a.tiles_n;
-  const int64_t part_stride = (int64_t)a.Rpad * a.tiles_n * 4;  // partials double-buffered by iteration parity
+  // partials double-buffered by iteration parity: 4 per (tile, replica) for DOCH, 8 for ADOCH
+  const int64_t part_stride = (int64_t)a.Rpad * a.tiles_n * (AD ? 8 : 4);
   // per-CTA phase sums (DCX_DENSE_TRACE): [0] MMA wait on full[], [1] GEMM1 issue span,
   // [2] update, [3] epilogue wait for GEMM1, [4] producer flag wait, [5] iterations, [6] control
   // rotation of the K order: start at the stage holding the first spin of tile (nt & ~1)
@@ -599,7 +605,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             if (kb < KB1) {
 #pragma unroll
               for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
-                mma_f16_g<NC>(tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
+                mma_f16_g<NC>(tmem + (AD ? d1col(p) : 0u), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
                               (kb | q | k) ? 1u : 0u);
             } else {
 #pragma unroll
@@ -687,7 +693,232 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       epi_sync();
     };
     if (threadIdx.x == 128) sm.tdbg[4] = sm.tdbg[5] = sm.tdbg[6] = sm.tdbg[7] = 0;
+    // ------------------------------------------------------------------ ADOCH
+    // Iteration p: (1) from GEMM1(p) = J x_p (TMEM, by parity), GEMM1(p-1) = J x_{p-1}
+    // (the other D1 buffer, still intact: GEMM1(p+1) waits for this iteration's operand
+    // flags) and x_{p-1} (global, stored by iteration p-1): Ax_p, the economy
+    // extrapolation y_p = x_p + c_p (x_p - x_{p-1}), Ay_p = Ax_p + c_p (Ax_p - Ax_{p-1})
+    // (doch.py:299-301), the partials of H(x_p), E(sign x_p) (GEMM2), H(y_p) and
+    // |x_p - x_{p-1}|; Ay_p is parked in the D2 columns, already read; (2) group
+    // barrier B(p) and the control of p (control_after_pass + adoch_decide, the same
+    // device code as the multipass path): stop decisions and the window test;
+    // (3) x_{p+1} = cbrt(v / beta), v = Ay_p if accepted else Ax_p (doch.py:313-318),
+    // and the operands of x_{p+1}.
+    auto ad_iteration = [&](const int pk) {
+      const int cur = pk & 1;
+      const RepCtl& c0 = sm.ctl[rl];
+      const bool live0 = valid && c0.status == DCX_STOP_RUNNING;
+      const float alpha = sm.alpha[rl], inv_beta = sm.inv_beta[rl], jl = sm.jl[rl], inv_lam = sm.inv_lam[rl];
+      const float cmf = float(c0.cm[pk & 1]);
+      const bool has_prev = pk > 0;
+      const int gbase = i0 + h * HW;
+      const int lim = valid ? max(0, min(HW, a.n - gbase)) : 0;
+      auto store_pm1 = [](int8_t* dst, const uint32_t* w, int words) {
+        for (int k = 0; k < words; k += 4) *reinterpret_cast<uint4*>(dst + 4 * k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+      };
+      if (valid && pk > 0 && c0.pend == pk - 1 && lim > 0) {  // best spins: sign(x_{p-1}), recorded by control p-1
+        uint32_t w[HW / 4];
+#pragma unroll
+        for (int k = 0; k < HW / 4; ++k) {
+          const uint32_t nib = uint32_t(prevmask >> (4 * k)) & 0xFu;
+          const uint32_t t = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+          w[k] = 0x01010101u + t * 0xfeu;
+        }
+        store_pm1(a.best8 + (int64_t)r * a.npad + gbase, w, HW / 4);
+      }
+      const float* xpg = a.xm[cur ^ 1] + (int64_t)r * a.npad + gbase;  // x_{p-1}
+      float* xcg = a.xm[cur] + (int64_t)r * a.npad + gbase;           // x_p, for iteration p+1
+      mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
+      mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
+      tc_fence_after();
+      float s4 = 0.f, sxax = 0.f, sy4 = 0.f, syay = 0.f, step = 0.f;
+      int es = 0;
+      uint64_t curmask = 0;
+      const uint32_t lb = tmem + (uint32_t(q * 32) << 16);
+#pragma unroll 1
+      for (int off = 0; off < HW; off += 16) {
+        uint32_t xv[16], d1[16], d1p[16], d2[16];
+        float xp[16];
+        // the first iteration of a resumed launch has no GEMM1(p-1) in TMEM: (J + aI) x_{p-1}
+        // comes from axm, stored by the previous launch's last iteration
+        const bool resumed = has_prev && pk == p_start;
+        tmem_ld16(xaddr + off, xv);
+        tmem_ld16(lb + d1col(pk) + h * HW + off, d1);
+        tmem_ld16(lb + TN + h * HW + off, d2);
+        if (has_prev && !resumed) tmem_ld16(lb + d1col(pk + 1) + h * HW + off, d1p);
+        if (resumed) {
+          const float* ag = a.axm + (int64_t)r * a.npad + gbase + off;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) d1p[j] = __float_as_uint(lim > 0 ? ag[j] : 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          const float4 v4 = (has_prev && lim > 0) ? *reinterpret_cast<const float4*>(xpg + off + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          xp[j] = v4.x;
+          xp[j + 1] = v4.y;
+          xp[j + 2] = v4.z;
+          xp[j + 3] = v4.w;
+        }
+        tmem_ld_wait();
+        uint32_t ayv[16];
+        uint32_t m = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float x = __uint_as_float(xv[j]);
+          const float ax = fmaf(alpha, x, jl * __uint_as_float(d1[j]));
+          const float x2 = x * x;
+          s4 = fmaf(x2, x2, s4);
+          sxax = fmaf(x, ax, sxax);
+          const uint32_t neg = xv[j] >> 31;
+          m |= neg << j;
+          const int mm = -int(neg);
+          const int v = (off + j < lim) ? int(d2[j]) : 0;
+          es += (v ^ mm) - mm;
+          float ay = ax;
+          if (has_prev) {
+            const float axp = resumed ? __uint_as_float(d1p[j]) : fmaf(alpha, xp[j], jl * __uint_as_float(d1p[j]));
+            const float y = extrap(x, xp[j], cmf);
+            ay = extrap(ax, axp, cmf);
+            const float y2 = mul_rn(y, y);
+            sy4 = fmaf(y2, y2, sy4);
+            syay = fmaf(y, ay, syay);
+            step = fmaxf(step, fabsf(x - xp[j]));
+          }
+          ayv[j] = __float_as_uint(ay);
+          d1[j] = __float_as_uint(ax);
+        }
+        if (pk == a.p_end - 1 && lim > 0) {  // a later launch resumes at p + 1
+          float* ag = a.axm + (int64_t)r * a.npad + gbase + off;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) ag[j] = __uint_as_float(d1[j]);
+        }
+        curmask |= uint64_t(m) << off;
+        if (has_prev) tmem_st16(lb + TN + h * HW + off, ayv);  // Ay_p over the drained D2 columns
+        if (live0 && lim > 0) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(xcg + off + j) =
+                make_float4(__uint_as_float(xv[j]), __uint_as_float(xv[j + 1]), __uint_as_float(xv[j + 2]),
+                            __uint_as_float(xv[j + 3]));
+        }
+      }
+      if (lim == 0) s4 = sxax = sy4 = syay = step = 0.f, es = 0;
+      sm.red[h][rl][0] = s4;
+      sm.red[h][rl][1] = sxax;
+      sm.red[h][rl][2] = float(es);
+      sm.red[h][rl][3] = step;
+      sm.red[h][rl][4] = sy4;
+      sm.red[h][rl][5] = syay;
+      tmem_st_wait();
+      epi_sync();
+      if (h == 0 && r < a.R) {
+        // layout [parity][replica tile][spin tile][replica in tile] x 8
+        double* dst = a.part + (pk & 1) * part_stride + (((int64_t)rt * a.tiles_n + nt) * TM + rl) * 8;
+        double4 v, w;
+        v.x = double(sm.red[0][rl][0]) + double(sm.red[1][rl][0]);
+        v.y = double(sm.red[0][rl][1]) + double(sm.red[1][rl][1]);
+        v.z = double(sm.red[0][rl][2]) + double(sm.red[1][rl][2]);
+        v.w = fmax(double(sm.red[0][rl][3]), double(sm.red[1][rl][3]));
+        w.x = double(sm.red[0][rl][4]) + double(sm.red[1][rl][4]);
+        w.y = double(sm.red[0][rl][5]) + double(sm.red[1][rl][5]);
+        w.z = w.w = 0.0;
+        *reinterpret_cast<double4*>(dst) = v;
+        *reinterpret_cast<double4*>(dst + 4) = w;
+      }
+      epi_sync();
+      if (threadIdx.x == 128) arriveB(pk);
+      // ---- control of p: every CTA of the group evaluates it (identical inputs)
+      if (threadIdx.x == 128) wait_gen(&grp->genB, genB0 + unsigned(pk - p_start + 1));
+      epi_sync();
+      if (h == 0 && r < a.R) {
+        RepCtl c = sm.ctl[rl];
+        if (c.status == DCX_STOP_RUNNING) {
+          const double* src = a.part + (pk & 1) * part_stride + ((int64_t)rt * a.tiles_n * TM + rl) * 8;
+          double tot[NQ] = {0, 0, 0, 0, 0, 0};
+          for (int t = 0; t < a.tiles_n; ++t) {  // tiles in order
+            const double2 u0 = __ldcg(reinterpret_cast<const double2*>(src + (int64_t)t * TM * 8));
+            const double2 u1 = __ldcg(reinterpret_cast<const double2*>(src + (int64_t)t * TM * 8 + 2));
+            const double2 u2 = __ldcg(reinterpret_cast<const double2*>(src + (int64_t)t * TM * 8 + 4));
+            tot[Q_S4] += u0.x;
+            tot[Q_SXAX] += u0.y;
+            tot[Q_ES] += u1.x;
+            tot[Q_STEP] = fmax(tot[Q_STEP], u1.y);
+            tot[Q_SY4] += u2.x;
+            tot[Q_SYAY] += u2.y;
+          }
+          const double now = double(__ldcg(&grp->stamp) - a.g->t0) * 1e-9;
+          if (pk > 0) c.step = tot[Q_STEP];  // |x_p - x_{p-1}|
+          const bool stopped = control_after_pass(c, cfg, r, tot, pk, now);
+          if (!stopped) adoch_decide(c, cfg, r, tot, pk);
+          sm.ctl[rl] = c;
+          if (nt == 0) {
+            a.ctl[r] = c;
+            if (stopped) {
+              atomicSub(&grp->running, 1);
+              atomicSub(&a.g->running, 1);
+            }
+          }
+        }
+      }
+      epi_sync();
+      // ---- update: x_{p+1} from Ay_p (accepted) or Ax_p
+      const RepCtl& c1 = sm.ctl[rl];
+      const bool running = valid && c1.status == DCX_STOP_RUNNING;
+      const bool use_y = has_prev && c1.accept;
+      __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
+      int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
+#pragma unroll 1
+      for (int off = 0; off < HW; off += 16) {
+        uint32_t xv[16], d1[16], ayv[16];
+        tmem_ld16(xaddr + off, xv);
+        tmem_ld16(lb + d1col(pk) + h * HW + off, d1);
+        tmem_ld16(lb + TN + h * HW + off, ayv);
+        tmem_ld_wait();
+        __align__(16) __half2 hv[8];
+        __align__(16) uint32_t sv[4];
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          float nx[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float x = __uint_as_float(xv[j + u]);
+            const float v = use_y ? __uint_as_float(ayv[j + u]) : fmaf(alpha, x, jl * __uint_as_float(d1[j + u]));
+            nx[u] = cbrt_lean(v * inv_beta);
+            xv[j + u] = running ? __float_as_uint(nx[u]) : xv[j + u];
+          }
+          hv[j / 2] = __floats2half2_rn(nx[0] * inv_lam, nx[1] * inv_lam);
+          if ((j & 3) == 2) {
+            const uint32_t t = (xv[j - 2] >> 31) | ((xv[j - 1] >> 31) << 8) | ((__float_as_uint(nx[0]) >> 31) << 16) |
+                               ((__float_as_uint(nx[1]) >> 31) << 24);
+            sv[j / 4] = 0x01010101u + t * 0xfeu;
+          }
+        }
+        tmem_st16(xaddr + off, xv);
+        if (running && lim > 0) {
+          *reinterpret_cast<uint4*>(hn + off) = *reinterpret_cast<uint4*>(hv);
+          *reinterpret_cast<uint4*>(hn + off + 8) = *reinterpret_cast<uint4*>(hv + 4);
+          *reinterpret_cast<uint4*>(sn + off) = *reinterpret_cast<uint4*>(sv);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(smem_u32(&sm.d1free));  // D1 read: GEMM1(p+1) may overwrite it
+        mbar_arrive(smem_u32(&sm.d2free));  // Ay_p read: GEMM2(p+1) may overwrite the D2 columns
+      }
+      tmem_st_wait();
+      fence_async_global();
+      epi_sync();
+      if (threadIdx.x == 128) st_release(my_flag, unsigned(pk + 1));
+      prevmask = curmask;
+    };
     for (; p < a.p_end; ++p) {
+      if constexpr (AD) {
+        if (p >= p_start + 2 && __ldcg(&grp->snapB[p & 1]) == 0) break;  // as the producer and MMA warps
+        ad_iteration(p);
+        acc_phase ^= 1;
+        continue;
+      }
       if (a.dbg && threadIdx.x == 128) sm.tdbg[0] = clock();
       if (p > p_start) {
         control(p - 1);  // waits B(p-1), hence B(p-2)
@@ -854,7 +1085,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       acc_phase ^= 1;
     }
     // the control of the last iteration of this launch (the next launch resumes at p)
-    if (p == a.p_end && p > p_start) control(p - 1);
+    if constexpr (!AD) {
+      if (p == a.p_end && p > p_start) control(p - 1);
+    }
     if (a.dbg && threadIdx.x == 128) {
       a.dbg[4096 * 14 + blockIdx.x * 8 + 2] = sm.tdbg[4];
       a.dbg[4096 * 14 + blockIdx.x * 8 + 3] = sm.tdbg[5];
@@ -865,7 +1098,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   // ---------------------------------------------------------------- teardown
   if (epi) {
     // the run's final (or frozen) states; a time-budget stop at p was persisted above
-    const bool budget_stop = sm.ctl[rl].status == DCX_STOP_TIME_BUDGET;
+    // DOCH: a time-budget stop at p persisted x_p above. ADOCH: the master state is x_p of
+    // the replica's last iteration; a replica still running keeps x_{p-1} in the other
+    // buffer for the extrapolation of the next launch
+    const bool budget_stop = !AD && sm.ctl[rl].status == DCX_STOP_TIME_BUDGET;
+    const bool keep_prev = AD && sm.ctl[rl].status == DCX_STOP_RUNNING;
     float* d0 = a.xm[0] + (int64_t)r * a.npad + i0 + h * HW;
     float* d1 = a.xm[1] + (int64_t)r * a.npad + i0 + h * HW;
     const int lim = max(0, min(HW, a.n - (i0 + h * HW)));
@@ -877,8 +1114,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll
       for (int j = 0; j < HW; ++j)
         if (j < lim) {
-          d0[j] = __uint_as_float(v[j]);
-          d1[j] = __uint_as_float(v[j]);
+          if (!keep_prev || (p & 1) == 0) d0[j] = __uint_as_float(v[j]);
+          if (!keep_prev || (p & 1) == 1) d1[j] = __uint_as_float(v[j]);
         }
   }
   // all CTAs of the group read p_exec before the first barrier and exit at the same p
@@ -1019,6 +1256,8 @@ void DenseDev::release_run() {
   if (best8) cudaFree(best8);
   if (part) cudaFree(part);
   if (sync) cudaFree(sync);
+  if (axm) cudaFree(axm);
+  axm = nullptr;
   best8 = nullptr;
   part = nullptr;
   sync = nullptr;
@@ -1097,16 +1336,18 @@ static size_t dense_smem_bytes(int nc, int tn) {
   return 1024 + tiles + sizeof(tc::Smem);
 }
 
-template <int NC, int TN>
+template <int NC, int TN, bool AD>
 static void dense_set_smem() {
-  DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<NC, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  DCK(cudaFuncSetAttribute(tc::dense_doch_kernel<NC, TN, AD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)dense_smem_bytes(NC, TN)));
 }
 
 void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (!d.exact) throw std::invalid_argument("tensor-core path needs small-integer dense couplings");
   const RunCfg& cfg = m.args.cfg;
-  if (cfg.solver != DCX_SOLVER_DOCH) throw std::invalid_argument("tensor-core path implements DOCH");
+  if (cfg.solver != DCX_SOLVER_DOCH && cfg.window_mode != DCX_WINDOW_ECONOMY)
+    throw std::invalid_argument("tensor-core path implements DOCH and ADOCH with the economy window");
+  d.ad = cfg.solver == DCX_SOLVER_ADOCH;
   const int Rpad_new = (cfg.R + 127) / 128 * 128;
   const bool reuse = d.xm[0] != nullptr && d.Rpad == Rpad_new;  // same shapes: keep the device buffers
   if (!reuse) d.release_run();
@@ -1124,6 +1365,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
     const int want = std::atoi(e);
     if (want == 128 || (want == 112 && t112 * 112 <= d.npad && t112 <= 32)) d.tn = want;
   }
+  if (d.ad) d.tn = 128;  // the ADOCH kernel is built for 128-wide tiles
   d.tiles_n = d.tn == 112 ? t112 : t128;
   const int tiles = (d.Rpad / 128) * d.tiles_n;
   if (tiles > nsm || tiles > tc::MAX_FLAGS || d.tiles_n > 32)
@@ -1145,11 +1387,12 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   }
   if (!reuse) {
     DCK(cudaMalloc(&d.best8, vec));
-    // by iteration parity, for the larger tile count of either width
-    DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 4 * ((d.npad + 111) / 112) * d.Rpad));
+    // by iteration parity, for the larger tile count of either width, 8 partials (ADOCH)
+    DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 8 * ((d.npad + 111) / 112) * d.Rpad));
     DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128) + sizeof(unsigned int) * tc::FLAG_STRIDE * tc::MAX_FLAGS));
   }
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
+  if (d.ad && !d.axm) DCK(cudaMalloc(&d.axm, vec * 4));
   {
     const int gsz = 128 * d.nc;
     const int ngroups = d.Rpad / gsz;
@@ -1178,12 +1421,15 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   make_map(&maps[3], d.s8[0], d.npad, d.Rpad, false);
   make_map(&maps[4], d.s8[1], d.npad, d.Rpad, false);
   make_map(&maps[5], d.q8, d.npad, d.npad, false, uint32_t(d.tn / d.nc));
-  if (d.nc == 1) {
-    if (d.tn == 112) dense_set_smem<1, 112>();
-    else dense_set_smem<1, 128>();
+  if (d.ad) {
+    if (d.nc == 1) dense_set_smem<1, 128, true>();
+    else dense_set_smem<2, 128, true>();
+  } else if (d.nc == 1) {
+    if (d.tn == 112) dense_set_smem<1, 112, false>();
+    else dense_set_smem<1, 128, false>();
   } else {
-    if (d.tn == 112) dense_set_smem<2, 112>();
-    else dense_set_smem<2, 128>();
+    if (d.tn == 112) dense_set_smem<2, 112, false>();
+    else dense_set_smem<2, 128, false>();
   }
 }
 
@@ -1203,6 +1449,7 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     a.s8[b] = reinterpret_cast<int8_t*>(d.s8[b]);
   }
   a.best8 = d.best8;
+  a.axm = reinterpret_cast<float*>(d.axm);
   a.part = d.part;
   a.ctl = m.args.ctl;
   a.g = m.args.g;
@@ -1226,7 +1473,9 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   const int grid = (d.Rpad / 128) * a.tiles_n;
   if (d.nc == 1) {
     void* args[] = {&a};
-    const void* fn = d.tn == 112 ? (const void*)tc::dense_doch_kernel<1, 112> : (const void*)tc::dense_doch_kernel<1, 128>;
+    const void* fn = d.ad ? (const void*)tc::dense_doch_kernel<1, 128, true>
+                          : (d.tn == 112 ? (const void*)tc::dense_doch_kernel<1, 112, false>
+                                         : (const void*)tc::dense_doch_kernel<1, 128, false>);
     DCK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(tc::THREADS), args, dense_smem_bytes(1, d.tn), s));
   } else {
     // CTA pairs: cluster of 2, every CTA co-resident (group barriers spin across CTAs)
@@ -1248,8 +1497,9 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     // cooperative cluster launch, so profiling runs use it
     const char* coop = std::getenv("DCX_DENSE_COOP");
     cfg.numAttrs = (coop && std::atoi(coop) == 0) ? 1 : 2;
-    if (d.tn == 112) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 112>, a));
-    else DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 128>, a));
+    if (d.ad) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 128, true>, a));
+    else if (d.tn == 112) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 112, false>, a));
+    else DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 128, false>, a));
   }
 }
 

@@ -17,7 +17,9 @@ struct DenseDev {
   // per-run buffers
   int R = 0, Rpad = 0;
   int nc = 1;  // CTAs per MMA (2: cta_group::2 pairs)
-  int tn = 128, tiles_n = 0;  // spin tile width (UMMA N: 128 or 112) and spin tiles per replica tile
+  int tn = 128, tiles_n = 0;
+  bool ad = false;         // ADOCH (economy window) kernel
+  void* axm = nullptr;     // ADOCH: (J + aI) x at launch ends [Rpad][npad] f32  // spin tile width (UMMA N: 128 or 112) and spin tiles per replica tile
   void* xm[2] = {nullptr, nullptr};  // f32 master states [Rpad][npad]
   void* xh[2] = {nullptr, nullptr};  // f16 x / lambda_r [Rpad][npad] (MMA operand A)
   void* s8[2] = {nullptr, nullptr};  // int8 sign(x) [Rpad][npad] (energy GEMM operand A)

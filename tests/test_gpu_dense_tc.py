@@ -165,3 +165,60 @@ def test_tc_112_wide_spin_tiles(gold):
     assert res[0].path == "dense_tc"
     for r in res[:32]:
         assert dc.energy(inst.coupling, r.spins) == r.energy
+
+
+# ------------------------------------------------------------------ ADOCH on the tensor cores
+def test_tc_adoch_first_iterates_track_f32(gold):
+    """ADOCH (economy window) in the persistent tensor-core kernel: the first iterates
+    follow the f32 multipass ADOCH within the f16-operand tolerance, with the same
+    accept decisions."""
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(128))
+    # the DOCH test's bounds (a replica whose windows reject every y follows DOCH bit for bit;
+    # measured worst at three iterations 1.67e-2 for both solvers)
+    for iters, tol in ((1, TC_STATE_TOL), (3, 4 * TC_STATE_TOL)):
+        tc = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=iters, precision="f16tc")
+        f32 = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=iters, precision="f32")
+        assert tc[0].path == "dense_tc"
+        agree = 0
+        for a, b in zip(tc, f32):
+            assert a.iterations == b.iterations
+            if a.accepted == b.accepted:
+                agree += 1
+                assert rel2(a.x, b.x) <= tol
+            assert a.energy == dc.energy(inst.coupling, a.spins)
+        assert agree >= len(tc) - 2  # a window test may resolve a near-tie differently at f16 operands
+
+
+def test_tc_adoch_resumed_launches_equal_one_launch(gold):
+    """A run split into launches of 7 iterations (the extrapolation of each resumed
+    launch reads (J + aI)x_{p-1} from global memory instead of TMEM) is bit-identical
+    to one launch."""
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(256))
+    one = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=40, precision="f16tc")
+    chunked = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=40, precision="f16tc", chunk=7)
+    for a, b in zip(one, chunked):
+        assert a.iterations == b.iterations and a.stop_reason == b.stop_reason
+        assert a.energy == b.energy and a.accepted == b.accepted
+        assert np.array_equal(a.x, b.x)
+        assert np.array_equal(a.spins, b.spins)
+
+
+def test_tc_adoch_quality(gold):
+    """1024 ADOCH replicas on the tensor cores: energies exact for the returned spins and a
+    distribution no worse than the reference's ADOCH runs on the same instance (32 seeds)."""
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(1024))
+    res = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=1000, precision="f16tc")
+    e = np.array([r.energy for r in res])
+    ref = np.array([row["energy"] for row in g["adoch"]])
+    se = ref.std() / np.sqrt(len(ref))
+    assert e[:32].mean() <= ref.mean() + 3 * se
+    assert e.mean() <= ref.mean() + 3 * se
+    for r in res[:16]:
+        assert dc.energy(inst.coupling, r.spins) == r.energy
+        assert r.accepted[0] is True and len(r.accepted) == r.iterations  # as assemble_results builds it for every path
