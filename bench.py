@@ -152,9 +152,9 @@ def x0_batch(seeds):
 
 
 # ------------------------------------------------------------------ CPU reference (oracle port)
-def cpu_sample(n_rep=8, max_iters=200, seed0=0):
+def cpu_sample(n_rep=8, max_iters=200, seed0=0, solver="doch"):
     """Bounded sample of the workload on the host: n_rep replicas run one after
-    another, each a full DOCH loop (2 dgemv per iteration at stride 1)."""
+    another, each a full DOCH / ADOCH loop (2 dgemv per iteration at stride 1)."""
     from oracle import dcising_oracle as orc
 
     J = -0.5 * instance()
@@ -162,7 +162,7 @@ def cpu_sample(n_rep=8, max_iters=200, seed0=0):
     updates = 0
     t0 = time.perf_counter()
     for r in range(n_rep):
-        out = orc.run(op, ALPHA, BETA, solver="doch", max_iters=max_iters, seed=seed0 + r, trace_stride=1)
+        out = orc.run(op, ALPHA, BETA, solver=solver, max_iters=max_iters, seed=seed0 + r, trace_stride=1)
         updates += N_SPINS * out["iterations"]
     dt = time.perf_counter() - t0
     return updates / dt, dt, updates
@@ -174,10 +174,10 @@ def run_reference(args):
         return
     n_rep, iters = 256, 1000  # ~10 s of host work per step (replicas converge in ~150-250 iterations)
     for _ in range(args.warmup):
-        cpu_sample(1, 20)
+        cpu_sample(1, 20, solver=args.solver)
     vals, times = [], []
     for s in range(args.steps):
-        v, dt, _ = cpu_sample(n_rep, iters, seed0=s * n_rep)
+        v, dt, _ = cpu_sample(n_rep, iters, seed0=s * n_rep, solver=args.solver)
         vals.append(v)
         times.append(dt)
     value = sum(vals) / len(vals)
@@ -187,10 +187,11 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "K2000 dense +-1 (gen_dense_pm1 seed 20240817), DOCH, eta=0.1, trace_stride=1",
+        "config": {"workload": f"K2000 dense +-1 (gen_dense_pm1 seed 20240817), {args.solver.upper()}, eta=0.1, "
+                               "trace_stride=1",
                    "n": N_SPINS, "replicas_per_step": n_rep, "max_iters": iters},
         "cpu_baseline": {"value": value, "unit": "spin-updates/s", "cores": cores, "kind": "port",
-                         "sample": f"{n_rep} replicas x <= {iters} DOCH iterations per step, sequential, "
+                         "sample": f"{n_rep} replicas x <= {iters} {args.solver.upper()} iterations per step, sequential, "
                                    f"numpy/OpenBLAS dgemv with {cores} BLAS threads (oracle/dcising_oracle.py)"},
         "e2e": {"value": value, "unit": "spin-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -216,7 +217,7 @@ def run_ours(args):
 
     X0 = [x0_batch(seeds_of(s)) for s in range(2)]
     for w in range(args.warmup):
-        dc.solve_replicas(inst, "doch", ALPHA, BETA, X0[w % 2], **kw)
+        dc.solve_replicas(inst, args.solver, ALPHA, BETA, X0[w % 2], **kw)
     # ---------------- device-resident timing (value)
     dev_s, updates, best_e, tts = [], 0, np.inf, []
     barrier(world)
@@ -225,7 +226,7 @@ def run_ours(args):
         for s in range(args.steps):
             flush.fill_(float(s))
             torch.cuda.synchronize()
-            res = dc.solve_replicas(inst, "doch", ALPHA, BETA, X0[s % 2], **kw)
+            res = dc.solve_replicas(inst, args.solver, ALPHA, BETA, X0[s % 2], **kw)
             dev_s.append(res[0].device_seconds)
             updates += N_SPINS * sum(r.iterations for r in res)
             max_iters_seen = max(r.iterations for r in res)
@@ -251,7 +252,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         # host buffers in, host results out: J (f64) and x0 are copied to the device every step
-        res = dc.solve_replicas(inst, "doch", ALPHA, BETA, X0[s % 2], reupload=True, **kw)
+        res = dc.solve_replicas(inst, args.solver, ALPHA, BETA, X0[s % 2], reupload=True, **kw)
         energies = np.array([r.energy for r in res])
         e2e_t += time.perf_counter() - t0
         e2e_upd += N_SPINS * sum(r.iterations for r in res)
@@ -260,7 +261,7 @@ def run_ours(args):
     e_max, = allreduce([e2e_t], "max", world)
     e_upd, = allreduce([float(e2e_upd)], "sum", world)
     # ---------------- dominant kernel roofline (measured live, CUDA events on the solver stream)
-    prof = dc.profile_dominant_kernel(inst, ALPHA, BETA, X0[0], precision=args.precision,
+    prof = dc.profile_dominant_kernel(inst, ALPHA, BETA, X0[0], solver=args.solver, precision=args.precision,
                                       path="multipass" if args.path == "auto" and args.precision != "f16tc"
                                       else args.path, launches=5 if args.precision == "f16tc" else 10)
     hbm, bf16, src = peaks()
@@ -282,9 +283,10 @@ def run_ours(args):
         launches_total = args.steps * (-(-its // MAX_ITERS) + 3)
     cpu = None
     if rank == 0:
-        v, dt, _ = cpu_sample(256, 1000)
+        v, dt, _ = cpu_sample(256, 1000, solver=args.solver)
         cpu = {"value": v, "unit": "spin-updates/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"256 replicas x <= 1000 DOCH iterations (to convergence), sequential, numpy/OpenBLAS dgemv "
+               "sample": f"256 replicas x <= 1000 {args.solver.upper()} iterations (to convergence), sequential, "
+                         f"numpy/OpenBLAS dgemv "
                          f"with {os.cpu_count()} BLAS threads ({dt:.1f} s)"}
     if rank == 0:
         mean_tts = float(np.mean(tts)) if tts else None
@@ -293,8 +295,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": {"f32": "f32", "f64": "f64", "f16tc": "f16"}[args.precision], "data": "synthetic",
-            "config": {"workload": "K2000 dense +-1 (gen_dense_pm1 seed 20240817, J=-W/2), DOCH, eta=0.1 "
-                                   "(alpha, beta of derive_params), max_iters=1000, trace_stride=1",
+            "config": {"workload": f"K2000 dense +-1 (gen_dense_pm1 seed 20240817, J=-W/2), {args.solver.upper()}, "
+                                   "eta=0.1 (alpha, beta of derive_params), max_iters=1000, trace_stride=1",
                        "n": N_SPINS, "replicas_per_gpu": REPLICAS, "path": res[0].path,
                        "precision": args.precision, "parallelism": f"replicas x{world}",
                        "l2": "256 MB buffer written between timed steps (instance fits in L2)"},
@@ -324,6 +326,8 @@ def main():
     ap.add_argument("--path", default=os.environ.get("DCX_BENCH_PATH", "auto"))
     ap.add_argument("--config", default="k2", choices=["k2", "g1", "t6", "e7", "r8", "gen9"],
                     help="k2 is the headline (BASELINE configs[1]); others: see bench_configs.py")
+    ap.add_argument("--solver", default="doch", choices=["doch", "adoch"],
+                    help="k2: DOCH (headline) or ADOCH with the economy window")
     ap.add_argument("--rowpart", action="store_true",
                     help="t6/e7/r8: row-partitioned solver (dist.py) even at one GPU")
     ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
