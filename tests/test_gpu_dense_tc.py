@@ -222,3 +222,21 @@ def test_tc_adoch_quality(gold):
     for r in res[:16]:
         assert dc.energy(inst.coupling, r.spins) == r.energy
         assert r.accepted[0] is True and len(r.accepted) == r.iterations  # as assemble_results builds it for every path
+
+
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+def test_tc_time_budget(gold, solver):
+    """A time budget stops every replica of the tensor-core kernel with stop reason
+    "time_budget" (dc/solvers/doch.py:221-223); the returned state is the last iterate
+    and the spins carry their exact energies."""
+    g = gold["k2"]
+    inst = k2_instance()
+    X0 = x0s(2000, g["alpha"], g["beta"], range(256))
+    res = dc.solve_replicas(inst, solver, g["alpha"], g["beta"], X0, max_iters=10**6, precision="f16tc",
+                            time_budget=0.005)
+    assert res[0].path == "dense_tc"
+    for r in res[:16]:
+        assert r.stop_reason == "time_budget"
+        assert 0 < r.iterations < 10**6
+        assert np.all(np.isfinite(r.x)) and np.any(r.x != 0)
+        assert dc.energy(inst.coupling, r.spins) == r.energy
