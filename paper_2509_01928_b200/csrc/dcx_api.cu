@@ -7,6 +7,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dcx_internal.h"
@@ -1152,29 +1153,44 @@ int dcx_result_summaries(dcx_ctx* c, int64_t* iterations, int32_t* stop_reason, 
 int dcx_result_history_all(dcx_ctx* c, int64_t K, double* h, double* e, double* t, int32_t* ev) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   if (!c->begun) return fail(c, DCX_E_STATE, "no run");
-  for (int r = 0; r < c->R; ++r) {
-    const int64_t cnt = std::min<int64_t>(K, c->nhist(r));
-    const int64_t base = (int64_t)r * K;
-    if (c->ring_direct && h && e && t && ev) {  // records in place in the pinned ring: one tight de-interleave
-      const HistRec* q = c->ring + size_t(r) * c->cap;
-      double *hp = h + base, *ep = e + base, *tp = t + base;
-      int32_t* vp = ev + base;
-      for (int64_t k = 0; k < cnt; ++k) {
-        hp[k] = q[k].h;
-        ep[k] = q[k].e;
-        tp[k] = q[k].t;
-        vp[k] = q[k].ev;
+  auto rows = [&](int r0, int r1) {
+    for (int r = r0; r < r1; ++r) {
+      const int64_t cnt = std::min<int64_t>(K, c->nhist(r));
+      const int64_t base = (int64_t)r * K;
+      if (c->ring_direct && h && e && t && ev) {  // records in place in the pinned ring: one tight de-interleave
+        const HistRec* q = c->ring + size_t(r) * c->cap;
+        double *hp = h + base, *ep = e + base, *tp = t + base;
+        int32_t* vp = ev + base;
+        for (int64_t k = 0; k < cnt; ++k) {
+          hp[k] = q[k].h;
+          ep[k] = q[k].e;
+          tp[k] = q[k].t;
+          vp[k] = q[k].ev;
+        }
+        continue;
       }
-      continue;
+      for (int64_t k = 0; k < cnt; ++k) {
+        const HistRec& q = c->rec(r, k);
+        if (h) h[base + k] = q.h;
+        if (e) e[base + k] = q.e;
+        if (t) t[base + k] = q.t;
+        if (ev) ev[base + k] = q.ev;
+      }
     }
-    for (int64_t k = 0; k < cnt; ++k) {
-      const HistRec& q = c->rec(r, k);
-      if (h) h[base + k] = q.h;
-      if (e) e[base + k] = q.e;
-      if (t) t[base + k] = q.t;
-      if (ev) ev[base + k] = q.ev;
-    }
+  };
+  // a bulk download of many replicas (K2000 x 1024: 1e6 records) is split over host threads
+  const int R = c->R;
+  const int64_t work = int64_t(R) * K;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = int(std::min<int64_t>({int64_t(hw), 8, work / 65536 + 1, int64_t(R)}));
+  if (nt <= 1) {
+    rows(0, R);
+    return DCX_OK;
   }
+  std::vector<std::thread> pool;
+  for (int i = 1; i < nt; ++i) pool.emplace_back(rows, int(int64_t(R) * i / nt), int(int64_t(R) * (i + 1) / nt));
+  rows(0, int(int64_t(R) / nt));
+  for (auto& th : pool) th.join();
   return DCX_OK;
 }
 
