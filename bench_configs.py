@@ -166,7 +166,7 @@ def run_gen9(args):
     for s in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        # device time: generation + CSR assembly (the download of the result is e2e)
+        # end to end: generation on the device + download into the reference's int64 / f64 arrays
         J = dc.gen_sparse_9bit(n, p, seed=100 + s)
         wall += time.perf_counter() - t0
     # device-only timing of the generation call through the context (result left on the device)
@@ -177,8 +177,10 @@ def run_gen9(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         out = ctypes.c_int64()
         e0.record(stream)
-        ctx.lib.dcx_gen_sparse_9bit(ctx.h, n, int(102300 // p), 200 + s, ctypes.byref(out))
+        rc = ctx.lib.dcx_gen_sparse_9bit(ctx.h, n, int(102300 // p), 200 + s, ctypes.byref(out))
         e1.record(stream)
+        if rc != 0:
+            raise RuntimeError(ctx.lib.dcx_last_error(ctx.h).decode())
         e1.synchronize()
         dev += e0.elapsed_time(e1) * 1e-3  # CUDA events on the context stream
     cpu_n = 8000
