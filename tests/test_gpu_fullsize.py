@@ -1,0 +1,97 @@
+"""GPU parity at BASELINE.json's full sizes, through size-independent properties.
+
+The oracle runs the small instances of test_gpu_parity.py in seconds; at the
+BASELINE sizes (T6 = 10^6-spin torus x 256 replicas, E7 = 10^7-spin
+Erdos-Renyi, configs[2] and [3]) the CPU cannot replay whole solves, so these
+tests check what holds at any size:
+
+* one teacher-forced step: x_1 = cbrt((J + aI) x_0 / b) (dc/solvers/doch.py:90-91,
+  :199) from the same x_0, against scipy's f64 product; ||dx||_2/||x||_2 <= 1e-5
+  (the north_star fp32 tolerance);
+* G-int: the reported best energy equals E(spins) = -1/2 s.Js of the returned
+  spins (dc/solvers/common.py:66-75), computed independently in f64 on the host
+  (exact: J is +-1 or -1/2), and cut = cut_offset - E (dc/model.py:45-76);
+* DOCH boundedness ||x_k||_inf <= max(1, ||x_0||_inf) (pkg/tests/test_doch.py:209-227);
+* the first ADOCH iterate equals the first DOCH iterate bitwise (no extrapolation
+  at k = 0, dc/solvers/doch.py:294-300);
+* h_values has iterations + 1 entries and the best-energy trace never increases.
+
+R8 (10^8 spins) is left to bench.py: its host build alone takes minutes.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2509_01928_b200 as dc
+from paper_2509_01928_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+
+
+def _check_common(J, rs, X0, cut_offset=None, doch=True):
+    for r, x0 in zip(rs, X0):
+        s = np.asarray(r.spins, dtype=np.float64)
+        assert np.all(np.abs(s) == 1.0)
+        e = -0.5 * float(s @ (J @ s))
+        assert r.energy == e
+        if cut_offset is not None:
+            assert all(t.cut_value == cut_offset - t.energy for t in r.trace)
+        assert len(r.h_values) == r.iterations + 1
+        best = [t.best_energy for t in r.trace]
+        assert all(b1 <= b0 for b0, b1 in zip(best, best[1:]))
+        if doch:
+            assert float(np.abs(r.x).max()) <= max(1.0, float(np.abs(x0).max()))
+
+
+def _one_step(J, alpha, beta, X0, rs):
+    X32 = X0.astype(np.float32).astype(np.float64)  # the f32 path starts from x_0 rounded to f32
+    AX = (J @ X32.T).T + alpha * X32
+    X1 = np.cbrt(AX / beta)
+    for r, x1 in zip(rs, X1):
+        assert r.iterations == 1
+        d = float(np.linalg.norm(np.asarray(r.x, dtype=np.float64) - x1) / np.linalg.norm(x1))
+        assert d <= FP32_TOL, d
+
+
+@pytest.fixture(scope="module")
+def t6():
+    v, c, o = synth.torus(1000, seed=0)
+    n = 10**6
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False))
+    J = sp.csr_matrix((v, c, o), shape=(n, n))
+    X0 = np.stack([dc.initial_state(n, 4.0, 8.0e9, np.random.default_rng(s)) for s in range(256)])
+    return inst, J, 4.0, 8.0e9, X0
+
+
+def test_t6_full_size_properties(t6):
+    inst, J, alpha, beta, X0 = t6
+    run = lambda solver, iters: dc.solve_replicas(inst, solver, alpha, beta, X0, max_iters=iters,  # noqa: E731
+                                                  precision="f32", path="multipass")
+    d1 = run("doch", 1)
+    _one_step(J, alpha, beta, X0[:16], d1[:16])
+    a1 = run("adoch", 1)
+    for rd, ra in zip(d1, a1):
+        assert np.array_equal(rd.x, ra.x)
+    sub = list(range(0, 256, 17))  # 16 replicas spread over both replica chunks
+    d = run("doch", 30)
+    _check_common(J, [d[i] for i in sub], X0[sub])
+    a = run("adoch", 30)
+    _check_common(J, [a[i] for i in sub], X0[sub], doch=False)
+    assert all(r.accepted[0] for r in a)
+
+
+def test_e7_full_size_properties():
+    n = 10**7
+    v, c, o, co = synth.erdos_renyi(n, 8, seed=0)
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False), cut_offset=co)
+    J = sp.csr_matrix((v, c, o), shape=(n, n))
+    alpha, beta = 2.828, 5.005e11  # SURVEY.md §8d E7 (eta = 1)
+    X0 = dc.initial_state(n, alpha, beta, np.random.default_rng(0))[None, :]
+    r1 = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=1, precision="f32", path="multipass")
+    _one_step(J, alpha, beta, X0, r1)
+    r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=20, precision="f32", path="multipass")
+    _check_common(J, r, X0, cut_offset=co)
+    assert r[0].iterations == 20 and r[0].stop_reason == "max_iters"
