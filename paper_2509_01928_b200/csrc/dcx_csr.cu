@@ -711,13 +711,33 @@ __global__ void __launch_bounds__(256) reduce_control(PassArgs a, const double* 
       if (stopped) atomicSub(&a.g->running, 1);
     }
   } else if (running) {
-    for (int q = 0; q < NQ; ++q) {
-      double acc = 0.0;
-      const bool ismax = q == Q_STEP;
-      const double* src = a.part + ((int64_t)r * NQ + q) * a.slots;
-      for (int s = threadIdx.x; s < a.slots; s += blockDim.x) acc = ismax ? fmax(acc, src[s]) : acc + src[s];
-      red[q][threadIdx.x] = acc;
+    // each thread folds slots t, t + 256, ... in increasing order; the loads of
+    // eight slots and all NQ quantities are issued before the folds (one L2
+    // round trip per 8 x NQ slots instead of one per slot; same order, same bits)
+    constexpr int U = 8;
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+    const double* src = a.part + (int64_t)r * NQ * a.slots;
+    for (int s0 = threadIdx.x; s0 < a.slots; s0 += U * blockDim.x) {
+      double v[NQ][U];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int s = s0 + u * blockDim.x;
+          v[q][u] = s < a.slots ? src[(int64_t)q * a.slots + s] : 0.0;  // 0: identity of + and of the step max
+        }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (s0 + u * blockDim.x >= a.slots) break;
+          acc[q] = (q == Q_STEP) ? fmax(acc[q], v[q][u]) : acc[q] + v[q][u];
+        }
     }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) red[q][threadIdx.x] = acc[q];
     double st = 0.0;
     if (spart) {
       for (int s = threadIdx.x; s < sslots; s += blockDim.x) st = fmax(st, spart[(int64_t)s * R + r]);
