@@ -740,7 +740,16 @@ __global__ void __launch_bounds__(256) reduce_control(PassArgs a, const double* 
     for (int q = 0; q < NQ; ++q) red[q][threadIdx.x] = acc[q];
     double st = 0.0;
     if (spart) {
-      for (int s = threadIdx.x; s < sslots; s += blockDim.x) st = fmax(st, spart[(int64_t)s * R + r]);
+      for (int s0 = threadIdx.x; s0 < sslots; s0 += 8 * blockDim.x) {  // eight loads in flight (max: any order)
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int s = s0 + u * blockDim.x;
+          v[u] = s < sslots ? spart[(int64_t)s * R + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) st = fmax(st, v[u]);
+      }
     }
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
