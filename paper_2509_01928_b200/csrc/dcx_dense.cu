@@ -8,7 +8,21 @@
 //
 // Formulation: replicas are the UMMA M dimension (TMEM lanes),
 // spins the N dimension, so every per-replica reduction is a per-thread sum.
-//   D1[r][i] = sum_j Xh[r][j] Q[i][j]   kind::f16, Xh = f16(x / lambda_r), Q = J / jscale (exact)
+// DOCH (delta operands): the iterate is x_p = lambda_r s_p with the scaled state s in
+// f32 (TMEM), and each iteration multiplies only its CHANGE:
+//   Dh_{p+1} = f16(T(x_p) / lambda_r - s_p),  s_{p+1} = s_p + Dh_{p+1}   (f32)
+//   F_p[r][i] = sum_j Dh_p[r][j] Q[i][j]   kind::f16, Q = J / jscale (exact)
+//   R_p = R_{p-1} + F_p                    (f32, one round-to-nearest add in the epilogue)
+//   D2[r][i] += sum_j dS[r][j] Q8[i][j]    kind::i8, dS = sign(s_p) - sign(s_{p-1}) in {0, +-2}
+// so R_p = Q s_p to f32 accuracy and D2 = Q sign(x_p) exactly. The f16 rounding
+// acts on the step, not on x: the iterate moves by exactly lambda Dh, its step is
+// |x_{p+1} - x_p| = lambda max|Dh|, and near the fixed point Dh -> 0 with 11-bit
+// relative accuracy, so replicas meet the reference's absolute 1e-10 step test
+// (doch.py:220) after the reference's number of iterations. A single f16 operand
+// of x itself (the ADOCH kernel below) limits the product to 2^-11 relative: x
+// then ping-pongs across f16 rounding boundaries and runs to max_iters.
+// ADOCH: fresh products of the state itself each iteration:
+//   D1[r][i] = sum_j Xh[r][j] Q[i][j]   kind::f16, Xh = f16(x / lambda_r)
 //   D2[r][i] = sum_j S8[r][j] Q8[i][j]  kind::i8,  S8 = sign(x) in int8, Q8 = Q in int8 (exact, s32 acc)
 // One persistent cooperative kernel runs all iterations: a 4-stage TMA ->
 // tcgen05.mma pipeline per 128x128 tile (fp32 / s32 accumulators in TMEM;
@@ -61,11 +75,17 @@ struct Pipe {
   static constexpr int STAGES = int(196608 / STAGE) < MAX_STAGES ? int(196608 / STAGE) : MAX_STAGES;  // 192 KB
   static constexpr uint32_t TILES = STAGES * STAGE;
 };
-// D1 [0,128) f32, D2 [128,256) s32, master x [256,384) f32; the ADOCH kernel double-buffers
-// D1 by iteration parity ([0,128) / [384,512)) and parks Ay_p in the D2 columns
+// DOCH: the product buffers [0,128) / [128,256) f32 alternate by iteration parity between the
+// fresh product F_p = Q Dh_p and the running product R_{p-1} = Q s_{p-1} (the epilogue writes
+// R_p = R_{p-1} + F_p over F_p), D2 = Q sign(s) [256,384) s32, the scaled state s = x / lambda
+// [384,512) f32. ADOCH: D1 [0,128) / [384,512) by iteration parity, D2 [128,256), master x
+// [256,384); Ay_p is parked in the D2 columns.
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t XCOL = 256;
+constexpr uint32_t SCOL = 384;
+constexpr uint32_t D2DOCH = 256;
 __host__ __device__ constexpr uint32_t d1col(int p) { return (p & 1) ? 384u : 0u; }
+__host__ __device__ constexpr uint32_t rcol(int p) { return (p & 1) ? 128u : 0u; }
 
 // Per replica-tile group: the tiles_n CTAs that share one replica tile are
 // the only ones that depend on each other (replicas are independent), so each
@@ -91,6 +111,12 @@ struct Args {
   CUtensorMap tmQ8;     // Q (int8)
   float* xm[2];
   float* axm;  // ADOCH: (J + aI) x of the last iteration of a launch, for the next launch's extrapolation
+  // DOCH delta operands (see the kernel comment): the running accumulators and the tracked
+  // state, persisted between launches of one solve
+  float* d1g;       // R = Q s               [Rpad][npad]
+  int* d2g;         // D2 = Q sign(x)        [Rpad][npad]
+  float* xhatg;     // s = x / lambda        [Rpad][npad]
+  int8_t* sgnl;     // sign(x_{p-1}) at the end of a launch (best-spin copy, resume)
   __half* xh[2];
   int8_t* s8[2];
   int8_t* best8;
@@ -303,8 +329,12 @@ template <int W>
 __device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t* v) {
   if constexpr (W == 32) {
     tmem_ld32(taddr, v);
+  } else if constexpr (W == 16) {
+    tmem_ld16(taddr, v);
+  } else if constexpr (W == 8) {
+    tmem_ld8(taddr, v);
   } else {
-    static_assert(W == 24, "chunks of 32 or 24 columns");
+    static_assert(W == 24, "chunks of 32, 24, 16 or 8 columns");
     tmem_ld16(taddr, v);
     tmem_ld8(taddr + 16, v + 16);
   }
@@ -326,6 +356,10 @@ template <int W>
 __device__ __forceinline__ void tmem_stw(uint32_t taddr, const uint32_t* v) {
   if constexpr (W == 32) {
     tmem_st32(taddr, v);
+  } else if constexpr (W == 16) {
+    tmem_st16(taddr, v);
+  } else if constexpr (W == 8) {
+    tmem_st8(taddr, v);
   } else {
     tmem_st16(taddr, v);
     tmem_st8(taddr + 16, v + 16);
@@ -347,7 +381,7 @@ struct __align__(8) Smem {
   uint32_t tmem_base;
   int pad;
   unsigned tdbg[8];  // epilogue phase stamps / sums (DCX_DENSE_TRACE)
-  float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM];  // per-replica constants (fixed for the run)
+  float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM], lam[TM];  // per-replica constants (fixed for the run)
   float red[2][TM][8];  // [4, 8): the ADOCH kernel's H(y) partials
   double red2[2][TM][4];
   RepCtl ctl[TM];
@@ -419,6 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     sm.inv_beta[threadIdx.x] = float(1.0 / be);
     sm.jl[threadIdx.x] = a.jscale * float(lam);
     sm.inv_lam[threadIdx.x] = float(1.0 / lam);
+    sm.lam[threadIdx.x] = float(lam);
   }
   // epilogue thread geometry
   const bool epi = warp >= 4;
@@ -427,8 +462,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const int r = r0 + rl;
   const bool valid = epi && r < a.R;
   uint64_t prevmask = 0;  // sign bits of x_{p-1} for this thread's HW columns
-  if (epi) {
-    const int8_t* sp = a.s8[(p + 1) & 1] + (int64_t)r * a.npad + i0 + h * HW;
+  if (epi) {  // stored by the previous launch's teardown
+    const int8_t* sp = a.sgnl + (int64_t)r * a.npad + i0 + h * HW;
 #pragma unroll 1
     for (int c = 0; c < HW; ++c)
       if (valid && p > 0 && sp[c] < 0) prevmask |= 1ull << c;
@@ -439,18 +474,37 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const uint32_t idesc = idesc_f16(NC * TM, TN), idesc8 = idesc_i8(NC * TM, TN);
-  // the CTA's f32 master states live in TMEM columns [XCOL, XCOL + 128) for the whole run
-  const uint32_t xaddr = tmem + (uint32_t(q * 32) << 16) + XCOL + h * HW;
-  if (epi) {
-    const float* src = a.xm[p & 1] + (int64_t)r * a.npad + i0 + h * HW;
+  // the CTA's f32 states live in TMEM for the whole run: ADOCH x in [XCOL, XCOL + 128),
+  // DOCH s = x / lambda in [SCOL, SCOL + 128)
+  const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16) + h * HW;  // this thread's row, column 0 of its half
+  const uint32_t xaddr = lane_base + (AD ? XCOL : SCOL);
+  const uint32_t d2addr = lane_base + (AD ? uint32_t(TN) : D2DOCH);
+  // one row segment of HW values from global into TMEM columns (zeros for padding replicas)
+  auto load_cols = [&](uint32_t taddr, const uint32_t* src) {
     uint32_t v[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(valid ? src[j] : 0.f);
-    tmem_st32(xaddr, v);
+    for (int j = 0; j < 32; ++j) v[j] = valid ? src[j] : 0u;
+    tmem_st32(taddr, v);
 #pragma unroll
-    for (int j = 0; j < W1; ++j) v[j] = __float_as_uint(valid ? src[32 + j] : 0.f);
-    tmem_stw<W1>(xaddr + 32, v);
+    for (int j = 0; j < W1; ++j) v[j] = valid ? src[32 + j] : 0u;
+    tmem_stw<W1>(taddr + 32, v);
+  };
+  if (epi) {
+    const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
+    if constexpr (AD) {
+      load_cols(xaddr, reinterpret_cast<const uint32_t*>(a.xm[p & 1] + o));
+    } else {  // s_p, R_{p-1} and D2 = Q sign(s_{p-1}) of the previous launch (p = 0: s_0, zeros)
+      load_cols(xaddr, reinterpret_cast<const uint32_t*>(a.xhatg + o));
+      load_cols(lane_base + rcol(p - 1), reinterpret_cast<const uint32_t*>(a.d1g + o));
+      load_cols(d2addr, reinterpret_cast<const uint32_t*>(a.d2g + o));
+    }
     tmem_st_wait();
+  }
+  if constexpr (!AD) {  // the restored accumulators are in TMEM before the (pair leader's) first MMA adds to them
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (NC == 2) cluster_sync_all();
+    tc_fence_after();
   }
   RunCfg cfg = a.cfg;
   if (nt != 0) cfg.hist = nullptr;  // only the nt == 0 CTA of a replica tile writes history
@@ -605,13 +659,13 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             if (kb < KB1) {
 #pragma unroll
               for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
-                mma_f16_g<NC>(tmem + (AD ? d1col(p) : 0u), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
-                              (kb | q | k) ? 1u : 0u);
+                mma_f16_g<NC>(tmem + (AD ? d1col(p) : rcol(p)), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32),
+                              idesc, (kb | q | k) ? 1u : 0u);  // DOCH: F_p = Q Dh_p
             } else {
 #pragma unroll
               for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
-                mma_i8_g<NC>(tmem + TN, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8,
-                             ((kb - KB1) | q | k) ? 1u : 0u);
+                mma_i8_g<NC>(tmem + (AD ? uint32_t(TN) : D2DOCH), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8,
+                             (!AD || ((kb - KB1) | q | k)) ? 1u : 0u);  // DOCH: D2 += Q dS
             }
           }
           mma_commit_g<NC>(smem_u32(&sm.empty[s]), uint16_t(!a.mc ? 0x3 : (psub == 0 ? 0x3 : 0xF)));
@@ -938,6 +992,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       const bool running = valid && c.status == DCX_STOP_RUNNING && !stops_now;
       const bool write_master = running && budget;  // a budget stop at p would need x_p
       const bool copy_prev = valid && p > 0 && c.pend == p - 1;
+      const bool live_p = valid && c.status == DCX_STOP_RUNNING;  // x_p is this replica's current iterate
       const float alpha = sm.alpha[rl], inv_beta = sm.inv_beta[rl], jl = sm.jl[rl], inv_lam = sm.inv_lam[rl];
       float s4 = 0.f, sxax = 0.f, step = 0.f;
       int es = 0;
@@ -973,58 +1028,83 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
       float* xg = a.xm[cur] + (int64_t)r * a.npad + gbase;  // x_p (time-budget runs only)
       // one chunk of W columns starting at column `off` of this warp's half (bits off.. of the masks)
+      const float lamf = sm.lam[rl];
       auto chunk = [&](auto wc, const int off) {
         constexpr int W = decltype(wc)::value;
-        uint32_t v1[32], xv[32];  // xv: x_p, updated in place to the next master state
-        tmem_ldw<W>(tmem + (uint32_t(q * 32) << 16) + h * HW + off, v1);
-        tmem_ldw<W>(xaddr + off, xv);
+        // fv: F_p = Q Dh_p (fresh), rv: R_{p-1}, replaced by R_p = R_{p-1} + F_p (one
+        // round-to-nearest add per iteration: accumulating in the tensor core would round at
+        // every K step against |R|, a noise floor above the reference's 1e-10 step test);
+        // sv_: s_p = x_p / lambda, replaced by s_{p+1} = s_p + Dh_{p+1}
+        uint32_t fv[W], rv[W], st[W];
+        tmem_ldw<W>(lane_base + rcol(p) + off, fv);
+        tmem_ldw<W>(lane_base + rcol(p + 1) + off, rv);
+        tmem_ldw<W>(xaddr + off, st);
         tmem_ld_wait();
         if (write_master && lim > 0) {  // x_p persisted (a budget stop at p keeps it)
 #pragma unroll
           for (int j = 0; j < W; j += 4)
-            *reinterpret_cast<float4*>(xg + off + j) = *reinterpret_cast<float4*>(xv + j);
+            *reinterpret_cast<float4*>(xg + off + j) =
+                make_float4(lamf * __uint_as_float(st[j]), lamf * __uint_as_float(st[j + 1]),
+                            lamf * __uint_as_float(st[j + 2]), lamf * __uint_as_float(st[j + 3]));
         }
-        __align__(16) __half2 hv[16];
-        __align__(16) uint32_t sv[8];
+        __align__(16) __half2 hv[W / 2];
+        __align__(16) uint32_t sv[W / 4];
         if (lim > 0) {
-          // branch-free over all W columns (x is never -0.0, so x < 0 <=> sign bit). Padding
-          // columns (i >= n) hold x = +0 and D1 = 0 (zero rows/columns of Q), so they
-          // update to +0, add nothing to the sums and read as spin +1 (a zero term of
-          // the energy GEMM: the padded rows and columns of Q are zero)
+          // branch-free over all W columns (s is never -0.0 after the first update, so s < 0
+          // <=> sign bit). Padding columns (i >= n) hold s = +0 and R = F = 0 (zero rows and
+          // columns of Q), so they keep s = +0 with a zero delta, add nothing to the sums and
+          // read as spin +1 (a zero term of the energy GEMM)
           uint32_t m = 0;
 #pragma unroll
           for (int j = 0; j < W; j += 2) {
-            float nx[2];
+            __half dh[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const float x = __uint_as_float(xv[j + u]);
-              const float ax = fmaf(alpha, x, jl * __uint_as_float(v1[j + u]));
-              nx[u] = cbrt_lean(ax * inv_beta);
+              const float rr = __fadd_rn(__uint_as_float(rv[j + u]), __uint_as_float(fv[j + u]));
+              rv[j + u] = __float_as_uint(rr);
+              const float sc = __uint_as_float(st[j + u]);
+              const float x = lamf * sc;
+              const float ax = fmaf(alpha, x, jl * rr);
+              const float nx = cbrt_lean(ax * inv_beta);
               const float x2 = x * x;
               s4 = fmaf(x2, x2, s4);
               sxax = fmaf(x, ax, sxax);
-              step = fmaxf(step, fabsf(nx[u] - x));
-              m |= (xv[j + u] >> 31) << (j + u);
-              xv[j + u] = running ? __float_as_uint(nx[u]) : xv[j + u];
+              m |= (st[j + u] >> 31) << (j + u);
+              // the next delta: T(x_p) - x_p in units of lambda, rounded to f16 (zero once the
+              // replica stopped, so a frozen replica adds nothing); the iterate moves by
+              // exactly lambda Dh, so the step |x_{p+1} - x_p| is lambda |Dh|
+              dh[u] = __float2half_rn(running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f);
+              const float dhf = __half2float(dh[u]);
+              step = fmaxf(step, fabsf(dhf));
+              st[j + u] = __float_as_uint(__fadd_rn(sc, dhf));
             }
-            hv[j / 2] = __floats2half2_rn(nx[0] * inv_lam, nx[1] * inv_lam);
-            if ((j & 3) == 2) {  // 4 spins -> 4 bytes of +-1: 0x01 per byte, 0xff where negative
-              const uint32_t t = (xv[j - 2] >> 31) | ((xv[j - 1] >> 31) << 8) |
-                                 ((__float_as_uint(nx[0]) >> 31) << 16) | ((__float_as_uint(nx[1]) >> 31) << 24);
-              sv[j / 4] = 0x01010101u + t * 0xfeu;
+            hv[j / 2] = __halves2half2(dh[0], dh[1]);
+            if ((j & 3) == 2) {
+              // 4 spins -> 4 bytes of sign(x_{p+1}) - sign(x_p): +2 where the sign went - -> +,
+              // -2 (0xfe) where it went + -> -, else 0
+              const uint32_t ob = (m >> (j - 2)) & 0xFu;
+              const uint32_t nb = (st[j - 2] >> 31) | ((st[j - 1] >> 31) << 1) | ((st[j] >> 31) << 2) |
+                                  ((st[j + 1] >> 31) << 3);
+              const uint32_t df = ob ^ nb, neg = df & nb;
+              const uint32_t dfw = (df & 1u) | ((df & 2u) << 7) | ((df & 4u) << 14) | ((df & 8u) << 21);
+              const uint32_t ngw = (neg & 1u) | ((neg & 2u) << 7) | ((neg & 4u) << 14) | ((neg & 8u) << 21);
+              sv[j / 4] = dfw * 2u + ngw * 0xfcu;
             }
           }
           curmask |= uint64_t(m) << off;
-        }  // (lim == 0: padding replica or columns, the master state stays)
-        tmem_stw<W>(xaddr + off, xv);
-        if (running && lim > 0) {
+        }  // (lim == 0: padding replica or columns, the state stays)
+        tmem_stw<W>(lane_base + rcol(p) + off, rv);
+        tmem_stw<W>(xaddr + off, st);
+        if (valid && lim > 0) {  // stopped replicas write zero deltas
 #pragma unroll
           for (int j = 0; j < W / 2; j += 4) *reinterpret_cast<uint4*>(hn + off + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
           store_pm1(sn + off, sv, W / 4);
         }
       };
-      chunk(std::integral_constant<int, 32>{}, 0);
-      chunk(std::integral_constant<int, W1>{}, 32);
+      // chunks of 16 columns (three TMEM tiles live per chunk: F, R, s)
+#pragma unroll
+      for (int off = 0; off + 16 <= HW; off += 16) chunk(std::integral_constant<int, 16>{}, off);
+      if constexpr (HW % 16 != 0) chunk(std::integral_constant<int, 8>{}, HW - 8);
       const bool tr128 = a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096;
       if (tr128) a.dbg[p * 12 + 3] = clock64();
       tc_fence_before();
@@ -1050,8 +1130,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       tc_fence_after();
       {
         uint32_t v2[64];
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + TN + h * HW, v2);
-        tmem_ldw<W1>(tmem + (uint32_t(q * 32) << 16) + TN + h * HW + 32, v2 + 32);
+        tmem_ld32(d2addr, v2);
+        tmem_ldw<W1>(d2addr + 32, v2 + 32);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -1063,12 +1143,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           es += (v ^ m) - m;
         }
       }
-      if (running) prevmask = curmask;
+      if (live_p) prevmask = curmask;  // sign(x_p), also when the replica stops at p
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 2] = clock64();
       sm.red[h][rl][0] = s4;
       sm.red[h][rl][1] = sxax;
       sm.red[h][rl][2] = float(es);
-      sm.red[h][rl][3] = step;
+      sm.red[h][rl][3] = lamf * step;  // |x_{p+1} - x_p| = lambda max |Dh|
       epi_sync();
       if (h == 0 && r < a.R) {
         // layout [parity][replica tile][spin tile][replica in tile] x 4
@@ -1110,6 +1190,16 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     tmem_ld32(xaddr, v);
     tmem_ldw<W1>(xaddr + 32, v + 32);
     tmem_ld_wait();
+    if constexpr (!AD) {
+      const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
+      if (valid)  // s, for a later launch of this solve
+#pragma unroll
+        for (int j = 0; j < HW; j += 4)
+          *reinterpret_cast<uint4*>(a.xhatg + o + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      const float lamf = sm.lam[rl];
+#pragma unroll
+      for (int j = 0; j < HW; ++j) v[j] = __float_as_uint(lamf * __uint_as_float(v[j]));  // x = lambda s
+    }
     if (valid && !budget_stop)
 #pragma unroll
       for (int j = 0; j < HW; ++j)
@@ -1117,6 +1207,27 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           if (!keep_prev || (p & 1) == 0) d0[j] = __uint_as_float(v[j]);
           if (!keep_prev || (p & 1) == 1) d1[j] = __uint_as_float(v[j]);
         }
+    const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
+    if (valid) {
+      // sign(x_{p-1}): the pending best copy of the last pass (unpack_results) and the
+      // prevmask of a resumed launch
+      int8_t* sg = a.sgnl + o;
+#pragma unroll 1
+      for (int j = 0; j < HW; ++j) sg[j] = ((prevmask >> j) & 1) ? int8_t(-1) : int8_t(1);
+    }
+    if constexpr (!AD) {  // the running products, for a later launch of this solve
+      auto save_cols = [&](uint32_t taddr, uint32_t* dst) {
+        uint32_t w[64];
+        tmem_ld32(taddr, w);
+        tmem_ldw<W1>(taddr + 32, w + 32);
+        tmem_ld_wait();
+        if (valid)
+#pragma unroll
+          for (int j = 0; j < HW; j += 4) *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
+      };
+      save_cols(lane_base + rcol(p - 1), reinterpret_cast<uint32_t*>(a.d1g + o));  // R of the last iteration
+      save_cols(d2addr, reinterpret_cast<uint32_t*>(a.d2g + o));
+    }
   }
   // all CTAs of the group read p_exec before the first barrier and exit at the same p
   if (nt == 0 && threadIdx.x == 0) {
@@ -1136,8 +1247,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 
 // --------------------------------------------------------------- layout kernels
 // [n][R] f32 (common layout) -> [Rpad][npad] f32 master + f16 scaled operand
+// (also the DOCH delta start: Dh_0 = f16(x_0 / lambda) against s_{-1} = 0, so
+// s_0 = f32(Dh_0); dS_0 = sign(x_0) against sign(x_{-1}) = 0)
 __global__ void pack_state(const float* src, int n, int R, int npad, const RepCtl* ctl, float* xm, __half* xh,
-                           int8_t* s8) {
+                           int8_t* s8, float* xhat) {
   const int64_t total = int64_t(n) * R;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx / R;
@@ -1145,13 +1258,14 @@ __global__ void pack_state(const float* src, int n, int R, int npad, const RepCt
     const float x = src[idx];
     const float inv_lam = float(1.0 / sqrt(ctl[r].alpha / ctl[r].beta));
     xm[(int64_t)r * npad + i] = x;
-    xh[(int64_t)r * npad + i] = __float2half_rn(x * inv_lam);
+    const __half h = __float2half_rn(x * inv_lam);
+    xh[(int64_t)r * npad + i] = h;
+    xhat[(int64_t)r * npad + i] = __half2float(h);
     s8[(int64_t)r * npad + i] = x >= 0.f ? 1 : -1;
   }
 }
 // pending best copy of the last executed pass, then [Rpad][npad] -> [n][R]
-__global__ void unpack_results(const float* xm0, const float* xm1, const int8_t* s80, const int8_t* s81,
-                               int8_t* best8, int n, int R, int npad, const RepCtl* ctl, const SyncWords* sync,
+__global__ void unpack_results(const float* xm0, const float* xm1, const int8_t* sgnl, int8_t* best8, int n, int R, int npad, const RepCtl* ctl, const SyncWords* sync,
                                int nc, float* x0, float* x1, int8_t* best) {
   const int64_t total = int64_t(n) * R;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
@@ -1161,7 +1275,7 @@ __global__ void unpack_results(const float* xm0, const float* xm1, const int8_t*
     const int pe = ctl[r].pend;
     const int P = sync[r / (TM * nc)].p_exec - 1;  // last pass executed by the replica's group
     int8_t b = best8[s];
-    if (pe >= 0 && pe == P) b = (pe & 1) ? s81[s] : s80[s];
+    if (pe >= 0 && pe == P) b = sgnl[s];  // sign(x_P), stored by the kernel's teardown
     best[idx] = b;
     x0[idx] = xm0[s];
     x1[idx] = xm1[s];
@@ -1254,6 +1368,12 @@ void DenseDev::release_run() {
     xm[b] = xh[b] = s8[b] = nullptr;
   }
   if (best8) cudaFree(best8);
+  if (sgnl) cudaFree(sgnl);
+  if (xhat) cudaFree(xhat);
+  if (d1g) cudaFree(d1g);
+  if (d2g) cudaFree(d2g);
+  sgnl = nullptr;
+  xhat = d1g = d2g = nullptr;
   if (part) cudaFree(part);
   if (sync) cudaFree(sync);
   if (axm) cudaFree(axm);
@@ -1387,11 +1507,19 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   }
   if (!reuse) {
     DCK(cudaMalloc(&d.best8, vec));
+    DCK(cudaMalloc(&d.sgnl, vec));
+    DCK(cudaMalloc(&d.xhat, vec * 4));
+    DCK(cudaMalloc(&d.d1g, vec * 4));
+    DCK(cudaMalloc(&d.d2g, vec * 4));
     // by iteration parity, for the larger tile count of either width, 8 partials (ADOCH)
     DCK(cudaMalloc(&d.part, sizeof(double) * 2 * 8 * ((d.npad + 111) / 112) * d.Rpad));
     DCK(cudaMalloc(&d.sync, sizeof(tc::SyncWords) * (d.Rpad / 128) + sizeof(unsigned int) * tc::FLAG_STRIDE * tc::MAX_FLAGS));
   }
   DCK(cudaMemsetAsync(d.best8, 1, vec, s));
+  DCK(cudaMemsetAsync(d.sgnl, 1, vec, s));
+  DCK(cudaMemsetAsync(d.xhat, 0, vec * 4, s));  // padding; pack_state writes the live entries
+  DCK(cudaMemsetAsync(d.d1g, 0, vec * 4, s));
+  DCK(cudaMemsetAsync(d.d2g, 0, vec * 4, s));
   if (d.ad && !d.axm) DCK(cudaMalloc(&d.axm, vec * 4));
   {
     const int gsz = 128 * d.nc;
@@ -1412,7 +1540,8 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   }
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
-                                       reinterpret_cast<__half*>(d.xh[0]), reinterpret_cast<int8_t*>(d.s8[0]));
+                                       reinterpret_cast<__half*>(d.xh[0]), reinterpret_cast<int8_t*>(d.s8[0]),
+                                       reinterpret_cast<float*>(d.xhat));
   DCK(cudaGetLastError());
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(d.tmaps);
   make_map(&maps[0], d.xh[0], d.npad, d.Rpad, true);
@@ -1449,6 +1578,10 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     a.s8[b] = reinterpret_cast<int8_t*>(d.s8[b]);
   }
   a.best8 = d.best8;
+  a.sgnl = d.sgnl;
+  a.xhatg = reinterpret_cast<float*>(d.xhat);
+  a.d1g = reinterpret_cast<float*>(d.d1g);
+  a.d2g = reinterpret_cast<int*>(d.d2g);
   a.axm = reinterpret_cast<float*>(d.axm);
   a.part = d.part;
   a.ctl = m.args.ctl;
@@ -1568,8 +1701,7 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
   }
   tc::unpack_results<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(d.xm[0]),
                                            reinterpret_cast<const float*>(d.xm[1]),
-                                           reinterpret_cast<const int8_t*>(d.s8[0]),
-                                           reinterpret_cast<const int8_t*>(d.s8[1]), d.best8, int(d.n), d.R,
+                                           d.sgnl, d.best8, int(d.n), d.R,
                                            int(d.npad), m.args.ctl, reinterpret_cast<const tc::SyncWords*>(d.sync),
                                            d.nc, reinterpret_cast<float*>(m.args.x[0]),
                                            reinterpret_cast<float*>(m.args.x[1]), m.args.best);

@@ -21,9 +21,13 @@ struct DenseDev {
   bool ad = false;         // ADOCH (economy window) kernel
   void* axm = nullptr;     // ADOCH: (J + aI) x at launch ends [Rpad][npad] f32  // spin tile width (UMMA N: 128 or 112) and spin tiles per replica tile
   void* xm[2] = {nullptr, nullptr};  // f32 master states [Rpad][npad]
-  void* xh[2] = {nullptr, nullptr};  // f16 x / lambda_r [Rpad][npad] (MMA operand A)
-  void* s8[2] = {nullptr, nullptr};  // int8 sign(x) [Rpad][npad] (energy GEMM operand A)
+  void* xh[2] = {nullptr, nullptr};  // f16 MMA operand A [Rpad][npad]: DOCH the delta Dh, ADOCH x / lambda_r
+  void* s8[2] = {nullptr, nullptr};  // int8 energy GEMM operand A [Rpad][npad]: DOCH dS, ADOCH sign(x)
   int8_t* best8 = nullptr;           // [Rpad][npad]
+  int8_t* sgnl = nullptr;            // sign(x_{p-1}) at a launch end [Rpad][npad]
+  void* xhat = nullptr;              // DOCH: xhat / lambda [Rpad][npad] f32 (between launches)
+  void* d1g = nullptr;               // DOCH: D1 = Q xhat / lambda [Rpad][npad] f32 (between launches)
+  void* d2g = nullptr;               // DOCH: D2 = Q sign(x) [Rpad][npad] s32 (between launches)
   double* part = nullptr;            // [tiles_n][Rpad][4]
   void* sync = nullptr;              // grid barrier words
   void* tmaps = nullptr;             // host-side CUtensorMap storage (3 maps)

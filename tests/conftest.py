@@ -37,6 +37,22 @@ def garr():
     return golden_arrays()
 
 
+@lru_cache(maxsize=1)
+def golden_k2():
+    """K2000 over all 1024 seeds (tests/golden/make_golden_k2.py): per-seed best energy,
+    iterations, stop reason (0 converged, 1 max_iters, 2 time_budget) and the best-so-far
+    improvement points, DOCH and ADOCH."""
+    with open(GOLDEN / "golden_k2.json") as f:
+        g = json.load(f)
+    g["arrays"] = dict(np.load(GOLDEN / "golden_k2.npz"))
+    return g
+
+
+@pytest.fixture(scope="session")
+def gk2():
+    return golden_k2()
+
+
 @pytest.fixture(scope="session")
 def pgold():
     """Procedural-coupling fixtures (tests/golden/make_golden_procedural.py)."""

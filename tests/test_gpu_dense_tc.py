@@ -1,11 +1,14 @@
 """GPU: the dense tcgen05 path (precision "f16tc") against the exact energy
 kernel, the f32 path and the reference's K2000 quality numbers.
 
-The states enter the tensor cores as f16(x / lambda_r) (10-bit mantissa, exact
-+-1 couplings, fp32 accumulation), so iterates track the f32 path to ~1e-3
-relative; energies of spin vectors are computed by an exact +-1 x +-1 GEMM
-and must match the integer energy kernel bit for bit; quality is judged on
-distributions (SURVEY.md §8c G-quality)."""
+DOCH: the iterate is x = lambda_r s with s in f32, and each iteration sends only
+its change through the tensor cores, x_{p+1} = x_p + lambda f16((T(x_p) - x_p) /
+lambda) with T(x_p) from the exact-to-f32 running product (csrc/dcx_dense.cu),
+so the first iterate sees x_0 rounded to f16 and later iterates converge like
+the f32 path. ADOCH: the state itself as f16(x / lambda_r) each iteration (~1e-3
+relative). Energies of spin vectors come from an exact +-1 x +-1 GEMM and must
+match the integer energy kernel bit for bit; quality is judged on distributions
+over the reference's own 1024 seeds (SURVEY.md §8c G-quality)."""
 
 import numpy as np
 import pytest
@@ -19,7 +22,17 @@ pytestmark = pytest.mark.gpu
 # cube root (ill-conditioned near 0): measured 2.24e-3 on K2000, identical to a
 # float64 emulation of the same operand rounding (see test below).
 TC_STATE_TOL = 5e-3   # one iteration; three iterations compound to ~6e-3 (checked at 1e-2)
-EMU_TOL = 5e-4  # TC iterate vs a float64 emulation of the f16 operand (f32 epilogue noise through cbrt)
+EMU_TOL = 5e-4  # TC iterate vs a float64 emulation: f32 epilogue noise moves a few f16 roundings of the step by one ulp
+
+
+def doch_first_iterate_emulation(J, x0, a, b):
+    """x_1 of the delta-operand DOCH kernel in float64: x_0 enters as its f16 rounding
+    xq = lambda f16(x_0 / lambda) (the first delta is the state itself), T(xq) =
+    cbrt((J + aI) xq / b), and the iterate moves by the f16-rounded step."""
+    lam = np.sqrt(a / b)
+    xq = (x0 / lam).astype(np.float16).astype(np.float64) * lam
+    t = np.cbrt((J @ xq + a * xq) / b)
+    return xq + lam * ((t - xq) / lam).astype(np.float16).astype(np.float64)
 
 
 def k2_instance():
@@ -39,14 +52,11 @@ def test_tc_first_iterate_equals_f16_operand_emulation(gold):
     g = gold["k2"]
     inst = k2_instance()
     a, b = g["alpha"], g["beta"]
-    lam = np.sqrt(a / b)
     X0 = x0s(2000, a, b, range(128))
     tc = dc.solve_replicas(inst, "doch", a, b, X0, max_iters=1, precision="f16tc")
     J = -0.5 * k2_W()
     for x0, r in zip(X0, tc):
-        xq = (x0 / lam).astype(np.float16).astype(np.float64) * lam
-        emu = np.cbrt((J @ xq + a * x0) / b)
-        assert rel2(r.x, emu) <= EMU_TOL
+        assert rel2(r.x, doch_first_iterate_emulation(J, x0, a, b)) <= EMU_TOL
 
 
 def test_tc_first_iterates_track_f32(gold):
@@ -90,26 +100,53 @@ def test_tc_padding_ragged_sizes():
     np.testing.assert_array_equal(dc.energies(J, np.stack([r.spins for r in full])), [r.energy for r in full])
 
 
-def test_tc_k2000_quality_vs_reference(gold):
-    """1024 replicas (BASELINE configs[1]) vs the CPU reference's 32-seed DOCH runs."""
-    g = gold["k2"]
-    inst = k2_instance()
-    X0 = x0s(2000, g["alpha"], g["beta"], range(1024))
-    res = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=1000, precision="f16tc")
+def k2_quality_gate(res, gk2, solver):
+    """SURVEY.md §8c G-quality on BASELINE configs[1], against the unmodified reference on
+    the SAME 1024 seeds (tests/golden/golden_k2.npz):
+      * stop reasons: the reference converges (step <= 1e-10, doch.py:220) on 1022 / 1024
+        DOCH and 1024 / 1024 ADOCH seeds; the tensor-core path must converge as often
+        (>= reference - 2 %), not run to max_iters;
+      * iterations: mean within 4 standard errors (of the difference of two 1024-sample
+        means) of the reference's, i.e. a solve does the reference's amount of work;
+      * energies: not stochastically worse (one-sided Mann-Whitney U, p >= 1e-3) and the
+        mean no worse than the reference's + 3 standard errors;
+      * the tail: best energy at or below the reference's 3rd best over the same seeds, and
+        the fraction of seeds reaching 0.99 x the reference's best cut (the TTS target,
+        dc/bench.py:219-231) no lower than the reference's - 3 binomial standard errors.
+    Per-seed trajectories are not compared: f16 operand rounding in the first steps sends
+    a replica to a different local minimum, exactly as a change of summation order does."""
+    from scipy.stats import mannwhitneyu
+
+    A = gk2["arrays"]
+    ref_e, ref_it, ref_st = A[f"{solver}_energy"], A[f"{solver}_iterations"], A[f"{solver}_stop"]
     e = np.array([r.energy for r in res])
-    ref = np.array([row["energy"] for row in g["doch"]])
-    se = ref.std() / np.sqrt(len(ref))
-    # distribution no worse than the f64 reference (one-sided, 3 standard errors of the
-    # reference mean), on the shared seeds 0..31 and on all 1024 replicas
-    assert e[:32].mean() <= ref.mean() + 3 * se
-    assert e.mean() <= ref.mean() + 3 * se
-    # the reference's own best over 32 seeds sits 2.4 sigma out; 1024 replicas reach 2 sigma
-    assert e.min() <= ref.mean() - 2.0 * ref.std()
-    # lower decile: the reference's is an order statistic of 32 samples, whose standard
-    # error is sqrt(q (1 - q) / m) / pdf(z_q) sigma = 0.30 sigma for q = 0.1, m = 32 under a
-    # normal fit (3 x that, not 3 x the standard error of the mean)
-    se_q = np.sqrt(0.1 * 0.9 / len(ref)) / (np.exp(-0.5 * 1.2816 ** 2) / np.sqrt(2 * np.pi)) * ref.std()
-    assert np.quantile(e, 0.1) <= np.quantile(ref, 0.1) + 3 * se_q
+    it = np.array([r.iterations for r in res])
+    conv = np.array([r.stop_reason == "converged" for r in res])
+    R = len(ref_e)
+    assert len(res) == R
+    assert conv.sum() >= (ref_st == 0).sum() - 0.02 * R, (conv.sum(), (ref_st == 0).sum())
+    se_it = np.sqrt(it.var(ddof=1) / R + ref_it.var(ddof=1) / R)
+    assert abs(it.mean() - ref_it.mean()) <= 4 * se_it, (it.mean(), ref_it.mean(), se_it)
+    assert mannwhitneyu(e, ref_e, alternative="greater").pvalue >= 1e-3
+    assert e.mean() <= ref_e.mean() + 3 * ref_e.std(ddof=1) / np.sqrt(R), (e.mean(), ref_e.mean())
+    assert e.min() <= np.sort(ref_e)[2], (e.min(), np.sort(ref_e)[:3])
+    target = -(0.99 * (gk2["cut_offset"] - ref_e.min()) - gk2["cut_offset"])  # E at 0.99 x best cut
+    f_ref, f = (ref_e <= target).mean(), (e <= target).mean()
+    assert f >= f_ref - 3 * np.sqrt(f_ref * (1 - f_ref) / R), (f, f_ref)
+    return dict(mean=e.mean(), best=e.min(), iters=it.mean(), converged=int(conv.sum()), reach=f)
+
+
+def test_tc_k2000_quality_vs_reference_1024_seeds(gk2):
+    """BASELINE configs[1]: 1024 DOCH replicas, seeds 0..1023, eta = 0.1, max_iters 1000,
+    trace_stride 1 -- the reference's stop reasons, iteration counts and energy
+    distribution on the same seeds."""
+    inst = k2_instance()
+    X0 = x0s(2000, gk2["alpha"], gk2["beta"], range(1024))
+    res = dc.solve_replicas(inst, "doch", gk2["alpha"], gk2["beta"], X0, max_iters=1000, precision="f16tc")
+    assert res[0].path == "dense_tc"
+    k2_quality_gate(res, gk2, "doch")
+    for r in res[:16]:
+        assert dc.energy(inst.coupling, r.spins) == r.energy
 
 
 def _run_with_env(env, fn):
@@ -152,14 +189,12 @@ def test_tc_112_wide_spin_tiles(gold):
     g = gold["k2"]
     inst = k2_instance()
     a, b = g["alpha"], g["beta"]
-    lam = np.sqrt(a / b)
     X0 = x0s(2000, a, b, range(256))
     J = -0.5 * k2_W()
     one = _run_with_env({"DCX_DENSE_TN": "112"},
                         lambda: dc.solve_replicas(inst, "doch", a, b, X0, max_iters=1, precision="f16tc"))
     for x0, r in zip(X0, one):
-        xq = (x0 / lam).astype(np.float16).astype(np.float64) * lam
-        assert rel2(r.x, np.cbrt((J @ xq + a * x0) / b)) <= EMU_TOL
+        assert rel2(r.x, doch_first_iterate_emulation(J, x0, a, b)) <= EMU_TOL
     res = _run_with_env({"DCX_DENSE_TN": "112"},
                         lambda: dc.solve_replicas(inst, "doch", a, b, X0, max_iters=60, precision="f16tc"))
     assert res[0].path == "dense_tc"
@@ -232,8 +267,9 @@ def test_tc_time_budget(gold, solver):
     g = gold["k2"]
     inst = k2_instance()
     X0 = x0s(2000, g["alpha"], g["beta"], range(256))
+    # 0.5 ms: about 30 iterations, well before any replica converges (>= 100 iterations)
     res = dc.solve_replicas(inst, solver, g["alpha"], g["beta"], X0, max_iters=10**6, precision="f16tc",
-                            time_budget=0.005)
+                            time_budget=0.0005)
     assert res[0].path == "dense_tc"
     for r in res[:16]:
         assert r.stop_reason == "time_budget"
