@@ -1446,6 +1446,7 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   }
   if (scale == 0.0) return;  // real-valued couplings: no exact int8 / f16 operand, tensor path unavailable
   d.jscale = float(scale);
+  d.jscale_d = scale;  // exact: the energies of returned spins are jscale_d * (integer GEMM)
   d.exact = true;
   if (!d.tmaps) d.tmaps = new CUtensorMap[6];
 }
@@ -1708,16 +1709,17 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
   DCK(cudaGetLastError());
 }
 
-// 100 iterations per launch: the solve runs the kernel once for up to max_iters
-// iterations, so the per-launch prologue (TMEM allocation, barrier setup, state
-// load) is amortised over the run; 10-iteration launches overstated it 30 %
+// 100 iterations per profiled launch (the solve itself runs the kernel once for up to
+// max_iters iterations): long enough to amortise the per-launch prologue (TMEM
+// allocation, barrier setup, state load), short enough that no K2000 replica has
+// converged (the reference's fewest iterations over 1024 seeds is 124), so every
+// replica-iteration in the window is live work
 int dense_iters_per_profile_launch() { return 100; }
 
-void dense_profile(DenseDev& d, MultiPass& m, int launches, cudaEvent_t ea, cudaEvent_t eb, cudaStream_t s) {
-  const int it = dense_iters_per_profile_launch();
-  launch_dense(d, m, it, s);  // warm (passes 0..it-1)
+// one timed launch of iterations [0, it) from the state dense_begin packed
+void dense_profile(DenseDev& d, MultiPass& m, cudaEvent_t ea, cudaEvent_t eb, cudaStream_t s) {
   DCK(cudaEventRecord(ea, s));
-  for (int l = 0; l < launches; ++l) launch_dense(d, m, it * (l + 2), s);
+  launch_dense(d, m, dense_iters_per_profile_launch(), s);
   DCK(cudaEventRecord(eb, s));
 }
 

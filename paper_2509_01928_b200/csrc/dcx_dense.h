@@ -11,7 +11,8 @@ namespace dcx {
 struct DenseDev {
   int64_t n = 0, npad = 0;
   bool exact = false;    // Q exactly representable in int8 (|q| <= 127)
-  float jscale = 1.0f;
+  float jscale = 1.0f;    // J = jscale * Q (the f32 epilogue's factor)
+  double jscale_d = 1.0;  // the same scale in double (energy scale: exact for non-dyadic scales)
   void* q16 = nullptr;   // f16 Q [npad][npad]
   void* q8 = nullptr;    // int8 Q [npad][npad] (energy GEMM)
   // per-run buffers
@@ -43,7 +44,7 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s);
 void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s);
 void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s);
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s);
-void dense_profile(DenseDev& d, MultiPass& m, int launches, cudaEvent_t a, cudaEvent_t b, cudaStream_t s);
+void dense_profile(DenseDev& d, MultiPass& m, cudaEvent_t a, cudaEvent_t b, cudaStream_t s);
 int dense_iters_per_profile_launch();
 
 }  // namespace dcx

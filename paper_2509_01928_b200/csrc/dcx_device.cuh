@@ -125,7 +125,8 @@ __device__ __forceinline__ float cbrt_fast(float t) {
 // so t = 0 gives +0 without a branch or select (the offset is a normal float: a
 // denormal one would be flushed by rcp.approx.ftz and turn t = 0 into NaN; it is
 // below 2e-12 of r^2 for every normal t, so <= 1 ulp from cbrtf on normal
-// arguments; denormal arguments would flush to zero).
+// arguments). Denormal arguments flush to zero explicitly: lg2.approx.ftz would see 0,
+// leave r = 0 and the Newton step would return a * 1e37 / 3.
 __device__ __forceinline__ float cbrt_lean(float t) {
   const float a = fabsf(t);
   float l, r, rc;
@@ -133,6 +134,7 @@ __device__ __forceinline__ float cbrt_lean(float t) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (1.0f / 3.0f)));
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaf(r, r, 1e-37f)));
   r = fmaf(fmaf(a, rc, -r), 1.0f / 3.0f, r);
+  r = a < 1.17549435e-38f ? 0.0f : r;
   return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
 }
 __device__ __forceinline__ double inv_beta(double beta) { return beta; }  // unused in f64

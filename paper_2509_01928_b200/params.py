@@ -185,6 +185,10 @@ def tune_eta(instance, candidate_etas: Sequence[float], probe_iters: int = 10, s
     etas = sorted(candidate_etas)
     alphas = np.array([eta * lam for eta in etas])
     betas = n * np.sqrt(n) * (alphas + row_max)
+    # the reference builds SolverParams per candidate (dc/spectral.py:288-292): an eta outside
+    # (0, 2] raises its ValueError -- here before the batch, with the same message
+    for eta, a, b in zip(etas, alphas, betas):
+        SolverParams(alpha=float(a), beta=float(b), eta=eta, max_iters=probe_iters, seed=seed)
     x0 = np.stack([initial_state(n, a, b, np.random.default_rng(seed)) for a, b in zip(alphas, betas)])
     res = solve_replicas(inst, "doch", alphas, betas, x0, max_iters=probe_iters, trace_stride=probe_iters,
                          precision=precision, seeds=[seed] * len(etas))

@@ -217,7 +217,10 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
     cut_offset = getattr(instance, "cut_offset", None)
     if callbacks and R == 1:
         # stream records to the callbacks in iteration order, chunk by chunk
+        # the running best over recorded iterations is carried across chunks, so every
+        # record's best_energy is the TraceCollector's (dc/solvers/common.py:70-73, :89-90)
         fed = 0
+        run_best = np.inf
         live = True
         while live:
             live = ctx.step()
@@ -225,8 +228,9 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
             if s.n_hist > fed:
                 h, e, t, ev = ctx.history(0, fed, int(s.n_hist) - fed)
                 for k in np.nonzero(ev & _native.EV_RECORDED)[0]:
+                    run_best = min(run_best, float(e[k]))
                     rec = LazyTrace(solver, np.array([fed + k]), t[k:k + 1] + offset, e[k:k + 1], cut_offset,
-                                    ev[k:k + 1])[0]
+                                    ev[k:k + 1], best=np.array([run_best]))[0]
                     for cb in callbacks:
                         cb(rec)
                 fed = int(s.n_hist)
@@ -370,12 +374,14 @@ def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", 
     dense = bool(info.dense)
     tb = 8 if precision == "f64" else (2 if precision == "f16tc" else 4)
     if kid == 3:
-        # one launch = 100 iterations of the persistent kernel (dense_iters_per_profile_launch,
-        # csrc/dcx_dense.cu; launches resume the run, so launches <= max_iters/100 - 1);
-        # per iteration two n x n x R products: J x (f16 -> f32) and J sign(x) (int8 -> s32)
+        # one launch = iterations [0, 100) of the persistent kernel from x0 (every launch
+        # restarts the same window, csrc/dcx_api.cu dcx_profile_kernel; no K2000 replica
+        # converges before iteration 124, so all R replicas are live throughout). Work per
+        # iteration: SURVEY.md §8d's 2 n^2 R -- ONE coupling product per replica, the
+        # delta product J Dh; the exact sign product (int8, incremental) is not counted
         name = "dense_doch_kernel"
         iters = 100
-        flops = iters * 2 * (2.0 * n * n * R)
+        flops = iters * 2.0 * n * n * R
         byts = float(iters * R * n * (2 + 1))  # f16 + int8 operands of the next iteration
     else:
         name = "pass_rv" if R > 1 else "pass_r1"

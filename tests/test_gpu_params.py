@@ -43,3 +43,65 @@ def test_power_iteration_zero_coupling_raises():
     J = dc.CsrCoupling(4, np.zeros(2), np.array([1, 0]), np.array([0, 1, 2, 2, 2]), validate=False)
     with pytest.raises(ValueError):
         dc.estimate_lambda_max_neg(J, method="power_iteration")
+
+
+# ------------------------------------------------------------------ tune_eta / solve() front door
+def _g1():
+    v, c, o, co = g1_csr()
+    return dc.ProblemInstance(coupling=dc.CsrCoupling(800, v, c, o, validate=False), cut_offset=co)
+
+
+@pytest.mark.gpu
+def test_tune_eta_g1_matches_reference(gold):
+    """All seven DEFAULT_ETA_GRID candidates as ONE replica batch of 10-iteration probes
+    (dc/spectral.py:259-298): the reference picked eta = 0.25 on this instance."""
+    eta = dc.tune_eta(_g1(), dc.DEFAULT_ETA_GRID, probe_iters=10, seed=0)
+    assert eta == gold["g1"]["eta"] == 0.25
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid", [(0.5, 2.5), (0.0, 1.0), (-1.0,)])
+def test_tune_eta_rejects_out_of_range_candidates(grid):
+    """The reference builds SolverParams(eta=...) per candidate, whose validation raises
+    ValueError for eta outside (0, 2] (dc/spectral.py:41-49, :288-292)."""
+    with pytest.raises(ValueError):
+        dc.tune_eta(_g1(), grid, probe_iters=3, seed=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+def test_solve_front_door_derives_params_and_matches_reference(gold, solver):
+    """solve(instance, solver, seed, eta) derives alpha / beta itself (dc/solvers/__init__.py:66-75,
+    device power iteration) and runs the solver with trace_stride 1: energies, stop reasons
+    and iteration counts equal the unmodified reference's G1 runs at eta = 0.25 (f64)."""
+    inst = _g1()
+    rows = gold["g1"][solver]
+    same = 0
+    for seed in range(6):
+        r = dc.solve(inst, solver, seed=seed, eta=0.25)
+        ref = rows[seed]
+        assert r.seed == seed and len(r.trace) == r.iterations + 1  # trace_stride None -> 1
+        assert r.energy == ref["energy"] and r.stop_reason == ref["stop_reason"]
+        same += r.iterations == ref["iterations"]
+    # DOCH: identical iteration counts; ADOCH's window test may flip on last-bit H differences (SURVEY §8c)
+    assert same == 6 if solver == "doch" else same >= 5
+
+
+@pytest.mark.gpu
+def test_solve_front_door_overrides(gold):
+    """params given: seed, budget_iters and budget_seconds override it (dc/solvers/__init__.py:76-81)."""
+    inst = _g1()
+    g = gold["g1"]
+    p = dc.SolverParams(alpha=g["alpha"], beta=g["beta"], eta=0.25, max_iters=1000, seed=99)
+    r = dc.solve(inst, "doch", seed=3, params=p, budget_iters=20)
+    direct = dc.doch_solve(inst, dc.SolverParams(alpha=g["alpha"], beta=g["beta"], eta=0.25, max_iters=20, seed=3))
+    assert r.seed == 3 and r.iterations == 20 and r.stop_reason == "max_iters"
+    assert r.energy == direct.energy and np.array_equal(r.x, direct.x)
+    r2 = dc.solve(inst, "doch", seed=3, params=p, trace_stride=7)
+    # stride 7 records fewer iterations: same run, best over a subset of the stride-1 records
+    assert r2.iterations == g["doch"][3]["iterations"] and r2.energy >= g["doch"][3]["energy"]
+    assert all(t.iteration % 7 == 0 or t.iteration == r2.iterations for t in r2.trace)
+    r3 = dc.solve(inst, "doch", seed=3, params=p, budget_iters=10**6, budget_seconds=1e-4)
+    assert r3.stop_reason in ("time_budget", "converged")
+    with pytest.raises(ValueError):
+        dc.solve(inst, "sa")

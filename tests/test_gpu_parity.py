@@ -263,6 +263,17 @@ def test_callbacks_in_order():
     p = dc.SolverParams(alpha=6.108031887826326, beta=884913.7454957356, max_iters=30, seed=0)
     r = dc.doch_solve(inst, p, callbacks=[seen.append])
     assert [t.iteration for t in seen] == [t.iteration for t in r.trace] == list(range(31))
+    # the full records, running best included (TraceCollector, dc/solvers/common.py:70-91);
+    # chunk=4 streams them across several device chunks
+    seen = []
+    r = dc.solve_replicas(inst, "doch", p.alpha, p.beta, dc.initial_state(800, p.alpha, p.beta,
+                                                                      np.random.default_rng(0))[None, :],
+                          max_iters=30, precision="f64", callbacks=[seen.append], chunk=4, path="multipass")[0]
+    assert len(seen) == len(r.trace) == 31
+    for a, b in zip(seen, r.trace):
+        assert (a.iteration, a.energy, a.best_energy, a.cut_value, a.event) == \
+            (b.iteration, b.energy, b.best_energy, b.cut_value, b.event)
+    assert [t.best_energy for t in seen] == list(np.minimum.accumulate([t.energy for t in seen]))
 
 
 # ------------------------------------------------------------------ sparse families (multipass)
