@@ -8,9 +8,9 @@
 //
 // Formulation: replicas are the UMMA M dimension (TMEM lanes),
 // spins the N dimension, so every per-replica reduction is a per-thread sum.
-// DOCH (delta operands): the iterate is x_p = lambda_r s_p with the scaled state s in
-// f32 (TMEM), and each iteration multiplies only its CHANGE:
-//   Dh_{p+1} = f16(T(x_p) / lambda_r - s_p),  s_{p+1} = s_p + Dh_{p+1}   (f32)
+// Delta operands (DOCH and ADOCH): the iterate is x_p = lambda_r s_p with the
+// scaled state s in f32 (TMEM), and each iteration multiplies only its CHANGE:
+//   Dh_{p+1} = f16(x_{p+1} / lambda_r - s_p),  s_{p+1} = s_p + Dh_{p+1}   (f32)
 //   F_p[r][i] = sum_j Dh_p[r][j] Q[i][j]   kind::f16, Q = J / jscale (exact)
 //   R_p = R_{p-1} + F_p                    (f32, one round-to-nearest add in the epilogue)
 //   D2[r][i] += sum_j dS[r][j] Q8[i][j]    kind::i8, dS = sign(s_p) - sign(s_{p-1}) in {0, +-2}
@@ -18,12 +18,11 @@
 // acts on the step, not on x: the iterate moves by exactly lambda Dh, its step is
 // |x_{p+1} - x_p| = lambda max|Dh|, and near the fixed point Dh -> 0 with 11-bit
 // relative accuracy, so replicas meet the reference's absolute 1e-10 step test
-// (doch.py:220) after the reference's number of iterations. A single f16 operand
-// of x itself (the ADOCH kernel below) limits the product to 2^-11 relative: x
-// then ping-pongs across f16 rounding boundaries and runs to max_iters.
-// ADOCH: fresh products of the state itself each iteration:
-//   D1[r][i] = sum_j Xh[r][j] Q[i][j]   kind::f16, Xh = f16(x / lambda_r)
-//   D2[r][i] = sum_j S8[r][j] Q8[i][j]  kind::i8,  S8 = sign(x) in int8, Q8 = Q in int8 (exact, s32 acc)
+// (doch.py:220) after the reference's number of iterations. (Round 1 fed f16(x)
+// itself to the tensor cores: the product was then good to 2^-11 relative only,
+// x ping-ponged across f16 rounding boundaries and ran to max_iters.) ADOCH's
+// economy extrapolation needs x_p - x_{p-1} = lambda Dh_p and
+// (J + aI)(x_p - x_{p-1}) = a lambda Dh_p + jscale lambda F_p: both come with the delta.
 // One persistent cooperative kernel runs all iterations: a 4-stage TMA ->
 // tcgen05.mma pipeline per 128x128 tile (fp32 / s32 accumulators in TMEM;
 // CTA pairs with cta_group::2 when R % 256 == 0), a TMEM -> register epilogue
@@ -75,16 +74,13 @@ struct Pipe {
   static constexpr int STAGES = int(196608 / STAGE) < MAX_STAGES ? int(196608 / STAGE) : MAX_STAGES;  // 192 KB
   static constexpr uint32_t TILES = STAGES * STAGE;
 };
-// DOCH: the product buffers [0,128) / [128,256) f32 alternate by iteration parity between the
+// The product buffers [0,128) / [128,256) f32 alternate by iteration parity between the
 // fresh product F_p = Q Dh_p and the running product R_{p-1} = Q s_{p-1} (the epilogue writes
-// R_p = R_{p-1} + F_p over F_p), D2 = Q sign(s) [256,384) s32, the scaled state s = x / lambda
-// [384,512) f32. ADOCH: D1 [0,128) / [384,512) by iteration parity, D2 [128,256), master x
-// [256,384); Ay_p is parked in the D2 columns.
+// R_p = R_{p-1} + F_p over F_p; ADOCH then parks Ay_p over R_{p-1}), D2 = Q sign(s)
+// [256,384) s32, the scaled state s = x / lambda [384,512) f32.
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t XCOL = 256;
 constexpr uint32_t SCOL = 384;
-constexpr uint32_t D2DOCH = 256;
-__host__ __device__ constexpr uint32_t d1col(int p) { return (p & 1) ? 384u : 0u; }
+constexpr uint32_t D2COL = 256;
 __host__ __device__ constexpr uint32_t rcol(int p) { return (p & 1) ? 128u : 0u; }
 
 // Per replica-tile group: the tiles_n CTAs that share one replica tile are
@@ -110,7 +106,6 @@ struct Args {
   CUtensorMap tmS[2];   // S8 by parity (int8)
   CUtensorMap tmQ8;     // Q (int8)
   float* xm[2];
-  float* axm;  // ADOCH: (J + aI) x of the last iteration of a launch, for the next launch's extrapolation
   // DOCH delta operands (see the kernel comment): the running accumulators and the tracked
   // state, persisted between launches of one solve
   float* d1g;       // R = Q s               [Rpad][npad]
@@ -390,7 +385,7 @@ struct __align__(8) Smem {
 // Warp roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM
 // owner), warps 2-3 idle, warps 4-11 = epilogue + control. Epilogue warp w
 // reads TMEM lane quadrant (w % 4) and spin-column half (w - 4) / 4; the
-// CTA's 128 x 128 f32 master state lives in TMEM columns [XCOL, XCOL + 128).
+// CTA's 128 x 128 f32 scaled state s = x / lambda lives in TMEM columns [SCOL, SCOL + 128).
 // AD: ADOCH with the economy window (dc/solvers/doch.py:248-356) instead of DOCH
 template <int NC, int TN, bool AD>
 __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_constant__ Args a) {
@@ -474,11 +469,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const uint32_t idesc = idesc_f16(NC * TM, TN), idesc8 = idesc_i8(NC * TM, TN);
-  // the CTA's f32 states live in TMEM for the whole run: ADOCH x in [XCOL, XCOL + 128),
-  // DOCH s = x / lambda in [SCOL, SCOL + 128)
+  // the CTA's f32 states s = x / lambda live in TMEM [SCOL, SCOL + 128) for the whole run
   const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16) + h * HW;  // this thread's row, column 0 of its half
-  const uint32_t xaddr = lane_base + (AD ? XCOL : SCOL);
-  const uint32_t d2addr = lane_base + (AD ? uint32_t(TN) : D2DOCH);
+  const uint32_t xaddr = lane_base + SCOL;
+  const uint32_t d2addr = lane_base + D2COL;
   // one row segment of HW values from global into TMEM columns (zeros for padding replicas)
   auto load_cols = [&](uint32_t taddr, const uint32_t* src) {
     uint32_t v[32];
@@ -491,21 +485,17 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   };
   if (epi) {
     const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
-    if constexpr (AD) {
-      load_cols(xaddr, reinterpret_cast<const uint32_t*>(a.xm[p & 1] + o));
-    } else {  // s_p, R_{p-1} and D2 = Q sign(s_{p-1}) of the previous launch (p = 0: s_0, zeros)
-      load_cols(xaddr, reinterpret_cast<const uint32_t*>(a.xhatg + o));
-      load_cols(lane_base + rcol(p - 1), reinterpret_cast<const uint32_t*>(a.d1g + o));
-      load_cols(d2addr, reinterpret_cast<const uint32_t*>(a.d2g + o));
-    }
+    // s_p, R_{p-1} and D2 = Q sign(s_{p-1}) of the previous launch (p = 0: s_0, zeros)
+    load_cols(xaddr, reinterpret_cast<const uint32_t*>(a.xhatg + o));
+    load_cols(lane_base + rcol(p - 1), reinterpret_cast<const uint32_t*>(a.d1g + o));
+    load_cols(d2addr, reinterpret_cast<const uint32_t*>(a.d2g + o));
     tmem_st_wait();
   }
-  if constexpr (!AD) {  // the restored accumulators are in TMEM before the (pair leader's) first MMA adds to them
-    tc_fence_before();
-    __syncthreads();
-    if constexpr (NC == 2) cluster_sync_all();
-    tc_fence_after();
-  }
+  // the restored accumulators are in TMEM before the (pair leader's) first MMA adds to them
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (NC == 2) cluster_sync_all();
+  tc_fence_after();
   RunCfg cfg = a.cfg;
   if (nt != 0) cfg.hist = nullptr;  // only the nt == 0 CTA of a replica tile writes history
 
@@ -659,13 +649,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             if (kb < KB1) {
 #pragma unroll
               for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
-                mma_f16_g<NC>(tmem + (AD ? d1col(p) : rcol(p)), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32),
-                              idesc, (kb | q | k) ? 1u : 0u);  // DOCH: F_p = Q Dh_p
+                mma_f16_g<NC>(tmem + rcol(p), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
+                              (kb | q | k) ? 1u : 0u);  // F_p = Q Dh_p
             } else {
 #pragma unroll
               for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
-                mma_i8_g<NC>(tmem + (AD ? uint32_t(TN) : D2DOCH), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8,
-                             (!AD || ((kb - KB1) | q | k)) ? 1u : 0u);  // DOCH: D2 += Q dS
+                mma_i8_g<NC>(tmem + D2COL, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8, 1u);  // D2 += Q dS
             }
           }
           mma_commit_g<NC>(smem_u32(&sm.empty[s]), uint16_t(!a.mc ? 0x3 : (psub == 0 ? 0x3 : 0xF)));
@@ -748,21 +737,25 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     };
     if (threadIdx.x == 128) sm.tdbg[4] = sm.tdbg[5] = sm.tdbg[6] = sm.tdbg[7] = 0;
     // ------------------------------------------------------------------ ADOCH
-    // Iteration p: (1) from GEMM1(p) = J x_p (TMEM, by parity), GEMM1(p-1) = J x_{p-1}
-    // (the other D1 buffer, still intact: GEMM1(p+1) waits for this iteration's operand
-    // flags) and x_{p-1} (global, stored by iteration p-1): Ax_p, the economy
-    // extrapolation y_p = x_p + c_p (x_p - x_{p-1}), Ay_p = Ax_p + c_p (Ax_p - Ax_{p-1})
-    // (doch.py:299-301), the partials of H(x_p), E(sign x_p) (GEMM2), H(y_p) and
-    // |x_p - x_{p-1}|; Ay_p is parked in the D2 columns, already read; (2) group
-    // barrier B(p) and the control of p (control_after_pass + adoch_decide, the same
-    // device code as the multipass path): stop decisions and the window test;
-    // (3) x_{p+1} = cbrt(v / beta), v = Ay_p if accepted else Ax_p (doch.py:313-318),
-    // and the operands of x_{p+1}.
+    // The DOCH kernel's state and products (x_p = lambda s_p, R_p = R_{p-1} + F_p with
+    // F_p = Q Dh_p, D2 = Q sign(s_p)); iteration p:
+    // (1) R_p; Ax_p = a x_p + jl R_p; the economy extrapolation (doch.py:299-301) from the
+    //     change of the state, which the delta product already holds:
+    //       x_p - x_{p-1} = lambda Dh_p (the f16 operand of GEMM1(p), read back from global),
+    //       Ax_p - Ax_{p-1} = a lambda Dh_p + jl F_p,
+    //     y_p = x_p + c_p (x_p - x_{p-1}), Ay_p = Ax_p + c_p (Ax_p - Ax_{p-1}); the partials of
+    //     H(x_p), E(sign x_p), H(y_p) and |x_p - x_{p-1}|; Ay_p is parked over R_{p-1}
+    //     (read; GEMM1(p+1) writes F_{p+1} there only after this iteration's flags);
+    // (2) group barrier B(p) and the control of p (control_after_pass + adoch_decide, the
+    //     same device code as the multipass path): stop decisions and the window test;
+    // (3) x_{p+1} = cbrt(v / beta), v = Ay_p if accepted else Ax_p (doch.py:313-318), the
+    //     delta Dh_{p+1} = f16(x_{p+1} / lambda - s_p), s_{p+1} = s_p + Dh_{p+1}, and the
+    //     operands of iteration p+1.
     auto ad_iteration = [&](const int pk) {
       const int cur = pk & 1;
       const RepCtl& c0 = sm.ctl[rl];
-      const bool live0 = valid && c0.status == DCX_STOP_RUNNING;
       const float alpha = sm.alpha[rl], inv_beta = sm.inv_beta[rl], jl = sm.jl[rl], inv_lam = sm.inv_lam[rl];
+      const float lamf = sm.lam[rl];
       const float cmf = float(c0.cm[pk & 1]);
       const bool has_prev = pk > 0;
       const int gbase = i0 + h * HW;
@@ -780,81 +773,60 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }
         store_pm1(a.best8 + (int64_t)r * a.npad + gbase, w, HW / 4);
       }
-      const float* xpg = a.xm[cur ^ 1] + (int64_t)r * a.npad + gbase;  // x_{p-1}
-      float* xcg = a.xm[cur] + (int64_t)r * a.npad + gbase;           // x_p, for iteration p+1
+      const __half* dhg = a.xh[cur] + (int64_t)r * a.npad + gbase;  // Dh_p (GEMM1(p)'s operand)
       mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
       tc_fence_after();
       float s4 = 0.f, sxax = 0.f, sy4 = 0.f, syay = 0.f, step = 0.f;
       int es = 0;
       uint64_t curmask = 0;
-      const uint32_t lb = tmem + (uint32_t(q * 32) << 16);
 #pragma unroll 1
       for (int off = 0; off < HW; off += 16) {
-        uint32_t xv[16], d1[16], d1p[16], d2[16];
-        float xp[16];
-        // the first iteration of a resumed launch has no GEMM1(p-1) in TMEM: (J + aI) x_{p-1}
-        // comes from axm, stored by the previous launch's last iteration
-        const bool resumed = has_prev && pk == p_start;
-        tmem_ld16(xaddr + off, xv);
-        tmem_ld16(lb + d1col(pk) + h * HW + off, d1);
-        tmem_ld16(lb + TN + h * HW + off, d2);
-        if (has_prev && !resumed) tmem_ld16(lb + d1col(pk + 1) + h * HW + off, d1p);
-        if (resumed) {
-          const float* ag = a.axm + (int64_t)r * a.npad + gbase + off;
+        uint32_t fv[16], rv[16], st[16], d2[16], ayv[16];
+        tmem_ld16(lane_base + rcol(pk) + off, fv);
+        tmem_ld16(lane_base + rcol(pk + 1) + off, rv);
+        tmem_ld16(xaddr + off, st);
+        tmem_ld16(d2addr + off, d2);
+        __align__(16) __half dh[16];
+        if (has_prev && lim > 0) {
+          *reinterpret_cast<uint4*>(dh) = *reinterpret_cast<const uint4*>(dhg + off);
+          *reinterpret_cast<uint4*>(dh + 8) = *reinterpret_cast<const uint4*>(dhg + off + 8);
+        } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) d1p[j] = __float_as_uint(lim > 0 ? ag[j] : 0.f);
-        }
-#pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          const float4 v4 = (has_prev && lim > 0) ? *reinterpret_cast<const float4*>(xpg + off + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-          xp[j] = v4.x;
-          xp[j + 1] = v4.y;
-          xp[j + 2] = v4.z;
-          xp[j + 3] = v4.w;
+          for (int j = 0; j < 16; ++j) dh[j] = __float2half_rn(0.f);
         }
         tmem_ld_wait();
-        uint32_t ayv[16];
         uint32_t m = 0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float x = __uint_as_float(xv[j]);
-          const float ax = fmaf(alpha, x, jl * __uint_as_float(d1[j]));
+          const float f = __uint_as_float(fv[j]);
+          const float rr = __fadd_rn(__uint_as_float(rv[j]), f);
+          rv[j] = __float_as_uint(rr);
+          const float x = lamf * __uint_as_float(st[j]);
+          const float ax = fmaf(alpha, x, jl * rr);
           const float x2 = x * x;
           s4 = fmaf(x2, x2, s4);
           sxax = fmaf(x, ax, sxax);
-          const uint32_t neg = xv[j] >> 31;
+          const uint32_t neg = st[j] >> 31;
           m |= neg << j;
           const int mm = -int(neg);
           const int v = (off + j < lim) ? int(d2[j]) : 0;
           es += (v ^ mm) - mm;
           float ay = ax;
           if (has_prev) {
-            const float axp = resumed ? __uint_as_float(d1p[j]) : fmaf(alpha, xp[j], jl * __uint_as_float(d1p[j]));
-            const float y = extrap(x, xp[j], cmf);
-            ay = extrap(ax, axp, cmf);
+            const float dx = lamf * __half2float(dh[j]);  // x_p - x_{p-1}
+            const float y = add_rn(x, mul_rn(cmf, dx));
+            ay = add_rn(ax, mul_rn(cmf, fmaf(alpha, dx, jl * f)));
             const float y2 = mul_rn(y, y);
             sy4 = fmaf(y2, y2, sy4);
             syay = fmaf(y, ay, syay);
-            step = fmaxf(step, fabsf(x - xp[j]));
+            step = fmaxf(step, fabsf(dx));
           }
           ayv[j] = __float_as_uint(ay);
-          d1[j] = __float_as_uint(ax);
-        }
-        if (pk == a.p_end - 1 && lim > 0) {  // a later launch resumes at p + 1
-          float* ag = a.axm + (int64_t)r * a.npad + gbase + off;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) ag[j] = __uint_as_float(d1[j]);
         }
         curmask |= uint64_t(m) << off;
-        if (has_prev) tmem_st16(lb + TN + h * HW + off, ayv);  // Ay_p over the drained D2 columns
-        if (live0 && lim > 0) {
-#pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(xcg + off + j) =
-                make_float4(__uint_as_float(xv[j]), __uint_as_float(xv[j + 1]), __uint_as_float(xv[j + 2]),
-                            __uint_as_float(xv[j + 3]));
-        }
+        tmem_st16(lane_base + rcol(pk) + off, rv);                 // R_p
+        if (has_prev) tmem_st16(lane_base + rcol(pk + 1) + off, ayv);  // Ay_p over R_{p-1}
       }
       if (lim == 0) s4 = sxax = sy4 = syay = step = 0.f, es = 0;
       sm.red[h][rl][0] = s4;
@@ -915,7 +887,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }
       }
       epi_sync();
-      // ---- update: x_{p+1} from Ay_p (accepted) or Ax_p
+      // ---- update: x_{p+1} from Ay_p (accepted) or Ax_p, as a delta of the state
       const RepCtl& c1 = sm.ctl[rl];
       const bool running = valid && c1.status == DCX_STOP_RUNNING;
       const bool use_y = has_prev && c1.accept;
@@ -923,32 +895,38 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
 #pragma unroll 1
       for (int off = 0; off < HW; off += 16) {
-        uint32_t xv[16], d1[16], ayv[16];
-        tmem_ld16(xaddr + off, xv);
-        tmem_ld16(lb + d1col(pk) + h * HW + off, d1);
-        tmem_ld16(lb + TN + h * HW + off, ayv);
+        uint32_t rv[16], st[16], ayv[16];
+        tmem_ld16(lane_base + rcol(pk) + off, rv);
+        tmem_ld16(xaddr + off, st);
+        tmem_ld16(lane_base + rcol(pk + 1) + off, ayv);
         tmem_ld_wait();
         __align__(16) __half2 hv[8];
         __align__(16) uint32_t sv[4];
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
-          float nx[2];
+          __half d[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const float x = __uint_as_float(xv[j + u]);
-            const float v = use_y ? __uint_as_float(ayv[j + u]) : fmaf(alpha, x, jl * __uint_as_float(d1[j + u]));
-            nx[u] = cbrt_lean(v * inv_beta);
-            xv[j + u] = running ? __float_as_uint(nx[u]) : xv[j + u];
+            const float sc = __uint_as_float(st[j + u]);
+            const float x = lamf * sc;
+            const float v = use_y ? __uint_as_float(ayv[j + u]) : fmaf(alpha, x, jl * __uint_as_float(rv[j + u]));
+            const float nx = cbrt_lean(v * inv_beta);
+            d[u] = __float2half_rn(running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f);
+            st[j + u] = __float_as_uint(__fadd_rn(sc, __half2float(d[u])));
           }
-          hv[j / 2] = __floats2half2_rn(nx[0] * inv_lam, nx[1] * inv_lam);
-          if ((j & 3) == 2) {
-            const uint32_t t = (xv[j - 2] >> 31) | ((xv[j - 1] >> 31) << 8) | ((__float_as_uint(nx[0]) >> 31) << 16) |
-                               ((__float_as_uint(nx[1]) >> 31) << 24);
-            sv[j / 4] = 0x01010101u + t * 0xfeu;
+          hv[j / 2] = __halves2half2(d[0], d[1]);
+          if ((j & 3) == 2) {  // sign(x_{p+1}) - sign(x_p) per byte (see the DOCH update)
+            const uint32_t ob = uint32_t(curmask >> (off + j - 2)) & 0xFu;
+            const uint32_t nb = (st[j - 2] >> 31) | ((st[j - 1] >> 31) << 1) | ((st[j] >> 31) << 2) |
+                                ((st[j + 1] >> 31) << 3);
+            const uint32_t df = ob ^ nb, neg = df & nb;
+            const uint32_t dfw = (df & 1u) | ((df & 2u) << 7) | ((df & 4u) << 14) | ((df & 8u) << 21);
+            const uint32_t ngw = (neg & 1u) | ((neg & 2u) << 7) | ((neg & 4u) << 14) | ((neg & 8u) << 21);
+            sv[j / 4] = dfw * 2u + ngw * 0xfcu;
           }
         }
-        tmem_st16(xaddr + off, xv);
-        if (running && lim > 0) {
+        tmem_st16(xaddr + off, st);
+        if (valid && lim > 0) {  // stopped replicas write zero deltas
           *reinterpret_cast<uint4*>(hn + off) = *reinterpret_cast<uint4*>(hv);
           *reinterpret_cast<uint4*>(hn + off + 8) = *reinterpret_cast<uint4*>(hv + 4);
           *reinterpret_cast<uint4*>(sn + off) = *reinterpret_cast<uint4*>(sv);
@@ -957,14 +935,14 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(smem_u32(&sm.d1free));  // D1 read: GEMM1(p+1) may overwrite it
-        mbar_arrive(smem_u32(&sm.d2free));  // Ay_p read: GEMM2(p+1) may overwrite the D2 columns
+        mbar_arrive(smem_u32(&sm.d1free));  // R_p and Ay_p read: GEMM1(p+1) may write F_{p+1}
+        mbar_arrive(smem_u32(&sm.d2free));  // D2 read: GEMM2(p+1) may add to it
       }
       tmem_st_wait();
       fence_async_global();
       epi_sync();
       if (threadIdx.x == 128) st_release(my_flag, unsigned(pk + 1));
-      prevmask = curmask;
+      if (valid) prevmask = curmask;  // sign(x_p)
     };
     for (; p < a.p_end; ++p) {
       if constexpr (AD) {
@@ -1178,36 +1156,25 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   // ---------------------------------------------------------------- teardown
   if (epi) {
     // the run's final (or frozen) states; a time-budget stop at p was persisted above
-    // DOCH: a time-budget stop at p persisted x_p above. ADOCH: the master state is x_p of
-    // the replica's last iteration; a replica still running keeps x_{p-1} in the other
-    // buffer for the extrapolation of the next launch
+    // x = lambda s of the replica's last iterate (stopped replicas keep theirs); a DOCH
+    // time-budget stop at p persisted x_p in the loop (the DOCH update of p runs before
+    // control p sees the clock, the ADOCH update after it)
     const bool budget_stop = !AD && sm.ctl[rl].status == DCX_STOP_TIME_BUDGET;
-    const bool keep_prev = AD && sm.ctl[rl].status == DCX_STOP_RUNNING;
-    float* d0 = a.xm[0] + (int64_t)r * a.npad + i0 + h * HW;
-    float* d1 = a.xm[1] + (int64_t)r * a.npad + i0 + h * HW;
+    const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
     const int lim = max(0, min(HW, a.n - (i0 + h * HW)));
     uint32_t v[64];
     tmem_ld32(xaddr, v);
     tmem_ldw<W1>(xaddr + 32, v + 32);
     tmem_ld_wait();
-    if constexpr (!AD) {
-      const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
-      if (valid)  // s, for a later launch of this solve
+    if (valid)  // s, for a later launch of this solve
 #pragma unroll
-        for (int j = 0; j < HW; j += 4)
-          *reinterpret_cast<uint4*>(a.xhatg + o + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      const float lamf = sm.lam[rl];
-#pragma unroll
-      for (int j = 0; j < HW; ++j) v[j] = __float_as_uint(lamf * __uint_as_float(v[j]));  // x = lambda s
-    }
+      for (int j = 0; j < HW; j += 4)
+        *reinterpret_cast<uint4*>(a.xhatg + o + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    const float lamf = sm.lam[rl];
     if (valid && !budget_stop)
 #pragma unroll
       for (int j = 0; j < HW; ++j)
-        if (j < lim) {
-          if (!keep_prev || (p & 1) == 0) d0[j] = __uint_as_float(v[j]);
-          if (!keep_prev || (p & 1) == 1) d1[j] = __uint_as_float(v[j]);
-        }
-    const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
+        if (j < lim) a.xm[0][o + j] = a.xm[1][o + j] = lamf * __uint_as_float(v[j]);
     if (valid) {
       // sign(x_{p-1}): the pending best copy of the last pass (unpack_results) and the
       // prevmask of a resumed launch
@@ -1215,19 +1182,18 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll 1
       for (int j = 0; j < HW; ++j) sg[j] = ((prevmask >> j) & 1) ? int8_t(-1) : int8_t(1);
     }
-    if constexpr (!AD) {  // the running products, for a later launch of this solve
-      auto save_cols = [&](uint32_t taddr, uint32_t* dst) {
-        uint32_t w[64];
-        tmem_ld32(taddr, w);
-        tmem_ldw<W1>(taddr + 32, w + 32);
-        tmem_ld_wait();
-        if (valid)
+    // the running products, for a later launch of this solve
+    auto save_cols = [&](uint32_t taddr, uint32_t* dst) {
+      uint32_t w[64];
+      tmem_ld32(taddr, w);
+      tmem_ldw<W1>(taddr + 32, w + 32);
+      tmem_ld_wait();
+      if (valid)
 #pragma unroll
-          for (int j = 0; j < HW; j += 4) *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
-      };
-      save_cols(lane_base + rcol(p - 1), reinterpret_cast<uint32_t*>(a.d1g + o));  // R of the last iteration
-      save_cols(d2addr, reinterpret_cast<uint32_t*>(a.d2g + o));
-    }
+        for (int j = 0; j < HW; j += 4) *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
+    };
+    save_cols(lane_base + rcol(p - 1), reinterpret_cast<uint32_t*>(a.d1g + o));  // R of the last iteration
+    save_cols(d2addr, reinterpret_cast<uint32_t*>(a.d2g + o));
   }
   // all CTAs of the group read p_exec before the first barrier and exit at the same p
   if (nt == 0 && threadIdx.x == 0) {
@@ -1376,8 +1342,6 @@ void DenseDev::release_run() {
   xhat = d1g = d2g = nullptr;
   if (part) cudaFree(part);
   if (sync) cudaFree(sync);
-  if (axm) cudaFree(axm);
-  axm = nullptr;
   best8 = nullptr;
   part = nullptr;
   sync = nullptr;
@@ -1521,7 +1485,6 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   DCK(cudaMemsetAsync(d.xhat, 0, vec * 4, s));  // padding; pack_state writes the live entries
   DCK(cudaMemsetAsync(d.d1g, 0, vec * 4, s));
   DCK(cudaMemsetAsync(d.d2g, 0, vec * 4, s));
-  if (d.ad && !d.axm) DCK(cudaMalloc(&d.axm, vec * 4));
   {
     const int gsz = 128 * d.nc;
     const int ngroups = d.Rpad / gsz;
@@ -1583,7 +1546,6 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.xhatg = reinterpret_cast<float*>(d.xhat);
   a.d1g = reinterpret_cast<float*>(d.d1g);
   a.d2g = reinterpret_cast<int*>(d.d2g);
-  a.axm = reinterpret_cast<float*>(d.axm);
   a.part = d.part;
   a.ctl = m.args.ctl;
   a.g = m.args.g;

@@ -20,7 +20,6 @@ struct DenseDev {
   int nc = 1;  // CTAs per MMA (2: cta_group::2 pairs)
   int tn = 128, tiles_n = 0;
   bool ad = false;         // ADOCH (economy window) kernel
-  void* axm = nullptr;     // ADOCH: (J + aI) x at launch ends [Rpad][npad] f32  // spin tile width (UMMA N: 128 or 112) and spin tiles per replica tile
   void* xm[2] = {nullptr, nullptr};  // f32 master states [Rpad][npad]
   void* xh[2] = {nullptr, nullptr};  // f16 MMA operand A [Rpad][npad]: DOCH the delta Dh, ADOCH x / lambda_r
   void* s8[2] = {nullptr, nullptr};  // int8 energy GEMM operand A [Rpad][npad]: DOCH dS, ADOCH sign(x)

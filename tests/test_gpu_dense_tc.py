@@ -100,7 +100,7 @@ def test_tc_padding_ragged_sizes():
     np.testing.assert_array_equal(dc.energies(J, np.stack([r.spins for r in full])), [r.energy for r in full])
 
 
-def k2_quality_gate(res, gk2, solver):
+def k2_quality_gate(res, gk2, solver, stops=True):
     """SURVEY.md §8c G-quality on BASELINE configs[1], against the unmodified reference on
     the SAME 1024 seeds (tests/golden/golden_k2.npz):
       * stop reasons: the reference converges (step <= 1e-10, doch.py:220) on 1022 / 1024
@@ -124,9 +124,10 @@ def k2_quality_gate(res, gk2, solver):
     conv = np.array([r.stop_reason == "converged" for r in res])
     R = len(ref_e)
     assert len(res) == R
-    assert conv.sum() >= (ref_st == 0).sum() - 0.02 * R, (conv.sum(), (ref_st == 0).sum())
-    se_it = np.sqrt(it.var(ddof=1) / R + ref_it.var(ddof=1) / R)
-    assert abs(it.mean() - ref_it.mean()) <= 4 * se_it, (it.mean(), ref_it.mean(), se_it)
+    if stops:
+        assert conv.sum() >= (ref_st == 0).sum() - 0.02 * R, (conv.sum(), (ref_st == 0).sum())
+        se_it = np.sqrt(it.var(ddof=1) / R + ref_it.var(ddof=1) / R)
+        assert abs(it.mean() - ref_it.mean()) <= 4 * se_it, (it.mean(), ref_it.mean(), se_it)
     assert mannwhitneyu(e, ref_e, alternative="greater").pvalue >= 1e-3
     assert e.mean() <= ref_e.mean() + 3 * ref_e.std(ddof=1) / np.sqrt(R), (e.mean(), ref_e.mean())
     assert e.min() <= np.sort(ref_e)[2], (e.min(), np.sort(ref_e)[:3])
@@ -226,37 +227,68 @@ def test_tc_adoch_first_iterates_track_f32(gold):
         assert agree >= len(tc) - 2  # a window test may resolve a near-tie differently at f16 operands
 
 
-def test_tc_adoch_resumed_launches_equal_one_launch(gold):
-    """A run split into launches of 7 iterations (the extrapolation of each resumed
-    launch reads (J + aI)x_{p-1} from global memory instead of TMEM) is bit-identical
-    to one launch."""
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+def test_tc_resumed_launches_equal_one_launch(gold, solver):
+    """A run split into launches of 7 iterations (each resumed launch restores the scaled
+    state, the running product R and the sign product D2 from global memory into TMEM) is
+    bit-identical to one launch."""
     g = gold["k2"]
     inst = k2_instance()
     X0 = x0s(2000, g["alpha"], g["beta"], range(256))
-    one = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=40, precision="f16tc")
-    chunked = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=40, precision="f16tc", chunk=7)
+    one = dc.solve_replicas(inst, solver, g["alpha"], g["beta"], X0, max_iters=40, precision="f16tc")
+    chunked = dc.solve_replicas(inst, solver, g["alpha"], g["beta"], X0, max_iters=40, precision="f16tc", chunk=7)
     for a, b in zip(one, chunked):
         assert a.iterations == b.iterations and a.stop_reason == b.stop_reason
         assert a.energy == b.energy and a.accepted == b.accepted
         assert np.array_equal(a.x, b.x)
         assert np.array_equal(a.spins, b.spins)
+        assert [t.energy for t in a.trace] == [t.energy for t in b.trace]
 
 
-def test_tc_adoch_quality(gold):
-    """1024 ADOCH replicas on the tensor cores: energies exact for the returned spins and a
-    distribution no worse than the reference's ADOCH runs on the same instance (32 seeds)."""
-    g = gold["k2"]
+def test_tc_adoch_k2000_quality_vs_reference_1024_seeds(gk2):
+    """BASELINE configs[1] with ADOCH (economy window, q = 5): the reference's energy
+    distribution on the same 1024 seeds; energies exact for the returned spins; the accept
+    log has one entry per iteration.
+
+    Stop reasons are NOT the reference's at this precision: ADOCH's Nesterov momentum
+    amplifies the state's rounding noise by about 1 / (1 - c_k) ~ k / 3, so the absolute
+    1e-10 step test needs an f64 state and product (numpy emulations of the exact update
+    rule on seeds 0-4: f64 state + f64 product + f64 evaluation converge in 150-362
+    iterations; f32 state or f32 product never converge, with or without f16 operands).
+    The tensor-core run goes to max_iters; the f64 path keeps the reference's stop
+    reasons (test_k2000_f64_matches_reference_seeds below)."""
     inst = k2_instance()
-    X0 = x0s(2000, g["alpha"], g["beta"], range(1024))
-    res = dc.solve_replicas(inst, "adoch", g["alpha"], g["beta"], X0, max_iters=1000, precision="f16tc")
-    e = np.array([r.energy for r in res])
-    ref = np.array([row["energy"] for row in g["adoch"]])
-    se = ref.std() / np.sqrt(len(ref))
-    assert e[:32].mean() <= ref.mean() + 3 * se
-    assert e.mean() <= ref.mean() + 3 * se
+    X0 = x0s(2000, gk2["alpha"], gk2["beta"], range(1024))
+    res = dc.solve_replicas(inst, "adoch", gk2["alpha"], gk2["beta"], X0, max_iters=1000, precision="f16tc")
+    assert res[0].path == "dense_tc"
+    k2_quality_gate(res, gk2, "adoch", stops=False)
     for r in res[:16]:
         assert dc.energy(inst.coupling, r.spins) == r.energy
         assert r.accepted[0] is True and len(r.accepted) == r.iterations  # as assemble_results builds it for every path
+
+
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+def test_k2000_f64_matches_reference_seeds(gk2, solver):
+    """G-fp64 on BASELINE configs[1]: the f64 path (the dense coupling as exact CSR, the
+    multipass kernels) reproduces the unmodified reference's per-seed stop reason, best
+    energy and (DOCH) iteration count on K2000 seeds 0..7 (tests/golden/golden_k2.npz)."""
+    A = gk2["arrays"]
+    inst = k2_instance()
+    seeds = range(8)
+    X0 = x0s(2000, gk2["alpha"], gk2["beta"], seeds)
+    res = dc.solve_replicas(inst, solver, gk2["alpha"], gk2["beta"], X0, max_iters=1000, precision="f64")
+    stop_name = {0: "converged", 1: "max_iters", 2: "time_budget"}
+    diffs = []
+    for s_, r in zip(seeds, res):
+        assert r.stop_reason == stop_name[int(A[f"{solver}_stop"][s_])]
+        assert r.energy == A[f"{solver}_energy"][s_]
+        diffs.append(r.iterations - int(A[f"{solver}_iterations"][s_]))
+    # ADOCH: the window test H(y) <= max(window) flips on last-bit H differences, which moves
+    # the convergence point by a few iterations (SURVEY.md §8c G-fp64: "iterations within a band")
+    if solver == "doch":
+        assert diffs == [0] * len(diffs), diffs
+    else:
+        assert max(abs(d) for d in diffs) <= 25, diffs
 
 
 @pytest.mark.parametrize("solver", ["doch", "adoch"])
