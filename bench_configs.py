@@ -37,6 +37,15 @@ def _peaks():
     return peaks()
 
 
+def _cuda_count():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        return 0
+
+
 def _instance(name):
     import paper_2509_01928_b200 as dc
     from paper_2509_01928_b200 import synth
@@ -52,7 +61,9 @@ def _instance(name):
         return dc.ProblemInstance(coupling=J), 4.0, 8.0e9, (v, c, o)
     if name in ("e7", "r8"):
         n = 10**7 if name == "e7" else 10**8
-        v, c, o, co = synth.erdos_renyi(n, 8, seed=0) if name == "e7" else synth.random_regular3(n, seed=0)
+        dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, _cuda_count()) if _cuda_count() else None
+        v, c, o, co = (synth.erdos_renyi(n, 8, seed=0, device=dev) if name == "e7"
+                       else synth.random_regular3(n, seed=0, device=dev))
         J = dc.CsrCoupling(n, v, c, o, validate=False)
         # Wigner estimate (n >= 1e4) of dc/spectral.py:175-189 at eta = 1
         s1, s2 = float(v.sum()), float((v * v).sum())

@@ -486,7 +486,9 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     c->nnz = nnz;
     c->rp.alloc((n + 1) * 4);
     CK(cudaMemcpy(c->rp.p, rp32.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
-    c->col.alloc(std::max<int64_t>(nnz, 1) * 4);
+    // 16 zero entries of padding: the R = 1 entry-parallel pass reads whole 16-byte vectors
+    c->col.alloc((nnz + 16) * 4);
+    CK(cudaMemset(static_cast<char*>(c->col.p) + nnz * 4, 0, 64));
     if (nnz) CK(cudaMemcpy(c->col.p, c32.data(), nnz * 4, cudaMemcpyHostToDevice));
     c->col16.release();
     if (n_cols <= 65536 && n == n_cols && nnz) {
@@ -509,7 +511,8 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
         const int q = int(std::nearbyint(v[e] / scale));
         if (b == 1) q8[e] = int8_t(q); else q16[e] = int16_t(q);
       }
-      c->vint.alloc(nnz * b);
+      c->vint.alloc((nnz + 16) * b);
+      CK(cudaMemset(static_cast<char*>(c->vint.p) + nnz * b, 0, 16 * b));
       CK(cudaMemcpy(c->vint.p, b == 1 ? (void*)q8.data() : (void*)q16.data(), nnz * b, cudaMemcpyHostToDevice));
     } else if (vk != VK_UNIFORM) {
       c->v64.alloc(nnz * 8);

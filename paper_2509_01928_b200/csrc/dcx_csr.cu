@@ -145,6 +145,154 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// R = 1, f32, integer couplings (UNIFORM / I8): entry-parallel pass. A warp owns
+// 32 consecutive rows (one per lane) and walks their contiguous CSR entries in
+// rounds of 32 x EPL: every lane loads EPL consecutive column indices with
+// 16-byte vector loads (coalesced across the warp) and issues all EPL gathers of
+// x before the first one is consumed, so a lane keeps EPL random loads in flight
+// (the degree-8 graphs of E7 / R8 are bound by the L1 wavefronts of these
+// gathers: one 32-byte sector per 4-byte load). The gathered values go to a
+// per-warp shared-memory tile, entry k of lane l at k * 33 + l (each store
+// instruction writes 32 consecutive words; the rows' reads below spread over the
+// banks by the pad), then every lane sums ITS row's entries in column order (f32
+// FMA, the order of the V = 1 kernel) with the exact integer spin-energy
+// accumulator, and runs the shared row epilogue. Rows longer than a round
+// continue into the next one.
+constexpr int R1W_EPL = 12;                    // entries per lane per round
+constexpr int R1W_ROUND = 32 * R1W_EPL;        // 384 entries per warp per round
+constexpr int R1W_SLOT = R1W_EPL * 33;
+// shared-memory slot of the round's entry e_rel = R1W_EPL * lane + k
+__device__ __forceinline__ int r1w_pos(int e_rel) {
+  const int l = e_rel / R1W_EPL;
+  return (e_rel - l * R1W_EPL) * 33 + l;
+}
+
+template <int VK, int MODE>
+__global__ void __launch_bounds__(256) pass_r1w(PassArgs a) {
+  using T = float;
+  static_assert(VK == VK_UNIFORM || VK == VK_I8, "integer couplings");
+  if (!a.g->live) return;
+  const int p = a.g->p;
+  if (MODE == MODE_ADOCH_Y && p == 0) return;  // no extrapolation at k = 0
+  const RowCtl<T> c = row_ctl<T>(a.ctl[0], p);
+  const bool running = c.running;
+  if (!running && !(MODE == MODE_DOCH && c.pend == p - 1)) return;
+  __shared__ float sx[8][R1W_SLOT];
+  __shared__ int8_t sq[VK == VK_I8 ? 8 : 1][VK == VK_I8 ? R1W_SLOT : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const T* xc = reinterpret_cast<const T*>(a.gx[p & 1]);
+  const T* xp = reinterpret_cast<const T*>(a.gx[(p + 1) & 1]);
+  const T cm = c.cm;
+  const T scale = T(a.scale);
+  const int64_t n = a.cfg.n;
+  const int32_t* colp = a.col;
+  const int8_t* valp = reinterpret_cast<const int8_t*>(a.val);
+  float* my = sx[warp];
+  RowOut<T, MODE> o;
+  for (int64_t i0 = gw * 32; i0 < n; i0 += nwarps * 32) {
+    const int64_t i = i0 + lane;
+    const bool ok = i < n;
+    uint32_t lo = 0, hi = 0;
+    if (ok) {
+      lo = __ldg(a.rp + i);
+      hi = __ldg(a.rp + i + 1);
+    }
+    const int last = int(n - 1 - i0 < 31 ? n - 1 - i0 : 31);
+    const uint32_t E0 = __shfl_sync(0xffffffffu, lo, 0), E1 = __shfl_sync(0xffffffffu, hi, last);
+    T acc = T(0);
+    int es = 0;
+    if (running) {
+      for (uint32_t base = E0 & ~3u; base < E1; base += R1W_ROUND) {
+        const uint32_t eb = base + uint32_t(R1W_EPL) * lane;  // 16-byte aligned
+        int cj[R1W_EPL];
+        if (eb < E1) {
+#pragma unroll
+          for (int v = 0; v < R1W_EPL / 4; ++v) {
+            const int4 q4 = __ldg(reinterpret_cast<const int4*>(colp + eb) + v);
+            cj[4 * v] = q4.x; cj[4 * v + 1] = q4.y; cj[4 * v + 2] = q4.z; cj[4 * v + 3] = q4.w;
+          }
+        }
+        T xv[R1W_EPL];
+#pragma unroll
+        for (int k = 0; k < R1W_EPL; ++k) {  // every gather of the lane in flight
+          const uint32_t e = eb + k;
+          xv[k] = T(0);
+          if (e >= E0 && e < E1) {
+            if constexpr (MODE == MODE_ADOCH_Y) xv[k] = extrap(xc[cj[k]], xp[cj[k]], cm);
+            else xv[k] = xc[cj[k]];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < R1W_EPL; ++k) my[k * 33 + lane] = xv[k];
+        if constexpr (VK == VK_I8) {
+          if (eb < E1) {
+            const int2 q8 = __ldg(reinterpret_cast<const int2*>(valp + eb));  // 8 bytes (EPL = 12: + 4)
+            const int q4 = __ldg(reinterpret_cast<const int*>(valp + eb) + 2);
+            const int8_t* b8 = reinterpret_cast<const int8_t*>(&q8);
+            const int8_t* b4 = reinterpret_cast<const int8_t*>(&q4);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sq[warp][k * 33 + lane] = b8[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sq[warp][(8 + k) * 33 + lane] = b4[k];
+          }
+        }
+        __syncwarp();
+        if (ok) {
+          const uint32_t a0 = max(lo, base), a1 = min(hi, base + uint32_t(R1W_ROUND));
+          for (uint32_t e = a0; e < a1; ++e) {  // this row's entries, column order
+            const int k = r1w_pos(int(e - base));
+            const T xj = my[k];
+            if constexpr (VK == VK_UNIFORM) {
+              acc = madd(acc, scale, xj);
+              es += negbit(xj) ? -1 : 1;
+            } else {
+              const int q = sq[warp][k];
+              acc = madd(acc, scale * T(q), xj);
+              es += negbit(xj) ? -q : q;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (ok) {
+      if (running) row_epilogue<T, MODE>(a, c, p, i, acc, double(es), o);
+      else if (MODE == MODE_DOCH) {  // stopped: only the pending copy
+        a.best[i] = reinterpret_cast<const T*>(a.x[(p + 1) & 1])[i] >= T(0) ? 1 : -1;
+      }
+    }
+  }
+  o.s4 = warp_sum(o.s4);
+  o.sxax = warp_sum(o.sxax);
+  o.es = warp_sum(o.es);
+  o.step = warp_max(o.step);
+  o.sy4 = warp_sum(o.sy4);
+  o.syay = warp_sum(o.syay);
+  __shared__ double red[8][NQ];
+  if (lane == 0) {
+    red[warp][Q_S4] = o.s4;
+    red[warp][Q_SXAX] = o.sxax;
+    red[warp][Q_ES] = o.es;
+    red[warp][Q_STEP] = o.step;
+    red[warp][Q_SY4] = o.sy4;
+    red[warp][Q_SYAY] = o.syay;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    RowOut<T, MODE> b;
+    b.s4 = red[0][Q_S4]; b.sxax = red[0][Q_SXAX]; b.es = red[0][Q_ES];
+    b.step = red[0][Q_STEP]; b.sy4 = red[0][Q_SY4]; b.syay = red[0][Q_SYAY];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      b.s4 += red[w][Q_S4]; b.sxax += red[w][Q_SXAX]; b.es += red[w][Q_ES];
+      b.step = fmax(b.step, red[w][Q_STEP]); b.sy4 += red[w][Q_SY4]; b.syay += red[w][Q_SYAY];
+    }
+    write_partials<T, MODE>(a, 0, (int)blockIdx.x, b);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // R > 1: replica-vector kernel. Layout x[j][r] (replicas contiguous per spin).
 // blockIdx.y selects a chunk of 32*VW replicas; each lane owns VW consecutive
 // replicas and moves them with one 16-byte load/store (VW = 16 / sizeof(T)
@@ -518,7 +666,7 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
         xn[v] = run[v] ? xnew : xn[v];
       }
       vstore<T, VW>(xn_buf + idx, xn);
-      if (a.states) vstore<T, VW>(reinterpret_cast<T*>(a.states) + (int64_t)(p + 1) * n * R + idx, xn);
+      if (a.states && p < a.cfg.max_iters) vstore<T, VW>(reinterpret_cast<T*>(a.states) + (int64_t)(p + 1) * n * R + idx, xn);
     } else if constexpr (MODE == MODE_ADOCH_X) {
       if (!any_run) continue;
       T ax[VW];
@@ -629,7 +777,7 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
       }
       const T xn = tmap_pass(av, beta, inv_beta(beta));
       xo[i] = xn;
-      if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + i] = xn;
+      if (a.states && p < a.cfg.max_iters) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + i] = xn;
       st = fmax(st, double(fabs(xn - xi)));
     }
     st = warp_max(st);
@@ -660,7 +808,7 @@ __global__ void __launch_bounds__(256) adoch_finalize(PassArgs a, double* spart,
     }
     const T xn = tmap_pass(av, beta, inv_beta(beta));
     xo[idx] = xn;
-    if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + idx] = xn;
+    if (a.states && p < a.cfg.max_iters) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * total + idx] = xn;
     st = fmax(st, double(fabs(xn - xi)));
   }
   spart[(tid / R) * R + r] = st;  // slot = tid / R, replica-minor
@@ -931,8 +1079,27 @@ int replica_vector_width(int R, bool f64) {
   return R % w == 0 ? w : 1;
 }
 
+// the entry-parallel R = 1 pass for f32 integer couplings (DCX_R1W=0 falls back to pass_r1)
+static bool use_r1w() {
+  static const bool on = [] {
+    const char* e = std::getenv("DCX_R1W");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 template <typename T, int VK>
 static void launch_pass_vk(int mode, const PassArgs& a, int V, int grid, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4 && (VK == VK_UNIFORM || VK == VK_I8)) {
+    if (a.cfg.R == 1 && use_r1w()) {
+      switch (mode) {
+        case MODE_DOCH: pass_r1w<VK, MODE_DOCH><<<grid, 256, 0, s>>>(a); break;
+        case MODE_ADOCH_X: pass_r1w<VK, MODE_ADOCH_X><<<grid, 256, 0, s>>>(a); break;
+        default: pass_r1w<VK, MODE_ADOCH_Y><<<grid, 256, 0, s>>>(a); break;
+      }
+      return;
+    }
+  }
   if (a.cfg.R == 1) {
     switch (V) {
       case 1: launch_r1<T, VK, 1>(mode, a, grid, s); break;

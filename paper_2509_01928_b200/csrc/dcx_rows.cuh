@@ -62,7 +62,8 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RowCtl<T>&
       if (c.running) {
         T xn = tmap_pass(ax, c.beta, c.ibeta);
         xnext[idx] = xn;
-        if (a.states) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * a.cfg.n * a.cfg.R + idx] = xn;
+        // slots 0..max_iters: the pass at p = max_iters computes an x that is never kept
+        if (a.states && p < a.cfg.max_iters) reinterpret_cast<T*>(a.states)[(int64_t)(p + 1) * a.cfg.n * a.cfg.R + idx] = xn;
         o.step = fmax(o.step, double(fabs(xn - xi)));
       }
     } else {  // MODE_ADOCH_X: store Ax_p, H(y_p) partials for the economy window test

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
           const T xn = tmap_pass(ax, beta, inv_beta(beta));
           v[Q_STEP] = fmax(v[Q_STEP], double(fabs(xn - xi)));
           xo[i] = xn;  // own row only: no other thread reads xo in this phase
-          if (states) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
+          if (states && p < a.cfg.max_iters) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
         } else {
           ac[i] = ax;
           if (p > 0 && !exact) {
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
         const T xn = tmap_pass(av, beta, inv_beta(beta));
         st = fmax(st, double(fabs(xn - xi)));
         xo[i] = xn;
-        if (states) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
+        if (states && p < a.cfg.max_iters) states[((int64_t)(p + 1) * n + i) * R + r] = xn;
       }
       double vv[NQ] = {0, 0, 0, st, 0, 0};
       block_reduce(vv, red, tot);

@@ -92,27 +92,52 @@ def torus(L: int = 1000, seed: int = 0):
     return vsum, cols, offs
 
 
-def _maxcut_unit(n, i, j):
+def _maxcut_unit(n, i, j, device=None):
+    """Dedupe undirected pairs on (min, max) and build the symmetric unit-weight CSR
+    (J = -1/2 per edge, columns sorted per row). ``device`` (a CUDA device index) runs
+    the sorts with torch on that GPU -- the same arrays as the numpy path (both sort
+    unique int64 keys), seconds instead of minutes at 10^8 spins."""
+    if device is not None:
+        import torch
+
+        dev = torch.device("cuda", device)
+        ti = torch.from_numpy(np.ascontiguousarray(i, dtype=np.int64)).to(dev)
+        tj = torch.from_numpy(np.ascontiguousarray(j, dtype=np.int64)).to(dev)
+        key = torch.unique(torch.minimum(ti, tj) * n + torch.maximum(ti, tj))  # sorted
+        del ti, tj
+        a, b = key // n, key % n
+        m = int(key.numel())
+        del key
+        k2 = torch.sort(torch.cat([a * n + b, b * n + a])).values
+        del a, b
+        rows, cols = k2 // n, k2 % n
+        del k2
+        offs = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        offs[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
+        out = cols.cpu().numpy(), offs.cpu().numpy()
+        del rows, cols, offs
+        torch.cuda.empty_cache()
+        return np.full(2 * m, -0.5), out[0], out[1], m / 2.0
     key = np.unique(np.minimum(i, j).astype(np.int64) * n + np.maximum(i, j))
     a, b = key // n, key % n
     vals, cols, offs = _csr_from_pairs(n, a, b, np.full(len(a), -0.5))
     return vals, cols, offs, len(a) / 2.0
 
 
-def erdos_renyi(n: int = 10**7, deg: int = 8, seed: int = 0):
+def erdos_renyi(n: int = 10**7, deg: int = 8, seed: int = 0, device=None):
     """(values, cols, offsets, cut_offset) for the E7 graph (Appendix A ``er``)."""
     rng = np.random.default_rng(seed)
     m = n * deg // 2
     i = rng.integers(0, n, m)
     j = rng.integers(0, n, m)
     keep = i != j
-    return _maxcut_unit(n, i[keep], j[keep])
+    return _maxcut_unit(n, i[keep], j[keep], device)
 
 
-def random_regular3(n: int = 10**8, seed: int = 0):
+def random_regular3(n: int = 10**8, seed: int = 0, device=None):
     """(values, cols, offsets, cut_offset) for the R8 graph (Appendix A ``reg3``)."""
     rng = np.random.default_rng(seed)
     stubs = rng.permutation(np.repeat(np.arange(n, dtype=np.int64), 3))
     i, j = stubs[0::2], stubs[1::2]
     keep = i != j
-    return _maxcut_unit(n, i[keep], j[keep])
+    return _maxcut_unit(n, i[keep], j[keep], device)

@@ -16,7 +16,13 @@ tests check what holds at any size:
   at k = 0, dc/solvers/doch.py:294-300);
 * h_values has iterations + 1 entries and the best-energy trace never increases.
 
-R8 (10^8 spins) is left to bench.py: its host build alone takes minutes.
+Plus the G-fp32 free-running gate: the oracle (numpy/scipy f64,
+oracle/dcising_oracle.py) runs the first five DOCH iterations from the same x_0
+at full E7 size (~3 s per iteration) and on 8 T6 replicas;
+||x_k - x_k^ref||_2 / ||x_k^ref||_2 <= 1e-5 for k <= 5. R8 (10^8 spins) gets the
+one-step and G-int checks (its scipy product takes ~10 s). The E7 / R8 graphs are
+built with their deduplicating sorts on the GPU (synth._maxcut_unit(device=...)),
+checked equal to the numpy build here.
 """
 
 import numpy as np
@@ -24,6 +30,7 @@ import pytest
 import scipy.sparse as sp
 
 import paper_2509_01928_b200 as dc
+from oracle import dcising_oracle as orc
 from paper_2509_01928_b200 import synth
 
 pytestmark = pytest.mark.gpu
@@ -83,9 +90,70 @@ def test_t6_full_size_properties(t6):
     assert all(r.accepted[0] for r in a)
 
 
-def test_e7_full_size_properties():
+def _free_running(J_arrays, alpha, beta, X0, rs, k_max=5):
+    """G-fp32 free-running: the oracle's first k_max iterates from the same x_0 (f64)
+    against the device's recorded f32 states."""
+    op = orc.Operator(J_arrays)
+    for x0, r in zip(X0, rs):
+        ref = orc.run(op, alpha, beta, solver="doch", max_iters=k_max, x0=x0, record_states=True)["states"]
+        assert len(r.states) == k_max + 1
+        for k in range(1, k_max + 1):
+            d = float(np.linalg.norm(np.asarray(r.states[k], np.float64) - ref[k]) / np.linalg.norm(ref[k]))
+            assert d <= FP32_TOL, (k, d)
+
+
+def test_device_instance_build_matches_numpy():
+    """synth's GPU build of the E7 / R8 recipes equals the numpy build byte for byte."""
+    for make in (lambda d: synth.erdos_renyi(200_000, 8, seed=0, device=d),
+                 lambda d: synth.random_regular3(300_000, seed=0, device=d)):
+        a, b = make(None), make(0)
+        assert a[3] == b[3]
+        for x, y in zip(a[:3], b[:3]):
+            assert x.dtype == y.dtype and np.array_equal(x, y)
+
+
+def test_t6_free_running_first_iterates(t6):
+    inst, J, alpha, beta, X0 = t6
+    pick = list(range(0, 256, 37))[:8]  # 8 of the 256 replicas (record_states of all 256 would be 6 GB)
+    rs = dc.solve_replicas(inst, "doch", alpha, beta, X0[pick], max_iters=5, precision="f32", path="multipass",
+                           record_states=True)
+    _free_running((J.data, J.indices.astype(np.int64), J.indptr.astype(np.int64)), alpha, beta, X0[pick], rs)
+
+
+@pytest.fixture(scope="module")
+def e7():
     n = 10**7
-    v, c, o, co = synth.erdos_renyi(n, 8, seed=0)
+    v, c, o, co = synth.erdos_renyi(n, 8, seed=0, device=0)
+    return n, v, c, o, co
+
+
+def test_e7_free_running_first_iterates(e7):
+    n, v, c, o, co = e7
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False), cut_offset=co)
+    alpha, beta = 2.828, 5.005e11
+    X0 = dc.initial_state(n, alpha, beta, np.random.default_rng(0))[None, :]
+    r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=5, precision="f32", path="multipass",
+                          record_states=True)
+    _free_running((v, c, o), alpha, beta, X0, r)
+
+
+def test_r8_full_size_one_step_and_energies():
+    """configs[4] on one GPU: 10^8-spin random 3-regular MaxCut."""
+    n = 10**8
+    v, c, o, co = synth.random_regular3(n, seed=0, device=0)
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False), cut_offset=co)
+    J = sp.csr_matrix((v, c, o), shape=(n, n))
+    alpha, beta = 1.732, 3.232e12  # SURVEY.md §8d R8 (eta = 1)
+    X0 = dc.initial_state(n, alpha, beta, np.random.default_rng(0))[None, :]
+    r1 = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=1, precision="f32", path="multipass")
+    _one_step(J, alpha, beta, X0, r1)
+    r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=3, precision="f32", path="multipass")
+    _check_common(J, r, X0, cut_offset=co)
+    assert r[0].iterations == 3
+
+
+def test_e7_full_size_properties(e7):
+    n, v, c, o, co = e7
     inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False), cut_offset=co)
     J = sp.csr_matrix((v, c, o), shape=(n, n))
     alpha, beta = 2.828, 5.005e11  # SURVEY.md §8d E7 (eta = 1)
