@@ -96,7 +96,7 @@ typedef struct {
   int32_t lanes;      /* lanes per row of the R=1 kernels */
   double scale;       /* value = scale * stored integer (integer kinds) */
   int32_t dense;      /* set through dcx_set_dense */
-  int32_t reserved;
+  int32_t lattice_L;  /* > 0: recognised as the periodic L x L torus (the stencil pass runs; R > 1, f32) */
 } dcx_coupling_info;
 
 DCX_API int dcx_abi_version(void);

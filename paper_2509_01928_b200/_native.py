@@ -64,7 +64,7 @@ class Summary(C.Structure):
 class CouplingInfo(C.Structure):
     _fields_ = [
         ("n", C.c_int64), ("nnz", C.c_int64), ("value_kind", C.c_int32), ("lanes", C.c_int32),
-        ("scale", C.c_double), ("dense", C.c_int32), ("reserved", C.c_int32),
+        ("scale", C.c_double), ("dense", C.c_int32), ("lattice_L", C.c_int32),
     ]
 
 

@@ -80,6 +80,8 @@ struct dcx_ctx {
   int64_t ell_entries = 0;  // 32-row sliced ELL size of the pattern (n <= 65536)
   double es_row_bound = 0;  // max over rows of sum_j |q_ij| (integer kinds; bound)
   DevBuf rp, col, col16, vint, v64, v32;
+  int64_t torus_L = 0;     // > 0: the coupling is the periodic torus_L x torus_L lattice (detect_torus)
+  DevBuf bond_r, bond_d;   // its bonds q(i, right(i)), q(i, down(i)) as int8
   DenseDev dn;  // dense tensor-core operands (dcx_dense.cu)
   // ---------------------------------------------------------- run state
   dcx_params prm{};
@@ -90,6 +92,7 @@ struct dcx_ctx {
   DevBuf ctl, g, hist, window, xb0, xb1, ax0, ax1, ay, best, states, part, spart;
   DevBuf scratch;  // grow-only staging (x0 upload, result gathers): no cudaMalloc / cudaFree per call
   DevBuf xmaps;    // pass_rv row-gather TMA maps over the two iterate buffers
+  DevBuf sgn0, sgn1;  // pass_torus sign words of x_p by pass parity
   MultiPass mp;
   CsrDev J;
   SmallPlan sp;
@@ -449,6 +452,47 @@ int dcx_set_csr_block(dcx_ctx* c, int64_t n_rows, int64_t n_cols, int64_t row_ba
   return upload_csr(c, n_rows, nnz, ro, ci, v, n_cols, row_base);
 }
 
+// The periodic L x L lattice of BASELINE configs[2] (SURVEY.md Appendix A ``torus``):
+// row i = (a, b) holds exactly up, left, right, down (ascending column order, L >= 3)
+// with +-1 integer values, symmetric. Recognised here so the stencil pass (pass_torus,
+// dcx_csr.cu) can read two int8 bond arrays instead of the CSR.
+static void detect_torus(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int32_t* col, const int8_t* q) {
+  c->torus_L = 0;
+  c->bond_r.release();
+  c->bond_d.release();
+  const int64_t L = int64_t(std::llround(std::sqrt(double(n))));
+  if (L < 3 || L * L != n || nnz != 4 * n) return;
+  std::vector<int8_t> br(n), bd(n), bl(n), bu(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (ro[i] != 4 * i) return;
+    const int64_t a = i / L, b = i % L;
+    const int64_t up = ((a + L - 1) % L) * L + b, left = a * L + (b + L - 1) % L, right = a * L + (b + 1) % L,
+                  down = ((a + 1) % L) * L + b;
+    int64_t want[4] = {up, left, right, down};
+    std::sort(want, want + 4);
+    for (int k = 0; k < 4; ++k)
+      if (col[4 * i + k] != want[k]) return;
+    for (int k = 0; k < 4; ++k) {
+      const int8_t v = q[4 * i + k];
+      if (v != 1 && v != -1) return;
+      const int64_t j = col[4 * i + k];
+      if (j == right) br[i] = v;
+      else if (j == down) bd[i] = v;
+      else if (j == left) bl[i] = v;
+      else bu[i] = v;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) {  // symmetric: q(i, left(i)) = q(left(i), i), q(i, up(i)) = q(up(i), i)
+    const int64_t a = i / L, b = i % L;
+    if (bl[i] != br[a * L + (b + L - 1) % L] || bu[i] != bd[((a + L - 1) % L) * L + b]) return;
+  }
+  c->bond_r.alloc(n);
+  c->bond_d.alloc(n);
+  CK(cudaMemcpy(c->bond_r.p, br.data(), n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->bond_d.p, bd.data(), n, cudaMemcpyHostToDevice));
+  c->torus_L = L;
+}
+
 static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v,
                       int64_t n_cols, int64_t row_base) {
   return guarded(c, [&] {
@@ -480,6 +524,7 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
       if (maxlen * (vk == VK_I8 ? 127 : 1) >= (int64_t(1) << 24) && scale != 0.0) vk = VK_I16;
     }
     c->have = false;
+    c->torus_L = 0;
     c->n = n;
     c->n_cols = n_cols;
     c->row_base = row_base;
@@ -514,6 +559,7 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
       c->vint.alloc((nnz + 16) * b);
       CK(cudaMemset(static_cast<char*>(c->vint.p) + nnz * b, 0, 16 * b));
       CK(cudaMemcpy(c->vint.p, b == 1 ? (void*)q8.data() : (void*)q16.data(), nnz * b, cudaMemcpyHostToDevice));
+      if (b == 1 && n == n_cols && row_base == 0) detect_torus(c, n, nnz, ro, c32.data(), q8.data());
     } else if (vk != VK_UNIFORM) {
       c->v64.alloc(nnz * 8);
       CK(cudaMemcpy(c->v64.p, v, nnz * 8, cudaMemcpyHostToDevice));
@@ -658,7 +704,7 @@ int dcx_coupling(const dcx_ctx* c, dcx_coupling_info* out) {
   out->lanes = c->V32;
   out->scale = c->scale;
   out->dense = c->dense ? 1 : 0;
-  out->reserved = 0;
+  out->lattice_L = int32_t(c->torus_L);
   return DCX_OK;
 }
 
@@ -850,6 +896,20 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.slots = slots;
     a.xmap[0] = a.xmap[1] = nullptr;
     a.proc_seed = c->J.proc_seed;
+    a.torus_L = (!dist && c->torus_L > 0 && !c->proc) ? int32_t(c->torus_L) : 0;
+    a.bond_r = c->bond_r.as<int8_t>();
+    a.bond_d = c->bond_d.as<int8_t>();
+    a.sgnw[0] = a.sgnw[1] = nullptr;
+    if (a.torus_L > 0 && R > 1 && !c->f64) {
+      const size_t words = size_t(n) * 4 * size_t((R + 127) / 128);
+      c->sgn0.alloc(words * 4);
+      c->sgn1.alloc(words * 4);
+      a.sgnw[0] = c->sgn0.as<uint32_t>();
+      a.sgnw[1] = c->sgn1.as<uint32_t>();
+    } else {
+      c->sgn0.release();
+      c->sgn1.release();
+    }
     if (R > 1 && !c->proc && replica_vector_width(R, c->f64) > 1) {
       const char* e = std::getenv("DCX_RV_TMA");
       if (!(e && std::atoi(e) == 0)) {

@@ -741,6 +741,283 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
 }
 
 // ---------------------------------------------------------------------------
+// 2-D periodic lattice (BASELINE configs[2], T6): stencil pass, R > 1, f32.
+// Replaces pass_rv when the coupling was recognised at upload as the L x L torus
+// of SURVEY.md Appendix A (every row i = (a, b) holds exactly its four lattice
+// neighbours, +-q bonds): no row pointers, no column indices -- the neighbours
+// are computed, the bonds come from two int8 arrays (q(i, right(i)), q(i, down(i))),
+// and a warp moves whole 512-byte replica rows (32 lanes x float4) of the site
+// and its four neighbours, for SITES sites at once so 5 * SITES 16-byte loads
+// per lane are in flight. The row sum runs over the neighbours in ascending
+// column order with the same FMA and epilogue as pass_rv, so the iterates are
+// bit-identical to it. The spin energy of the pass is accumulated per replica
+// over FORWARD edges only: sum_i s_i (J s)_i = 2 sum_i (q_r(i) s_i s_right + q_d(i)
+// s_i s_down), exact as an integer count of negative products.
+
+
+__device__ __forceinline__ void sort4_cols(int64_t (&c)[4], int (&k)[4]) {
+  // 5-comparator network on (column, slot); columns are distinct for L >= 3
+  auto cx = [&](int i, int j) {
+    if (c[j] < c[i]) {
+      const int64_t t = c[i]; c[i] = c[j]; c[j] = t;
+      const int u = k[i]; k[i] = k[j]; k[j] = u;
+    }
+  };
+  cx(0, 1); cx(2, 3); cx(0, 2); cx(1, 3); cx(1, 2);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) pass_torus(PassArgs a) {
+  using T = float;
+  constexpr int VW = 4;
+  static_assert(MODE != MODE_ADOCH_Y, "exact-window ADOCH stays on pass_rv");
+  if (!a.g->live) return;
+  const int p = a.g->p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int R = a.cfg.R;
+  const int n = int(a.cfg.n);  // L <= 46340 and n * R / 4 < 2^31 (checked at launch): 32-bit offsets
+  const int L = a.torus_L;
+  const int r0 = blockIdx.y * 32 * VW + lane * VW;
+  const bool lane_on = r0 < R;
+  T alpha[VW], beta[VW], ibeta[VW], cm[VW];
+  bool run[VW], copy[VW];
+  bool any_run = false, all_run = true, any_copy = false;
+#pragma unroll
+  for (int v = 0; v < VW; ++v) {
+    run[v] = copy[v] = false;
+    alpha[v] = beta[v] = cm[v] = T(0);
+    ibeta[v] = T(1);
+    if (lane_on) {
+      const RepCtl& c = a.ctl[r0 + v];
+      run[v] = c.status == DCX_STOP_RUNNING;
+      copy[v] = MODE == MODE_DOCH && p > 0 && c.pend == p - 1;
+      alpha[v] = T(c.alpha);
+      beta[v] = T(c.beta);
+      ibeta[v] = inv_beta(beta[v]);
+      cm[v] = T(c.cm[p & 1]);
+    }
+    any_run |= run[v];
+    all_run &= run[v];
+    any_copy |= copy[v];
+  }
+  if (!__syncthreads_or(any_run || any_copy)) return;
+  // float4 views: a spin's replica row is R / 4 float4; this lane's column is r0 / 4
+  const int RV = R / VW, c4 = r0 / VW;
+  const float4* xc = reinterpret_cast<const float4*>(a.x[p & 1]) + c4;
+  const float4* xp = reinterpret_cast<const float4*>(a.x[(p + 1) & 1]) + c4;
+  float4* xn_buf = reinterpret_cast<float4*>(a.x[(p + 1) & 1]) + c4;
+  const T scale = T(a.scale);
+  T s4[VW], sxax[VW], sy4[VW], syay[VW], step[VW];
+  int neg[VW], nedge = 0;  // forward-edge products q s_i s_j < 0, and forward edges counted
+#pragma unroll
+  for (int v = 0; v < VW; ++v) {
+    s4[v] = sxax[v] = sy4[v] = syay[v] = step[v] = T(0);
+    neg[v] = 0;
+  }
+  // site (ar, b) of this warp, advanced by S = grid * 8 sites per step without divisions
+  const int S = int(gridDim.x) * 8;
+  const int Sa = S / L, Sb = S - Sa * L;
+  int i_cur = int(blockIdx.x) * 8 + warp;
+  int a_cur = i_cur / L, b_cur = i_cur - a_cur * L;
+  auto advance = [&](int& i, int& ar, int& b) {
+    i += S;
+    ar += Sa;
+    b += Sb;
+    if (b >= L) { b -= L; ++ar; }
+  };
+  auto f4 = [](const float4& q, int v) { return v == 0 ? q.x : v == 1 ? q.y : v == 2 ? q.z : q.w; };
+  // two register stages: the loads of the next site are in flight while this one computes
+  struct Stage {
+    float4 xs[5];  // 0 = own row, 1..4 = neighbours in ascending column order
+    float4 xo, axo;
+    T qv[4];
+    uint32_t qr, qd;
+    int slot_r, slot_d, isite;
+    bool on;
+  };
+  auto load_stage = [&](Stage& st, const int iu, const int au, const int bu) {
+      st.on = iu < n;
+      st.isite = iu;
+      const int ii = st.on ? iu : 0, ar = st.on ? au : 0, b = st.on ? bu : 0;
+      const int c_up = ar == 0 ? ii + (L - 1) * L : ii - L;
+      const int c_left = b == 0 ? ii + L - 1 : ii - 1;
+      const int c_right = b == L - 1 ? ii - L + 1 : ii + 1;
+      const int c_down = ar == L - 1 ? ii - (L - 1) * L : ii + L;
+      const int q_up = __ldg(a.bond_d + c_up), q_left = __ldg(a.bond_r + c_left), q_right = __ldg(a.bond_r + ii),
+                q_down = __ldg(a.bond_d + ii);
+      st.qr = q_right < 0 ? 0x80000000u : 0u;
+      st.qd = q_down < 0 ? 0x80000000u : 0u;
+      int col[4];
+      // ascending column order: interior (and most border) sites up < left < right < down;
+      // the wrapped ones are sorted (warp-uniform branch)
+      if (c_up < c_left && c_left < c_right && c_right < c_down) {
+        col[0] = c_up; col[1] = c_left; col[2] = c_right; col[3] = c_down;
+        st.qv[0] = scale * T(q_up); st.qv[1] = scale * T(q_left); st.qv[2] = scale * T(q_right);
+        st.qv[3] = scale * T(q_down);
+        st.slot_r = 2;
+        st.slot_d = 3;
+      } else {
+        int64_t cc[4] = {c_up, c_left, c_right, c_down};
+        int k[4] = {0, 1, 2, 3};
+        sort4_cols(cc, k);
+        const int qs[4] = {q_up, q_left, q_right, q_down};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          col[m] = int(cc[m]);
+          const int km = k[m];
+          st.qv[m] = scale * T(km == 0 ? qs[0] : km == 1 ? qs[1] : km == 2 ? qs[2] : qs[3]);
+          if (km == 2) st.slot_r = m;
+          if (km == 3) st.slot_d = m;
+        }
+      }
+      const bool ld = st.on && lane_on;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      st.xs[0] = (ld && any_run) ? __ldg(xc + ii * RV) : z;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) st.xs[1 + m] = (ld && any_run) ? __ldg(xc + col[m] * RV) : z;
+      st.xo = st.axo = z;
+      if constexpr (MODE == MODE_DOCH) {
+        // the pending copy reads the sign words of x_{p-1} (1 bit per replica), not x_{p-1}
+        if (ld && any_copy) {
+          const uint32_t* sw = a.sgnw[(p + 1) & 1] + int64_t(ii) * (4 * gridDim.y) + blockIdx.y * 4;
+          st.xo = make_float4(__uint_as_float(__ldg(sw)), __uint_as_float(__ldg(sw + 1)),
+                              __uint_as_float(__ldg(sw + 2)), __uint_as_float(__ldg(sw + 3)));
+        }
+      } else {
+        if (ld && any_run && p > 0 && a.cfg.window_mode == DCX_WINDOW_ECONOMY) {
+          st.xo = __ldg(xp + ii * RV);
+          st.axo = __ldg(reinterpret_cast<const float4*>(a.ax[(p + 1) & 1]) + c4 + ii * RV);
+        }
+      }
+  };
+  auto compute_stage = [&](const Stage& st) {
+      if (!st.on || !lane_on) return;
+      const int ofs = st.isite * RV;
+      if constexpr (MODE == MODE_DOCH) {
+        if (any_copy) {  // pending best copy: sign(x_{p-1}) of the copying replicas, one 32-bit store
+          uint32_t* bp = reinterpret_cast<uint32_t*>(a.best + int64_t(st.isite) * R + r0);
+          uint32_t w = *bp;
+#pragma unroll
+          for (int v = 0; v < VW; ++v)
+            if (copy[v]) {
+              const uint32_t negb = (__float_as_uint(f4(st.xo, v)) >> lane) & 1u;  // word v, bit lane
+              w = (w & ~(0xffu << (8 * v))) | ((negb ? 0xffu : 0x01u) << (8 * v));
+            }
+          *bp = w;
+        }
+        // sign words of x_p for the copy of pass p + 1 (x is never -0.0: sign bit <=> x < 0)
+        const unsigned am = __activemask();
+        uint32_t bw[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) bw[v] = __ballot_sync(am, __float_as_uint(f4(st.xs[0], v)) >> 31);
+        const bool wany = __any_sync(am, any_run);  // every lane of am votes (no short-circuit)
+        if (lane < VW && wany)
+          a.sgnw[p & 1][int64_t(st.isite) * (4 * gridDim.y) + blockIdx.y * 4 + lane] =
+              lane == 0 ? bw[0] : lane == 1 ? bw[1] : lane == 2 ? bw[2] : bw[3];
+      }
+      if (!any_run) return;
+      T xi[VW], acc[VW];
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        xi[v] = f4(st.xs[0], v);
+        acc[v] = T(0);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[v] = madd(acc[v], st.qv[m], f4(st.xs[1 + m], v));
+      }
+      nedge += 2;
+      const float4 xr = st.slot_r == 2 ? st.xs[3] : st.slot_r == 0 ? st.xs[1] : st.slot_r == 1 ? st.xs[2] : st.xs[4];
+      const float4 xd = st.slot_d == 3 ? st.xs[4] : st.slot_d == 0 ? st.xs[1] : st.slot_d == 1 ? st.xs[2] : st.xs[3];
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        const uint32_t xb = __float_as_uint(xi[v]);
+        neg[v] += int((xb ^ __float_as_uint(f4(xr, v)) ^ st.qr) >> 31) + int((xb ^ __float_as_uint(f4(xd, v)) ^ st.qd) >> 31);
+      }
+      if constexpr (MODE == MODE_DOCH) {
+        T xn[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+          const T ax = shifted(acc[v], alpha[v], xi[v]);
+          const T x2 = mul_rn(xi[v], xi[v]);
+          s4[v] += x2 * x2;
+          sxax[v] += xi[v] * ax;
+          const T xnew = tmap_pass(ax, beta[v], ibeta[v]);
+          step[v] = fmax(step[v], fabs(xnew - xi[v]));
+          xn[v] = xnew;
+        }
+        const float4 o4 = make_float4(xn[0], xn[1], xn[2], xn[3]);
+        if (all_run) {
+          xn_buf[ofs] = o4;
+        } else {  // stopped replicas keep their x_{p-1} in this buffer: store the running ones only
+          float* e = reinterpret_cast<float*>(xn_buf + ofs);
+#pragma unroll
+          for (int v = 0; v < VW; ++v)
+            if (run[v]) e[v] = xn[v];
+        }
+        if (a.states && p < a.cfg.max_iters) {
+          float* st = reinterpret_cast<float*>(reinterpret_cast<float4*>(a.states) + (int64_t)(p + 1) * n * RV + c4 + ofs);
+#pragma unroll
+          for (int v = 0; v < VW; ++v) st[v] = run[v] ? xn[v] : reinterpret_cast<const float*>(xn_buf + ofs)[v];
+        }
+      } else {  // MODE_ADOCH_X
+        T ax[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+          ax[v] = shifted(acc[v], alpha[v], xi[v]);
+          const T x2 = mul_rn(xi[v], xi[v]);
+          s4[v] += x2 * x2;
+          sxax[v] += xi[v] * ax[v];
+        }
+        reinterpret_cast<float4*>(a.ax[p & 1])[c4 + ofs] = make_float4(ax[0], ax[1], ax[2], ax[3]);
+        if (p > 0 && a.cfg.window_mode == DCX_WINDOW_ECONOMY) {
+#pragma unroll
+          for (int v = 0; v < VW; ++v) {
+            const T yi = extrap(xi[v], f4(st.xo, v), cm[v]);
+            const T ayi = extrap(ax[v], f4(st.axo, v), cm[v]);
+            const T y2 = mul_rn(yi, yi);
+            sy4[v] += y2 * y2;
+            syay[v] += yi * ayi;
+          }
+        }
+      }
+  };
+  Stage sa, sb;
+  load_stage(sa, i_cur, a_cur, b_cur);
+  while (sa.on) {
+    advance(i_cur, a_cur, b_cur);
+    load_stage(sb, i_cur, a_cur, b_cur);
+    compute_stage(sa);
+    if (!sb.on) break;
+    advance(i_cur, a_cur, b_cur);
+    load_stage(sa, i_cur, a_cur, b_cur);
+    compute_stage(sb);
+  }
+  // block reduction of the per-replica partials, warps in a fixed order (as pass_rv)
+  __shared__ double red[NQ][32 * VW];
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int v = 0; v < VW; ++v) {
+        const int c = lane * VW + v;
+        // sum over this warp's sites of s_i (J s)_i = 2 * (forward edges - 2 * negative ones)
+        const double es = 2.0 * double(nedge - 2 * neg[v]);
+        const double q[NQ] = {double(s4[v]), double(sxax[v]), es, double(step[v]), double(sy4[v]), double(syay[v])};
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          if (w == 0) red[k][c] = q[k];
+          else red[k][c] = (k == Q_STEP) ? fmax(red[k][c], q[k]) : red[k][c] + q[k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < NQ * 32 * VW; t += blockDim.x) {
+    const int k = t / (32 * VW), c = t % (32 * VW);
+    const int r = blockIdx.y * 32 * VW + c;
+    if (r < R) a.part[((int64_t)r * NQ + k) * a.slots + blockIdx.x] = red[k][c];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // ADOCH finalize (elementwise): x_{p+1} = cbrt(Av/beta) with v = y or x_p as
 // decided by control p (doch.py:313-318); pending best copy of x_p; step
 // partials. Buffer holding x_{p-1} receives x_{p+1}.
@@ -1079,6 +1356,15 @@ int replica_vector_width(int R, bool f64) {
   return R % w == 0 ? w : 1;
 }
 
+// the lattice stencil pass for recognised tori: opt-in (DCX_TORUS=1). It is bit-identical
+// to pass_rv but measured slower on T6 (1.59 vs 1.41 ms per iteration):
+// register-staged neighbour rows hide less latency than pass_rv's TMA staging into
+// shared memory. Read per launch so one process can A/B both kernels (tests).
+static bool use_torus() {
+  const char* e = std::getenv("DCX_TORUS");
+  return e && std::atoi(e) == 1;
+}
+
 // the entry-parallel R = 1 pass for f32 integer couplings (DCX_R1W=0 falls back to pass_r1)
 static bool use_r1w() {
   static const bool on = [] {
@@ -1112,6 +1398,14 @@ static void launch_pass_vk(int mode, const PassArgs& a, int V, int grid, cudaStr
   } else {
     const int R = a.cfg.R;
     const int W = replica_vector_width(R, sizeof(T) == 8);
+    if constexpr (sizeof(T) == 4 && VK == VK_I8) {
+      if (a.torus_L > 0 && W == 4 && mode != MODE_ADOCH_Y && use_torus() && a.cfg.n * R / 4 < (int64_t(1) << 31)) {
+        const dim3 g(grid, (R + 127) / 128);
+        if (mode == MODE_DOCH) pass_torus<MODE_DOCH><<<g, 256, 0, s>>>(a);
+        else pass_torus<MODE_ADOCH_X><<<g, 256, 0, s>>>(a);
+        return;
+      }
+    }
     if constexpr (sizeof(T) == 8) {
       if (W == 2) launch_rv<T, VK, 2>(mode, a, dim3(grid, (R + 63) / 64), s);
       else launch_rv<T, VK, 1>(mode, a, dim3(grid, (R + 31) / 32), s);

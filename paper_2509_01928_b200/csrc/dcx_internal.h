@@ -41,6 +41,15 @@ struct PassArgs {
   int32_t es_f32;  // pass_rv: per-lane spin-energy sums exact in f32 (integer couplings, bounded rows)
   const void* xmap[2];  // pass_rv: tile::gather4 maps over gx[0] / gx[1] (device copies), or null (cp.async staging)
   long long proc_seed;  // procedural coupling (vk == VK_PROC): seed of sin(i*j + seed)
+  // 2-D periodic L x L lattice detected at upload (dcx_api.cu detect_torus): the stencil
+  // pass reads the bonds instead of the CSR. torus_L = 0: not a lattice
+  int32_t torus_L;
+  const int8_t* bond_r;  // q(i, right(i))  [n]
+  const int8_t* bond_d;  // q(i, down(i))   [n]
+  // pass_torus: sign bits of x_p written by pass p into sgnw[p & 1], [n][R / 32] words
+  // (word 4c + v of a site: bit l = replica 128c + 4l + v); the pending best copy of
+  // pass p + 1 reads them instead of x_p
+  uint32_t* sgnw[2];
   RunCfg cfg;
 };
 

@@ -16,6 +16,7 @@ the benchmark use.
 
 from __future__ import annotations
 
+import os
 import time
 import warnings
 from dataclasses import dataclass, field, replace
@@ -383,8 +384,15 @@ def profile_dominant_kernel(instance, alpha, beta, x0, *, solver: str = "doch", 
         iters = 100
         flops = iters * 2.0 * n * n * R
         byts = float(iters * R * n * (2 + 1))  # f16 + int8 operands of the next iteration
+    elif R > 1 and info.lattice_L > 0 and precision == "f32" and R % 4 == 0 and os.environ.get("DCX_TORUS") == "1":
+        # the lattice stencil pass (csrc/dcx_csr.cu pass_torus): two int8 bond arrays and
+        # the state read once + written once (2 n + 8 R n bytes)
+        name = "pass_torus"
+        flops = 2.0 * info.nnz * R
+        byts = float(2 * n + R * n * tb * 2)
     else:
-        name = "pass_rv" if R > 1 else "pass_r1"
+        name = "pass_rv" if R > 1 else ("pass_r1w" if precision == "f32" and info.value_kind in (0, 1)
+                                        else "pass_r1")
         vbytes = {0: 0, 1: 1, 2: 2, 3: 4, 4: 8}[info.value_kind]
         if info.value_kind in (3, 4):
             vbytes = tb

@@ -163,3 +163,31 @@ def test_e7_full_size_properties(e7):
     r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=20, precision="f32", path="multipass")
     _check_common(J, r, X0, cut_offset=co)
     assert r[0].iterations == 20 and r[0].stop_reason == "max_iters"
+
+
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+def test_torus_stencil_bitwise_equals_csr_pass(solver):
+    """The lattice stencil pass (pass_torus, DCX_TORUS=1, available when the upload recognises
+    the periodic L x L torus) sums the four neighbours in the CSR's column order with the
+    CSR pass's arithmetic: iterates, energies, traces and stop reasons equal pass_rv's bit
+    for bit, including the wrap-around rows and columns."""
+    import os
+
+    L, R = 37, 128  # odd L: every wrap case; R = 128 (one replica chunk)
+    v, c, o = synth.torus(L, seed=5)
+    n = L * L
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False))
+    p = dc.derive_params(inst.coupling, eta=1.0)
+    X0 = np.stack([dc.initial_state(n, p.alpha, p.beta, np.random.default_rng(s)) for s in range(R)])
+    kw = dict(max_iters=60, precision="f32", path="multipass")
+    ref = dc.solve_replicas(inst, solver, p.alpha, p.beta, X0, **kw)
+    os.environ["DCX_TORUS"] = "1"
+    try:
+        fast = dc.solve_replicas(inst, solver, p.alpha, p.beta, X0, reupload=True, **kw)
+    finally:
+        os.environ.pop("DCX_TORUS")
+    for a_, b_ in zip(fast, ref):
+        assert a_.iterations == b_.iterations and a_.stop_reason == b_.stop_reason
+        assert a_.energy == b_.energy and np.array_equal(a_.x, b_.x) and np.array_equal(a_.spins, b_.spins)
+        assert [t.energy for t in a_.trace] == [t.energy for t in b_.trace]
+        assert np.array_equal(np.asarray(a_.h_values), np.asarray(b_.h_values))
