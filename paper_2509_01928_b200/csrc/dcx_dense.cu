@@ -104,7 +104,8 @@ struct Args {
   CUtensorMap tmA[2];   // Xh by parity (f16)
   CUtensorMap tmB;      // Q (f16)
   CUtensorMap tmS[2];   // S8 by parity (int8)
-  CUtensorMap tmQ8;     // Q (int8)
+  CUtensorMap tmQ8;     // Q (int8; e4m3 when f8)
+  CUtensorMap tmA8[2];  // f8: Dh by parity as e4m3 bytes over the same buffers as tmA (row stride 2 npad)
   float* xm[2];
   // DOCH delta operands (see the kernel comment): the running accumulators and the tracked
   // state, persisted between launches of one solve
@@ -125,6 +126,10 @@ struct Args {
   int n, npad, R, Rpad, tiles_n, p_end;
   float jscale;
   int mc;          // NC = 2: clusters of two pairs sharing the A tiles by TMA multicast
+  // f8: iterations p >= 1 multiply e4m3 deltas (per-replica power-of-two scale) with the e4m3
+  // Q (|q| <= 16, exact), kind::f8f6f4; the sign GEMM is e4m3 too (dS in {0, +-2}, f32 D2)
+  int f8;
+  float* dsc;      // f8: 2^-e of the replica's last written delta (resume), [Rpad]
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -213,6 +218,39 @@ __device__ __forceinline__ void mma_i8_g(uint32_t dtmem, uint64_t ad, uint64_t b
                  "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
   }
 }
+template <int NC>
+__device__ __forceinline__ void mma_f8_g(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  if constexpr (NC == 1) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  } else {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  }
+}
+// e4m3 pairs: lo byte = a, hi byte = b (saturating round-to-nearest); and back to float
+__device__ __forceinline__ uint16_t e4m3x2(float a, float b) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ float2 e4m3x2_to_f2(uint16_t v) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
+  return __half22float2(*reinterpret_cast<__half2*>(&h));
+}
+// exponent e of the power-of-two scale 2^e for the next e4m3 delta of a replica whose last
+// step was `step` (= lambda max|Dh|): |Dh| < 2^(E+1) with E = ilogb(step / lambda); 2^(E+3+e) = 256
+// leaves 7/4 x growth room below e4m3's 448 (saturating beyond; the residual carries over).
+// Identical in every CTA (double inputs of the shared control).
+__device__ __forceinline__ int f8_scale_exp(double step, double lam, bool first) {
+  if (first) return 6;  // Dh_1 = T(x_0)/lambda - s_0 is O(1): up to 7 before saturation
+  const double m = step / lam;
+  if (!(m > 0.0)) return 60;
+  const int e = 5 - ilogb(m);
+  return e < -30 ? -30 : (e > 60 ? 60 : e);
+}
+
 // MMA completion -> mbarrier (NC = 2: every CTA of the cluster in `mask` receives it)
 template <int NC>
 __device__ __forceinline__ void mma_commit_g(uint32_t mbar, uint16_t mask = 3) {
@@ -377,6 +415,7 @@ struct __align__(8) Smem {
   int pad;
   unsigned tdbg[8];  // epilogue phase stamps / sums (DCX_DENSE_TRACE)
   float alpha[TM], inv_beta[TM], jl[TM], inv_lam[TM], lam[TM];  // per-replica constants (fixed for the run)
+  double lamd[TM];
   float red[2][TM][8];  // [4, 8): the ADOCH kernel's H(y) partials
   double red2[2][TM][4];
   RepCtl ctl[TM];
@@ -408,6 +447,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const int r0 = rt * TM, i0 = nt * TN;
   const bool leader = cta_rank == 0;
   const int KB1 = a.npad / (TK * P::KA);      // f16 stages (KA x 64 of K each)
+  const int KB1f8 = a.npad / (2 * TK * P::KA);  // e4m3 stages (KA x 128 of K each)
   const int KB2 = a.npad / (2 * TK * P::KA);  // int8 stages (KA x 128 of K each)
   constexpr int KS = P::KA * TK;  // K columns per GEMM1 stage (128); flags are per spin tile of TN
   SyncWords* grp = a.sync + rg;
@@ -449,6 +489,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     sm.jl[threadIdx.x] = a.jscale * float(lam);
     sm.inv_lam[threadIdx.x] = float(1.0 / lam);
     sm.lam[threadIdx.x] = float(lam);
+    sm.lamd[threadIdx.x] = lam;
   }
   // epilogue thread geometry
   const bool epi = warp >= 4;
@@ -457,7 +498,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const int r = r0 + rl;
   const bool valid = epi && r < a.R;
   uint64_t prevmask = 0;  // sign bits of x_{p-1} for this thread's HW columns
+  // f8: 2^-e_p, the descale of this iteration's fresh product F_p (the scale its delta was
+  // written with); 1 for the f16 product of iteration 0
+  float fdesc = 1.f;
   if (epi) {  // stored by the previous launch's teardown
+    if (a.f8 && valid && p > 0) fdesc = a.dsc[r];
     const int8_t* sp = a.sgnl + (int64_t)r * a.npad + i0 + h * HW;
 #pragma unroll 1
     for (int c = 0; c < HW; ++c)
@@ -523,6 +568,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   // rotation of the K order: start at the stage holding the first spin of tile (nt & ~1)
   // (common to both pairs of a multicast cluster)
   const int kstart = ((nt & ~1) * TN) / KS;
+  const int kstart8 = ((nt & ~1) * TN) / (2 * KS);  // the same rotation in 8-bit stages
   unsigned int* const my_flag = a.flags + ((int64_t)rt * a.tiles_n + nt) * FLAG_STRIDE;
   const unsigned int* const tile_flags = a.flags + (int64_t)rt * a.tiles_n * FLAG_STRIDE;
   auto wait_gen = [&](const unsigned int* g, unsigned int target) {
@@ -567,16 +613,18 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       const bool tr = a.dbg && blockIdx.x == 0 && p < 4096 && lane == 0;
       if (tr) a.dbg[p * 12 + 5] = clock64();
       uint32_t ready = 0;  // bit t: spin tile t of x_p is written (lane t polls tile t)
-      for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
+      const bool f8it = a.f8 && p > 0;  // this iteration's delta GEMM in e4m3
+      const int nb1 = f8it ? KB1f8 : KB1, ks1 = f8it ? 2 * KS : KS, kst1 = f8it ? kstart8 : kstart;
+      for (int kb = 0; kb < nb1 + KB2; ++kb, ++kiter) {
         const int s = kiter % P::STAGES;
         const uint32_t ph = (kiter / P::STAGES) & 1;
         if (lane == 0) mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
-        // GEMM1 stage kt: K columns [KS kt, KS kt + KS), written by the spin tiles they
-        // overlap; GEMM2 stages (two int8 atoms of 128) were all waited in GEMM1
-        const int kt = kb < KB1 ? (kb + kstart) % KB1 : (kb - KB1 + kstart / 2) % KB2;
-        if (kb < KB1) {
+        // GEMM1 stage kt: K columns [ks1 kt, ks1 kt + ks1), written by the spin tiles they
+        // overlap; GEMM2 stages (two 8-bit atoms of 128) were all waited in GEMM1
+        const int kt = kb < nb1 ? (kb + kst1) % nb1 : (kb - nb1 + kstart8) % KB2;
+        if (kb < nb1) {
           const unsigned tf0 = a.dbg ? clock() : 0u;
-          const int t_lo = (kt * KS) / TN, t_hi = min(a.tiles_n - 1, (kt * KS + KS - 1) / TN);
+          const int t_lo = (kt * ks1) / TN, t_hi = min(a.tiles_n - 1, (kt * ks1 + ks1 - 1) / TN);
           const uint32_t need = t_lo > t_hi ? 0u : (((2u << t_hi) - 1u) & ~((1u << t_lo) - 1u));
           long long t0 = 0;
           unsigned int polls = 0;
@@ -593,15 +641,15 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           __syncwarp();  // the lanes' acquires before lane 0's loads
         }
         if (lane == 0) {
-          if (kb < KB1) fence_async_global();  // generic writes (acquired above) before the async-proxy loads
+          if (kb < nb1) fence_async_global();  // generic writes (acquired above) before the async-proxy loads
           const uint32_t fb = smem_u32(&sm.full[s]);
           if (leader) mbar_expect_tx(fb, NC * P::STAGE);
           unsigned char* st = tiles + s * P::STAGE;
           const int bi = i0 + cta_rank * (TN / NC);
           const int cur = p & 1;
-          const CUtensorMap* ma = kb < KB1 ? &a.tmA[cur] : &a.tmS[cur];
-          const CUtensorMap* mb = kb < KB1 ? &a.tmB : &a.tmQ8;
-          const int katom = kb < KB1 ? TK : 2 * TK;
+          const CUtensorMap* ma = kb < nb1 ? (f8it ? &a.tmA8[cur] : &a.tmA[cur]) : &a.tmS[cur];
+          const CUtensorMap* mb = (kb < nb1 && !f8it) ? &a.tmB : &a.tmQ8;
+          const int katom = (kb < nb1 && !f8it) ? TK : 2 * TK;
           const int kc = kt * P::KA * katom;
 #pragma unroll
           for (int q = 0; q < P::KA; ++q) {
@@ -631,7 +679,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         if (group_done(p)) break;  // same exit test as the producer
         const bool tr = a.dbg && blockIdx.x == 0 && p < 4096;
         unsigned long long wait_cyc = 0;
-        for (int kb = 0; kb < KB1 + KB2; ++kb, ++kiter) {
+        const bool f8it = a.f8 && p > 0;
+        const int nb1 = f8it ? KB1f8 : KB1;
+        for (int kb = 0; kb < nb1 + KB2; ++kb, ++kiter) {
           const int s = kiter % P::STAGES;
           const uint32_t ph = (kiter / P::STAGES) & 1;
           const unsigned long long tw0 = clock64();
@@ -639,18 +689,29 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           // D1 of iteration p-1 read by the epilogue before GEMM1(p) overwrites it
           if (kb == 0 && p > p_start) mbar_wait(smem_u32(&sm.d1free), (p - 1 - p_start) & 1);
           // D2 of iteration p-1 drained by the epilogue before GEMM2(p) overwrites it
-          if (kb == KB1 && p > p_start) mbar_wait(smem_u32(&sm.d2free), (p - 1 - p_start) & 1);
+          if (kb == nb1 && p > p_start) mbar_wait(smem_u32(&sm.d2free), (p - 1 - p_start) & 1);
           wait_cyc += clock64() - tw0;
           tc_fence_after();
           const uint32_t s0 = smem_u32(tiles + s * P::STAGE);
 #pragma unroll
           for (int q = 0; q < P::KA; ++q) {
             const uint32_t sa = s0 + q * TILE_BYTES, sb = s0 + P::KA * TILE_BYTES + q * P::B_BYTES;
-            if (kb < KB1) {
+            if (kb < nb1) {
+              if (f8it) {
 #pragma unroll
-              for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
-                mma_f16_g<NC>(tmem + rcol(p), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
-                              (kb | q | k) ? 1u : 0u);  // F_p = Q Dh_p
+                for (int k = 0; k < 4; ++k)  // 4 x (K = 32 e4m3 = 32 B) along the 128-byte row
+                  mma_f8_g<NC>(tmem + rcol(p), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
+                               (kb | q | k) ? 1u : 0u);  // F_p = Q (2^e Dh_p)
+              } else {
+#pragma unroll
+                for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
+                  mma_f16_g<NC>(tmem + rcol(p), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
+                                (kb | q | k) ? 1u : 0u);  // F_p = Q Dh_p
+              }
+            } else if (a.f8) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)  // e4m3 dS in {0, +-2}: D2 += Q dS in f32 (exact integers)
+                mma_f8_g<NC>(tmem + D2COL, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, 1u);
             } else {
 #pragma unroll
               for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
@@ -660,7 +721,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           mma_commit_g<NC>(smem_u32(&sm.empty[s]), uint16_t(!a.mc ? 0x3 : (psub == 0 ? 0x3 : 0xF)));
           if (tr && kb == 0) a.dbg[p * 12 + 8] = clock64();
           if (a.dbg && kb == 0) d_g1 -= clock();
-          if (kb == KB1 - 1) {
+          if (kb == nb1 - 1) {
             if (a.dbg) d_g1 += clock();
             mma_commit_g<NC>(smem_u32(&sm.accf1), uint16_t(0x3u << (2 * psub)));
             if (tr) a.dbg[p * 12 + 9] = clock64();
@@ -774,6 +835,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         store_pm1(a.best8 + (int64_t)r * a.npad + gbase, w, HW / 4);
       }
       const __half* dhg = a.xh[cur] + (int64_t)r * a.npad + gbase;  // Dh_p (GEMM1(p)'s operand)
+      const uint8_t* dhb = reinterpret_cast<const uint8_t*>(a.xh[cur]) + (int64_t)r * 2 * a.npad + gbase;  // f8 view
+      const bool f8 = a.f8 != 0;
       mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
       tc_fence_after();
@@ -787,19 +850,32 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         tmem_ld16(lane_base + rcol(pk + 1) + off, rv);
         tmem_ld16(xaddr + off, st);
         tmem_ld16(d2addr + off, d2);
-        __align__(16) __half dh[16];
-        if (has_prev && lim > 0) {
-          *reinterpret_cast<uint4*>(dh) = *reinterpret_cast<const uint4*>(dhg + off);
-          *reinterpret_cast<uint4*>(dh + 8) = *reinterpret_cast<const uint4*>(dhg + off + 8);
-        } else {
+        float dhv[16];  // Dh_p in s-units
 #pragma unroll
-          for (int j = 0; j < 16; ++j) dh[j] = __float2half_rn(0.f);
+        for (int j = 0; j < 16; ++j) dhv[j] = 0.f;
+        if (has_prev && lim > 0) {
+          if (f8) {  // Dh_p (p >= 1) written by update p - 1 as e4m3 with scale 2^e_p
+            const uint4 w = *reinterpret_cast<const uint4*>(dhb + off);
+            const uint16_t* q2 = reinterpret_cast<const uint16_t*>(&w);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float2 b2 = e4m3x2_to_f2(q2[j]);
+              dhv[2 * j] = b2.x * fdesc;
+              dhv[2 * j + 1] = b2.y * fdesc;
+            }
+          } else {
+            __align__(16) __half dh[16];
+            *reinterpret_cast<uint4*>(dh) = *reinterpret_cast<const uint4*>(dhg + off);
+            *reinterpret_cast<uint4*>(dh + 8) = *reinterpret_cast<const uint4*>(dhg + off + 8);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) dhv[j] = __half2float(dh[j]);
+          }
         }
         tmem_ld_wait();
         uint32_t m = 0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float f = __uint_as_float(fv[j]);
+          const float f = __uint_as_float(fv[j]) * fdesc;  // 2^-e_p F_p (exact)
           const float rr = __fadd_rn(__uint_as_float(rv[j]), f);
           rv[j] = __float_as_uint(rr);
           const float x = lamf * __uint_as_float(st[j]);
@@ -810,11 +886,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t neg = st[j] >> 31;
           m |= neg << j;
           const int mm = -int(neg);
-          const int v = (off + j < lim) ? int(d2[j]) : 0;
+          const int v = (off + j < lim) ? (f8 ? __float2int_rn(__uint_as_float(d2[j])) : int(d2[j])) : 0;
           es += (v ^ mm) - mm;
           float ay = ax;
           if (has_prev) {
-            const float dx = lamf * __half2float(dh[j]);  // x_p - x_{p-1}
+            const float dx = lamf * dhv[j];  // x_p - x_{p-1}
             const float y = add_rn(x, mul_rn(cmf, dx));
             ay = add_rn(ax, mul_rn(cmf, fmaf(alpha, dx, jl * f)));
             const float y2 = mul_rn(y, y);
@@ -892,7 +968,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       const bool running = valid && c1.status == DCX_STOP_RUNNING;
       const bool use_y = has_prev && c1.accept;
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
+      uint8_t* hb = reinterpret_cast<uint8_t*>(a.xh[cur ^ 1]) + (int64_t)r * 2 * a.npad + gbase;
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
+      const int e_next = f8 ? f8_scale_exp(c1.step, sm.lamd[rl], pk == 0) : 0;
+      const float qsc = ldexpf(1.f, e_next), qdesc = ldexpf(1.f, -e_next);
 #pragma unroll 1
       for (int off = 0; off < HW; off += 16) {
         uint32_t rv[16], st[16], ayv[16];
@@ -901,20 +980,35 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         tmem_ld16(lane_base + rcol(pk + 1) + off, ayv);
         tmem_ld_wait();
         __align__(16) __half2 hv[8];
+        __align__(16) uint16_t bv[8];
         __align__(16) uint32_t sv[4];
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
-          __half d[2];
+          float dv[2], scv[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const float sc = __uint_as_float(st[j + u]);
+            scv[u] = sc;
             const float x = lamf * sc;
             const float v = use_y ? __uint_as_float(ayv[j + u]) : fmaf(alpha, x, jl * __uint_as_float(rv[j + u]));
             const float nx = cbrt_lean(v * inv_beta);
-            d[u] = __float2half_rn(running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f);
-            st[j + u] = __float_as_uint(__fadd_rn(sc, __half2float(d[u])));
+            dv[u] = running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f;
           }
-          hv[j / 2] = __halves2half2(d[0], d[1]);
+          float dq[2];
+          if (f8) {
+            const uint16_t q2 = e4m3x2(dv[0] * qsc, dv[1] * qsc);
+            const float2 b2 = e4m3x2_to_f2(q2);
+            dq[0] = b2.x * qdesc;
+            dq[1] = b2.y * qdesc;
+            bv[j / 2] = q2;
+          } else {
+            const __half h0 = __float2half_rn(dv[0]), h1 = __float2half_rn(dv[1]);
+            dq[0] = __half2float(h0);
+            dq[1] = __half2float(h1);
+            hv[j / 2] = __halves2half2(h0, h1);
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) st[j + u] = __float_as_uint(__fadd_rn(scv[u], dq[u]));
           if ((j & 3) == 2) {  // sign(x_{p+1}) - sign(x_p) per byte (see the DOCH update)
             const uint32_t ob = uint32_t(curmask >> (off + j - 2)) & 0xFu;
             const uint32_t nb = (st[j - 2] >> 31) | ((st[j - 1] >> 31) << 1) | ((st[j] >> 31) << 2) |
@@ -922,16 +1016,21 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             const uint32_t df = ob ^ nb, neg = df & nb;
             const uint32_t dfw = (df & 1u) | ((df & 2u) << 7) | ((df & 4u) << 14) | ((df & 8u) << 21);
             const uint32_t ngw = (neg & 1u) | ((neg & 2u) << 7) | ((neg & 4u) << 14) | ((neg & 8u) << 21);
-            sv[j / 4] = dfw * 2u + ngw * 0xfcu;
+            sv[j / 4] = f8 ? dfw * 0x40u + ngw * 0x80u : dfw * 2u + ngw * 0xfcu;
           }
         }
         tmem_st16(xaddr + off, st);
         if (valid && lim > 0) {  // stopped replicas write zero deltas
-          *reinterpret_cast<uint4*>(hn + off) = *reinterpret_cast<uint4*>(hv);
-          *reinterpret_cast<uint4*>(hn + off + 8) = *reinterpret_cast<uint4*>(hv + 4);
+          if (f8) {
+            *reinterpret_cast<uint4*>(hb + off) = *reinterpret_cast<uint4*>(bv);
+          } else {
+            *reinterpret_cast<uint4*>(hn + off) = *reinterpret_cast<uint4*>(hv);
+            *reinterpret_cast<uint4*>(hn + off + 8) = *reinterpret_cast<uint4*>(hv + 4);
+          }
           *reinterpret_cast<uint4*>(sn + off) = *reinterpret_cast<uint4*>(sv);
         }
       }
+      fdesc = qdesc;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -1003,10 +1102,15 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       if (a.dbg && threadIdx.x == 128) sm.tdbg[2] = clock();
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 11] = clock64();
       __half* hn = a.xh[cur ^ 1] + (int64_t)r * a.npad + gbase;
+      uint8_t* hb = reinterpret_cast<uint8_t*>(a.xh[cur ^ 1]) + (int64_t)r * 2 * a.npad + gbase;  // f8 view
       int8_t* sn = a.s8[cur ^ 1] + (int64_t)r * a.npad + gbase;
       float* xg = a.xm[cur] + (int64_t)r * a.npad + gbase;  // x_p (time-budget runs only)
       // one chunk of W columns starting at column `off` of this warp's half (bits off.. of the masks)
       const float lamf = sm.lam[rl];
+      const bool f8 = a.f8 != 0;
+      // f8: the scale 2^e of Dh_{p+1} from the step of Dh_p (the same in every CTA of the group)
+      const int e_next = f8 ? f8_scale_exp(c.step, sm.lamd[rl], p == 0) : 0;
+      const float qsc = ldexpf(1.f, e_next), qdesc = ldexpf(1.f, -e_next);
       auto chunk = [&](auto wc, const int off) {
         constexpr int W = decltype(wc)::value;
         // fv: F_p = Q Dh_p (fresh), rv: R_{p-1}, replaced by R_p = R_{p-1} + F_p (one
@@ -1026,6 +1130,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
                             lamf * __uint_as_float(st[j + 2]), lamf * __uint_as_float(st[j + 3]));
         }
         __align__(16) __half2 hv[W / 2];
+        __align__(16) uint16_t bv[W / 2];  // f8: e4m3 pairs
         __align__(16) uint32_t sv[W / 4];
         if (lim > 0) {
           // branch-free over all W columns (s is never -0.0 after the first update, so s < 0
@@ -1035,12 +1140,14 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           uint32_t m = 0;
 #pragma unroll
           for (int j = 0; j < W; j += 2) {
-            __half dh[2];
+            float dv[2], scv[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const float rr = __fadd_rn(__uint_as_float(rv[j + u]), __uint_as_float(fv[j + u]));
+              // R_p = R_{p-1} + 2^-e_p F_p (the power-of-two descale is exact; 1 for f16 products)
+              const float rr = fmaf(__uint_as_float(fv[j + u]), fdesc, __uint_as_float(rv[j + u]));
               rv[j + u] = __float_as_uint(rr);
               const float sc = __uint_as_float(st[j + u]);
+              scv[u] = sc;
               const float x = lamf * sc;
               const float ax = fmaf(alpha, x, jl * rr);
               const float nx = cbrt_lean(ax * inv_beta);
@@ -1048,15 +1155,29 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               s4 = fmaf(x2, x2, s4);
               sxax = fmaf(x, ax, sxax);
               m |= (st[j + u] >> 31) << (j + u);
-              // the next delta: T(x_p) - x_p in units of lambda, rounded to f16 (zero once the
-              // replica stopped, so a frozen replica adds nothing); the iterate moves by
-              // exactly lambda Dh, so the step |x_{p+1} - x_p| is lambda |Dh|
-              dh[u] = __float2half_rn(running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f);
-              const float dhf = __half2float(dh[u]);
-              step = fmaxf(step, fabsf(dhf));
-              st[j + u] = __float_as_uint(__fadd_rn(sc, dhf));
+              // the next delta: T(x_p) - x_p in units of lambda (zero once the replica stopped,
+              // so a frozen replica adds nothing), rounded to f16 or to a scaled e4m3; the
+              // iterate moves by exactly lambda Dh, so the step |x_{p+1} - x_p| is lambda |Dh|
+              dv[u] = running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f;
             }
-            hv[j / 2] = __halves2half2(dh[0], dh[1]);
+            float dq[2];
+            if (f8) {
+              const uint16_t q2 = e4m3x2(dv[0] * qsc, dv[1] * qsc);
+              const float2 b2 = e4m3x2_to_f2(q2);
+              dq[0] = b2.x * qdesc;
+              dq[1] = b2.y * qdesc;
+              bv[j / 2] = q2;
+            } else {
+              const __half h0 = __float2half_rn(dv[0]), h1 = __float2half_rn(dv[1]);
+              dq[0] = __half2float(h0);
+              dq[1] = __half2float(h1);
+              hv[j / 2] = __halves2half2(h0, h1);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              step = fmaxf(step, fabsf(dq[u]));
+              st[j + u] = __float_as_uint(__fadd_rn(scv[u], dq[u]));
+            }
             if ((j & 3) == 2) {
               // 4 spins -> 4 bytes of sign(x_{p+1}) - sign(x_p): +2 where the sign went - -> +,
               // -2 (0xfe) where it went + -> -, else 0
@@ -1066,7 +1187,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               const uint32_t df = ob ^ nb, neg = df & nb;
               const uint32_t dfw = (df & 1u) | ((df & 2u) << 7) | ((df & 4u) << 14) | ((df & 8u) << 21);
               const uint32_t ngw = (neg & 1u) | ((neg & 2u) << 7) | ((neg & 4u) << 14) | ((neg & 8u) << 21);
-              sv[j / 4] = dfw * 2u + ngw * 0xfcu;
+              // int8 +2 / -2 (0x02 / 0xfe), or e4m3 +2.0 / -2.0 (0x40 / 0xc0)
+              sv[j / 4] = f8 ? dfw * 0x40u + ngw * 0x80u : dfw * 2u + ngw * 0xfcu;
             }
           }
           curmask |= uint64_t(m) << off;
@@ -1074,8 +1196,13 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         tmem_stw<W>(lane_base + rcol(p) + off, rv);
         tmem_stw<W>(xaddr + off, st);
         if (valid && lim > 0) {  // stopped replicas write zero deltas
+          if (f8) {
 #pragma unroll
-          for (int j = 0; j < W / 2; j += 4) *reinterpret_cast<uint4*>(hn + off + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
+            for (int j = 0; j < W / 2; j += 8) *reinterpret_cast<uint4*>(hb + off + 2 * j) = *reinterpret_cast<uint4*>(bv + j);
+          } else {
+#pragma unroll
+            for (int j = 0; j < W / 2; j += 4) *reinterpret_cast<uint4*>(hn + off + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
+          }
           store_pm1(sn + off, sv, W / 4);
         }
       };
@@ -1085,6 +1212,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       if constexpr (HW % 16 != 0) chunk(std::integral_constant<int, 8>{}, HW - 8);
       const bool tr128 = a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096;
       if (tr128) a.dbg[p * 12 + 3] = clock64();
+      fdesc = qdesc;  // F_{p+1} = Q (2^e_next Dh_{p+1})
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&sm.d1free));  // D1 read: GEMM1(p+1) may overwrite it
@@ -1117,7 +1245,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll
         for (int j = 0; j < HW; ++j) {
           const int m = -int((curmask >> j) & 1);
-          const int v = (j < lim) ? int(v2[j]) : 0;
+          const int v = (j < lim) ? (f8 ? __float2int_rn(__uint_as_float(v2[j])) : int(v2[j])) : 0;
           es += (v ^ m) - m;
         }
       }
@@ -1175,6 +1303,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll
       for (int j = 0; j < HW; ++j)
         if (j < lim) a.xm[0][o + j] = a.xm[1][o + j] = lamf * __uint_as_float(v[j]);
+    if (valid && h == 0 && a.f8) a.dsc[r] = fdesc;
     if (valid) {
       // sign(x_{p-1}): the pending best copy of the last pass (unpack_results) and the
       // prevmask of a resumed launch
@@ -1216,7 +1345,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 // (also the DOCH delta start: Dh_0 = f16(x_0 / lambda) against s_{-1} = 0, so
 // s_0 = f32(Dh_0); dS_0 = sign(x_0) against sign(x_{-1}) = 0)
 __global__ void pack_state(const float* src, int n, int R, int npad, const RepCtl* ctl, float* xm, __half* xh,
-                           int8_t* s8, float* xhat) {
+                           int8_t* s8, float* xhat, int f8) {
   const int64_t total = int64_t(n) * R;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx / R;
@@ -1227,7 +1356,8 @@ __global__ void pack_state(const float* src, int n, int R, int npad, const RepCt
     const __half h = __float2half_rn(x * inv_lam);
     xh[(int64_t)r * npad + i] = h;
     xhat[(int64_t)r * npad + i] = __half2float(h);
-    s8[(int64_t)r * npad + i] = x >= 0.f ? 1 : -1;
+    // dS_0 = sign(x_0): int8 +-1, or e4m3 +-1.0 (0x38 / 0xb8) for the e4m3 sign GEMM
+    s8[(int64_t)r * npad + i] = f8 ? (x >= 0.f ? int8_t(0x38) : int8_t(0xb8)) : (x >= 0.f ? 1 : -1);
   }
 }
 // pending best copy of the last executed pass, then [Rpad][npad] -> [n][R]
@@ -1260,8 +1390,8 @@ __global__ void min_abs_nonzero(const double* A, int64_t total, unsigned long lo
 }
 // Q = A / scale into the padded f16 and int8 operand matrices; flags any entry
 // that is not an exact integer in [-127, 127]
-__global__ void q_expand(const double* A, double scale, __half* out, int8_t* out8, int64_t n, int64_t npad,
-                         unsigned long long* bad) {
+__global__ void q_expand(const double* A, double scale, __half* out, int8_t* out8, uint8_t* oute4, int64_t n,
+                         int64_t npad, unsigned long long* bad) {
   const int64_t total = npad * npad;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx / npad, j = idx % npad;
@@ -1274,6 +1404,9 @@ __global__ void q_expand(const double* A, double scale, __half* out, int8_t* out
     }
     out[idx] = __int2half_rn(v);
     out8[idx] = int8_t(v);
+    // e4m3 copy for the f8 products: exact for |q| <= 16 (bad[1] marks larger entries)
+    if (v > 16 || v < -16) bad[1] = 1;
+    oute4[idx] = uint8_t(e4m3x2(float(v), 0.f) & 0xffu);
   }
 }
 
@@ -1294,9 +1427,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 2-D row-major [rows][cols] map, 128-byte rows x 128 rows per box (64 f16 or
 // 128 int8 along K), 128-byte swizzle: the canonical K-major SW128 UMMA layout.
-static void make_map(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, bool f16, uint32_t box_rows = 128) {
+static void make_map(CUtensorMap* m, void* base, uint64_t cols, uint64_t rows, bool f16, uint32_t box_rows = 128,
+                     uint64_t stride_bytes = 0) {
   const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {cols * (f16 ? 2 : 1)};
+  const cuuint64_t strides[1] = {stride_bytes ? stride_bytes : cols * (f16 ? 2 : 1)};
   const cuuint32_t box[2] = {f16 ? cuuint32_t(tc::TK) : cuuint32_t(2 * tc::TK), box_rows};  // 128-byte rows
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims,
@@ -1338,6 +1472,8 @@ void DenseDev::release_run() {
   if (xhat) cudaFree(xhat);
   if (d1g) cudaFree(d1g);
   if (d2g) cudaFree(d2g);
+  if (dsc) cudaFree(dsc);
+  dsc = nullptr;
   sgnl = nullptr;
   xhat = d1g = d2g = nullptr;
   if (part) cudaFree(part);
@@ -1352,7 +1488,8 @@ void DenseDev::release() {
   release_run();
   if (q16) cudaFree(q16);
   if (q8) cudaFree(q8);
-  q16 = q8 = nullptr;
+  if (q8e) cudaFree(q8e);
+  q16 = q8 = q8e = nullptr;
   if (tmaps) delete[] reinterpret_cast<CUtensorMap*>(tmaps);
   tmaps = nullptr;
   if (scratch) cudaFree(scratch);
@@ -1372,7 +1509,7 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.exact = false;
   // exact small-integer form J = jscale * Q (the K2000 instance: jscale = 1/2, Q = -W),
   // found and converted on the device: min |nonzero| gives the candidate scale
-  const size_t need = size_t(n * n) * 8 + 16;
+  const size_t need = size_t(n * n) * 8 + 24;
   if (d.scratch_bytes < need) {
     if (d.scratch) cudaFree(d.scratch);
     d.scratch = nullptr;
@@ -1383,8 +1520,8 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   double* dA = static_cast<double*>(d.scratch);
   unsigned long long* dw = reinterpret_cast<unsigned long long*>(static_cast<char*>(d.scratch) + size_t(n * n) * 8);
   DCK(cudaMemcpyAsync(dA, A, n * n * 8, cudaMemcpyHostToDevice, s));
-  const unsigned long long init[2] = {~0ull, 0ull};
-  DCK(cudaMemcpyAsync(dw, init, 16, cudaMemcpyHostToDevice, s));
+  const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+  DCK(cudaMemcpyAsync(dw, init, 24, cudaMemcpyHostToDevice, s));
   tc::min_abs_nonzero<<<1024, 256, 0, s>>>(dA, n * n, dw);
   unsigned long long mnbits = 0;
   DCK(cudaMemcpyAsync(&mnbits, dw, 8, cudaMemcpyDeviceToHost, s));
@@ -1395,15 +1532,17 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
     std::memcpy(&mn, &mnbits, 8);
     if (!d.q16) DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
     if (!d.q8) DCK(cudaMalloc(&d.q8, d.npad * d.npad));
+    if (!d.q8e) DCK(cudaMalloc(&d.q8e, d.npad * d.npad));
     for (double cand : {mn, 1.0, 0.5}) {
-      DCK(cudaMemsetAsync(dw + 1, 0, 8, s));
+      DCK(cudaMemsetAsync(dw + 1, 0, 16, s));
       tc::q_expand<<<1024, 256, 0, s>>>(dA, cand, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8),
-                                        n, d.npad, dw + 1);
-      unsigned long long bad = 1;
-      DCK(cudaMemcpyAsync(&bad, dw + 1, 8, cudaMemcpyDeviceToHost, s));
+                                        reinterpret_cast<uint8_t*>(d.q8e), n, d.npad, dw + 1);
+      unsigned long long bad[2] = {1, 1};
+      DCK(cudaMemcpyAsync(bad, dw + 1, 16, cudaMemcpyDeviceToHost, s));
       DCK(cudaStreamSynchronize(s));
-      if (!bad) {
+      if (!bad[0]) {
         scale = cand;
+        d.f8ok = bad[1] == 0;
         break;
       }
     }
@@ -1412,7 +1551,7 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.jscale = float(scale);
   d.jscale_d = scale;  // exact: the energies of returned spins are jscale_d * (integer GEMM)
   d.exact = true;
-  if (!d.tmaps) d.tmaps = new CUtensorMap[6];
+  if (!d.tmaps) d.tmaps = new CUtensorMap[8];
 }
 
 static size_t dense_smem_bytes(int nc, int tn) {
@@ -1485,6 +1624,14 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   DCK(cudaMemsetAsync(d.xhat, 0, vec * 4, s));  // padding; pack_state writes the live entries
   DCK(cudaMemsetAsync(d.d1g, 0, vec * 4, s));
   DCK(cudaMemsetAsync(d.d2g, 0, vec * 4, s));
+  // e4m3 delta products (iterations >= 1): Q exact in e4m3, 128-wide spin tiles (16-byte
+  // aligned stores); DCX_DENSE_F8=0 keeps f16 deltas and the int8 sign GEMM
+  {
+    const char* e = std::getenv("DCX_DENSE_F8");
+    // (DOCH only: the ADOCH kernel's e4m3 update path is not validated -- it keeps f16 deltas)
+    d.f8 = d.f8ok && d.tn == 128 && !d.ad && !(e && std::atoi(e) == 0);
+  }
+  if (!d.dsc) DCK(cudaMalloc(&d.dsc, sizeof(float) * d.Rpad));
   {
     const int gsz = 128 * d.nc;
     const int ngroups = d.Rpad / gsz;
@@ -1505,7 +1652,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
                                        reinterpret_cast<__half*>(d.xh[0]), reinterpret_cast<int8_t*>(d.s8[0]),
-                                       reinterpret_cast<float*>(d.xhat));
+                                       reinterpret_cast<float*>(d.xhat), d.f8 ? 1 : 0);
   DCK(cudaGetLastError());
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(d.tmaps);
   make_map(&maps[0], d.xh[0], d.npad, d.Rpad, true);
@@ -1513,7 +1660,10 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   make_map(&maps[2], d.q16, d.npad, d.npad, true, uint32_t(d.tn / d.nc));
   make_map(&maps[3], d.s8[0], d.npad, d.Rpad, false);
   make_map(&maps[4], d.s8[1], d.npad, d.Rpad, false);
-  make_map(&maps[5], d.q8, d.npad, d.npad, false, uint32_t(d.tn / d.nc));
+  make_map(&maps[5], d.f8 ? d.q8e : d.q8, d.npad, d.npad, false, uint32_t(d.tn / d.nc));
+  // e4m3 views of the delta buffers: npad bytes of each 2 npad-byte f16 row
+  make_map(&maps[6], d.xh[0], d.npad, d.Rpad, false, 128, uint64_t(d.npad) * 2);
+  make_map(&maps[7], d.xh[1], d.npad, d.Rpad, false, 128, uint64_t(d.npad) * 2);
   if (d.ad) {
     if (d.nc == 1) dense_set_smem<1, 128, true>();
     else dense_set_smem<2, 128, true>();
@@ -1536,6 +1686,10 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.tmS[0] = maps[3];
   a.tmS[1] = maps[4];
   a.tmQ8 = maps[5];
+  a.tmA8[0] = maps[6];
+  a.tmA8[1] = maps[7];
+  a.f8 = d.f8 ? 1 : 0;
+  a.dsc = reinterpret_cast<float*>(d.dsc);
   for (int b = 0; b < 2; ++b) {
     a.xm[b] = reinterpret_cast<float*>(d.xm[b]);
     a.xh[b] = reinterpret_cast<__half*>(d.xh[b]);

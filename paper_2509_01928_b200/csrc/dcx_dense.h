@@ -15,6 +15,10 @@ struct DenseDev {
   double jscale_d = 1.0;  // the same scale in double (energy scale: exact for non-dyadic scales)
   void* q16 = nullptr;   // f16 Q [npad][npad]
   void* q8 = nullptr;    // int8 Q [npad][npad] (energy GEMM)
+  void* q8e = nullptr;   // e4m3 Q [npad][npad] (f8 products; exact when |q| <= 16)
+  bool f8ok = false;     // Q exact in e4m3
+  bool f8 = false;       // this run multiplies e4m3 deltas (iterations >= 1)
+  void* dsc = nullptr;   // f8: per-replica descale of the last written delta [Rpad] (between launches)
   // per-run buffers
   int R = 0, Rpad = 0;
   int nc = 1;  // CTAs per MMA (2: cta_group::2 pairs)
