@@ -9,7 +9,9 @@ NVLink). Per iteration every rank
   1. runs the fused pass over its rows (``dcx_dist_pass``): (J+aI)x, the cube-root
      update of its slice of x, and its share of the per-replica sums
      (sum x^4, sum x.Ax, sum s.Js, max |dx|),
-  2. all-reduces those sums (SUM) and maxima (MAX) -- 8 doubles per replica,
+  2. combines those sums and maxima over the ranks with ONE collective: an
+     all-gather of every rank's 8 doubles per replica, reduced on the device in
+     rank order (so the totals do not depend on the collective's reduction order),
   3. runs the control on the reduced values (``dcx_dist_control``): identical on
      every rank, so stop / record / ADOCH-accept decisions agree,
   4. exchanges the new x slices for the next pass: either an all-gather of every
@@ -20,11 +22,17 @@ NVLink). Per iteration every rank
      moves less than 3/4 of the all-gather volume.
 
 Blocks are padded to a common row count B so the all-gather is a plain
-``all_gather_into_tensor``; columns are remapped into that padded index space
-(rank q's rows live at [q*B, q*B + rows_q)). The remap is monotone, so each
-row's sum order -- and therefore every iterate -- is bit-identical to the
-single-GPU multipass path; only the order of the H partial sums across blocks
-differs.
+``all_gather_into_tensor``; with the all-gather exchange the columns are
+remapped into that padded index space (rank q's rows live at [q*B, q*B + rows_q)).
+With the neighbour-only exchange each rank's columns are remapped into a
+COMPACT space [own rows | halo rows]: its B own rows first, then exactly the H
+remote rows it references, in the order they arrive (source rank, position), so
+a rank holds B + H rows of x instead of world * B (the 10^8-spin R8 graph: a
+fraction of the 400 MB state per GPU) and receives its halo straight into the
+tail of its x buffer. The CSR entries of a row keep their order under either
+remap, so each row's sum order -- and therefore every iterate -- is
+bit-identical to the single-GPU multipass path; only the order of the H partial
+sums across blocks differs.
 
 With the NCCL backend the collectives run on the context stream directly on
 device buffers; with gloo (CPU transport) they are staged through host memory.
@@ -170,6 +178,42 @@ class Exchange:
             out = o.cpu()
         return out.numpy()
 
+    def halo_compact(self, X, plan: HaloPlan, send_local, B: int):
+        """Neighbour-only exchange into the compact space X [B + H, R]: own rows send_local go out,
+        the halo arrives in rows [B, B + H) in plan order."""
+        dist = self.dist
+        send = X.index_select(0, send_local)
+        tail = X[B:B + plan.volume]
+        if not self.host_staged:
+            dist.all_to_all_single(tail, send, plan.recv_counts, plan.send_counts, group=self.group)
+            return
+        h = tail.cpu()
+        dist.all_to_all_single(h, send.cpu(), plan.recv_counts, plan.send_counts, group=self.group)
+        tail.copy_(h.to(X.device))
+
+    def combine(self, qs, qm):
+        """One collective for the per-replica partials: all-gather every rank's [R][QSUM + QMAX],
+        then sum / max over ranks in rank order (deterministic, collective-order independent)."""
+        import torch
+
+        mine = torch.cat([qs, qm], 1).contiguous()
+        allq = torch.empty((self.world,) + tuple(mine.shape), dtype=mine.dtype, device=mine.device)
+        if not self.host_staged:
+            self.dist.all_gather_into_tensor(allq, mine, group=self.group)
+        else:
+            h = mine.cpu()
+            parts = [torch.empty_like(h) for _ in range(self.world)]
+            self.dist.all_gather(parts, h, group=self.group)
+            allq.copy_(torch.stack(parts, 0))
+        ks = qs.shape[1]
+        s = allq[0, :, :ks].clone()
+        m = allq[0, :, ks:].clone()
+        for q in range(1, self.world):
+            s += allq[q, :, :ks]
+            m = torch.maximum(m, allq[q, :, ks:])
+        qs.copy_(s)
+        qm.copy_(m)
+
     def halo(self, X, plan: HaloPlan, send_idx, recv_idx, recv_buf):
         """Neighbour-only exchange into X [world*B, R]: rows send_idx go out, rows recv_idx come in."""
         dist = self.dist
@@ -220,6 +264,22 @@ def halo_needs(cols_padded, rb: RowBlocks, rank: int):
     remote = c[(c < lo) | (c >= hi)]
     counts = np.bincount(remote // rb.B, minlength=rb.world).astype(np.int64)
     return remote, [int(k) for k in counts]
+
+
+def compact_columns(cols_padded, rb: RowBlocks, rank: int, plan: "HaloPlan"):
+    """Padded-space columns of this rank's block -> the compact [own B rows | halo rows] space:
+    own positions p -> p - rank * B, remote ones -> B + their index in plan.recv_pos (sorted)."""
+    c = np.asarray(cols_padded, dtype=np.int64)
+    lo = rank * rb.B
+    own = (c >= lo) & (c < lo + rb.B)
+    out = np.empty_like(c)
+    out[own] = c[own] - lo
+    rem = ~own
+    idx = np.searchsorted(plan.recv_pos, c[rem])
+    if rem.any() and (idx.max() >= plan.recv_pos.size or np.any(plan.recv_pos[idx] != c[rem])):
+        raise RuntimeError("compact remap: a remote column is missing from the halo plan")
+    out[rem] = rb.B + idx
+    return out
 
 
 def halo_plan(ex: "Exchange", cols_padded, rb: RowBlocks) -> HaloPlan:
@@ -276,9 +336,24 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         tdev = torch.device("cuda", dev)
     else:
         ctx, tdev = _context, torch.device("cpu")
-    ctx.set_csr_block(n_rows, rb.n_space, ex.rank * rb.B, vals, cols, ro)
+    # exchange plan (setup, once per solve): neighbour-only halo in a compact index space, or
+    # the all-gather of the padded space
+    use_halo = False
+    if exchange != "allgather" and ex.world > 1:
+        plan = halo_plan(ex, cols, rb)
+        use_halo = exchange == "halo"
+        if exchange == "auto":
+            vol = torch.tensor([float(plan.volume), float(rb.n_space - rb.B)], dtype=torch.float64, device=tdev)
+            ex.all_reduce(vol, "sum")
+            use_halo = bool(vol[0] < 0.75 * vol[1])
+    if use_halo:
+        space, base = rb.B + plan.volume, 0
+        ctx.set_csr_block(n_rows, space, base, vals, compact_columns(cols, rb, ex.rank, plan), ro)
+    else:
+        space, base = rb.n_space, ex.rank * rb.B
+        ctx.set_csr_block(n_rows, space, base, vals, cols, ro)
     dt = torch.float64 if precision == "f64" else torch.float32
-    X = [torch.zeros(rb.n_space, R, dtype=dt, device=tdev) for _ in range(2)]
+    X = [torch.zeros(space, R, dtype=dt, device=tdev) for _ in range(2)]
     qs = torch.zeros(R, _native.QSUM, dtype=torch.float64, device=tdev)
     qm = torch.zeros(R, _native.QMAX, dtype=torch.float64, device=tdev)
     prm = _native.Params(
@@ -289,22 +364,13 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         path=_native.PATH["multipass"], chunk=0, reserved=0)
     stream = (torch.cuda.ExternalStream(ctx.stream(), device=tdev) if tdev.type == "cuda" else None)
     with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
-        use_halo = exchange == "halo"
-        if exchange != "allgather" and ex.world > 1:
-            plan = halo_plan(ex, cols, rb)
-            if exchange == "auto":
-                vol = torch.tensor([float(plan.volume), float(rb.n_space - rb.B)], dtype=torch.float64,
-                                   device=tdev)
-                ex.all_reduce(vol, "sum")
-                use_halo = bool(vol[0] < 0.75 * vol[1])
-        if use_halo and ex.world > 1:
-            send_idx = torch.from_numpy(plan.send_pos).to(tdev)
-            recv_idx = torch.from_numpy(plan.recv_pos).to(tdev)
-            recv_buf = torch.empty(plan.volume, R, dtype=dt, device=tdev)
-            step = lambda Xp: ex.halo(Xp, plan, send_idx, recv_idx, recv_buf)  # noqa: E731
-        else:
-            use_halo = False
+        if use_halo:
+            send_local = torch.from_numpy(plan.send_pos - ex.rank * rb.B).to(tdev)
+            step = lambda Xp: ex.halo_compact(Xp, plan, send_local, rb.B)  # noqa: E731
+        elif ex.world > 1:
             step = lambda Xp: ex.all_gather_rows(Xp, rb.B)  # noqa: E731
+        else:
+            step = lambda Xp: None  # noqa: E731  (one rank: x is all local)
         ctx.dist_begin(prm, alpha, beta, X0[:, r0:r1], X[0].data_ptr(), X[1].data_ptr(), qs.data_ptr(),
                        qm.data_ptr())
         offset = time.perf_counter() - t_entry
@@ -313,8 +379,8 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         while live:
             for _ in range(max(1, int(poll_every))):
                 ctx.dist_pass()
-                ex.all_reduce(qs, "sum")
-                ex.all_reduce(qm, "max")
+                if ex.world > 1:
+                    ex.combine(qs, qm)  # one collective for the SUM and MAX partials
                 ctx.dist_control()
                 p += 1
                 step(X[p & 1])

@@ -262,3 +262,46 @@ def gpu_worker(rank, world, init_file, out_file, solver, precision, R, max_iters
                                     for r in res], dtype=bool))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def compact_worker(rank, world, init_file, out_file, kind, n):
+    """Compact [own | halo] space: after the exchange every referenced remote row sits at
+    B + its plan index, so the compact block's product equals the padded block's; and the
+    one-collective combine of the per-replica partials equals SUM / MAX."""
+    import torch
+
+    import paper_2509_01928_b200 as dc
+    from paper_2509_01928_b200 import dist as dd
+
+    dist = init_group(rank, world, init_file)
+    v, c, o, _ = graph_of(kind, n, 0)
+    J = dc.CsrCoupling(n, v, c, o, validate=False)
+    rb = dd.RowBlocks(dd.partition_rows(o, world), n)
+    n_rows, vals, cols, ro = dd.local_block(J, rb, rank)
+    ex = dd.Exchange()
+    plan = dd.halo_plan(ex, cols, rb)
+    ccols = dd.compact_columns(cols, rb, rank, plan)
+    space = rb.B + plan.volume
+    # a state defined on the padded space: row value = f(global spin index)
+    full = np.zeros((rb.n_space, 2))
+    glob = np.concatenate([np.arange(r0, r1) for r0, r1 in rb.blocks])
+    pos = rb.position(glob)
+    full[pos, 0] = np.sin(glob + 0.5)
+    full[pos, 1] = np.cos(3.0 * glob)
+    X = torch.zeros(space, 2, dtype=torch.float64)
+    lo = rank * rb.B
+    X[:rb.B] = torch.from_numpy(full[lo:lo + rb.B])
+    ex.halo_compact(X, plan, torch.from_numpy(plan.send_pos - lo), rb.B)
+    A_pad = sp.csr_matrix((vals, cols, ro), shape=(n_rows, rb.n_space))
+    A_cmp = sp.csr_matrix((vals, ccols, ro), shape=(n_rows, space))
+    ok = bool(np.array_equal(A_pad @ full, A_cmp @ X.numpy()))
+    qs = torch.full((3, 5), float(rank + 1), dtype=torch.float64) * torch.arange(1, 6, dtype=torch.float64)
+    qm = torch.tensor([[float(rank), -float(rank), 0.5]] * 3, dtype=torch.float64)
+    ex.combine(qs, qm)
+    info = torch.tensor([plan.volume, space, rb.n_space, int(ok)], dtype=torch.int64)
+    allinfo = [torch.zeros_like(info) for _ in range(world)]
+    dist.all_gather(allinfo, info)
+    if rank == 0:
+        np.savez(out_file, info=torch.stack(allinfo).numpy(), qs=qs.numpy(), qm=qm.numpy())
+    dist.barrier()
+    dist.destroy_process_group()

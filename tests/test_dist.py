@@ -19,7 +19,7 @@ import scipy.sparse as sp
 import paper_2509_01928_b200 as dc
 from paper_2509_01928_b200 import dist as dd, synth
 
-from _dist_helpers import exchange_worker, fake_worker, gpu_worker, halo_plan_worker
+from _dist_helpers import compact_worker, exchange_worker, fake_worker, gpu_worker, halo_plan_worker
 
 
 def _spawn(fn, world, *args):
@@ -100,6 +100,22 @@ def test_halo_plan_random_3_regular_is_a_fraction_of_allgather():
     B = out[0, 3]
     # each rank references ~ (1 - exp(-3 x rows/remote rows)) of the remote rows
     assert np.all(out[:, 0] < 2 * B * 0.85)
+
+
+@pytest.mark.parametrize("kind,world", [("reg3", 4), ("torus", 3)])
+def test_compact_halo_space_and_one_collective_combine(kind, world):
+    """Neighbour-only exchange into the compact [own | halo] space: a rank holds B + H rows of x
+    (not world * B), the compact CSR block reproduces the padded block's product exactly, and
+    the per-replica partials need one all-gather (sum / max in rank order)."""
+    out = _spawn(compact_worker, world, kind, 24_000 if kind == "reg3" else 48 * 48)
+    info = out["info"]
+    assert np.all(info[:, 3] == 1)
+    assert np.all(info[:, 1] < info[:, 2])  # compact space smaller than the padded one
+    if kind == "torus":
+        assert np.all(info[:, 1] <= info[:, 2] / world + 2 * 48 + 8)  # own strip + two lattice rows
+    ranks = np.arange(1, world + 1, dtype=np.float64)
+    np.testing.assert_array_equal(out["qs"], np.tile(ranks.sum() * np.arange(1, 6), (3, 1)))
+    np.testing.assert_array_equal(out["qm"], np.tile([world - 1.0, 0.0, 0.5], (3, 1)))
 
 
 # ---------------------------------------------------- driver (CPU, gloo, fake)
