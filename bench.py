@@ -60,12 +60,14 @@ def reference_k2(solver="doch"):
 
 def traffic_bytes(config: str, kernel: str, iterations: int):
     """DRAM bytes of one profiled launch of `kernel` on `config` from the committed ncu
-    capture (profiles/r1_traffic.json: dram__bytes_read + dram__bytes_write per iteration)."""
-    try:
-        with open(ROOT / "profiles" / "r1_traffic.json") as f:
-            return float(json.load(f)[f"{config}:{kernel}"]["dram_bytes_per_iteration"]) * iterations
-    except (OSError, KeyError, ValueError):
-        return None
+    captures (profiles/r2_traffic.json, then r1: dram__bytes_read + dram__bytes_write per iteration)."""
+    for name in ("r2_traffic.json", "r1_traffic.json"):  # newest capture first
+        try:
+            with open(ROOT / "profiles" / name) as f:
+                return float(json.load(f)[f"{config}:{kernel}"]["dram_bytes_per_iteration"]) * iterations
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def peaks():
