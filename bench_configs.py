@@ -65,16 +65,10 @@ def _instance(name):
         v, c, o, co = (synth.erdos_renyi(n, 8, seed=0, device=dev) if name == "e7"
                        else synth.random_regular3(n, seed=0, device=dev))
         J = dc.CsrCoupling(n, v, c, o, validate=False)
-        # Wigner estimate (n >= 1e4) of dc/spectral.py:175-189 at eta = 1
-        s1, s2 = float(v.sum()), float((v * v).sum())
-        cnt = n * (n - 1)
-        mean = s1 / cnt
-        lam = 2.0 * np.sqrt(max(s2 / cnt - mean * mean, 0.0)) * np.sqrt(n)
-        rows = np.repeat(np.arange(n), np.diff(o))
-        rmax = float(np.bincount(rows, weights=np.abs(v), minlength=n).max())
-        alpha = lam
-        beta = n * np.sqrt(n) * (alpha + rmax)
-        return dc.ProblemInstance(coupling=J, cut_offset=co), alpha, beta, (v, c, o)
+        # derive_params at eta = 1: the Wigner estimate (n >= 1e4, dc/spectral.py:175-189) and
+        # beta's max row |J|_1, both from the device row statistics (dcx_row_stats)
+        p = dc.derive_params(J, eta=1.0)
+        return dc.ProblemInstance(coupling=J, cut_offset=co), p.alpha, p.beta, (v, c, o)
     raise ValueError(name)
 
 

@@ -128,6 +128,11 @@ DCX_API int dcx_coupling(const dcx_ctx* ctx, dcx_coupling_info* out);
  * over j != i, f64 -- offdiag_moments and abs_row_sums (dc/coupling.py:248-268). */
 DCX_API int dcx_set_procedural(dcx_ctx* ctx, int64_t n, int64_t seed, int32_t formula);
 DCX_API int dcx_proc_row_stats(dcx_ctx* ctx, double* out /* [n][3] */);
+/* dcx_row_stats: the same [n][3] row statistics for any coupling on the device (CSR rows
+ * summed in column order, dense rows by a fixed-order warp tree, procedural as above):
+ * offdiag_moments and abs_row_sums (dc/coupling.py:104-109, :197-206) for the Wigner
+ * estimate and beta of derive_params (dc/spectral.py:175-189, :246-247). */
+DCX_API int dcx_row_stats(dcx_ctx* ctx, double* out /* [n][3] */);
 
 /* Operator seam (dc/matvec.py:99-114 matvec; :181-190 operator_energy;
  * dc/model.py:79-87 energy; dc/solvers/doch.py:76-103 hamiltonian/apply_T).

@@ -39,7 +39,7 @@ EXPORTS = (
     "dcx_result_history_all", "dcx_result_best_spins", "dcx_result_state", "dcx_result_states",
     "dcx_result_device_seconds", "dcx_profile_kernel", "dcx_set_csr_block", "dcx_stream", "dcx_dist_begin",
     "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish", "dcx_power",
-    "dcx_set_procedural", "dcx_proc_row_stats", "dcx_gen_sparse_9bit", "dcx_gen_result", "dcx_validate_csr",
+    "dcx_set_procedural", "dcx_proc_row_stats", "dcx_row_stats", "dcx_gen_sparse_9bit", "dcx_gen_result", "dcx_validate_csr",
 )
 QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
@@ -98,6 +98,7 @@ def load(path: Path | str | None = None):
         "dcx_set_dense": (C.c_int, [_P, C.c_int64, _PD]),
         "dcx_set_procedural": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32]),
         "dcx_proc_row_stats": (C.c_int, [_P, _PD]),
+        "dcx_row_stats": (C.c_int, [_P, _PD]),
         "dcx_coupling": (C.c_int, [_P, C.POINTER(CouplingInfo)]),
         "dcx_matvec": (C.c_int, [_P, C.c_int32, _PD, _PD, C.c_int32]),
         "dcx_apply": (C.c_int, [_P, C.c_int32, _PD, _PD, _PD, _PD, _PD, C.c_int32]),
@@ -190,6 +191,12 @@ class Context:
     def set_procedural(self, n, seed, formula="sin_product"):
         check(self.lib.dcx_set_procedural(self.h, int(n), int(seed), FORMULA[formula]), self.h)
         self.n = int(n)
+
+    def row_stats(self) -> np.ndarray:
+        """[n][3]: per-row sum, sum of squares and sum of |J_ij| over j != i (any coupling)."""
+        out = np.empty((self.n, 3))
+        check(self.lib.dcx_row_stats(self.h, ptr(out, C.c_double)), self.h)
+        return out
 
     def proc_row_stats(self) -> np.ndarray:
         """[n][3]: per-row sum, sum of squares and sum of |J_ij| over j != i."""

@@ -112,9 +112,12 @@ struct dcx_ctx {
   size_t ring_n = 0;
   GState hg{};
   GenCsr gen;  // dcx_gen_sparse_9bit result until dcx_gen_result
+  unsigned char* pin = nullptr;  // grow-only pinned staging of CSR uploads (row offsets + columns)
+  size_t pin_bytes = 0;
 
   ~dcx_ctx() {
     if (ring) cudaFreeHost(ring);
+    if (pin) cudaFreeHost(pin);
     if (graph) cudaGraphExecDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -162,24 +165,69 @@ int lanes_for_degree(double d) {
 }
 
 // Detect the narrowest exact storage of the coupling values.
+// Host passes over the uploaded arrays (10^8 entries at R8) run on all host threads:
+// f(lo, hi, t) over contiguous chunks [lo, hi) of [0, n), chunk t of T.
+template <class F>
+static void par_for(int64_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int T = n < (int64_t(1) << 20) ? 1 : int(std::min<unsigned>(hw, 32u));
+  if (T == 1) {
+    f(int64_t(0), n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t chunk = (n + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    const int64_t lo = std::min(n, t * chunk), hi = std::min(n, lo + chunk);
+    th.emplace_back([&f, lo, hi, t] { f(lo, hi, t); });
+  }
+  for (auto& x : th) x.join();
+}
+
 void classify_values(const double* v, int64_t nnz, int& vk, double& scale) {
   if (nnz == 0) { vk = VK_UNIFORM; scale = 0.0; return; }
+  std::vector<unsigned char> uni(32, 1), fin(32, 1);
+  std::vector<double> mns(32, std::numeric_limits<double>::infinity());
+  par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
+    bool u = true, f = true;
+    double mn = std::numeric_limits<double>::infinity();
+    for (int64_t e = lo; e < hi; ++e) {
+      f &= bool(std::isfinite(v[e]));
+      u &= v[e] == v[0];
+      if (v[e] != 0.0) mn = std::min(mn, std::fabs(v[e]));
+    }
+    uni[t] = u;
+    fin[t] = f;
+    mns[t] = mn;
+  });
   bool uniform = true;
   double mn = std::numeric_limits<double>::infinity();
-  for (int64_t e = 0; e < nnz; ++e) {
-    if (!std::isfinite(v[e])) throw InvalidArg("couplings must be finite");
-    if (v[e] != v[0]) uniform = false;
-    if (v[e] != 0.0) mn = std::min(mn, std::fabs(v[e]));
+  for (int t = 0; t < 32; ++t) {
+    if (!fin[t]) throw InvalidArg("couplings must be finite");
+    uniform = uniform && uni[t];
+    mn = std::min(mn, mns[t]);
   }
   if (uniform) { vk = VK_UNIFORM; scale = v[0]; return; }
   if (!std::isfinite(mn)) { vk = VK_UNIFORM; scale = 0.0; return; }
   for (double s : {mn, 1.0, 0.5, 0.25}) {
-    double amax = 0.0;
+    std::vector<unsigned char> oks(32, 1);
+    std::vector<double> amaxs(32, 0.0);
+    par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
+      bool okt = true;
+      double am = 0.0;
+      for (int64_t e = lo; e < hi && okt; ++e) {
+        const double q = v[e] / s;
+        if (q != std::nearbyint(q) || s * std::nearbyint(q) != v[e]) okt = false;
+        am = std::max(am, std::fabs(q));
+      }
+      oks[t] = okt;
+      amaxs[t] = am;
+    });
     bool ok = true;
-    for (int64_t e = 0; e < nnz && ok; ++e) {
-      const double q = v[e] / s;
-      if (q != std::nearbyint(q) || s * std::nearbyint(q) != v[e]) ok = false;
-      amax = std::max(amax, std::fabs(q));
+    double amax = 0.0;
+    for (int t = 0; t < 32; ++t) {
+      ok = ok && oks[t];
+      amax = std::max(amax, amaxs[t]);
     }
     if (!ok) continue;
     if (amax <= 127) { vk = VK_I8; scale = s; return; }
@@ -502,16 +550,42 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     if (nnz >= (int64_t(1) << 32) - 1) throw InvalidArg("nnz >= 2^32 is not supported");
     if (n >= (int64_t(1) << 31)) throw InvalidArg("n >= 2^31 is not supported");
     if (ro[0] != 0 || ro[n] != nnz) throw InvalidArg("row_offsets must start at 0 and end at nnz");
-    std::vector<uint32_t> rp32(n + 1);
-    for (int64_t i = 0; i <= n; ++i) {
-      if (i > 0 && ro[i] < ro[i - 1]) throw InvalidArg("row_offsets must be nondecreasing");
-      rp32[i] = uint32_t(ro[i]);
+    // row offsets and columns are converted straight into pinned staging (no host vectors
+    // to zero-fill, DMA at full PCIe rate); the staging is kept for re-uploads
+    const size_t stage = size_t(n + 1) * 4 + size_t(nnz) * 4;
+    if (c->pin_bytes < stage) {
+      if (c->pin) cudaFreeHost(c->pin);
+      c->pin = nullptr;
+      c->pin_bytes = 0;
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), stage, cudaHostAllocDefault));
+      c->pin_bytes = stage;
     }
-    std::vector<int32_t> c32(nnz);
-    for (int64_t e = 0; e < nnz; ++e) {
-      if (ci[e] < 0 || ci[e] >= n_cols) throw InvalidArg("column index out of range");
-      c32[e] = int32_t(ci[e]);
-    }
+    uint32_t* rp32 = reinterpret_cast<uint32_t*>(c->pin);
+    int32_t* c32 = reinterpret_cast<int32_t*>(c->pin + size_t(n + 1) * 4);
+    std::vector<unsigned char> bad(32, 0);
+    std::vector<int64_t> maxlens(32, 0);
+    par_for(n + 1, [&](int64_t lo, int64_t hi, int t) {
+      int64_t ml = 0;
+      for (int64_t i = lo; i < hi; ++i) {
+        if (i > 0) {
+          if (ro[i] < ro[i - 1]) bad[t] = 1;
+          ml = std::max<int64_t>(ml, ro[i] - ro[i - 1]);
+        }
+        rp32[i] = uint32_t(ro[i]);
+      }
+      maxlens[t] = ml;
+    });
+    for (int t = 0; t < 32; ++t)
+      if (bad[t]) throw InvalidArg("row_offsets must be nondecreasing");
+    const int64_t row_maxlen = *std::max_element(maxlens.begin(), maxlens.end());
+    par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
+      for (int64_t e = lo; e < hi; ++e) {
+        if (ci[e] < 0 || ci[e] >= n_cols) bad[t] = 1;
+        c32[e] = int32_t(ci[e]);
+      }
+    });
+    for (int t = 0; t < 32; ++t)
+      if (bad[t]) throw InvalidArg("column index out of range");
     int vk;
     double scale;
     classify_values(v, nnz, vk, scale);
@@ -519,8 +593,7 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
       // the UNIFORM / I8 kernels sum q * sign(x) per row in f32, exact while
       // every row's sum of |q| stays below 2^24; longer rows use the int32
       // (I16) path
-      int64_t maxlen = 0;
-      for (int64_t i = 0; i < n; ++i) maxlen = std::max<int64_t>(maxlen, ro[i + 1] - ro[i]);
+      const int64_t maxlen = row_maxlen;
       if (maxlen * (vk == VK_I8 ? 127 : 1) >= (int64_t(1) << 24) && scale != 0.0) vk = VK_I16;
     }
     c->have = false;
@@ -530,11 +603,11 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     c->row_base = row_base;
     c->nnz = nnz;
     c->rp.alloc((n + 1) * 4);
-    CK(cudaMemcpy(c->rp.p, rp32.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->rp.p, rp32, (n + 1) * 4, cudaMemcpyHostToDevice));
     // 16 zero entries of padding: the R = 1 entry-parallel pass reads whole 16-byte vectors
     c->col.alloc((nnz + 16) * 4);
     CK(cudaMemset(static_cast<char*>(c->col.p) + nnz * 4, 0, 64));
-    if (nnz) CK(cudaMemcpy(c->col.p, c32.data(), nnz * 4, cudaMemcpyHostToDevice));
+    if (nnz) CK(cudaMemcpy(c->col.p, c32, nnz * 4, cudaMemcpyHostToDevice));
     c->col16.release();
     if (n_cols <= 65536 && n == n_cols && nnz) {
       std::vector<uint16_t> c16(nnz);
@@ -552,14 +625,16 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
       std::vector<int16_t> q16;
       std::vector<int8_t> q8;
       if (b == 1) q8.resize(nnz); else q16.resize(nnz);
-      for (int64_t e = 0; e < nnz; ++e) {
-        const int q = int(std::nearbyint(v[e] / scale));
-        if (b == 1) q8[e] = int8_t(q); else q16[e] = int16_t(q);
-      }
+      par_for(nnz, [&](int64_t lo, int64_t hi, int) {
+        for (int64_t e = lo; e < hi; ++e) {
+          const int q = int(std::nearbyint(v[e] / scale));
+          if (b == 1) q8[e] = int8_t(q); else q16[e] = int16_t(q);
+        }
+      });
       c->vint.alloc((nnz + 16) * b);
       CK(cudaMemset(static_cast<char*>(c->vint.p) + nnz * b, 0, 16 * b));
       CK(cudaMemcpy(c->vint.p, b == 1 ? (void*)q8.data() : (void*)q16.data(), nnz * b, cudaMemcpyHostToDevice));
-      if (b == 1 && n == n_cols && row_base == 0) detect_torus(c, n, nnz, ro, c32.data(), q8.data());
+      if (b == 1 && n == n_cols && row_base == 0) detect_torus(c, n, nnz, ro, c32, q8.data());
     } else if (vk != VK_UNIFORM) {
       c->v64.alloc(nnz * 8);
       CK(cudaMemcpy(c->v64.p, v, nnz * 8, cudaMemcpyHostToDevice));
@@ -571,11 +646,17 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     c->V32 = lanes_for_degree(double(nnz) / double(n));
     c->ell_entries = 0;
     {
-      int64_t maxlen = 0;
-      for (int64_t i = 0; i < n; ++i) maxlen = std::max<int64_t>(maxlen, ro[i + 1] - ro[i]);
+      const int64_t maxlen = row_maxlen;
       double qmax = vk == VK_UNIFORM ? 1.0 : 0.0;
-      if (vk == VK_I8 || vk == VK_I16)
-        for (int64_t e = 0; e < nnz; ++e) qmax = std::max(qmax, std::fabs(std::nearbyint(v[e] / scale)));
+      if (vk == VK_I8 || vk == VK_I16) {
+        std::vector<double> qm(32, 0.0);
+        par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
+          double m = 0.0;
+          for (int64_t e = lo; e < hi; ++e) m = std::max(m, std::fabs(std::nearbyint(v[e] / scale)));
+          qm[t] = m;
+        });
+        qmax = std::max(qmax, *std::max_element(qm.begin(), qm.end()));
+      }
       c->es_row_bound = double(maxlen) * qmax;
     }
     if (n_cols <= 65536 && n == n_cols)
@@ -689,6 +770,82 @@ int dcx_proc_row_stats(dcx_ctx* c, double* out) {
     DevBuf& tmp = c->scratch;
     if (tmp.bytes < size_t(n) * 24) tmp.alloc(size_t(n) * 24);
     launch_proc_row_stats(n, c->proc_seed, tmp.as<double>(), c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp.p, size_t(n) * 24, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// Row statistics of a stored coupling over j != i: (sum J_ij, sum J_ij^2, sum |J_ij|) per row,
+// the inputs of offdiag_moments and abs_row_sums (dc/coupling.py:104-109 dense,
+// :197-206 CSR) for derive_params' Wigner estimate and beta (dc/spectral.py:175-189, 246-247).
+// Each row is summed sequentially in column order (numpy's bincount order for CSR).
+namespace {
+__global__ void csr_row_stats(const uint32_t* rp, const int32_t* col, const void* val, int vk, double scale,
+                              int64_t n, int64_t row_base, double* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double s1 = 0.0, s2 = 0.0, sa = 0.0;
+    for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) {
+      double v;
+      if (vk == VK_UNIFORM) v = scale;
+      else if (vk == VK_I8) v = scale * double(reinterpret_cast<const int8_t*>(val)[e]);
+      else if (vk == VK_I16) v = scale * double(reinterpret_cast<const int16_t*>(val)[e]);
+      else v = reinterpret_cast<const double*>(val)[e];
+      if (int64_t(col[e]) == row_base + i) continue;  // the diagonal is excluded (zero for valid couplings)
+      s1 += v;
+      s2 += v * v;
+      sa += fabs(v);
+    }
+    out[3 * i] = s1;
+    out[3 * i + 1] = s2;
+    out[3 * i + 2] = sa;
+  }
+}
+__global__ void dense_row_stats(const double* A, int64_t n, double* out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < n;
+       i += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    double s1 = 0.0, s2 = 0.0, sa = 0.0;
+    for (int64_t j = lane; j < n; j += 32) {  // lane-strided, then a fixed-order warp tree
+      const double v = j == i ? 0.0 : A[i * n + j];
+      s1 += v;
+      s2 += v * v;
+      sa += fabs(v);
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    sa = warp_sum(sa);
+    if (lane == 0) {
+      out[3 * i] = s1;
+      out[3 * i + 1] = s2;
+      out[3 * i + 2] = sa;
+    }
+  }
+}
+}  // namespace
+
+int dcx_row_stats(dcx_ctx* c, double* out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  return guarded(c, [&] {
+    require_coupling(c);
+    const int64_t n = c->n;
+    DevBuf& tmp = c->scratch;
+    if (c->proc) {
+      if (tmp.bytes < size_t(n) * 24) tmp.alloc(size_t(n) * 24);
+      launch_proc_row_stats(n, c->proc_seed, tmp.as<double>(), c->stream);
+    } else if (c->dense) {
+      // the f64 coupling as uploaded stays in dn.scratch; row stats go to a separate buffer
+      if (!c->dn.scratch || c->dn.scratch_bytes < size_t(n * n) * 8) throw InvalidArg("dense coupling not on the device");
+      if (tmp.bytes < size_t(n) * 24) tmp.alloc(size_t(n) * 24);
+      dense_row_stats<<<int(std::min<int64_t>((n + 7) / 8, 148 * 16)), 256, 0, c->stream>>>(
+          static_cast<const double*>(c->dn.scratch), n, tmp.as<double>());
+    } else {
+      if (tmp.bytes < size_t(n) * 24) tmp.alloc(size_t(n) * 24);
+      const void* val = c->vk_int >= 0 ? c->vint.p : c->v64.p;
+      const int vk = c->vk_int >= 0 ? c->vk_int : VK_F64;
+      csr_row_stats<<<grid_for(n), 256, 0, c->stream>>>(c->rp.as<uint32_t>(), c->col.as<int32_t>(), val, vk,
+                                                       c->scale, n, c->row_base, tmp.as<double>());
+    }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, tmp.p, size_t(n) * 24, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

@@ -45,24 +45,22 @@ class SolverParams:
             raise ValueError("lookback_q must be >= 1")
 
 
+def row_stats(J) -> np.ndarray:
+    """[n][3] per-row (sum J_ij, sum J_ij^2, sum |J_ij|) over j != i, computed on the device
+    (dcx_row_stats: one pass over the stored coupling, or a regeneration pass for a procedural
+    one) -- offdiag_moments and abs_row_sums of dc/coupling.py:104-109, :197-206. At the
+    BASELINE sizes the reference's host loops (np.add.at / bincount over 10^8 entries) take
+    seconds to minutes."""
+    return device_context(J).row_stats()
+
+
 def _moments(J):
-    if is_procedural(J):
-        return J.offdiag_moments()  # device row statistics (dcx_proc_row_stats)
-    if hasattr(J, "array"):
-        a = np.asarray(J.array)
-        return float(a.sum()), float((a * a).sum())
-    v = np.asarray(J.values)
-    return float(v.sum()), float((v * v).sum())
+    st = row_stats(J)
+    return float(st[:, 0].sum()), float(st[:, 1].sum())
 
 
 def _abs_row_max(J) -> float:
-    if is_procedural(J):
-        return float(J.abs_row_sums().max())
-    if hasattr(J, "array"):
-        return float(np.abs(np.asarray(J.array)).sum(axis=1).max())
-    ro = np.asarray(J.row_offsets)
-    rows = np.repeat(np.arange(J.n), np.diff(ro))
-    return float(np.bincount(rows, weights=np.abs(np.asarray(J.values)), minlength=J.n).max())
+    return float(row_stats(J)[:, 2].max())
 
 
 def estimate_lambda_max_neg(J, method="auto", tol=1e-10, max_iters=20_000) -> float:

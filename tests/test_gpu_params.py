@@ -105,3 +105,45 @@ def test_solve_front_door_overrides(gold):
     assert r3.stop_reason in ("time_budget", "converged")
     with pytest.raises(ValueError):
         dc.solve(inst, "sa")
+
+
+# ------------------------------------------------------------------ device row statistics (Wigner, beta)
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["er1e4", "reg3_1e4"])
+def test_derive_params_wigner_on_device_matches_reference(gold, name):
+    """n >= 1e4: the Wigner estimate from offdiag_moments and beta from abs_row_sums
+    (dc/spectral.py:175-189, :246-247), both from the device row statistics (dcx_row_stats):
+    the unmodified reference's alpha / beta on these graphs (unit weights: exact sums)."""
+    from paper_2509_01928_b200 import synth
+
+    g = gold["families"][name]
+    v, c, o, *_ = synth.erdos_renyi(10**4) if name == "er1e4" else synth.random_regular3(10**4)
+    J = dc.CsrCoupling(10**4, v, c, o, validate=False)
+    p = dc.derive_params(J, eta=1.0, max_iters=100, seed=0)
+    assert p.alpha == g["alpha"] and p.beta == g["beta"]
+
+
+@pytest.mark.gpu
+def test_row_stats_match_host_sums():
+    """dcx_row_stats against numpy on real-valued CSR and dense couplings (j != i)."""
+    from paper_2509_01928_b200 import params as prm
+    from conftest import sk_dense
+
+    rng = np.random.default_rng(2)
+    n = 3000
+    a = np.triu(rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.01), 1)
+    a = a + a.T
+    import scipy.sparse as sp
+
+    m = sp.csr_matrix(a)
+    m.sort_indices()
+    J = dc.CsrCoupling(n, m.data, m.indices.astype(np.int64), m.indptr.astype(np.int64), validate=False)
+    st = prm.row_stats(J)
+    np.testing.assert_allclose(st[:, 0], a.sum(1), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(st[:, 1], (a * a).sum(1), rtol=1e-12)
+    np.testing.assert_allclose(st[:, 2], np.abs(a).sum(1), rtol=1e-12)
+    D = sk_dense(200, 3)
+    std = prm.row_stats(dc.DenseCoupling(D, validate=False))
+    off = D - np.diag(np.diag(D))
+    np.testing.assert_allclose(std[:, 0], off.sum(1), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(std[:, 2], np.abs(off).sum(1), rtol=1e-12)
