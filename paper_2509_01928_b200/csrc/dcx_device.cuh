@@ -137,6 +137,17 @@ __device__ __forceinline__ float cbrt_lean(float t) {
   r = a < 1.17549435e-38f ? 0.0f : r;
   return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
 }
+// Cube root of the tensor-core DOCH update: t |t|^(-2/3) from the MUFU log2 / exp2 estimates
+// alone (2 MUFU + 3 FP ops; no Newton step, so ~1e-7 relative instead of <= 1 ulp). The
+// delta iteration rounds each step to e4m3 / f16 anyway and converges to the fixed point of
+// this (deterministic) map; zero and denormal arguments give +0.
+__device__ __forceinline__ float cbrt_mufu(float t) {
+  const float a = fabsf(t);
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * (-2.0f / 3.0f)));
+  return a < 1.17549435e-38f ? 0.0f : t * r;
+}
 __device__ __forceinline__ double inv_beta(double beta) { return beta; }  // unused in f64
 __device__ __forceinline__ float inv_beta(float beta) { return __frcp_rn(beta); }
 __device__ __forceinline__ double tmap(double ax, double beta, double) { return cbrt(__ddiv_rn(ax, beta)); }
