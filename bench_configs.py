@@ -75,27 +75,56 @@ def _instance(name):
 CFG = {
     "g1": dict(R=100, max_iters=1000, precision="f64", desc="800-spin G1-shape MaxCut, eta=0.25, DOCH, 100 seeds"),
     "t6": dict(R=256, max_iters=200, precision="f32", desc="1000x1000 +-1 torus, 256 replicas, DOCH, eta=1"),
-    "e7": dict(R=1, max_iters=100, precision="f32", desc="Erdos-Renyi n=1e7 deg 8 unit MaxCut, 1 replica, DOCH, eta=1"),
+    "e7": dict(R=1, max_iters=200, precision="f32",
+               desc="Erdos-Renyi n=1e7 deg 8 unit MaxCut, 1 replica, DOCH, eta=1, 200 iterations (the reference run's budget)"),
     "r8": dict(R=1, max_iters=20, precision="f32", desc="random 3-regular n=1e8 unit MaxCut, 1 replica, DOCH, eta=1, 1 GPU"),
 }
 
 
-def cpu_sample(name, inst, alpha, beta, arrays, budget_s=20.0):
-    """Oracle port on the host: replicas one after another, bounded in time."""
+def reference_quality(name):
+    """The unmodified reference's quality on this config, computed offline (tests/golden):
+    G1 -- best cut over 100 seeds x DOCH/ADOCH at eta = 0.25 (golden.json); E7 -- the best cut of
+    one 200-iteration DOCH run (golden_e7.json). None when not available."""
+    import json
+    from pathlib import Path
+
+    gdir = Path(__file__).resolve().parent / "tests" / "golden"
+    try:
+        if name == "g1":
+            g = json.loads((gdir / "golden.json").read_text())["g1"]
+            return max(max(r["cut"] for r in g[s]) for s in ("doch", "adoch")), "best cut of the reference over 100 seeds x DOCH/ADOCH"
+        if name == "e7":
+            g = json.loads((gdir / "golden_e7.json").read_text())
+            return g["best_cut"], f"best cut of one {g['iterations']}-iteration reference DOCH run (seed 0)"
+    except (OSError, KeyError, ValueError):
+        return None
+    return None
+
+
+def cpu_sample(name, inst, alpha, beta, arrays, budget_s=20.0, target=None):
+    """Oracle port on the host: replicas one after another, bounded in time; with `target`
+    also the time to reach it (dc/bench.py:219-231 semantics, on the port's own clock)."""
     from oracle import dcising_oracle as orc
 
     op = orc.Operator(arrays)
     n = op.n
     iters = {"g1": 1000, "t6": 20, "e7": 3, "r8": 1}[name]
     upd, t0, r = 0, time.perf_counter(), 0
+    tts = []
+    co = getattr(inst, "cut_offset", None)
     while True:
-        out = orc.run(op, alpha, beta, solver="doch", max_iters=iters, seed=r, trace_stride=1)
+        out = orc.run(op, alpha, beta, solver="doch", max_iters=iters, seed=r, trace_stride=1, cut_offset=co)
         upd += n * out["iterations"]
+        if target is not None and co is not None:
+            hit = [t["elapsed_s"] for t in out["trace"] if co - t["best_energy"] >= target]
+            if hit:
+                tts.append(hit[0])
         r += 1
         if time.perf_counter() - t0 > budget_s or r >= 8:
             break
     dt = time.perf_counter() - t0
-    return upd / dt, dt, f"{r} replicas x <= {iters} DOCH iterations, numpy/scipy csr_matvec ({dt:.1f} s)"
+    sample = f"{r} replicas x <= {iters} DOCH iterations, numpy/scipy csr_matvec ({dt:.1f} s)"
+    return upd / dt, dt, sample, (float(np.mean(tts)) if tts else None, len(tts), r)
 
 
 def run_rowpart(args, name, cfg, inst, alpha, beta, X0, t_build):
@@ -265,11 +294,21 @@ def run(args):
         line["roofline"] = {"bound": "latency", "achieved": None, "peak": None, "unit": "us/iteration",
                             "frac": None, "traffic": None,
                             "us_per_iteration": 1e6 * dev / args.steps / max(r.iterations for r in res)}
-    v, dt, sample = cpu_sample(name, inst, alpha, beta, arrays)
+    ref_q = reference_quality(name)
+    target = 0.99 * ref_q[0] if ref_q else None  # dc/bench.py:111 tts_fraction
+    v, dt, sample, cpu_tts = cpu_sample(name, inst, alpha, beta, arrays, target=target)
     line["cpu_baseline"] = {"value": v, "unit": "spin-updates/s", "cores": os.cpu_count(), "kind": "port",
                             "sample": sample}
     e = np.array([r.energy for r in res])
     line["quality"] = {"best_energy": float(e.min()), "mean_energy": float(e.mean())}
     if inst.cut_offset is not None:
         line["quality"]["best_cut"] = float(inst.cut_offset - e.min())
+    if target is not None:
+        # time to target (dc/bench.py:219-231): first elapsed_s whose best-so-far cut reaches
+        # 0.99 x the reference's quality; GPU on the solve's device clock, the port on its own
+        tts = [t for t in (r.trace.first_reach_time(target) for r in res) if t is not None]
+        line["quality"].update({"tts_target_cut": target, "reference_quality": ref_q[1], "reference_best_cut": ref_q[0],
+                                "tts_s_mean": float(np.mean(tts)) if tts else None, "tts_reached": len(tts),
+                                "replicas": len(res), "cpu_tts_s_mean": cpu_tts[0],
+                                "cpu_tts_reached": f"{cpu_tts[1]} of {cpu_tts[2]}"})
     print(json.dumps(line), flush=True)
