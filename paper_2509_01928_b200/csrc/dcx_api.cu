@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -83,6 +84,7 @@ struct dcx_ctx {
   int64_t torus_L = 0;     // > 0: the coupling is the periodic torus_L x torus_L lattice (detect_torus)
   DevBuf bond_r, bond_d;   // its bonds q(i, right(i)), q(i, down(i)) as int8
   DenseDev dn;  // dense tensor-core operands (dcx_dense.cu)
+  ChunkPlan chunks;  // column-chunked R = 1 pass plan (dcx_chunk.cu), built on first use per coupling
   // ---------------------------------------------------------- run state
   dcx_params prm{};
   int R = 0;
@@ -454,9 +456,16 @@ int dcx_create(int device, dcx_ctx** out) {
   if (!c) return fail(nullptr, DCX_E_OOM, "host allocation failed");
   c->device = device;
   int rc = guarded(c, [&] {
+    CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
+    if (const char* g = std::getenv("DCX_L2_FETCH")) {  // experiment: L2 fetch granularity of random gathers
+      CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(g))));
+      size_t v = 0;
+      CK(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
+      std::fprintf(stderr, "dcx: L2 fetch granularity %zu\n", v);
+    }
   });
   if (rc != DCX_OK) {
     g_last_error = c->err;
@@ -482,6 +491,7 @@ int dcx_set_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int
   c->dense = false;
   c->proc = false;
   c->csr_ready = false;
+  c->chunks.release();
   c->dense_host.clear();
   c->dn.release();
   return upload_csr(c, n, nnz, ro, ci, v, n, 0);
@@ -495,6 +505,7 @@ int dcx_set_csr_block(dcx_ctx* c, int64_t n_rows, int64_t n_cols, int64_t row_ba
   c->dense = false;
   c->proc = false;
   c->csr_ready = false;
+  c->chunks.release();
   c->dense_host.clear();
   c->dn.release();
   return upload_csr(c, n_rows, nnz, ro, ci, v, n_cols, row_base);
@@ -544,6 +555,7 @@ static void detect_torus(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, 
 static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v,
                       int64_t n_cols, int64_t row_base) {
   return guarded(c, [&] {
+    c->chunks.release();
     if (n < 1) throw InvalidArg("n must be >= 1");
     if (n_cols >= (int64_t(1) << 31)) throw InvalidArg("n >= 2^31 is not supported");
     if (nnz < 0 || (nnz > 0 && (!ci || !v)) || !ro) throw InvalidArg("null CSR array");
@@ -716,6 +728,7 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
     c->have = false;
     c->proc = false;
     c->csr_ready = false;
+    c->chunks.release();
     c->dense_host.clear();  // no 8 n^2-byte host copy per upload: ensure_csr reads the device copy
     c->n = n;
     c->n_cols = n;
@@ -738,6 +751,7 @@ int dcx_set_procedural(dcx_ctx* c, int64_t n, int64_t seed, int32_t formula) {
     c->have = false;
     c->dense = false;
     c->csr_ready = false;
+    c->chunks.release();
     c->dense_host.clear();
     c->dn.release();
     c->rp.release();
@@ -1057,6 +1071,17 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.bond_r = c->bond_r.as<int8_t>();
     a.bond_d = c->bond_d.as<int8_t>();
     a.sgnw[0] = a.sgnw[1] = nullptr;
+    a.chunks = ChunkArgs{};
+    if (!dist && R == 1 && !c->f64 && !c->proc && (c->vk_int == VK_UNIFORM || c->vk_int == VK_I8)) {
+      const int C = chunk_count(n);
+      if (C != c->chunks.C)
+        build_chunk_plan(c->chunks, c->J.rp, c->J.col, c->vk_int == VK_I8 ? static_cast<const int8_t*>(c->J.val) : nullptr,
+                         n, c->nnz, C, c->stream);
+      if (c->chunks.C > 0) {
+        CK(cudaMemsetAsync(c->chunks.acc, 0, size_t(n) * sizeof(float2), c->stream));
+        a.chunks = c->chunks;
+      }
+    }
     if (a.torus_L > 0 && R > 1 && !c->f64) {
       const size_t words = size_t(n) * 4 * size_t((R + 127) / 128);
       c->sgn0.alloc(words * 4);

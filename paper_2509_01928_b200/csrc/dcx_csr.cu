@@ -228,14 +228,13 @@ __global__ void __launch_bounds__(256) pass_r1w(PassArgs a) {
         for (int k = 0; k < R1W_EPL; ++k) my[k * 33 + lane] = xv[k];
         if constexpr (VK == VK_I8) {
           if (eb < E1) {
-            const int2 q8 = __ldg(reinterpret_cast<const int2*>(valp + eb));  // 8 bytes (EPL = 12: + 4)
-            const int q4 = __ldg(reinterpret_cast<const int*>(valp + eb) + 2);
-            const int8_t* b8 = reinterpret_cast<const int8_t*>(&q8);
-            const int8_t* b4 = reinterpret_cast<const int8_t*>(&q4);
+            // 12 bytes at a 4-byte aligned offset (eb % 4 == 0): three word loads
+            int qw[3];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) sq[warp][k * 33 + lane] = b8[k];
+            for (int v = 0; v < 3; ++v) qw[v] = __ldg(reinterpret_cast<const int*>(valp + eb) + v);
+            const int8_t* b = reinterpret_cast<const int8_t*>(qw);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) sq[warp][(8 + k) * 33 + lane] = b4[k];
+            for (int k = 0; k < 12; ++k) sq[warp][k * 33 + lane] = b[k];
           }
         }
         __syncwarp();
@@ -1377,6 +1376,10 @@ static bool use_r1w() {
 template <typename T, int VK>
 static void launch_pass_vk(int mode, const PassArgs& a, int V, int grid, cudaStream_t s) {
   if constexpr (sizeof(T) == 4 && (VK == VK_UNIFORM || VK == VK_I8)) {
+    if (a.cfg.R == 1 && a.chunks.C > 0 && mode != MODE_ADOCH_Y) {
+      launch_chunked_pass(mode, VK, a, grid, s);
+      return;
+    }
     if (a.cfg.R == 1 && use_r1w()) {
       switch (mode) {
         case MODE_DOCH: pass_r1w<VK, MODE_DOCH><<<grid, 256, 0, s>>>(a); break;

@@ -22,6 +22,30 @@ struct CsrDev {
   long long proc_seed = 0;  // VK_PROC: seed of sin(i*j + seed)
 };
 
+// Column-chunked R = 1 pass (dcx_chunk.cu): a coupling's entries regrouped by
+// column chunk into row segments, and the per-row running sums carried between
+// the chunk sweeps of one pass. Non-owning view (kernel argument).
+struct ChunkArgs {
+  int C = 0;                        // chunks; 0 = no plan (row kernels)
+  int64_t nseg = 0;
+  const int64_t* chunk_begin = nullptr;  // [C + 1] first segment of each chunk
+  const uint32_t* seg_row = nullptr;     // [nseg] row of the segment
+  const uint8_t* seg_cnt = nullptr;      // [nseg] entries (<= 255)
+  const uint32_t* seg_start = nullptr;   // [nseg] first entry in ecol / eq
+  const int32_t* ecol = nullptr;         // [nnz] columns, segment order
+  const int8_t* eq = nullptr;            // [nnz] int8 values (VK_I8), segment order
+  float2* acc = nullptr;                 // [n] (f32 row sum, int32 spin-energy sum as bits)
+};
+// owning form, kept by the context next to its coupling
+struct ChunkPlan : ChunkArgs {
+  void release();
+  ~ChunkPlan() { release(); }
+};
+constexpr int64_t CHUNK_BYTES = int64_t(48) << 20;  // x per chunk: leaves L2 room for the streams
+int chunk_count(int64_t n);
+void build_chunk_plan(ChunkPlan& k, const uint32_t* rp, const int32_t* col, const int8_t* q, int64_t n, int64_t nnz,
+                      int C, cudaStream_t s);
+
 // Kernel argument block of one multi-pass iteration (passed by value).
 struct PassArgs {
   const uint32_t* rp;
@@ -50,6 +74,7 @@ struct PassArgs {
   // (word 4c + v of a site: bit l = replica 128c + 4l + v); the pending best copy of
   // pass p + 1 reads them instead of x_p
   uint32_t* sgnw[2];
+  ChunkArgs chunks;  // C > 0: the R = 1 pass runs as C column-chunk sweeps + a row epilogue
   RunCfg cfg;
 };
 
@@ -71,6 +96,8 @@ void enqueue_flush(const MultiPass& m, cudaStream_t s);
 void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
 void enqueue_start_clock(GState* g, cudaStream_t s);
 int replica_vector_width(int R, bool f64);
+// dcx_chunk.cu
+void launch_chunked_pass(int mode, int vk, const PassArgs& a, int grid, cudaStream_t s);
 // dcx_dense.cu: row-gather TMA map ([rows][cols], box = one row of box_cols elements)
 void encode_row_gather_map(void* map_out, void* base, uint64_t cols, uint64_t rows, bool f64, uint32_t box_cols);
 // dcx_power.cu

@@ -150,6 +150,11 @@ def test_r8_full_size_one_step_and_energies():
     r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=3, precision="f32", path="multipass")
     _check_common(J, r, X0, cut_offset=co)
     assert r[0].iterations == 3
+    # x (400 MB) exceeds L2: the opt-in column-chunked pass agrees with the row kernel bit for bit
+    with _env("DCX_CHUNKS", "auto"):
+        rr = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=3, precision="f32", path="multipass",
+                               reupload=True)
+    _assert_same(r, rr)
 
 
 def test_e7_full_size_properties(e7):
@@ -163,6 +168,63 @@ def test_e7_full_size_properties(e7):
     r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=20, precision="f32", path="multipass")
     _check_common(J, r, X0, cut_offset=co)
     assert r[0].iterations == 20 and r[0].stop_reason == "max_iters"
+
+
+class _env:
+    def __init__(self, k, v):
+        self.k, self.v = k, v
+
+    def __enter__(self):
+        import os
+        self.old = os.environ.get(self.k)
+        os.environ[self.k] = self.v
+
+    def __exit__(self, *exc):
+        import os
+        if self.old is None:
+            os.environ.pop(self.k, None)
+        else:
+            os.environ[self.k] = self.old
+
+
+def _assert_same(fast, ref):
+    for a_, b_ in zip(fast, ref):
+        assert a_.iterations == b_.iterations and a_.stop_reason == b_.stop_reason
+        assert a_.energy == b_.energy and np.array_equal(a_.x, b_.x) and np.array_equal(a_.spins, b_.spins)
+        assert [t.energy for t in a_.trace] == [t.energy for t in b_.trace]
+        assert np.array_equal(np.asarray(a_.h_values), np.asarray(b_.h_values))
+
+
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+@pytest.mark.parametrize("graph", ["er_uniform", "torus_int8", "hub_rows"])
+@pytest.mark.parametrize("chunks", ["3", "7"])
+def test_column_chunked_pass_bitwise_equals_row_pass(solver, graph, chunks):
+    """The column-chunked R = 1 pass (dcx_chunk.cu; opt-in, DCX_CHUNKS=C) applies each row's entries in column order with the row kernel's
+    arithmetic, carrying the running sum between chunk sweeps: iterates, energies, traces
+    and stop reasons equal pass_r1w's bit for bit. hub_rows: rows with > 255 entries in
+    one chunk, where the plan falls back to the row kernel."""
+    if graph == "er_uniform":
+        n = 300_000
+        v, c, o, _ = synth.erdos_renyi(n, 8, seed=3, device=0)
+    elif graph == "torus_int8":
+        v, c, o = synth.torus(400, seed=3)
+        n = 400 * 400
+    else:
+        n = 4000
+        Jd = np.zeros((n, n))
+        Jd[:50, :] = Jd[:, :50] = -0.5  # 50 hub rows with n - 1 entries
+        np.fill_diagonal(Jd, 0.0)
+        Js = sp.csr_matrix(Jd)
+        v, c, o = Js.data, Js.indices.astype(np.int64), Js.indptr.astype(np.int64)
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False))
+    p = dc.derive_params(inst.coupling, eta=1.0)
+    X0 = dc.initial_state(n, p.alpha, p.beta, np.random.default_rng(7))[None, :]
+    kw = dict(max_iters=80, precision="f32", path="multipass", reupload=True)
+    with _env("DCX_CHUNKS", "0"):
+        ref = dc.solve_replicas(inst, solver, p.alpha, p.beta, X0, **kw)
+    with _env("DCX_CHUNKS", chunks):
+        fast = dc.solve_replicas(inst, solver, p.alpha, p.beta, X0, **kw)
+    _assert_same(fast, ref)
 
 
 @pytest.mark.parametrize("solver", ["doch", "adoch"])
