@@ -137,6 +137,8 @@ struct Args {
   // Q (|q| <= 16, exact), kind::f8f6f4; the sign GEMM is e4m3 too (dS in {0, +-2}, f32 D2)
   int f8;
   float* dsc;      // f8: 2^-e of the replica's last written delta (resume), [Rpad]
+  int exp;         // timing experiments only (DCX_DENSE_EXP, wrong results): 1 skip A loads,
+                   // 2 skip B loads, 4 skip GEMM2 (the sign GEMM); 8: spin (no sleep) on GEMM1 done
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -364,6 +366,59 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
                "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
+// Loads fused with their wait::ld in ONE asm statement: the compiler sees the destination
+// registers written only when the data is there, so it cannot spill them (or read them)
+// between the asynchronous tcgen05.ld and the wait (which it did under register pressure)
+__device__ __forceinline__ void tmem_ld3x16_wait(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t* v0, uint32_t* v1, uint32_t* v2) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%48];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%49];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%50];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v0[0]), "=r"(v0[1]), "=r"(v0[2]), "=r"(v0[3]), "=r"(v0[4]), "=r"(v0[5]), "=r"(v0[6]), "=r"(v0[7]), "=r"(v0[8]), "=r"(v0[9]), "=r"(v0[10]), "=r"(v0[11]), "=r"(v0[12]), "=r"(v0[13]), "=r"(v0[14]), "=r"(v0[15]), "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]), "=r"(v1[6]), "=r"(v1[7]), "=r"(v1[8]), "=r"(v1[9]), "=r"(v1[10]), "=r"(v1[11]), "=r"(v1[12]), "=r"(v1[13]), "=r"(v1[14]), "=r"(v1[15]), "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3]), "=r"(v2[4]), "=r"(v2[5]), "=r"(v2[6]), "=r"(v2[7]), "=r"(v2[8]), "=r"(v2[9]), "=r"(v2[10]), "=r"(v2[11]), "=r"(v2[12]), "=r"(v2[13]), "=r"(v2[14]), "=r"(v2[15])
+      : "r"(a0), "r"(a1), "r"(a2)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld3x8_wait(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t* v0, uint32_t* v1, uint32_t* v2) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%24];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%25];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%26];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v0[0]), "=r"(v0[1]), "=r"(v0[2]), "=r"(v0[3]), "=r"(v0[4]), "=r"(v0[5]), "=r"(v0[6]), "=r"(v0[7]), "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]), "=r"(v1[6]), "=r"(v1[7]), "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3]), "=r"(v2[4]), "=r"(v2[5]), "=r"(v2[6]), "=r"(v2[7])
+      : "r"(a0), "r"(a1), "r"(a2)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld64_wait(uint32_t a0, uint32_t a1, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+      : "r"(a0), "r"(a1)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld56_wait(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%56];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%57];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%58];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55])
+      : "r"(a0), "r"(a1), "r"(a2)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld4x16_wait(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t* v0, uint32_t* v1, uint32_t* v2, uint32_t* v3) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%65];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%66];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%67];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v0[0]), "=r"(v0[1]), "=r"(v0[2]), "=r"(v0[3]), "=r"(v0[4]), "=r"(v0[5]), "=r"(v0[6]), "=r"(v0[7]), "=r"(v0[8]), "=r"(v0[9]), "=r"(v0[10]), "=r"(v0[11]), "=r"(v0[12]), "=r"(v0[13]), "=r"(v0[14]), "=r"(v0[15]), "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]), "=r"(v1[6]), "=r"(v1[7]), "=r"(v1[8]), "=r"(v1[9]), "=r"(v1[10]), "=r"(v1[11]), "=r"(v1[12]), "=r"(v1[13]), "=r"(v1[14]), "=r"(v1[15]), "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3]), "=r"(v2[4]), "=r"(v2[5]), "=r"(v2[6]), "=r"(v2[7]), "=r"(v2[8]), "=r"(v2[9]), "=r"(v2[10]), "=r"(v2[11]), "=r"(v2[12]), "=r"(v2[13]), "=r"(v2[14]), "=r"(v2[15]), "=r"(v3[0]), "=r"(v3[1]), "=r"(v3[2]), "=r"(v3[3]), "=r"(v3[4]), "=r"(v3[5]), "=r"(v3[6]), "=r"(v3[7]), "=r"(v3[8]), "=r"(v3[9]), "=r"(v3[10]), "=r"(v3[11]), "=r"(v3[12]), "=r"(v3[13]), "=r"(v3[14]), "=r"(v3[15])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3)
+      : "memory");
+}
 // W = 32 or 24 consecutive TMEM columns of this warp's lane quadrant
 template <int W>
 __device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t* v) {
@@ -455,7 +510,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   const bool leader = cta_rank == 0;
   const int KB1 = a.npad / (TK * P::KA);      // f16 stages (KA x 64 of K each)
   const int KB1f8 = a.npad / (2 * TK * P::KA);  // e4m3 stages (KA x 128 of K each)
-  const int KB2 = a.npad / (2 * TK * P::KA);  // int8 stages (KA x 128 of K each)
+  const int KB2 = (a.exp & 4) ? 0 : a.npad / (2 * TK * P::KA);  // int8 stages (KA x 128 of K each)
   constexpr int KS = P::KA * TK;  // K columns per GEMM1 stage (128); flags are per spin tile of TN
   SyncWords* grp = a.sync + rg;
 
@@ -650,7 +705,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         if (lane == 0) {
           if (kb < nb1) fence_async_global();  // generic writes (acquired above) before the async-proxy loads
           const uint32_t fb = smem_u32(&sm.full[s]);
-          if (leader) mbar_expect_tx(fb, NC * P::STAGE);
+          if (leader)
+            mbar_expect_tx(fb, NC * P::KA * (((a.exp & 1) ? 0u : TILE_BYTES) + ((a.exp & 2) ? 0u : P::B_BYTES)));
           unsigned char* st = tiles + s * P::STAGE;
           const int bi = i0 + cta_rank * (TN / NC);
           const int cur = p & 1;
@@ -666,10 +722,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
               tma_load_2d(da, ma, kc + q * katom, r0, fb);
               tma_load_2d(db, mb, kc + q * katom, bi, fb);
             } else {
-              if (!a.mc) tma_load_2d_pair(da, ma, kc + q * katom, r0, fb);
-              else if (psub == 0)
-                tma_load_2d_pair_mc(da, ma, kc + q * katom, r0, fb, uint16_t((1u << cta_rank) | (1u << (cta_rank + 2))));
-              tma_load_2d_pair(db, mb, kc + q * katom, bi, fb);
+              if (!(a.exp & 1)) {
+                if (!a.mc) tma_load_2d_pair(da, ma, kc + q * katom, r0, fb);
+                else if (psub == 0)
+                  tma_load_2d_pair_mc(da, ma, kc + q * katom, r0, fb, uint16_t((1u << cta_rank) | (1u << (cta_rank + 2))));
+              }
+              if (!(a.exp & 2)) tma_load_2d_pair(db, mb, kc + q * katom, bi, fb);
             }
           }
         }
@@ -844,7 +902,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       const __half* dhg = a.xh[cur] + (int64_t)r * a.npad + gbase;  // Dh_p (GEMM1(p)'s operand)
       const uint8_t* dhb = reinterpret_cast<const uint8_t*>(a.xh[cur]) + (int64_t)r * 2 * a.npad + gbase;  // f8 view
       const bool f8 = a.f8 != 0;
-      mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
+      if (a.exp & 8) mbar_wait(smem_u32(&sm.accf1), acc_phase);
+      else mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
       mbar_wait_sleep(smem_u32(&sm.accf2), acc_phase);
       tc_fence_after();
       float s4 = 0.f, sxax = 0.f, sy4 = 0.f, syay = 0.f, step = 0.f;
@@ -853,32 +912,33 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll 1
       for (int off = 0; off < HW; off += 16) {
         uint32_t fv[16], rv[16], st[16], d2[16], ayv[16];
-        tmem_ld16(lane_base + rcol(pk) + off, fv);
-        tmem_ld16(lane_base + rcol(pk + 1) + off, rv);
-        tmem_ld16(xaddr + off, st);
-        tmem_ld16(d2addr + off, d2);
+        // Dh_p from global (update p - 1 wrote it) as four 32-bit words per 16 bytes
+        uint4 dw0 = make_uint4(0u, 0u, 0u, 0u), dw1 = dw0;
+        if (has_prev && lim > 0) {
+          if (f8) dw0 = *reinterpret_cast<const uint4*>(dhb + off);
+          else {
+            dw0 = *reinterpret_cast<const uint4*>(dhg + off);
+            dw1 = *reinterpret_cast<const uint4*>(dhg + off + 8);
+          }
+        }
+        tmem_ld4x16_wait(lane_base + rcol(pk) + off, lane_base + rcol(pk + 1) + off, xaddr + off, d2addr + off, fv, rv, st, d2);
         float dhv[16];  // Dh_p in s-units
 #pragma unroll
         for (int j = 0; j < 16; ++j) dhv[j] = 0.f;
         if (has_prev && lim > 0) {
+          const uint32_t wd[8] = {dw0.x, dw0.y, dw0.z, dw0.w, dw1.x, dw1.y, dw1.z, dw1.w};
           if (f8) {  // Dh_p (p >= 1) written by update p - 1 as e4m3 with scale 2^e_p
-            const uint4 w = *reinterpret_cast<const uint4*>(dhb + off);
-            const uint16_t* q2 = reinterpret_cast<const uint16_t*>(&w);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float2 b2 = e4m3x2_to_f2(q2[j]);
+              const float2 b2 = e4m3x2_to_f2(uint16_t(wd[j / 2] >> (16 * (j & 1))));
               dhv[2 * j] = b2.x * fdesc;
               dhv[2 * j + 1] = b2.y * fdesc;
             }
           } else {
-            __align__(16) __half dh[16];
-            *reinterpret_cast<uint4*>(dh) = *reinterpret_cast<const uint4*>(dhg + off);
-            *reinterpret_cast<uint4*>(dh + 8) = *reinterpret_cast<const uint4*>(dhg + off + 8);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) dhv[j] = __half2float(dh[j]);
+            for (int j = 0; j < 16; ++j) dhv[j] = __half2float(__ushort_as_half(uint16_t(wd[j / 2] >> (16 * (j & 1)))));
           }
         }
-        tmem_ld_wait();
         uint32_t m = 0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -982,13 +1042,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll 1
       for (int off = 0; off < HW; off += 16) {
         uint32_t rv[16], st[16], ayv[16];
-        tmem_ld16(lane_base + rcol(pk) + off, rv);
-        tmem_ld16(xaddr + off, st);
-        tmem_ld16(lane_base + rcol(pk + 1) + off, ayv);
-        tmem_ld_wait();
-        __align__(16) __half2 hv[8];
-        __align__(16) uint16_t bv[8];
-        __align__(16) uint32_t sv[4];
+        tmem_ld3x16_wait(lane_base + rcol(pk) + off, xaddr + off, lane_base + rcol(pk + 1) + off, rv, st, ayv);
+        uint32_t hw[8];  // packed delta words (f16 pairs, or 4 e4m3 bytes), see the DOCH update
+        uint32_t sv[4];
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
           float dv[2], scv[2];
@@ -1007,12 +1063,13 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
             const float2 b2 = e4m3x2_to_f2(q2);
             dq[0] = b2.x * qdesc;
             dq[1] = b2.y * qdesc;
-            bv[j / 2] = q2;
+            if (j & 2) hw[j / 4] |= uint32_t(q2) << 16;
+            else hw[j / 4] = q2;
           } else {
             const __half h0 = __float2half_rn(dv[0]), h1 = __float2half_rn(dv[1]);
             dq[0] = __half2float(h0);
             dq[1] = __half2float(h1);
-            hv[j / 2] = __halves2half2(h0, h1);
+            hw[j / 2] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
           }
 #pragma unroll
           for (int u = 0; u < 2; ++u) st[j + u] = __float_as_uint(__fadd_rn(scv[u], dq[u]));
@@ -1029,12 +1086,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         tmem_st16(xaddr + off, st);
         if (valid && lim > 0) {  // stopped replicas write zero deltas
           if (f8) {
-            *reinterpret_cast<uint4*>(hb + off) = *reinterpret_cast<uint4*>(bv);
+            *reinterpret_cast<uint4*>(hb + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
           } else {
-            *reinterpret_cast<uint4*>(hn + off) = *reinterpret_cast<uint4*>(hv);
-            *reinterpret_cast<uint4*>(hn + off + 8) = *reinterpret_cast<uint4*>(hv + 4);
+            *reinterpret_cast<uint4*>(hn + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(hn + off + 8) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
           }
-          *reinterpret_cast<uint4*>(sn + off) = *reinterpret_cast<uint4*>(sv);
+          *reinterpret_cast<uint4*>(sn + off) = make_uint4(sv[0], sv[1], sv[2], sv[3]);
         }
       }
       fdesc = qdesc;
@@ -1104,7 +1161,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       }
       uint64_t curmask = 0;
       if (a.dbg && threadIdx.x == 128) sm.tdbg[1] = clock();
-      mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
+      if (a.exp & 8) mbar_wait(smem_u32(&sm.accf1), acc_phase);
+      else mbar_wait_sleep(smem_u32(&sm.accf1), acc_phase);
       tc_fence_after();
       if (a.dbg && threadIdx.x == 128) sm.tdbg[2] = clock();
       if (a.dbg && blockIdx.x == 0 && threadIdx.x == 128 && p < 4096) a.dbg[p * 12 + 11] = clock64();
@@ -1125,10 +1183,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         // every K step against |R|, a noise floor above the reference's 1e-10 step test);
         // sv_: s_p = x_p / lambda, replaced by s_{p+1} = s_p + Dh_{p+1}
         uint32_t fv[W], rv[W], st[W];
-        tmem_ldw<W>(lane_base + rcol(p) + off, fv);
-        tmem_ldw<W>(lane_base + rcol(p + 1) + off, rv);
-        tmem_ldw<W>(xaddr + off, st);
-        tmem_ld_wait();
+        if constexpr (W == 16) tmem_ld3x16_wait(lane_base + rcol(p) + off, lane_base + rcol(p + 1) + off, xaddr + off, fv, rv, st);
+        else tmem_ld3x8_wait(lane_base + rcol(p) + off, lane_base + rcol(p + 1) + off, xaddr + off, fv, rv, st);
         if (write_master && lim > 0) {  // x_p persisted (a budget stop at p keeps it)
 #pragma unroll
           for (int j = 0; j < W; j += 4)
@@ -1136,8 +1192,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
                 make_float4(lamf * __uint_as_float(st[j]), lamf * __uint_as_float(st[j + 1]),
                             lamf * __uint_as_float(st[j + 2]), lamf * __uint_as_float(st[j + 3]));
         }
-        __align__(16) __half2 hv[W / 2];
-        __align__(16) uint16_t bv[W / 2];  // f8: e4m3 pairs
+        // the delta operand packed into 32-bit words (built with shifts, not by type punning:
+        // reading a uint16 / half2 array through uint4 pointers is undefined and was
+        // miscompiled once the loop was restructured): f16 pairs, or 4 e4m3 bytes per word
+        uint32_t hw[W / 2];
         __align__(16) uint32_t sv[W / 4];
         if (lim > 0) {
           // branch-free over all W columns (s is never -0.0 after the first update, so s < 0
@@ -1145,58 +1203,66 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           // columns of Q), so they keep s = +0 with a zero delta, add nothing to the sums and
           // read as spin +1 (a zero term of the energy GEMM)
           uint32_t m = 0;
+          // three branch-free passes over the W columns (a runtime f8 test per column pair split
+          // the loop into one basic block per pair: latency bound at 2 warps per scheduler):
+          // (1) R_p, the map T and the next delta in f32
+          float dv[W];
 #pragma unroll
-          for (int j = 0; j < W; j += 2) {
-            float dv[2], scv[2];
+          for (int j = 0; j < W; ++j) {
+            // R_p = R_{p-1} + 2^-e_p F_p (the power-of-two descale is exact; 1 for f16 products)
+            const float rr = fmaf(__uint_as_float(fv[j]), fdesc, __uint_as_float(rv[j]));
+            rv[j] = __float_as_uint(rr);
+            const float sc = __uint_as_float(st[j]);
+            const float x = lamf * sc;
+            const float ax = fmaf(alpha, x, jl * rr);
+            const float nx = DCX_DENSE_CBRT(ax * inv_beta);
+            const float x2 = x * x;
+            s4 = fmaf(x2, x2, s4);
+            sxax = fmaf(x, ax, sxax);
+            m |= (st[j] >> 31) << j;
+            // the next delta: T(x_p) - x_p in units of lambda (zero once the replica stopped,
+            // so a frozen replica adds nothing), rounded to f16 or to a scaled e4m3; the
+            // iterate moves by exactly lambda Dh, so the step |x_{p+1} - x_p| is lambda |Dh|
+            dv[j] = running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f;
+          }
+          // (2) the rounded delta (the MMA operand) and its exact value
+          if (f8) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              // R_p = R_{p-1} + 2^-e_p F_p (the power-of-two descale is exact; 1 for f16 products)
-              const float rr = fmaf(__uint_as_float(fv[j + u]), fdesc, __uint_as_float(rv[j + u]));
-              rv[j + u] = __float_as_uint(rr);
-              const float sc = __uint_as_float(st[j + u]);
-              scv[u] = sc;
-              const float x = lamf * sc;
-              const float ax = fmaf(alpha, x, jl * rr);
-              const float nx = DCX_DENSE_CBRT(ax * inv_beta);
-              const float x2 = x * x;
-              s4 = fmaf(x2, x2, s4);
-              sxax = fmaf(x, ax, sxax);
-              m |= (st[j + u] >> 31) << (j + u);
-              // the next delta: T(x_p) - x_p in units of lambda (zero once the replica stopped,
-              // so a frozen replica adds nothing), rounded to f16 or to a scaled e4m3; the
-              // iterate moves by exactly lambda Dh, so the step |x_{p+1} - x_p| is lambda |Dh|
-              dv[u] = running ? __fsub_rn(__fmul_rn(nx, inv_lam), sc) : 0.f;
-            }
-            float dq[2];
-            if (f8) {
-              const uint16_t q2 = e4m3x2(dv[0] * qsc, dv[1] * qsc);
+            for (int j = 0; j < W; j += 2) {
+              const uint16_t q2 = e4m3x2(dv[j] * qsc, dv[j + 1] * qsc);
               const float2 b2 = e4m3x2_to_f2(q2);
-              dq[0] = b2.x * qdesc;
-              dq[1] = b2.y * qdesc;
-              bv[j / 2] = q2;
-            } else {
-              const __half h0 = __float2half_rn(dv[0]), h1 = __float2half_rn(dv[1]);
-              dq[0] = __half2float(h0);
-              dq[1] = __half2float(h1);
-              hv[j / 2] = __halves2half2(h0, h1);
+              dv[j] = b2.x * qdesc;
+              dv[j + 1] = b2.y * qdesc;
+              if (j & 2) hw[j / 4] |= uint32_t(q2) << 16;
+              else hw[j / 4] = q2;
             }
+          } else {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              step = fmaxf(step, fabsf(dq[u]));
-              st[j + u] = __float_as_uint(__fadd_rn(scv[u], dq[u]));
+            for (int j = 0; j < W; j += 2) {
+              const __half h0 = __float2half_rn(dv[j]), h1 = __float2half_rn(dv[j + 1]);
+              dv[j] = __half2float(h0);
+              dv[j + 1] = __half2float(h1);
+              hw[j / 2] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
             }
-            if ((j & 3) == 2) {
-              // 4 spins -> 4 bytes of sign(x_{p+1}) - sign(x_p): +2 where the sign went - -> +,
-              // -2 (0xfe) where it went + -> -, else 0
-              const uint32_t ob = (m >> (j - 2)) & 0xFu;
-              const uint32_t nb = (st[j - 2] >> 31) | ((st[j - 1] >> 31) << 1) | ((st[j] >> 31) << 2) |
-                                  ((st[j + 1] >> 31) << 3);
-              const uint32_t df = ob ^ nb, neg = df & nb;
-              const uint32_t dfw = (df & 1u) | ((df & 2u) << 7) | ((df & 4u) << 14) | ((df & 8u) << 21);
-              const uint32_t ngw = (neg & 1u) | ((neg & 2u) << 7) | ((neg & 4u) << 14) | ((neg & 8u) << 21);
-              // int8 +2 / -2 (0x02 / 0xfe), or e4m3 +2.0 / -2.0 (0x40 / 0xc0)
-              sv[j / 4] = f8 ? dfw * 0x40u + ngw * 0x80u : dfw * 2u + ngw * 0xfcu;
-            }
+          }
+          // (3) s_{p+1} = s_p + Dh_{p+1} exactly, the step, and the sign-change operand
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            step = fmaxf(step, fabsf(dv[j]));
+            st[j] = __float_as_uint(__fadd_rn(__uint_as_float(st[j]), dv[j]));
+          }
+#pragma unroll
+          for (int j = 0; j < W; j += 4) {
+            // 4 spins -> 4 bytes of sign(x_{p+1}) - sign(x_p): +2 where the sign went - -> +,
+            // -2 (0xfe) where it went + -> -, else 0
+            const uint32_t ob = (m >> j) & 0xFu;
+            const uint32_t nb = (st[j] >> 31) | ((st[j + 1] >> 31) << 1) | ((st[j + 2] >> 31) << 2) |
+                                ((st[j + 3] >> 31) << 3);
+            const uint32_t df = ob ^ nb, neg = df & nb;
+            const uint32_t dfw = (df & 1u) | ((df & 2u) << 7) | ((df & 4u) << 14) | ((df & 8u) << 21);
+            const uint32_t ngw = (neg & 1u) | ((neg & 2u) << 7) | ((neg & 4u) << 14) | ((neg & 8u) << 21);
+            // int8 +2 / -2 (0x02 / 0xfe), or e4m3 +2.0 / -2.0 (0x40 / 0xc0)
+            sv[j / 4] = f8 ? dfw * 0x40u + ngw * 0x80u : dfw * 2u + ngw * 0xfcu;
           }
           curmask |= uint64_t(m) << off;
         }  // (lim == 0: padding replica or columns, the state stays)
@@ -1205,10 +1271,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         if (valid && lim > 0) {  // stopped replicas write zero deltas
           if (f8) {
 #pragma unroll
-            for (int j = 0; j < W / 2; j += 8) *reinterpret_cast<uint4*>(hb + off + 2 * j) = *reinterpret_cast<uint4*>(bv + j);
+            for (int k = 0; k < W / 4; k += 4) *reinterpret_cast<uint4*>(hb + off + 4 * k) = make_uint4(hw[k], hw[k + 1], hw[k + 2], hw[k + 3]);
           } else {
 #pragma unroll
-            for (int j = 0; j < W / 2; j += 4) *reinterpret_cast<uint4*>(hn + off + 2 * j) = *reinterpret_cast<uint4*>(hv + j);
+            for (int k = 0; k < W / 2; k += 4) *reinterpret_cast<uint4*>(hn + off + 2 * k) = make_uint4(hw[k], hw[k + 1], hw[k + 2], hw[k + 3]);
           }
           store_pm1(sn + off, sv, W / 4);
         }
@@ -1243,17 +1309,28 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       tc_fence_after();
       {
         uint32_t v2[64];
-        tmem_ld32(d2addr, v2);
-        tmem_ldw<W1>(d2addr + 32, v2 + 32);
-        tmem_ld_wait();
+        if constexpr (W1 == 32) tmem_ld64_wait(d2addr, d2addr + 32, v2);
+        else tmem_ld56_wait(d2addr, d2addr + 32, d2addr + 48, v2);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sm.d2free));  // D2 drained: GEMM2(p+1) may overwrite it
+        if (f8) {
+          // f32 D2 holds exact integers (|D2| <= 16 n < 2^15): their signed sum over this
+          // warp's HW columns (< 2^21) is exact in f32 in any order, no conversions needed
+          float esf = 0.f;
 #pragma unroll
-        for (int j = 0; j < HW; ++j) {
-          const int m = -int((curmask >> j) & 1);
-          const int v = (j < lim) ? (f8 ? __float2int_rn(__uint_as_float(v2[j])) : int(v2[j])) : 0;
-          es += (v ^ m) - m;
+          for (int j = 0; j < HW; ++j) {
+            const float v = __uint_as_float(v2[j] ^ (uint32_t((curmask >> j) & 1) << 31));
+            esf += j < lim ? v : 0.f;
+          }
+          es = int(esf);
+        } else {
+#pragma unroll
+          for (int j = 0; j < HW; ++j) {
+            const int m = -int((curmask >> j) & 1);
+            const int v = (j < lim) ? int(v2[j]) : 0;
+            es += (v ^ m) - m;
+          }
         }
       }
       if (live_p) prevmask = curmask;  // sign(x_p), also when the replica stops at p
@@ -1298,9 +1375,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
     const int lim = max(0, min(HW, a.n - (i0 + h * HW)));
     uint32_t v[64];
-    tmem_ld32(xaddr, v);
-    tmem_ldw<W1>(xaddr + 32, v + 32);
-    tmem_ld_wait();
+    if constexpr (W1 == 32) tmem_ld64_wait(xaddr, xaddr + 32, v);
+    else tmem_ld56_wait(xaddr, xaddr + 32, xaddr + 48, v);
     if (valid)  // s, for a later launch of this solve
 #pragma unroll
       for (int j = 0; j < HW; j += 4)
@@ -1321,9 +1397,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     // the running products, for a later launch of this solve
     auto save_cols = [&](uint32_t taddr, uint32_t* dst) {
       uint32_t w[64];
-      tmem_ld32(taddr, w);
-      tmem_ldw<W1>(taddr + 32, w + 32);
-      tmem_ld_wait();
+      if constexpr (W1 == 32) tmem_ld64_wait(taddr, taddr + 32, w);
+      else tmem_ld56_wait(taddr, taddr + 32, taddr + 48, w);
       if (valid)
 #pragma unroll
         for (int j = 0; j < HW; j += 4) *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
@@ -1635,8 +1710,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   // aligned stores); DCX_DENSE_F8=0 keeps f16 deltas and the int8 sign GEMM
   {
     const char* e = std::getenv("DCX_DENSE_F8");
-    // (DOCH only: the ADOCH kernel's e4m3 update path is not validated -- it keeps f16 deltas)
-    d.f8 = d.f8ok && d.tn == 128 && !d.ad && !(e && std::atoi(e) == 0);
+    d.f8 = d.f8ok && d.tn == 128 && !(e && std::atoi(e) == 0);
   }
   if (!d.dsc) DCK(cudaMalloc(&d.dsc, sizeof(float) * d.Rpad));
   {
@@ -1713,6 +1787,8 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.sync = reinterpret_cast<tc::SyncWords*>(d.sync);
   a.flags = reinterpret_cast<unsigned int*>(a.sync + d.Rpad / 128);
   a.dbg = reinterpret_cast<unsigned long long*>(d.dbg);
+  a.exp = 0;
+  if (const char* e = std::getenv("DCX_DENSE_EXP")) a.exp = std::atoi(e);
   a.cfg = m.args.cfg;
   a.n = int(d.n);
   a.npad = int(d.npad);

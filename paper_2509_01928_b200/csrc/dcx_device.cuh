@@ -137,6 +137,20 @@ __device__ __forceinline__ float cbrt_lean(float t) {
   r = a < 1.17549435e-38f ? 0.0f : r;
   return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
 }
+// Cube root from the inverse cube root: y = 2^(-log2|t| / 3) (2 MUFU), one FMA-only Newton
+// step y(4 - |t| y^3)/3 (relative error ~1e-13 before rounding), then |t| y^2: <= ~1 ulp
+// like cbrt_lean with one MUFU (the reciprocal) fewer. Zero and denormal arguments give +0.
+__device__ __forceinline__ float cbrt_inv(float t) {
+  const float a = fabsf(t);
+  float l, y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(l * (-1.0f / 3.0f)));
+  const float y3 = y * y * y;
+  y = fmaf(y * fmaf(-a, y3, 1.0f), 1.0f / 3.0f, y);
+  float r = (a * y) * y;
+  r = a < 1.17549435e-38f ? 0.0f : r;
+  return __uint_as_float((__float_as_uint(r) & 0x7fffffffu) | (__float_as_uint(t) & 0x80000000u)) + 0.0f;
+}
 // Cube root of the tensor-core DOCH update: t |t|^(-2/3) from the MUFU log2 / exp2 estimates
 // alone (2 MUFU + 3 FP ops; no Newton step, so ~1e-7 relative instead of <= 1 ulp). The
 // delta iteration rounds each step to e4m3 / f16 anyway and converges to the fixed point of

@@ -238,6 +238,26 @@ def test_tc_112_wide_spin_tiles(gold):
 
 
 # ------------------------------------------------------------------ ADOCH on the tensor cores
+def test_tc_adoch_e4m3_first_iterates(gold):
+    """ADOCH with the default e4m3 deltas: its first iterate is the DOCH step (no
+    extrapolation at k = 0, dc/solvers/doch.py:294-300) with the same e4m3 rounding, so it
+    matches the e4m3 emulation like the DOCH kernel's; and the first three iterates equal
+    the DOCH kernel's wherever every window rejected y (ADOCH then follows DOCH)."""
+    g = gold["k2"]
+    inst = k2_instance()
+    a, b = g["alpha"], g["beta"]
+    X0 = x0s(2000, a, b, range(128))
+    J = -0.5 * k2_W()
+    ad = dc.solve_replicas(inst, "adoch", a, b, X0, max_iters=1, precision="f16tc")
+    do = dc.solve_replicas(inst, "doch", a, b, X0, max_iters=1, precision="f16tc")
+    for x0, r, d in zip(X0, ad, do):
+        emu = doch_first_iterate_emulation(J, x0, a, b)
+        assert np.mean(np.isclose(r.x, emu, rtol=1e-5, atol=0)) >= 0.99
+        assert rel2(r.x, emu) <= 1e-2
+        assert np.array_equal(r.x, d.x)
+        assert r.energy == dc.energy(inst.coupling, r.spins)
+
+
 def test_tc_adoch_first_iterates_track_f32(gold):
     """ADOCH (economy window) in the persistent tensor-core kernel: the first iterates
     follow the f32 multipass ADOCH within the f16-operand tolerance, with the same
