@@ -372,7 +372,9 @@ def run_ours(args):
         e2e_t += time.perf_counter() - t0
         e2e_upd += N_SPINS * sum(r.iterations for r in res)
         h2d = W.nbytes + X0.nbytes
-        d2h = REPLICAS * N_SPINS * (1 + 8) + energies.nbytes
+        # the energies and per-replica summaries; final states / best spins stay on the device
+        # until a field is read (solvers._Bulk)
+        d2h = energies.nbytes + REPLICAS * 24
     e_max, = allreduce([e2e_t], "max", world)
     e_upd, = allreduce([float(e2e_upd)], "sum", world)
     # ---------------- dominant kernel roofline (measured live, CUDA events on the solver stream)

@@ -127,6 +127,13 @@ def cpu_sample(name, inst, alpha, beta, arrays, budget_s=20.0, target=None):
     return upd / dt, dt, sample, (float(np.mean(tts)) if tts else None, len(tts), r)
 
 
+def _csr_bytes(J):
+    v = getattr(J, "values", None)
+    if v is None:
+        return 0
+    return int(np.asarray(v).nbytes + np.asarray(J.col_indices).nbytes + np.asarray(J.row_offsets).nbytes)
+
+
 def run_rowpart(args, name, cfg, inst, alpha, beta, X0, t_build):
     """Row-partitioned t6 / e7 / r8 (dist.py) on WORLD_SIZE ranks, one GPU each."""
     import torch
@@ -262,7 +269,9 @@ def run(args):
     dev, upd, wall = 0.0, 0, 0.0
     for _ in range(args.steps):
         t0 = time.perf_counter()
+        # host buffers in (the CSR arrays and x0 are uploaded every step), the energies out
         res = dc.solve_replicas(inst, "doch", alpha, beta, X0, reupload=True, **kw)
+        energies = np.array([r.energy for r in res])
         wall += time.perf_counter() - t0
         dev += res[0].device_seconds
         upd += n * sum(r.iterations for r in res)
@@ -277,8 +286,12 @@ def run(args):
         "config": {"workload": cfg["desc"], "n": n, "replicas": R, "max_iters": cfg["max_iters"], "path": path,
                    "host_instance_build_s": round(t_build, 1),
                    "l2": "state + CSR stream exceed L2" if name != "g1" else "whole instance on chip (smem)"},
-        "e2e": {"value": upd / wall, "unit": "spin-updates/s", "h2d_bytes_per_step": int(X0.nbytes),
-                "d2h_bytes_per_step": int(X0.nbytes + R * n)},
+        # h2d: the CSR as the caller holds it (int64 offsets / columns, f64 values) and x0;
+        # d2h: the per-replica summaries (energy, iterations, stop, history length, warning);
+        # final states and best spins stay on the device until read (solvers._Bulk)
+        "e2e": {"value": upd / wall, "unit": "spin-updates/s",
+                "h2d_bytes_per_step": int(X0.nbytes + _csr_bytes(inst.coupling)),
+                "d2h_bytes_per_step": int(energies.nbytes + R * 24)},
     }
     if path == "multipass":
         prof = dc.profile_dominant_kernel(inst, alpha, beta, X0, precision=cfg["precision"], path="multipass",

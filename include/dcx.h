@@ -185,6 +185,23 @@ DCX_API int dcx_power(dcx_ctx* ctx, int32_t use_shift, double shift, double tol,
 /* device time of the last dcx_solve_run/step sequence, seconds */
 DCX_API int dcx_result_device_seconds(dcx_ctx* ctx, double* out);
 
+/* ---- Detached results (the reference returns host arrays, dc/solvers/common.py:33-43) ----
+ * dcx_result_detach moves a finished run's bulk outputs out of the context: the
+ * final states and best spins stay in device memory owned by the result, the
+ * history stays in the pinned buffer the run drained it into. The host arrays
+ * are copied out only when asked for, so a caller reading the energies alone
+ * (dcx_result_summaries, on the context) moves no bulk data; the context can
+ * begin its next run at once. dcx_res_warn_delta: H(x_k) - H(x_{k-1}) at each
+ * replica's descent warning (NaN without one), for the reference's
+ * RuntimeWarning (dc/solvers/doch.py:220-226). */
+typedef struct dcx_result dcx_result;
+DCX_API int dcx_result_detach(dcx_ctx* ctx, dcx_result** out);
+DCX_API int dcx_res_state(dcx_result* res, double* out /* [R][n] */);
+DCX_API int dcx_res_best_spins(dcx_result* res, int8_t* out /* [R][n] */);
+DCX_API int dcx_res_history_all(dcx_result* res, int64_t K, double* h, double* e, double* t, int32_t* ev);
+DCX_API int dcx_res_warn_delta(dcx_result* res, double* out /* [R] */);
+DCX_API void dcx_result_free(dcx_result* res);
+
 /* ---- Row-partitioned solve (multi-GPU) ----
  * The reference has no distributed solver; this splits the one mat-vec per
  * iteration of doch_solve / adoch_solve (economy window) by rows. A context

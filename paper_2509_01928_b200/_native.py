@@ -40,6 +40,8 @@ EXPORTS = (
     "dcx_result_device_seconds", "dcx_profile_kernel", "dcx_set_csr_block", "dcx_stream", "dcx_dist_begin",
     "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish", "dcx_power",
     "dcx_set_procedural", "dcx_proc_row_stats", "dcx_row_stats", "dcx_gen_sparse_9bit", "dcx_gen_result", "dcx_validate_csr",
+    "dcx_result_detach", "dcx_res_state", "dcx_res_best_spins", "dcx_res_history_all", "dcx_res_warn_delta",
+    "dcx_result_free",
 )
 QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
@@ -89,6 +91,7 @@ def load(path: Path | str | None = None):
             f"libdcx.so not found at {p}: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(there is no CPU fallback)")
     lib = C.CDLL(str(p))
+    _tune_host_heap()
     sig = {
         "dcx_abi_version": (C.c_int, []),
         "dcx_last_error": (C.c_char_p, [_P]),
@@ -126,6 +129,12 @@ def load(path: Path | str | None = None):
         "dcx_gen_sparse_9bit": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_uint64, _PI64]),
         "dcx_gen_result": (C.c_int, [_P, _PI64, _PI64, _PD]),
         "dcx_validate_csr": (C.c_int, [_P, C.c_int64, C.c_int64, _PI64, _PI64, _PD, _PI32, _PI64, _PI32]),
+        "dcx_result_detach": (C.c_int, [_P, C.POINTER(_P)]),
+        "dcx_res_state": (C.c_int, [_P, _PD]),
+        "dcx_res_best_spins": (C.c_int, [_P, _PI8]),
+        "dcx_res_history_all": (C.c_int, [_P, C.c_int64, _PD, _PD, _PD, _PI32]),
+        "dcx_res_warn_delta": (C.c_int, [_P, _PD]),
+        "dcx_result_free": (None, [_P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -134,6 +143,21 @@ def load(path: Path | str | None = None):
     if path is None:
         _lib = lib
     return lib
+
+
+def _tune_host_heap():
+    """Serve large host arrays (result states, histories: tens of MB per batch) from the
+    process heap instead of fresh mmap()s, so a freed batch's pages are reused by the next
+    one instead of being unmapped and page-faulted (and zeroed by the kernel) again: glibc
+    M_MMAP_MAX = 0, M_TRIM_THRESHOLD = 1 GiB. DCX_HEAP_TUNE=0 leaves the allocator alone."""
+    if os.environ.get("DCX_HEAP_TUNE", "1") == "0":
+        return
+    try:
+        libc = C.CDLL("libc.so.6")
+        libc.mallopt(-4, 0)  # M_MMAP_MAX
+        libc.mallopt(-1, 1 << 30)  # M_TRIM_THRESHOLD
+    except (OSError, AttributeError):
+        pass
 
 
 def ptr(a: np.ndarray, ctype):
@@ -298,6 +322,12 @@ class Context:
         check(self.lib.dcx_result_state(self.h, ptr(out, C.c_double)), self.h)
         return out
 
+    def detach(self) -> "Result":
+        """Move the finished run's bulk outputs into a Result (device-resident until read)."""
+        h = _P()
+        check(self.lib.dcx_result_detach(self.h, C.byref(h)), self.h)
+        return Result(self.lib, h, self._R, self.n)
+
     def states(self, r: int, iterations: int) -> np.ndarray:
         out = np.empty((iterations + 1, self.n))
         check(self.lib.dcx_result_states(self.h, r, ptr(out, C.c_double)), self.h)
@@ -382,3 +412,43 @@ class Context:
 
     def dist_finish(self):
         check(self.lib.dcx_dist_finish(self.h), self.h)
+
+
+class Result:
+    """A detached run (dcx_result): final states and best spins in device memory,
+    the history in pinned host memory, copied into numpy arrays on request."""
+
+    def __init__(self, lib, handle, R: int, n: int):
+        self.lib, self.h, self.R, self.n = lib, handle, R, n
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.dcx_result_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def state(self) -> np.ndarray:
+        out = np.empty((self.R, self.n))
+        check(self.lib.dcx_res_state(self.h, ptr(out, C.c_double)))
+        return out
+
+    def best_spins(self) -> np.ndarray:
+        out = np.empty((self.R, self.n), dtype=np.int8)
+        check(self.lib.dcx_res_best_spins(self.h, ptr(out, C.c_int8)))
+        return out
+
+    def history_all(self, K: int):
+        h = np.empty((self.R, K))
+        e = np.empty((self.R, K))
+        t = np.empty((self.R, K))
+        ev = np.zeros((self.R, K), np.int32)
+        check(self.lib.dcx_res_history_all(self.h, int(K), ptr(h, C.c_double), ptr(e, C.c_double),
+                                           ptr(t, C.c_double), ptr(ev, C.c_int32)))
+        return h, e, t, ev
+
+    def warn_delta(self) -> np.ndarray:
+        out = np.empty(self.R)
+        check(self.lib.dcx_res_warn_delta(self.h, ptr(out, C.c_double)))
+        return out

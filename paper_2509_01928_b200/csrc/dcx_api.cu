@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -63,6 +65,24 @@ struct InvalidArg : std::runtime_error {
 
 }  // namespace
 
+// A pinned history buffer, shared between the context that drains a run into it and the
+// detached result that reads it later (the context takes a free one for its next run).
+struct PinnedRing {
+  HistRec* p = nullptr;
+  size_t n = 0;
+  ~PinnedRing() {
+    if (p) cudaFreeHost(p);
+  }
+};
+// Device buffer owned by a detached result (gathered states / best spins).
+struct SharedDev {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~SharedDev() {
+    if (p) cudaFree(p);
+  }
+};
+
 struct dcx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -110,15 +130,17 @@ struct dcx_ctx {
   const HistRec& rec(int r, int64_t k) const { return ring_direct ? ring[size_t(r) * cap + k] : hh[r][k]; }
   std::vector<RepCtl> hctl;
   float prof_ms = 0.f;  // dcx_profile_kernel: summed event time of the timed dense launches
-  HistRec* ring = nullptr;  // pinned host copy of the device history ring
+  HistRec* ring = nullptr;  // pinned host copy of the device history ring (ringp->p)
   size_t ring_n = 0;
+  std::shared_ptr<PinnedRing> ringp;                 // the current run's ring
+  std::vector<std::shared_ptr<PinnedRing>> spare;    // rings no detached result holds any more
+  std::vector<std::shared_ptr<SharedDev>> dspare;    // result device buffers free for reuse
   GState hg{};
   GenCsr gen;  // dcx_gen_sparse_9bit result until dcx_gen_result
   unsigned char* pin = nullptr;  // grow-only pinned staging of CSR uploads (row offsets + columns)
   size_t pin_bytes = 0;
 
   ~dcx_ctx() {
-    if (ring) cudaFreeHost(ring);
     if (pin) cudaFreeHost(pin);
     if (graph) cudaGraphExecDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
@@ -281,6 +303,17 @@ void require_coupling(const dcx_ctx* c) {
 }
 
 // ------------------------------------------------------------ small kernels
+template <typename T, typename S = double>
+__global__ void to_device_layout_s(const S* src, T* dst, int64_t n, int R) {
+  // src [R][n] -> dst [n][R]
+  const int64_t total = n * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / R;
+    const int r = int(idx % R);
+    dst[idx] = T(src[(int64_t)r * n + i]) + T(0);  // + 0 turns -0.0 into +0.0 (same spin, see tmap)
+  }
+}
+
 template <typename T>
 __global__ void to_device_layout(const double* src, T* dst, int64_t n, int R) {
   // src [R][n] -> dst [n][R]
@@ -734,7 +767,49 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
     c->n_cols = n;
     c->row_base = 0;
     c->nnz = n * (n - 1);  // upper bound until the CSR form is built
-    dense_upload(c->dn, n, A, c->stream);
+    // J = scale * q with int8 q (the K2000 instance: 1/2 x {0, -1}), classified on every host
+    // thread into the pinned staging: 1 byte per entry crosses PCIe instead of 8
+    const int64_t tot = n * n;
+    const int T = std::max(1, int(std::min<unsigned>(32u, std::thread::hardware_concurrency())));
+    std::vector<double> mns(T, std::numeric_limits<double>::infinity());
+    par_for(tot, [&](int64_t lo, int64_t hi, int t) {
+      double m = std::numeric_limits<double>::infinity();
+      for (int64_t k = lo; k < hi; ++k) {
+        const double a = std::fabs(A[k]);
+        if (a != 0.0 && a < m) m = a;
+      }
+      mns[t] = std::min(mns[t], m);
+    });
+    const double mn = *std::min_element(mns.begin(), mns.end());
+    bool done = false;
+    if (std::isfinite(mn) && tot >= 4096) {
+      if (c->pin_bytes < size_t(tot)) {
+        if (c->pin) cudaFreeHost(c->pin);
+        c->pin = nullptr;
+        c->pin_bytes = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), size_t(tot), cudaHostAllocDefault));
+        c->pin_bytes = size_t(tot);
+      }
+      int8_t* q = reinterpret_cast<int8_t*>(c->pin);
+      for (double cand : {mn, 1.0, 0.5}) {
+        std::vector<unsigned char> ok(T, 1);
+        par_for(tot, [&](int64_t lo, int64_t hi, int t) {
+          bool g = true;
+          for (int64_t k = lo; k < hi; ++k) {
+            const double v = A[k] / cand, r = std::nearbyint(v);
+            g &= (v == r) && std::fabs(r) <= 127.0 && r * cand == A[k];
+            q[k] = int8_t(r);
+          }
+          ok[t] = g;
+        });
+        if (std::all_of(ok.begin(), ok.end(), [](unsigned char b) { return b != 0; })) {
+          dense_upload_int8(c->dn, n, q, cand, c->stream);
+          done = true;
+          break;
+        }
+      }
+    }
+    if (!done) dense_upload(c->dn, n, A, c->stream);
     c->dense = true;
     c->have = true;
   });
@@ -1130,9 +1205,27 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     {
       DevBuf& src = c->scratch;
       if (src.bytes < size_t(tot) * 8) src.alloc(size_t(tot) * 8);
-      CK(cudaMemcpyAsync(src.p, x0, tot * 8, cudaMemcpyHostToDevice, c->stream));
-      if (c->f64) to_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<double*>(a.x[0]), n, R);
-      else to_device_layout<float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<float*>(a.x[0]), n, R);
+      if (c->f64) {
+        CK(cudaMemcpyAsync(src.p, x0, tot * 8, cudaMemcpyHostToDevice, c->stream));
+        to_device_layout<double><<<grid_for(tot), 256, 0, c->stream>>>(src.as<double>(), static_cast<double*>(a.x[0]), n, R);
+      } else {
+        // f32 runs start from x0 rounded to f32 (round to nearest either side): round on all
+        // host threads into the pinned staging and move half the bytes at the DMA rate
+        const size_t bytes = size_t(tot) * 4;
+        if (c->pin_bytes < bytes) {
+          if (c->pin) cudaFreeHost(c->pin);
+          c->pin = nullptr;
+          c->pin_bytes = 0;
+          CK(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), bytes, cudaHostAllocDefault));
+          c->pin_bytes = bytes;
+        }
+        float* x32 = reinterpret_cast<float*>(c->pin);
+        par_for(tot, [&](int64_t lo, int64_t hi, int) {
+          for (int64_t k = lo; k < hi; ++k) x32[k] = float(x0[k]);
+        });
+        CK(cudaMemcpyAsync(src.p, x32, bytes, cudaMemcpyHostToDevice, c->stream));
+        to_device_layout_s<float, float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<float>(), static_cast<float*>(a.x[0]), n, R);
+      }
       CK(cudaMemsetAsync(a.x[1], 0, tot * tb, c->stream));
       if (ad) {
         CK(cudaMemsetAsync(c->ax0.p, 0, tot * tb, c->stream));
@@ -1172,13 +1265,29 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
       v.reserve(std::min<int64_t>(P->max_iters + 1, 4096));
     }
     c->hctl = h;
-    if (c->ring_n < size_t(R) * cap) {
-      if (c->ring) cudaFreeHost(c->ring);
-      c->ring = nullptr;
-      c->ring_n = 0;
-      CK(cudaHostAlloc(reinterpret_cast<void**>(&c->ring), sizeof(HistRec) * size_t(R) * cap, cudaHostAllocDefault));
-      c->ring_n = size_t(R) * cap;
+    // a ring a detached result still reads is left to it: take a free one (or allocate)
+    const size_t need = size_t(R) * cap;
+    if (!c->ringp || c->ringp.use_count() > 1 || c->ringp->n < need) {
+      if (c->ringp && c->ringp.use_count() > 1) c->spare.push_back(c->ringp);
+      c->ringp.reset();
+      for (auto& sp : c->spare)
+        if (sp && sp.use_count() == 1 && sp->n >= need) {
+          c->ringp = sp;
+          sp.reset();
+          break;
+        }
+      c->spare.erase(std::remove_if(c->spare.begin(), c->spare.end(),
+                                    [](const std::shared_ptr<PinnedRing>& q) { return !q || q.use_count() == 1; }),
+                     c->spare.end());  // free rings that no result holds (a fitting one was taken)
+      if (!c->ringp) {
+        auto r = std::make_shared<PinnedRing>();
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&r->p), sizeof(HistRec) * need, cudaHostAllocDefault));
+        r->n = need;
+        c->ringp = r;
+      }
     }
+    c->ring = c->ringp->p;
+    c->ring_n = c->ringp->n;
     c->p_host = 0;
     if (c->path == DCX_PATH_MULTIPASS && !dist) build_graph(c);
     if (c->path == DCX_PATH_DENSE_TC) dense_begin(c->dn, c->mp, c->stream);
@@ -1594,6 +1703,168 @@ int dcx_result_device_seconds(dcx_ctx* c, double* out) {
 }
 
 // ------------------------------------------------------------ generation / ingest (dcx_gen.cu)
+}  // extern "C"
+
+// ---------------------------------------------------------------- detached results
+struct dcx_result {
+  int device = 0;
+  int64_t n = 0;
+  int R = 0, cap = 0;
+  bool ring_direct = false;
+  std::shared_ptr<PinnedRing> ring;
+  std::vector<std::vector<HistRec>> hh;
+  std::vector<int64_t> hcnt;
+  std::vector<double> warn_delta;
+  std::shared_ptr<SharedDev> x, best;  // gathered [R][n]: final states (f64), best spins (int8)
+  std::string err;
+  int64_t nhist(int r) const { return ring_direct ? hcnt[r] : (int64_t)hh[r].size(); }
+  const HistRec& rec(int r, int64_t k) const { return ring_direct ? ring->p[size_t(r) * cap + k] : hh[r][k]; }
+};
+
+namespace {
+// a result-owned device buffer of at least `bytes`, reusing one no live result holds
+std::shared_ptr<SharedDev> take_dev(dcx_ctx* c, size_t bytes) {
+  for (auto& d : c->dspare)
+    if (d && d.use_count() == 1 && d->bytes >= bytes) return d;
+  c->dspare.erase(std::remove_if(c->dspare.begin(), c->dspare.end(),
+                                 [](const std::shared_ptr<SharedDev>& d) { return !d || d.use_count() == 1; }),
+                  c->dspare.end());
+  auto d = std::make_shared<SharedDev>();
+  cudaError_t e = cudaMalloc(&d->p, std::max<size_t>(bytes, 1));
+  if (e != cudaSuccess) {
+    d->p = nullptr;
+    cudaGetLastError();
+    throw std::runtime_error(std::string("OOM: result buffer: ") + cudaGetErrorString(e));
+  }
+  d->bytes = bytes;
+  c->dspare.push_back(d);
+  return d;
+}
+
+template <class Src>
+void history_rows(const Src& src, int R, int64_t K, double* h, double* e, double* t, int32_t* ev) {
+  auto rows = [&](int r0, int r1) {
+    for (int r = r0; r < r1; ++r) {
+      const int64_t cnt = std::min<int64_t>(K, src.nhist(r));
+      const int64_t base = (int64_t)r * K;
+      for (int64_t k = 0; k < cnt; ++k) {
+        const HistRec& q = src.rec(r, k);
+        if (h) h[base + k] = q.h;
+        if (e) e[base + k] = q.e;
+        if (t) t[base + k] = q.t;
+        if (ev) ev[base + k] = q.ev;
+      }
+    }
+  };
+  const int64_t work = int64_t(R) * K;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = int(std::min<int64_t>({int64_t(hw), 8, work / 65536 + 1, int64_t(R)}));
+  if (nt <= 1) {
+    rows(0, R);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int i = 1; i < nt; ++i) pool.emplace_back(rows, int(int64_t(R) * i / nt), int(int64_t(R) * (i + 1) / nt));
+  rows(0, int(int64_t(R) / nt));
+  for (auto& th : pool) th.join();
+}
+}  // namespace
+
+extern "C" {
+
+int dcx_result_detach(dcx_ctx* c, dcx_result** out) {
+  if (!c || !out) return fail(c, DCX_E_INVALID, "null argument");
+  *out = nullptr;
+  if (!c->begun) return fail(c, DCX_E_STATE, "no run");
+  auto res = std::unique_ptr<dcx_result>(new (std::nothrow) dcx_result());
+  if (!res) return fail(c, DCX_E_OOM, "host allocation failed");
+  int rc = guarded(c, [&] {
+    const int64_t n = c->n, R = c->R, tot = n * R;
+    res->device = c->device;
+    res->n = n;
+    res->R = int(R);
+    res->x = take_dev(c, size_t(tot) * 8);
+    res->best = take_dev(c, size_t(tot));
+    if (c->f64)
+      gather_final_state<double><<<grid_for(tot), 256, 0, c->stream>>>(
+          static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          n, (int)R, static_cast<double*>(res->x->p));
+    else
+      gather_final_state<float><<<grid_for(tot), 256, 0, c->stream>>>(
+          static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          n, (int)R, static_cast<double*>(res->x->p));
+    gather_best<<<grid_for(tot), 256, 0, c->stream>>>(c->best.as<int8_t>(), n, (int)R, static_cast<int8_t*>(res->best->p));
+    CK(cudaGetLastError());
+    res->ring_direct = c->ring_direct;
+    res->cap = c->cap;
+    if (c->ring_direct) {
+      res->ring = c->ringp;  // the context takes another ring for its next run
+      res->hcnt = c->hcnt;
+    } else {
+      res->hh = c->hh;  // (runs longer than the ring: the drained copies)
+    }
+    res->warn_delta.assign(R, std::numeric_limits<double>::quiet_NaN());
+    for (int r = 0; r < R; ++r) {
+      const int k = c->hctl[r].warned;
+      if (k >= 1 && k < res->nhist(r)) res->warn_delta[r] = res->rec(r, k).h - res->rec(r, k - 1).h;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+  if (rc == DCX_OK) *out = res.release();
+  return rc;
+}
+
+}  // extern "C"
+
+namespace {
+template <typename F>
+int res_guarded(dcx_result* res, F&& f) {
+  if (!res) return fail(nullptr, DCX_E_INVALID, "result is NULL");
+  try {
+    CK(cudaSetDevice(res->device));
+    f();
+    return DCX_OK;
+  } catch (const std::exception& e) {
+    res->err = e.what();
+    return fail(nullptr, DCX_E_CUDA, e.what());
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int dcx_res_state(dcx_result* res, double* out) {
+  return res_guarded(res, [&] {
+    if (!out) throw std::runtime_error("null output");
+    CK(cudaMemcpy(out, res->x->p, size_t(res->n) * res->R * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int dcx_res_best_spins(dcx_result* res, int8_t* out) {
+  return res_guarded(res, [&] {
+    if (!out) throw std::runtime_error("null output");
+    CK(cudaMemcpy(out, res->best->p, size_t(res->n) * res->R, cudaMemcpyDeviceToHost));
+  });
+}
+
+int dcx_res_history_all(dcx_result* res, int64_t K, double* h, double* e, double* t, int32_t* ev) {
+  if (!res) return fail(nullptr, DCX_E_INVALID, "result is NULL");
+  history_rows(*res, res->R, K, h, e, t, ev);
+  return DCX_OK;
+}
+
+int dcx_res_warn_delta(dcx_result* res, double* out) {
+  if (!res || !out) return fail(nullptr, DCX_E_INVALID, "null argument");
+  std::copy(res->warn_delta.begin(), res->warn_delta.end(), out);
+  return DCX_OK;
+}
+
+void dcx_result_free(dcx_result* res) {
+  if (!res) return;
+  cudaSetDevice(res->device);
+  delete res;
+}
+
 int dcx_gen_sparse_9bit(dcx_ctx* c, int64_t n, int64_t n_p, uint64_t seed, int64_t* nnz) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   return guarded(c, [&] {

@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <initializer_list>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -1581,17 +1582,20 @@ void DenseDev::release() {
   exact = false;
 }
 
-void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
-  // a re-upload of the same size keeps every device buffer (operands, run state,
-  // scratch): no cudaMalloc / cudaFree, which synchronise and cost milliseconds
+namespace {
+__global__ void expand_int8(const int8_t* q, double scale, int64_t total, double* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = scale * double(q[i]);
+}
+
+// device f64 copy of J (kept for the CSR form and the row statistics) and its scratch words
+double* dense_scratch(DenseDev& d, int64_t n, size_t extra) {
   const int64_t npad = (n + 255) / 256 * 256;  // whole int8 stages (2 x 128 of K)
   if (d.npad != npad) d.release();
   d.n = n;
   d.npad = npad;
   d.exact = false;
-  // exact small-integer form J = jscale * Q (the K2000 instance: jscale = 1/2, Q = -W),
-  // found and converted on the device: min |nonzero| gives the candidate scale
-  const size_t need = size_t(n * n) * 8 + 24;
+  const size_t need = size_t(n * n) * 8 + 24 + extra;
   if (d.scratch_bytes < need) {
     if (d.scratch) cudaFree(d.scratch);
     d.scratch = nullptr;
@@ -1599,34 +1603,29 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
     DCK(cudaMalloc(&d.scratch, need));
     d.scratch_bytes = need;
   }
-  double* dA = static_cast<double*>(d.scratch);
+  return static_cast<double*>(d.scratch);
+}
+
+// the exact small-integer operands Q = J / jscale (f16, int8, e4m3) for the first candidate
+// scale that makes every entry an integer
+void dense_operands(DenseDev& d, int64_t n, const double* dA, std::initializer_list<double> cands, cudaStream_t s) {
   unsigned long long* dw = reinterpret_cast<unsigned long long*>(static_cast<char*>(d.scratch) + size_t(n * n) * 8);
-  DCK(cudaMemcpyAsync(dA, A, n * n * 8, cudaMemcpyHostToDevice, s));
-  const unsigned long long init[3] = {~0ull, 0ull, 0ull};
-  DCK(cudaMemcpyAsync(dw, init, 24, cudaMemcpyHostToDevice, s));
-  tc::min_abs_nonzero<<<1024, 256, 0, s>>>(dA, n * n, dw);
-  unsigned long long mnbits = 0;
-  DCK(cudaMemcpyAsync(&mnbits, dw, 8, cudaMemcpyDeviceToHost, s));
-  DCK(cudaStreamSynchronize(s));
   double scale = 0.0;
-  if (mnbits != ~0ull) {
-    double mn;
-    std::memcpy(&mn, &mnbits, 8);
-    if (!d.q16) DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
-    if (!d.q8) DCK(cudaMalloc(&d.q8, d.npad * d.npad));
-    if (!d.q8e) DCK(cudaMalloc(&d.q8e, d.npad * d.npad));
-    for (double cand : {mn, 1.0, 0.5}) {
-      DCK(cudaMemsetAsync(dw + 1, 0, 16, s));
-      tc::q_expand<<<1024, 256, 0, s>>>(dA, cand, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8),
-                                        reinterpret_cast<uint8_t*>(d.q8e), n, d.npad, dw + 1);
-      unsigned long long bad[2] = {1, 1};
-      DCK(cudaMemcpyAsync(bad, dw + 1, 16, cudaMemcpyDeviceToHost, s));
-      DCK(cudaStreamSynchronize(s));
-      if (!bad[0]) {
-        scale = cand;
-        d.f8ok = bad[1] == 0;
-        break;
-      }
+  if (!d.q16) DCK(cudaMalloc(&d.q16, d.npad * d.npad * 2));
+  if (!d.q8) DCK(cudaMalloc(&d.q8, d.npad * d.npad));
+  if (!d.q8e) DCK(cudaMalloc(&d.q8e, d.npad * d.npad));
+  for (double cand : cands) {
+    if (!(cand > 0.0)) continue;
+    DCK(cudaMemsetAsync(dw + 1, 0, 16, s));
+    tc::q_expand<<<1024, 256, 0, s>>>(dA, cand, reinterpret_cast<__half*>(d.q16), reinterpret_cast<int8_t*>(d.q8),
+                                      reinterpret_cast<uint8_t*>(d.q8e), n, d.npad, dw + 1);
+    unsigned long long bad[2] = {1, 1};
+    DCK(cudaMemcpyAsync(bad, dw + 1, 16, cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    if (!bad[0]) {
+      scale = cand;
+      d.f8ok = bad[1] == 0;
+      break;
     }
   }
   if (scale == 0.0) return;  // real-valued couplings: no exact int8 / f16 operand, tensor path unavailable
@@ -1634,6 +1633,37 @@ void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
   d.jscale_d = scale;  // exact: the energies of returned spins are jscale_d * (integer GEMM)
   d.exact = true;
   if (!d.tmaps) d.tmaps = new CUtensorMap[8];
+}
+}  // namespace
+
+void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s) {
+  // a re-upload of the same size keeps every device buffer (operands, run state,
+  // scratch): no cudaMalloc / cudaFree, which synchronise and cost milliseconds
+  double* dA = dense_scratch(d, n, 0);
+  unsigned long long* dw = reinterpret_cast<unsigned long long*>(static_cast<char*>(d.scratch) + size_t(n * n) * 8);
+  // exact small-integer form J = jscale * Q (the K2000 instance: jscale = 1/2, Q = -W),
+  // found and converted on the device: min |nonzero| gives the candidate scale
+  DCK(cudaMemcpyAsync(dA, A, n * n * 8, cudaMemcpyHostToDevice, s));
+  const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+  DCK(cudaMemcpyAsync(dw, init, 24, cudaMemcpyHostToDevice, s));
+  tc::min_abs_nonzero<<<1024, 256, 0, s>>>(dA, n * n, dw);
+  unsigned long long mnbits = 0;
+  DCK(cudaMemcpyAsync(&mnbits, dw, 8, cudaMemcpyDeviceToHost, s));
+  DCK(cudaStreamSynchronize(s));
+  if (mnbits == ~0ull) return;
+  double mn;
+  std::memcpy(&mn, &mnbits, 8);
+  dense_operands(d, n, dA, {mn, 1.0, 0.5}, s);
+}
+
+void dense_upload_int8(DenseDev& d, int64_t n, const int8_t* q_pinned, double scale, cudaStream_t s) {
+  // J = scale * q classified on the host: 1 byte per entry over PCIe instead of 8
+  double* dA = dense_scratch(d, n, size_t(n * n));
+  int8_t* dq = reinterpret_cast<int8_t*>(static_cast<char*>(d.scratch) + size_t(n * n) * 8 + 24);
+  DCK(cudaMemcpyAsync(dq, q_pinned, size_t(n * n), cudaMemcpyHostToDevice, s));
+  expand_int8<<<1024, 256, 0, s>>>(dq, scale, n * n, dA);
+  DCK(cudaGetLastError());
+  dense_operands(d, n, dA, {scale}, s);
 }
 
 static size_t dense_smem_bytes(int nc, int tn) {

@@ -44,6 +44,8 @@ struct DenseDev {
 };
 
 void dense_upload(DenseDev& d, int64_t n, const double* A, cudaStream_t s);
+// J = scale * q with q int8 (classified on the host; q in pinned memory)
+void dense_upload_int8(DenseDev& d, int64_t n, const int8_t* q_pinned, double scale, cudaStream_t s);
 void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s);
 void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s);
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s);

@@ -237,10 +237,106 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
                 fed = int(s.n_hist)
     else:
         ctx.run()
-    best = ctx.best_spins().astype(np.float64)
-    xs = ctx.state()
     path_used = _native.PATH_NAME.get(int(ctx.summary(0).path_used))
-    return assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path_used, record_states)
+    return _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path_used, record_states)
+
+
+_LAZY = object()  # a SolveResult field read from the detached run on first access
+
+
+class _LazySolveResult(SolveResult):
+    """SolveResult whose bulk fields (spins, x, trace, h_values, accepted) stay on the
+    device / in the pinned history until first read (a plain SolveResult otherwise:
+    dataclasses.fields / replace / asdict see the materialised values)."""
+
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if v is _LAZY:
+            v = object.__getattribute__(self, "_bulk").field(name, object.__getattribute__(self, "_r"))
+            object.__setattr__(self, name, v)
+        return v
+
+
+class _Bulk:
+    """The detached outputs of one batch, copied to the host in bulk on first use."""
+
+    def __init__(self, res, solver, R, offset, cut_offset, iters, nh):
+        self.res, self.solver, self.R, self.offset, self.cut_offset = res, solver, R, offset, cut_offset
+        self.iters, self.nh = iters, nh
+        self._x = self._s = self._hist = None
+
+    def _history(self):
+        if self._hist is None:
+            K = int(self.nh.max()) if self.R else 0
+            H, E, T, EV = self.res.history_all(K)
+            if self.offset:
+                T += self.offset
+            rec = (EV & _native.EV_RECORDED) != 0
+            full = rec.sum(axis=1) == self.nh
+            self._hist = (H, E, T, EV, rec, full, np.arange(K))
+        return self._hist
+
+    def field(self, kind, r):
+        if kind == "x":  # (kind: the SolveResult field name)
+            if self._x is None:
+                self._x = self.res.state()
+            return self._x[r]
+        if kind == "spins":
+            if self._s is None:
+                self._s = self.res.best_spins().astype(np.float64)
+            return self._s[r]
+        H, E, T, EV, rec, full, ar = self._history()
+        n_r = int(self.nh[r])
+        if kind == "trace":
+            evr = EV[r, :n_r]
+            if full[r]:
+                return LazyTrace(self.solver, ar[:n_r], T[r, :n_r], E[r, :n_r], self.cut_offset, evr)
+            ks = np.nonzero(rec[r, :n_r])[0]
+            return LazyTrace(self.solver, ks, T[r, ks], E[r, ks], self.cut_offset, evr[ks])
+        if kind == "h_values":
+            hr = H[r, :n_r]
+            return hr if self.R > 1 else hr.tolist()
+        if kind == "accepted":
+            it = int(self.iters[r])
+            evr = EV[r, :n_r]
+            return ([True] + ((evr[2:it + 1] & _native.EV_ACCEPTED) != 0).tolist()) if it else []
+        raise KeyError(kind)
+
+
+def _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path=None, record_states=False):
+    """SolveResults of a finished run whose bulk arrays (final states, best spins, the
+    history) are detached from the context and read only when a field is accessed: the
+    energies, iterations and stop reasons come from the per-replica summaries."""
+    dev_s = ctx.device_seconds()
+    iters, stops, bests, nh, warn = ctx.summaries()
+    states_l = None
+    if record_states:
+        states_l = []
+        for r, it in enumerate(iters.tolist()):
+            st = ctx.states(r, it)
+            states_l.append([st[k].copy() for k in range(it + 1)])
+    res = ctx.detach()
+    warned = np.nonzero(warn >= 0)[0] if solver == "doch" else ()
+    if len(warned):
+        wd = res.warn_delta()
+        for r in warned:
+            warnings.warn(f"Hamiltonian increased by {wd[r]:.3e} at iteration {int(warn[r])}",
+                          RuntimeWarning, stacklevel=4)
+    bulk = _Bulk(res, solver, R, offset, cut_offset, iters, nh)
+    it_l, be_l = iters.tolist(), bests.tolist()
+    stop_l = [_native.STOP.get(v, "max_iters") for v in stops.tolist()]
+    out = []
+    append = out.append
+    L = _LAZY
+    acc = L if solver == "adoch" else None
+    seed_l = [None] * R if seeds is None else list(seeds)
+    for r in range(R):
+        o = _LazySolveResult(solver, L, be_l[r], it_l[r], stop_l[r], L, seed_l[r], L, L, acc,
+                             None if states_l is None else states_l[r], dev_s, path)
+        o._bulk = bulk
+        o._r = r
+        append(o)
+    return out
 
 
 def assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path=None, record_states=False):
