@@ -766,7 +766,13 @@ __device__ __forceinline__ void sort4_cols(int64_t (&c)[4], int (&k)[4]) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) pass_torus(PassArgs a) {
+#ifndef DCX_TORUS_MINB
+#define DCX_TORUS_MINB 2
+#endif
+#ifndef DCX_TORUS_THREADS
+#define DCX_TORUS_THREADS 256
+#endif
+__global__ void __launch_bounds__(DCX_TORUS_THREADS, DCX_TORUS_MINB) pass_torus(PassArgs a) {
   using T = float;
   constexpr int VW = 4;
   static_assert(MODE != MODE_ADOCH_Y, "exact-window ADOCH stays on pass_rv");
@@ -814,9 +820,10 @@ __global__ void __launch_bounds__(256, 2) pass_torus(PassArgs a) {
     neg[v] = 0;
   }
   // site (ar, b) of this warp, advanced by S = grid * 8 sites per step without divisions
-  const int S = int(gridDim.x) * 8;
+  const int NW = int(blockDim.x >> 5);
+  const int S = int(gridDim.x) * NW;
   const int Sa = S / L, Sb = S - Sa * L;
-  int i_cur = int(blockIdx.x) * 8 + warp;
+  int i_cur = int(blockIdx.x) * NW + warp;
   int a_cur = i_cur / L, b_cur = i_cur - a_cur * L;
   auto advance = [&](int& i, int& ar, int& b) {
     i += S;
@@ -979,6 +986,16 @@ __global__ void __launch_bounds__(256, 2) pass_torus(PassArgs a) {
         }
       }
   };
+#if DCX_TORUS_MINB > 2 || DCX_TORUS_THREADS > 256
+  // one register stage, more resident warps (latency hidden across warps)
+  for (;;) {
+    Stage sa;
+    load_stage(sa, i_cur, a_cur, b_cur);
+    if (!sa.on) break;
+    compute_stage(sa);
+    advance(i_cur, a_cur, b_cur);
+  }
+#else
   Stage sa, sb;
   load_stage(sa, i_cur, a_cur, b_cur);
   while (sa.on) {
@@ -990,9 +1007,10 @@ __global__ void __launch_bounds__(256, 2) pass_torus(PassArgs a) {
     load_stage(sa, i_cur, a_cur, b_cur);
     compute_stage(sb);
   }
+#endif
   // block reduction of the per-replica partials, warps in a fixed order (as pass_rv)
   __shared__ double red[NQ][32 * VW];
-  for (int w = 0; w < 8; ++w) {
+  for (int w = 0; w < NW; ++w) {
     if (warp == w) {
 #pragma unroll
       for (int v = 0; v < VW; ++v) {
@@ -1404,8 +1422,8 @@ static void launch_pass_vk(int mode, const PassArgs& a, int V, int grid, cudaStr
     if constexpr (sizeof(T) == 4 && VK == VK_I8) {
       if (a.torus_L > 0 && W == 4 && mode != MODE_ADOCH_Y && use_torus() && a.cfg.n * R / 4 < (int64_t(1) << 31)) {
         const dim3 g(grid, (R + 127) / 128);
-        if (mode == MODE_DOCH) pass_torus<MODE_DOCH><<<g, 256, 0, s>>>(a);
-        else pass_torus<MODE_ADOCH_X><<<g, 256, 0, s>>>(a);
+        if (mode == MODE_DOCH) pass_torus<MODE_DOCH><<<g, DCX_TORUS_THREADS, 0, s>>>(a);
+        else pass_torus<MODE_ADOCH_X><<<g, DCX_TORUS_THREADS, 0, s>>>(a);
         return;
       }
     }

@@ -77,7 +77,10 @@ struct Pipe {
   static_assert(B_BYTES % 1024 == 0, "SW128 tiles: whole 8-row groups");
   // KA K-atoms (128 bytes of K each) per stage: fewer mbarrier round trips per MMA,
   // which is what paces tcgen05 at N = 128 (measured: 4 MMAs/stage 124 cyc/MMA, 8: 101)
-  static constexpr int KA = 2;
+#ifndef DCX_DENSE_KA
+#define DCX_DENSE_KA 2
+#endif
+  static constexpr int KA = DCX_DENSE_KA;
   static constexpr uint32_t STAGE = KA * (TILE_BYTES + B_BYTES);  // A atoms then B atoms
   static constexpr int STAGES = int(196608 / STAGE) < MAX_STAGES ? int(196608 / STAGE) : MAX_STAGES;  // 192 KB
   static constexpr uint32_t TILES = STAGES * STAGE;
@@ -106,6 +109,8 @@ static_assert(sizeof(SyncWords) == 64, "one line per group");
 // replica tile rt and spin tile t has written its part of x_v (f16 and sign
 // operands). Own 64-byte line each; stored after the SyncWords array.
 constexpr int FLAG_STRIDE = 16;
+constexpr int DBG_STAGE = 4096 * 14 + 256 * 8;  // DCX_DENSE_TRACE per-stage stamps of CTA 0, p < 128
+constexpr int DBG_TOTAL = DBG_STAGE + 128 * 32 * 2;
 constexpr int MAX_FLAGS = 256;
 
 struct Args {
@@ -704,6 +709,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           __syncwarp();  // the lanes' acquires before lane 0's loads
         }
         if (lane == 0) {
+          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 2] = clock64();
           if (kb < nb1) fence_async_global();  // generic writes (acquired above) before the async-proxy loads
           const uint32_t fb = smem_u32(&sm.full[s]);
           if (leader)
@@ -752,6 +758,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t ph = (kiter / P::STAGES) & 1;
           const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
+          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 2 + 1] = clock64();
           // D1 of iteration p-1 read by the epilogue before GEMM1(p) overwrites it
           if (kb == 0 && p > p_start) mbar_wait(smem_u32(&sm.d1free), (p - 1 - p_start) & 1);
           // D2 of iteration p-1 drained by the epilogue before GEMM2(p) overwrites it
@@ -1757,8 +1764,8 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) cudaFree(d.dbg);
   d.dbg = nullptr;
   if (std::getenv("DCX_DENSE_TRACE")) {
-    DCK(cudaMalloc(&d.dbg, (4096 * 14 + 256 * 8) * 8));
-    DCK(cudaMemsetAsync(d.dbg, 0, (4096 * 14 + 256 * 8) * 8, s));
+    DCK(cudaMalloc(&d.dbg, size_t(tc::DBG_TOTAL) * 8));
+    DCK(cudaMemsetAsync(d.dbg, 0, size_t(tc::DBG_TOTAL) * 8, s));
   }
   tc::pack_state<<<1024, 256, 0, s>>>(reinterpret_cast<const float*>(m.args.x[0]), int(d.n), d.R, int(d.npad),
                                        m.args.ctl, reinterpret_cast<float*>(d.xm[0]),
@@ -1877,7 +1884,7 @@ void dense_step(DenseDev& d, MultiPass& m, int chunk, cudaStream_t s) {
 
 void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
   if (d.dbg) {  // phase breakdown of CTA 0 (DCX_DENSE_TRACE=1)
-    std::vector<unsigned long long> t(4096 * 14 + 256 * 8);
+    std::vector<unsigned long long> t(tc::DBG_TOTAL);
     DCK(cudaMemcpyAsync(t.data(), d.dbg, t.size() * 8, cudaMemcpyDeviceToHost, s));
     DCK(cudaStreamSynchronize(s));
     const unsigned long long* gt = t.data() + 4096 * 13;
@@ -1887,6 +1894,27 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
       std::fprintf(stderr, "[dcx dense trace] SM clock %.0f MHz, %.2f us/iter over %d iterations\n",
                    double(t[last * 12] - t[12]) / double(gt[last] - gt[1]) * 1e3,
                    double(gt[last] - gt[1]) / 1e3 / (last - 1), last - 1);
+    {  // per-stage timeline of CTA 0 relative to its own operand publication of the previous update
+      const int p1 = std::min(last, 120);
+      double pr[32] = {0}, mf[32] = {0};
+      int np = 0;
+      for (int p = 10; p < p1; ++p, ++np) {
+        const double t0 = double(t[(p - 1) * 12 + 1]);
+        for (int kb = 0; kb < 32; ++kb) {
+          pr[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 2]) - t0;
+          mf[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 2 + 1]) - t0;
+        }
+      }
+      if (np) {
+        std::fprintf(stderr, "[dcx dense trace] stage stamps (kcycles after CTA 0 published x_p): TMA issue | MMA data ready\n");
+        for (int kb = 0; kb < 32; ++kb)
+          if (pr[kb] != 0.0 || mf[kb] != 0.0)
+            std::fprintf(stderr, "  kb %2d  %7.2f | %7.2f\n", kb, pr[kb] / np / 1e3, mf[kb] / np / 1e3);
+        double gd = 0;
+        for (int p = 10; p < p1; ++p) gd += double(t[p * 12 + 11]) - double(t[(p - 1) * 12 + 1]);
+        std::fprintf(stderr, "  GEMM1 complete (epilogue) %7.2f\n", gd / np / 1e3);
+      }
+    }
     double m[8] = {0, 0, 0, 0, 0, 0, 0, 0}, u[4] = {0, 0, 0, 0};
     int cnt = 0;
     for (int p = 2; p < last; ++p, ++cnt) {
