@@ -361,6 +361,7 @@ def run_ours(args):
     # ---------------- end-to-end through the public API with host buffers
     e2e_t, e2e_upd = 0.0, 0
     h2d = d2h = 0
+    dc.solve_replicas(inst, args.solver, ALPHA, BETA, X0, reupload=True, **kw)  # warm the upload path
     barrier(world)
     for s in range(args.steps):
         flush.fill_(float(s))

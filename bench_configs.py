@@ -267,6 +267,7 @@ def run(args):
     for _ in range(args.warmup):
         dc.solve_replicas(inst, "doch", alpha, beta, X0, **kw)
     dev, upd, wall = 0.0, 0, 0.0
+    dc.solve_replicas(inst, "doch", alpha, beta, X0, reupload=True, **kw)  # warm the upload path (untimed)
     for _ in range(args.steps):
         t0 = time.perf_counter()
         # host buffers in (the CSR arrays and x0 are uploaded every step), the energies out
