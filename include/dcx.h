@@ -225,6 +225,13 @@ DCX_API int dcx_dist_begin(dcx_ctx* ctx, const dcx_params* params, int32_t R, co
                            const double* x0_rows /* [R][n_rows] */, void* x_buf0, void* x_buf1, double* q_sum,
                            double* q_max);
 DCX_API int dcx_dist_pass(dcx_ctx* ctx);
+/* The pass split in two row ranges so the x exchange can overlap it: the caller orders its
+ * rows [interior | boundary] (boundary = rows that reference halo rows or that other ranks
+ * read), runs [0, n_interior) while the halo of x_p is in flight, then the boundary rows,
+ * then dcx_dist_reduce (both halves of the partial slots into q_sum / q_max), in place of
+ * dcx_dist_pass. half: 0 or 1, the slot half the range writes. */
+DCX_API int dcx_dist_pass_rows(dcx_ctx* ctx, int64_t row_lo, int64_t row_hi, int32_t half);
+DCX_API int dcx_dist_reduce(dcx_ctx* ctx);
 DCX_API int dcx_dist_control(dcx_ctx* ctx);
 /* synchronises the stream, drains the history; *live = 0 once every replica stopped */
 DCX_API int dcx_dist_poll(dcx_ctx* ctx, int32_t* live, int64_t* passes);

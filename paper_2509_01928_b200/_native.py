@@ -41,7 +41,7 @@ EXPORTS = (
     "dcx_dist_pass", "dcx_dist_control", "dcx_dist_poll", "dcx_dist_finish", "dcx_power",
     "dcx_set_procedural", "dcx_proc_row_stats", "dcx_row_stats", "dcx_gen_sparse_9bit", "dcx_gen_result", "dcx_validate_csr",
     "dcx_result_detach", "dcx_res_state", "dcx_res_best_spins", "dcx_res_history_all", "dcx_res_warn_delta",
-    "dcx_result_free",
+    "dcx_result_free", "dcx_dist_pass_rows", "dcx_dist_reduce",
 )
 QSUM, QMAX = 5, 3  # DCX_QSUM / DCX_QMAX
 
@@ -123,6 +123,8 @@ def load(path: Path | str | None = None):
         "dcx_dist_begin": (C.c_int, [_P, C.POINTER(Params), C.c_int32, _PD, _PD, _PD, _P, _P, _P, _P]),
         "dcx_dist_pass": (C.c_int, [_P]),
         "dcx_dist_control": (C.c_int, [_P]),
+        "dcx_dist_pass_rows": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32]),
+        "dcx_dist_reduce": (C.c_int, [_P]),
         "dcx_dist_poll": (C.c_int, [_P, _PI32, _PI64]),
         "dcx_dist_finish": (C.c_int, [_P]),
         "dcx_power": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_int64, _PD, _PD, _PD, _PI64, _PI32]),
@@ -400,6 +402,12 @@ class Context:
 
     def dist_pass(self):
         check(self.lib.dcx_dist_pass(self.h), self.h)
+
+    def dist_pass_rows(self, lo: int, hi: int, half: int):
+        check(self.lib.dcx_dist_pass_rows(self.h, int(lo), int(hi), int(half)), self.h)
+
+    def dist_reduce(self):
+        check(self.lib.dcx_dist_reduce(self.h), self.h)
 
     def dist_control(self):
         check(self.lib.dcx_dist_control(self.h), self.h)

@@ -1107,7 +1107,11 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
       c->mp.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, std::max(1, 148 * per_sm / chunks)));
       slots = c->mp.grid;
     }
+    // a row-partitioned run may split its pass into two row ranges (dcx_dist_pass_rows):
+    // each writes its own half of the slots, zero until written
+    if (dist) slots *= 2;
     c->part.alloc(sizeof(double) * R * NQ * slots);
+    if (dist) CK(cudaMemsetAsync(c->part.p, 0, c->part.bytes, c->stream));
     {
       int64_t fthreads = std::min<int64_t>(std::max<int64_t>(tot, R), int64_t(148) * 8 * 256);
       int fg = (int)((fthreads + 255) / 256);
@@ -1325,6 +1329,26 @@ int dcx_dist_pass(dcx_ctx* c) {
   return guarded(c, [&] {
     if (!c->begun || !c->dist || c->finished) throw InvalidArg("no row-partitioned run in progress");
     enqueue_dist_pass(c->mp, c->qs, c->qm, c->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+int dcx_dist_pass_rows(dcx_ctx* c, int64_t row_lo, int64_t row_hi, int32_t half) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun || !c->dist || c->finished) throw InvalidArg("no row-partitioned run in progress");
+    if (row_lo < 0 || row_hi < row_lo || row_hi > c->n || (half != 0 && half != 1))
+      throw InvalidArg("row range outside the block");
+    if (row_hi > row_lo) enqueue_dist_pass_rows(c->mp, row_lo, row_hi, half, c->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+int dcx_dist_reduce(dcx_ctx* c) {
+  if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
+  return guarded(c, [&] {
+    if (!c->begun || !c->dist || c->finished) throw InvalidArg("no row-partitioned run in progress");
+    enqueue_dist_reduce(c->mp, c->qs, c->qm, c->stream);
     CK(cudaGetLastError());
   });
 }

@@ -1516,6 +1516,35 @@ void enqueue_dist_pass(const MultiPass& m, double* qs, double* qm, cudaStream_t 
   reduce_control<<<a.cfg.R, 256, 0, s>>>(a, doch ? nullptr : m.spart, doch ? 0 : m.sslots, doch ? 0 : 1, 0, 1, qs, qm);
 }
 
+// The pass over own rows [lo, hi) only (the interior / boundary split of the exchange
+// overlap): every row-indexed pointer moves to row lo; the gather source
+// (gx, the whole local + halo space) does not. Partials go to slot half `half` of the 2 x grid
+// slots a row-partitioned run allocates; enqueue_dist_reduce folds both halves.
+void enqueue_dist_pass_rows(const MultiPass& m, int64_t lo, int64_t hi, int half, cudaStream_t s) {
+  PassArgs a = m.args;
+  const int64_t R = a.cfg.R;
+  const size_t tb = m.f64 ? 8 : 4;
+  auto shift = [&](void* p) { return p ? static_cast<void*>(static_cast<char*>(p) + size_t(lo) * R * tb) : p; };
+  a.rp += lo;
+  a.x[0] = shift(a.x[0]);
+  a.x[1] = shift(a.x[1]);
+  a.ax[0] = shift(a.ax[0]);
+  a.ax[1] = shift(a.ax[1]);
+  a.ay = shift(a.ay);
+  a.best += lo * R;
+  a.cfg.n = hi - lo;
+  a.part += int64_t(half) * (a.slots / 2);
+  const int mode = m.solver == DCX_SOLVER_DOCH ? MODE_DOCH : MODE_ADOCH_X;
+  if (m.f64) launch_pass_t<double>(mode, a, m.vk, m.V, m.grid, s);
+  else launch_pass_t<float>(mode, a, m.vk, m.V, m.grid, s);
+}
+
+void enqueue_dist_reduce(const MultiPass& m, double* qs, double* qm, cudaStream_t s) {
+  const PassArgs& a = m.args;
+  const bool doch = m.solver == DCX_SOLVER_DOCH;
+  reduce_control<<<a.cfg.R, 256, 0, s>>>(a, doch ? nullptr : m.spart, doch ? 0 : m.sslots, doch ? 0 : 1, 0, 1, qs, qm);
+}
+
 void enqueue_dist_control(const MultiPass& m, const double* qs, const double* qm, cudaStream_t s) {
   const PassArgs& a = m.args;
   double* q0 = const_cast<double*>(qs);

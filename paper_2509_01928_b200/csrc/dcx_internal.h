@@ -92,6 +92,9 @@ void enqueue_iteration(const MultiPass& m, cudaStream_t s);
 // the per-replica partials: pass + per-rank reduction into qs/qm, then control
 void enqueue_dist_pass(const MultiPass& m, double* qs, double* qm, cudaStream_t s);
 void enqueue_dist_control(const MultiPass& m, const double* qs, const double* qm, cudaStream_t s);
+// the pass over own rows [lo, hi) into slot half `half`, and the fold of both halves into qs / qm
+void enqueue_dist_pass_rows(const MultiPass& m, int64_t lo, int64_t hi, int half, cudaStream_t s);
+void enqueue_dist_reduce(const MultiPass& m, double* qs, double* qm, cudaStream_t s);
 void enqueue_flush(const MultiPass& m, cudaStream_t s);
 void enqueue_pass_only(const MultiPass& m, cudaStream_t s);
 void enqueue_start_clock(GState* g, cudaStream_t s);

@@ -34,8 +34,18 @@ remap, so each row's sum order -- and therefore every iterate -- is
 bit-identical to the single-GPU multipass path; only the order of the H partial
 sums across blocks differs.
 
+With the neighbour-only exchange the rows of a block are also reordered
+[interior | boundary] (boundary: rows that reference a halo row, or that another
+rank reads) and the pass runs as two row ranges (``dcx_dist_pass_rows``): the
+interior range reads own rows only, so with NCCL the halo exchange of x_p runs on
+its own stream and communicator while the interior rows of pass p compute; the
+boundary range waits for it (a CUDA event), then both halves of the partials are
+folded (``dcx_dist_reduce``). Each row keeps its entries in their stored order, so
+the iterates stay bit-identical.
+
 With the NCCL backend the collectives run on the context stream directly on
-device buffers; with gloo (CPU transport) they are staged through host memory.
+device buffers; with gloo (CPU transport) they are staged through host memory
+(and the exchange is not overlapped).
 """
 
 from __future__ import annotations
@@ -282,6 +292,37 @@ def compact_columns(cols_padded, rb: RowBlocks, rank: int, plan: "HaloPlan"):
     return out
 
 
+def interior_first(n_rows: int, ro, ccols, B: int, send_local):
+    """Row order [interior | boundary] of a halo-exchanging block: boundary rows reference a
+    halo row (compact column >= B) or are read by another rank (send_local); interior rows do
+    neither, so their pass can run while the halo of x_p is still in flight. Returns
+    (perm: new row k = old row perm[k], inverse, interior count)."""
+    ro = np.asarray(ro, dtype=np.int64)
+    rid = np.repeat(np.arange(n_rows, dtype=np.int64), np.diff(ro))
+    bnd = np.zeros(n_rows, dtype=bool)
+    bnd[rid[np.asarray(ccols) >= B]] = True
+    bnd[np.asarray(send_local, dtype=np.int64)] = True
+    perm = np.concatenate([np.nonzero(~bnd)[0], np.nonzero(bnd)[0]])
+    inv = np.empty(n_rows, dtype=np.int64)
+    inv[perm] = np.arange(n_rows, dtype=np.int64)
+    return perm, inv, int((~bnd).sum())
+
+
+def permute_rows(perm, inv, ro, vals, ccols, B: int):
+    """The block's CSR with rows in `perm` order and own columns renamed through `inv`
+    (halo columns >= B unchanged). Each row keeps its entries in their stored order, so its
+    sum -- and every iterate -- is bit-identical."""
+    ro = np.asarray(ro, dtype=np.int64)
+    lengths = np.diff(ro)[perm]
+    new_ro = np.zeros(len(perm) + 1, dtype=np.int64)
+    np.cumsum(lengths, out=new_ro[1:])
+    idx = np.repeat(ro[perm] - new_ro[:-1], lengths) + np.arange(int(new_ro[-1]), dtype=np.int64)
+    c = np.asarray(ccols, dtype=np.int64)[idx]
+    own = c < B
+    c[own] = inv[c[own]]
+    return new_ro, np.asarray(vals)[idx], c
+
+
 def halo_plan(ex: "Exchange", cols_padded, rb: RowBlocks) -> HaloPlan:
     """Every rank states what it needs; two all-to-alls (counts, then positions) turn
     the needs into send lists. Setup only (once per solve)."""
@@ -292,6 +333,22 @@ def halo_plan(ex: "Exchange", cols_padded, rb: RowBlocks) -> HaloPlan:
     if send_pos.size and (send_pos.min() < lo or send_pos.max() >= lo + rb.B):
         raise RuntimeError("halo plan: a peer asked for rows this rank does not own")
     return HaloPlan(send_pos, send_counts, recv_pos, recv_counts)
+
+
+_XGROUPS = {}
+
+
+def _exchange_group(group, world: int):
+    """A second communicator over the same ranks for the x exchange (made once per group): NCCL
+    collectives of one communicator must not run concurrently on two streams, and the halo
+    exchange overlaps the partials' all-gather of the next iteration's pass."""
+    import torch.distributed as tdist
+
+    key = (id(group), world)
+    if key not in _XGROUPS:
+        ranks = list(range(world)) if group is None else tdist.get_process_group_ranks(group)
+        _XGROUPS[key] = tdist.new_group(ranks)
+    return _XGROUPS[key]
 
 
 # -------------------------------------------------------------------- driver
@@ -346,9 +403,15 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
             vol = torch.tensor([float(plan.volume), float(rb.n_space - rb.B)], dtype=torch.float64, device=tdev)
             ex.all_reduce(vol, "sum")
             use_halo = bool(vol[0] < 0.75 * vol[1])
+    perm = None
     if use_halo:
         space, base = rb.B + plan.volume, 0
-        ctx.set_csr_block(n_rows, space, base, vals, compact_columns(cols, rb, ex.rank, plan), ro)
+        # rows [interior | boundary]: the interior pass overlaps the halo exchange of x_p
+        cc = compact_columns(cols, rb, ex.rank, plan)
+        send_old = plan.send_pos - ex.rank * rb.B
+        perm, inv, n_int = interior_first(n_rows, ro, cc, rb.B, send_old)
+        ro_p, vals_p, cc_p = permute_rows(perm, inv, ro, vals, cc, rb.B)
+        ctx.set_csr_block(n_rows, space, base, vals_p, cc_p, ro_p)
     else:
         space, base = rb.n_space, ex.rank * rb.B
         ctx.set_csr_block(n_rows, space, base, vals, cols, ro)
@@ -363,37 +426,65 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         conv_tol=CONVERGENCE_TOL, descent_tol=DESCENT_WARN_TOL, record_states=0,
         path=_native.PATH["multipass"], chunk=0, reserved=0)
     stream = (torch.cuda.ExternalStream(ctx.stream(), device=tdev) if tdev.type == "cuda" else None)
+    # with NCCL the halo exchange runs on its own stream and communicator, overlapped with the
+    # interior rows of the next pass; the partials' all-gather stays on the context stream
+    overlap = use_halo and stream is not None and not ex.host_staged
+    if overlap:
+        ex_x = Exchange(_exchange_group(group, ex.world))
+        comm = torch.cuda.Stream(device=tdev)
     with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
+        x0_rows = X0[:, r0:r1] if perm is None else X0[:, r0:r1][:, perm]
         if use_halo:
-            send_local = torch.from_numpy(plan.send_pos - ex.rank * rb.B).to(tdev)
+            send_local = torch.from_numpy(inv[send_old]).to(tdev)
             step = lambda Xp: ex.halo_compact(Xp, plan, send_local, rb.B)  # noqa: E731
         elif ex.world > 1:
             step = lambda Xp: ex.all_gather_rows(Xp, rb.B)  # noqa: E731
         else:
             step = lambda Xp: None  # noqa: E731  (one rank: x is all local)
-        ctx.dist_begin(prm, alpha, beta, X0[:, r0:r1], X[0].data_ptr(), X[1].data_ptr(), qs.data_ptr(),
+        ctx.dist_begin(prm, alpha, beta, x0_rows, X[0].data_ptr(), X[1].data_ptr(), qs.data_ptr(),
                        qm.data_ptr())
         offset = time.perf_counter() - t_entry
         step(X[0])
         p, live = 0, True
+        halo_done = None
         while live:
             for _ in range(max(1, int(poll_every))):
-                ctx.dist_pass()
+                if perm is not None:
+                    ctx.dist_pass_rows(0, n_int, 0)  # interior rows: own x only
+                    if halo_done is not None:
+                        stream.wait_event(halo_done)  # the halo of x_p has landed
+                    ctx.dist_pass_rows(n_int, n_rows, 1)
+                    ctx.dist_reduce()
+                else:
+                    ctx.dist_pass()
                 if ex.world > 1:
                     ex.combine(qs, qm)  # one collective for the SUM and MAX partials
                 ctx.dist_control()
                 p += 1
-                step(X[p & 1])
+                if overlap:  # x_{p+1} is final once control p ran: exchange it behind the next interior pass
+                    ready = torch.cuda.Event()
+                    ready.record(stream)
+                    comm.wait_event(ready)
+                    with torch.cuda.stream(comm):
+                        ex_x.halo_compact(X[p & 1], plan, send_local, rb.B)
+                        halo_done = torch.cuda.Event()
+                        halo_done.record(comm)
+                else:
+                    step(X[p & 1])
             live, _ = ctx.dist_poll()
+        if halo_done is not None:
+            stream.wait_event(halo_done)
         ctx.dist_finish()
         # gather best spins and final states of every row block (padded space)
         pad = np.zeros((R, rb.B))
-        pad[:, :n_rows] = ctx.best_spins().astype(np.float64)
+        bs = ctx.best_spins().astype(np.float64)
+        pad[:, :n_rows] = bs if perm is None else bs[:, inv]
         best_t = torch.from_numpy(pad.T.copy()).to(tdev)
         full_b = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
         full_b[ex.rank * rb.B:(ex.rank + 1) * rb.B] = best_t
         ex.all_gather_rows(full_b, rb.B)
-        pad[:, :n_rows] = ctx.state()
+        st = ctx.state()
+        pad[:, :n_rows] = st if perm is None else st[:, inv]
         full_x = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
         full_x[ex.rank * rb.B:(ex.rank + 1) * rb.B] = torch.from_numpy(pad.T.copy()).to(tdev)
         ex.all_gather_rows(full_x, rb.B)

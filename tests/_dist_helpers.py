@@ -85,6 +85,40 @@ class FakeRowContext:
         Xn[rows] = np.where(run[None, :], xn.T, Xn[rows])
         self._x = x
 
+    def dist_pass_rows(self, lo, hi, half):
+        """dcx_dist_pass_rows: rows [lo, hi) only, reading the buffers as they are at the call
+        (a boundary range run before its halo landed would read a stale halo)."""
+        p = self.p
+        Xc, Xn = self.X[p & 1], self.X[(p + 1) & 1]
+        if not hasattr(self, "_hp") or self._hp[0] != p:
+            R = self._R
+            self._hp = (p, np.zeros((2, R, _native.QSUM)), np.zeros((2, R, _native.QMAX)), np.zeros((R, self.n)))
+        _, hs, hm, xall = self._hp
+        if hi <= lo:
+            return
+        rows = slice(self.row_base + lo, self.row_base + hi)
+        A = self.A[lo:hi]
+        x = Xc[rows].T.astype(np.float64)
+        jx = (A @ Xc.astype(np.float64)).T
+        js = (A @ np.where(Xc >= 0, 1.0, -1.0)).T
+        ax = jx + self.alpha[:, None] * x
+        xn = np.cbrt(ax / self.beta[:, None])
+        run = self.status == 0
+        hs[half] = 0
+        hs[half, :, 0] = (x * x * x * x).sum(1)
+        hs[half, :, 1] = (x * ax).sum(1)
+        hs[half, :, 2] = (np.where(x >= 0, 1.0, -1.0) * js).sum(1)
+        hm[half] = 0
+        hm[half, :, 0] = np.abs(xn - x).max(1)
+        Xn[rows] = np.where(run[None, :], xn.T, Xn[rows])
+        xall[:, lo:hi] = x
+
+    def dist_reduce(self):
+        _, hs, hm, xall = self._hp
+        self.qs[:] = hs[0] + hs[1]
+        self.qm[:] = np.maximum(hm[0], hm[1])
+        self._x = xall.copy()
+
     def dist_control(self):
         p = self.p
         for r in np.nonzero(self.status == 0)[0]:
