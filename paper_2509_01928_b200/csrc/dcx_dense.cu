@@ -144,7 +144,8 @@ struct Args {
   int f8;
   float* dsc;      // f8: 2^-e of the replica's last written delta (resume), [Rpad]
   int exp;         // timing experiments only (DCX_DENSE_EXP, wrong results): 1 skip A loads,
-                   // 2 skip B loads, 4 skip GEMM2 (the sign GEMM); 8: spin (no sleep) on GEMM1 done
+                   // 2 skip B loads, 4 skip GEMM2 (the sign GEMM); 8: spin (no sleep) on GEMM1 done;
+                   // 32: wait for every tile's flag before the first GEMM1 stage (exact results)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -693,7 +694,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         if (kb < nb1) {
           const unsigned tf0 = a.dbg ? clock() : 0u;
           const int t_lo = (kt * ks1) / TN, t_hi = min(a.tiles_n - 1, (kt * ks1 + ks1 - 1) / TN);
-          const uint32_t need = t_lo > t_hi ? 0u : (((2u << t_hi) - 1u) & ~((1u << t_lo) - 1u));
+          uint32_t need = t_lo > t_hi ? 0u : (((2u << t_hi) - 1u) & ~((1u << t_lo) - 1u));
+          // (timing experiment, DCX_DENSE_EXP & 32: every tile of the group before the first stage)
+          if ((a.exp & 32) && kb == 0) need = a.tiles_n >= 32 ? 0xffffffffu : ((1u << a.tiles_n) - 1u);
           long long t0 = 0;
           unsigned int polls = 0;
           while ((ready & need) != need) {
