@@ -110,7 +110,7 @@ static_assert(sizeof(SyncWords) == 64, "one line per group");
 // operands). Own 64-byte line each; stored after the SyncWords array.
 constexpr int FLAG_STRIDE = 16;
 constexpr int DBG_STAGE = 4096 * 14 + 256 * 8;  // DCX_DENSE_TRACE per-stage stamps of CTA 0, p < 128
-constexpr int DBG_TOTAL = DBG_STAGE + 128 * 32 * 2;
+constexpr int DBG_TOTAL = DBG_STAGE + 128 * 32 * 4;
 constexpr int MAX_FLAGS = 256;
 
 struct Args {
@@ -688,6 +688,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         const int s = kiter % P::STAGES;
         const uint32_t ph = (kiter / P::STAGES) & 1;
         if (lane == 0) mbar_wait(smem_u32(&sm.empty[s]), ph ^ 1);
+        if (a.dbg && lane == 0 && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 4 + 2] = clock64();
         // GEMM1 stage kt: K columns [ks1 kt, ks1 kt + ks1), written by the spin tiles they
         // overlap; GEMM2 stages (two 8-bit atoms of 128) were all waited in GEMM1
         const int kt = kb < nb1 ? (kb + kst1) % nb1 : (kb - nb1 + kstart8) % KB2;
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           __syncwarp();  // the lanes' acquires before lane 0's loads
         }
         if (lane == 0) {
-          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 2] = clock64();
+          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 4] = clock64();
           if (kb < nb1) fence_async_global();  // generic writes (acquired above) before the async-proxy loads
           const uint32_t fb = smem_u32(&sm.full[s]);
           if (leader)
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           const uint32_t ph = (kiter / P::STAGES) & 1;
           const unsigned long long tw0 = clock64();
           mbar_wait(smem_u32(&sm.full[s]), ph);
-          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 2 + 1] = clock64();
+          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 4 + 1] = clock64();
           // D1 of iteration p-1 read by the epilogue before GEMM1(p) overwrites it
           if (kb == 0 && p > p_start) mbar_wait(smem_u32(&sm.d1free), (p - 1 - p_start) & 1);
           // D2 of iteration p-1 drained by the epilogue before GEMM2(p) overwrites it
@@ -769,31 +770,34 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           wait_cyc += clock64() - tw0;
           tc_fence_after();
           const uint32_t s0 = smem_u32(tiles + s * P::STAGE);
+          // the stage's MMAs with the operand descriptors advanced by constant offsets from two base
+          // descriptors (the 14-bit start-address field holds smem byte address >> 4 < 2^14): a few
+          // uniform adds per MMA instead of rebuilding each descriptor, so the one issuing thread --
+          // which shares its scheduler with two epilogue warps -- keeps the tensor pipe fed
+          auto issue = [&](auto kindc, const uint32_t dcol, const uint32_t id, const bool first) {
+            constexpr int KIND = decltype(kindc)::value;  // 0 e4m3, 1 f16, 2 int8
+            const uint64_t da = sw128_desc(s0), db = sw128_desc(s0 + P::KA * TILE_BYTES);
 #pragma unroll
-          for (int q = 0; q < P::KA; ++q) {
-            const uint32_t sa = s0 + q * TILE_BYTES, sb = s0 + P::KA * TILE_BYTES + q * P::B_BYTES;
-            if (kb < nb1) {
-              if (f8it) {
+            for (int q = 0; q < P::KA; ++q)
 #pragma unroll
-                for (int k = 0; k < 4; ++k)  // 4 x (K = 32 e4m3 = 32 B) along the 128-byte row
-                  mma_f8_g<NC>(tmem + rcol(p), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
-                               (kb | q | k) ? 1u : 0u);  // F_p = Q (2^e Dh_p)
-              } else {
-#pragma unroll
-                for (int k = 0; k < TK / UK; ++k)  // 4 x (K = 16 f16 = 32 B) along the 128-byte row
-                  mma_f16_g<NC>(tmem + rcol(p), sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc,
-                                (kb | q | k) ? 1u : 0u);  // F_p = Q Dh_p
+              for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K along the 128-byte swizzled row
+                const uint64_t ad = da + uint64_t((q * TILE_BYTES + k * 32) >> 4);
+                const uint64_t bd = db + uint64_t((q * P::B_BYTES + k * 32) >> 4);
+                const uint32_t acc = (first && q == 0 && k == 0) ? 0u : 1u;
+                if constexpr (KIND == 0) mma_f8_g<NC>(dcol, ad, bd, id, acc);
+                else if constexpr (KIND == 1) mma_f16_g<NC>(dcol, ad, bd, id, acc);
+                else mma_i8_g<NC>(dcol, ad, bd, id, acc);
               }
-            } else if (a.f8) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)  // e4m3 dS in {0, +-2}: D2 += Q dS in f32 (exact integers)
-                mma_f8_g<NC>(tmem + D2COL, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc, 1u);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)  // 4 x (K = 32 int8 = 32 B) along the 128-byte row
-                mma_i8_g<NC>(tmem + D2COL, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), idesc8, 1u);  // D2 += Q dS
-            }
+          };
+          if (kb < nb1) {  // F_p = Q (2^e Dh_p) (e4m3), or Q Dh_p (f16, p = 0)
+            if (f8it) issue(std::integral_constant<int, 0>{}, tmem + rcol(p), idesc, kb == 0);
+            else issue(std::integral_constant<int, 1>{}, tmem + rcol(p), idesc, kb == 0);
+          } else if (a.f8) {  // e4m3 dS in {0, +-2}: D2 += Q dS in f32 (exact integers)
+            issue(std::integral_constant<int, 0>{}, tmem + D2COL, idesc, false);
+          } else {  // D2 += Q dS (int8)
+            issue(std::integral_constant<int, 2>{}, tmem + D2COL, idesc8, false);
           }
+          if (a.dbg && blockIdx.x == 0 && p < 128 && kb < 32) a.dbg[DBG_STAGE + (p * 32 + kb) * 4 + 3] = clock64();
           mma_commit_g<NC>(smem_u32(&sm.empty[s]), uint16_t(!a.mc ? 0x3 : (psub == 0 ? 0x3 : 0xF)));
           if (tr && kb == 0) a.dbg[p * 12 + 8] = clock64();
           if (a.dbg && kb == 0) d_g1 -= clock();
@@ -1899,20 +1903,22 @@ void dense_finish(DenseDev& d, MultiPass& m, cudaStream_t s) {
                    double(gt[last] - gt[1]) / 1e3 / (last - 1), last - 1);
     {  // per-stage timeline of CTA 0 relative to its own operand publication of the previous update
       const int p1 = std::min(last, 120);
-      double pr[32] = {0}, mf[32] = {0};
+      double pr[32] = {0}, mf[32] = {0}, ew[32] = {0}, mi[32] = {0};
       int np = 0;
       for (int p = 10; p < p1; ++p, ++np) {
         const double t0 = double(t[(p - 1) * 12 + 1]);
         for (int kb = 0; kb < 32; ++kb) {
-          pr[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 2]) - t0;
-          mf[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 2 + 1]) - t0;
+          pr[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 4]) - t0;
+          mf[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 4 + 1]) - t0;
+          ew[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 4 + 2]) - t0;
+          mi[kb] += double(t[tc::DBG_STAGE + (p * 32 + kb) * 4 + 3]) - t0;
         }
       }
       if (np) {
-        std::fprintf(stderr, "[dcx dense trace] stage stamps (kcycles after CTA 0 published x_p): TMA issue | MMA data ready\n");
+        std::fprintf(stderr, "[dcx dense trace] stage stamps (kcycles after CTA 0 published x_p): slot free | TMA issue | MMA data ready | MMAs issued\n");
         for (int kb = 0; kb < 32; ++kb)
-          if (pr[kb] != 0.0 || mf[kb] != 0.0)
-            std::fprintf(stderr, "  kb %2d  %7.2f | %7.2f\n", kb, pr[kb] / np / 1e3, mf[kb] / np / 1e3);
+          if (pr[kb] > 0.0 || mf[kb] > 0.0)
+            std::fprintf(stderr, "  kb %2d  %7.2f | %7.2f | %7.2f | %7.2f\n", kb, ew[kb] / np / 1e3, pr[kb] / np / 1e3, mf[kb] / np / 1e3, mi[kb] / np / 1e3);
         double gd = 0;
         for (int p = 10; p < p1; ++p) gd += double(t[p * 12 + 11]) - double(t[(p - 1) * 12 + 1]);
         std::fprintf(stderr, "  GEMM1 complete (epilogue) %7.2f\n", gd / np / 1e3);

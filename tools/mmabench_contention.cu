@@ -21,18 +21,27 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t ph) {
   asm volatile("{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(a), "r"(ph) : "memory");
 }
 
+template <int CE, int LAYOUT = 0, bool RANDOM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int iters, int copy_kb, const char* gsrc, long long* out, int tmem_ld) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t bar, cbar;
+  __shared__ __align__(8) uint64_t bar, cbar, sbar[8];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int opbytes = 4 * 16384 + 4 * 8192;  // A 64 KB + B 32 KB (resident operands)
-  for (int i = threadIdx.x; i < opbytes / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0x38383838u;
+  for (int i = threadIdx.x; i < opbytes / 4; i += blockDim.x) {
+    uint32_t h = uint32_t(i) * 2654435761u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    // RANDOM: e4m3 bytes of random sign and magnitude in [2^-6, 2^3) (no NaN), like the deltas
+    reinterpret_cast<uint32_t*>(base)[i] = RANDOM ? ((h & 0x3f3f3f3fu) | 0x08080808u) ^ (h & 0x80808080u) : 0x38383838u;
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar)), "r"(1) : "memory");
+    for (int k = 0; k < 8; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sbar[k])), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < 32) {
@@ -87,13 +96,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int it
   if (rank == 0 && threadIdx.x == 0) {
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it)
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t acc = (it | q | k) ? 1u : 0u;
+          const uint32_t aa = LAYOUT == 0 ? sa + q * 16384 : sa + (q >> 1) * 49152 + (q & 1) * 16384;
+          const uint32_t bb = LAYOUT == 0 ? sb + q * 8192 : sa + (q >> 1) * 49152 + 32768 + (q & 1) * 8192;
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                       "l"(sw128_desc(sa + q * 16384 + k * 32)), "l"(sw128_desc(sb + q * 8192 + k * 32)), "r"(idesc), "r"(acc) : "memory");
+                       "l"(sw128_desc(aa + k * 32)), "l"(sw128_desc(bb + k * 32)), "r"(idesc), "r"(acc) : "memory");
         }
+        // a completion signal every CE MMAs (CE = 4: per atom, 8: per 2-atom stage as the kernel, 16: per 4 atoms)
+        if (CE == 4 || (CE == 8 && (q & 1)) || (CE == 16 && q == 3))
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                           smem_u32(&sbar[q])), "h"(uint16_t(3)) : "memory");
+      }
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                      smem_u32(&bar)), "h"(uint16_t(3)) : "memory");
     mbar_wait(smem_u32(&bar), 0);
@@ -114,12 +130,48 @@ int main() {
   cudaMalloc(&g, size_t(148) * 6 * 16384);
   cudaMemset(g, 0x38, size_t(148) * 6 * 16384);
   const int smem = 4 * 16384 + 4 * 8192 + 6 * 16384 + 1024;
-  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int rep = 0; rep < 2; ++rep) {
+    bench<8, 1, true><<<128, 256, smem>>>(256, 0, g, d, 0);
+    cudaDeviceSynchronize();
+  }
+  {
+    long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("kernel stage layout, random e4m3 operands: %.1f cycles per MMA\n", h / (256 * 16.0));
+  }
   const int iters = 256;
+  for (int rep = 0; rep < 2; ++rep) {
+    bench<8, 1><<<128, 256, smem>>>(iters, 0, g, d, 0);
+    cudaDeviceSynchronize();
+  }
+  {
+    long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("kernel stage layout (A A B B per 48 KB), commit per 8: %.1f cycles per MMA\n", h / (iters * 16.0));
+  }
+  
+  for (int ce : {4, 8, 16}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (ce == 4) bench<4><<<128, 256, smem>>>(iters, 0, g, d, 0);
+      else if (ce == 8) bench<8><<<128, 256, smem>>>(iters, 0, g, d, 0);
+      else bench<16><<<128, 256, smem>>>(iters, 0, g, d, 0);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+    }
+    long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("commit (multicast arrive) every %2d MMAs: %.1f cycles per MMA\n", ce, h / (iters * 16.0));
+  }
   for (int mode = 0; mode < 6; ++mode) {
     const int copy_kb = mode < 3 ? 0 : 96, tl = (mode % 3 == 0) ? 0 : (mode % 3 == 1 ? 1 : 4);
     for (int rep = 0; rep < 2; ++rep) {
-      bench<<<128, 256, smem>>>(iters, copy_kb, g, d, tl);
+      bench<0><<<128, 256, smem>>>(iters, copy_kb, g, d, tl);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
