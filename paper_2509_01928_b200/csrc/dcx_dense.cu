@@ -1099,7 +1099,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
           }
         }
         tmem_st16(xaddr + off, st);
-        if (valid && lim > 0) {  // stopped replicas write zero deltas
+        // every column of a live replica's operand row is written, padding included (zero deltas):
+        // the e4m3 view of a delta buffer aliases the f16 deltas of iteration 0, so a padding
+        // column left unwritten would read stale f16 bytes -- NaN patterns among them -- which
+        // the zero rows of Q turn into 0 x NaN = NaN in every product (a fully padded warp,
+        // lim == 0, happens when n mod 128 <= 64 or a whole spin tile is padding)
+        if (valid) {  // stopped replicas write zero deltas
           if (f8) {
             *reinterpret_cast<uint4*>(hb + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
           } else {
@@ -1210,8 +1215,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         // the delta operand packed into 32-bit words (built with shifts, not by type punning:
         // reading a uint16 / half2 array through uint4 pointers is undefined and was
         // miscompiled once the loop was restructured): f16 pairs, or 4 e4m3 bytes per word
-        uint32_t hw[W / 2];
-        __align__(16) uint32_t sv[W / 4];
+        uint32_t hw[W / 2] = {};
+        __align__(16) uint32_t sv[W / 4] = {};
         if (lim > 0) {
           // branch-free over all W columns (s is never -0.0 after the first update, so s < 0
           // <=> sign bit). Padding columns (i >= n) hold s = +0 and R = F = 0 (zero rows and
@@ -1283,7 +1288,12 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
         }  // (lim == 0: padding replica or columns, the state stays)
         tmem_stw<W>(lane_base + rcol(p) + off, rv);
         tmem_stw<W>(xaddr + off, st);
-        if (valid && lim > 0) {  // stopped replicas write zero deltas
+        // every column of a live replica's operand row is written, padding included (zero deltas):
+        // the e4m3 view of a delta buffer aliases the f16 deltas of iteration 0, so a padding
+        // column left unwritten would read stale f16 bytes -- NaN patterns among them -- which
+        // the zero rows of Q turn into 0 x NaN = NaN in every product (a fully padded warp,
+        // lim == 0, happens when n mod 128 <= 64 or a whole spin tile is padding)
+        if (valid) {  // stopped replicas write zero deltas
           if (f8) {
 #pragma unroll
             for (int k = 0; k < W / 4; k += 4) *reinterpret_cast<uint4*>(hb + off + 4 * k) = make_uint4(hw[k], hw[k + 1], hw[k + 2], hw[k + 3]);

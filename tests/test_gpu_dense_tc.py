@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import paper_2509_01928_b200 as dc
+from paper_2509_01928_b200 import synth
 from conftest import k2_W
 
 pytestmark = pytest.mark.gpu
@@ -115,6 +116,27 @@ def test_tc_energies_exact():
     for r in res[:8]:
         assert all(t.energy == t.energy for t in r.trace)  # recorded every iteration (stride 1)
         assert len(r.trace) == r.iterations + 1
+
+
+@pytest.mark.parametrize("n", [300, 384, 640])
+@pytest.mark.parametrize("solver", ["doch", "adoch"])
+def test_tc_padding_columns_stay_finite(n, solver):
+    """Sizes whose padding fills whole epilogue halves or spin tiles (n mod 128 <= 64): the
+    e4m3 operand rows alias the iteration-0 f16 deltas, so every padding column must be
+    written (zero) each iteration -- a stale byte read as e4m3 NaN poisoned every product of
+    its replica row (0 x NaN). States and H stay finite, and runs are reproducible."""
+    W = synth.dense_pm1(n, seed=3)
+    inst = dc.ProblemInstance(coupling=dc.maxcut_to_ising(dc.DenseCoupling(W, validate=False)))
+    a, b = 3.0, n ** 1.5 * 300.0
+    X0 = x0s(n, a, b, range(32))
+    r1 = dc.solve_replicas(inst, solver, a, b, X0, max_iters=60, precision="f16tc")
+    assert r1[0].path == "dense_tc"
+    for r in r1:
+        assert np.all(np.isfinite(r.x)) and np.all(np.isfinite(np.asarray(r.h_values)))
+    dc.solve_replicas(inst, solver, a, b, x0s(n, a, b, range(100, 132)), max_iters=60, precision="f16tc")
+    r2 = dc.solve_replicas(inst, solver, a, b, X0, max_iters=60, precision="f16tc")
+    for p_, q_ in zip(r1, r2):
+        assert np.array_equal(p_.x, q_.x) and p_.energy == q_.energy and p_.iterations == q_.iterations
 
 
 def test_tc_padding_ragged_sizes():
