@@ -1,6 +1,7 @@
 // libdcx C ABI (include/dcx.h): context, coupling upload, operator seam and
 // the chunked solve driver. No exception crosses the ABI.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -80,6 +81,24 @@ struct SharedDev {
   size_t bytes = 0;
   ~SharedDev() {
     if (p) cudaFree(p);
+  }
+};
+
+// DCX_TIMING=1: wall-clock phases of the host entry points on stderr (e2e analysis)
+static bool timing_on() {
+  static const bool on = std::getenv("DCX_TIMING") != nullptr;
+  return on;
+}
+struct PhaseClock {
+  const char* what;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  explicit PhaseClock(const char* w) : what(w) {}
+  void mark(const char* phase) {
+    if (!timing_on()) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dcx timing] %s %-18s %8.3f ms\n", what, phase,
+                 std::chrono::duration<double, std::milli>(t - last).count());
+    last = t;
   }
 };
 
@@ -192,9 +211,9 @@ int lanes_for_degree(double d) {
 // Host passes over the uploaded arrays (10^8 entries at R8) run on all host threads:
 // f(lo, hi, t) over contiguous chunks [lo, hi) of [0, n), chunk t of T.
 template <class F>
-static void par_for(int64_t n, F&& f) {
+static void par_for(int64_t n, F&& f, int max_threads = 32) {
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const int T = n < (int64_t(1) << 20) ? 1 : int(std::min<unsigned>(hw, 32u));
+  const int T = n < (int64_t(1) << 20) ? 1 : int(std::min<unsigned>(std::min<unsigned>(hw, 32u), unsigned(max_threads)));
   if (T == 1) {
     f(int64_t(0), n, 0);
     return;
@@ -769,20 +788,10 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
     c->nnz = n * (n - 1);  // upper bound until the CSR form is built
     // J = scale * q with int8 q (the K2000 instance: 1/2 x {0, -1}), classified on every host
     // thread into the pinned staging: 1 byte per entry crosses PCIe instead of 8
+    PhaseClock pc("set_dense");
     const int64_t tot = n * n;
-    const int T = std::max(1, int(std::min<unsigned>(32u, std::thread::hardware_concurrency())));
-    std::vector<double> mns(T, std::numeric_limits<double>::infinity());
-    par_for(tot, [&](int64_t lo, int64_t hi, int t) {
-      double m = std::numeric_limits<double>::infinity();
-      for (int64_t k = lo; k < hi; ++k) {
-        const double a = std::fabs(A[k]);
-        if (a != 0.0 && a < m) m = a;
-      }
-      mns[t] = std::min(mns[t], m);
-    });
-    const double mn = *std::min_element(mns.begin(), mns.end());
     bool done = false;
-    if (std::isfinite(mn) && tot >= 4096) {
+    if (tot >= 4096) {
       if (c->pin_bytes < size_t(tot)) {
         if (c->pin) cudaFreeHost(c->pin);
         c->pin = nullptr;
@@ -791,8 +800,14 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
         c->pin_bytes = size_t(tot);
       }
       int8_t* q = reinterpret_cast<int8_t*>(c->pin);
-      for (double cand : {mn, 1.0, 0.5}) {
-        std::vector<unsigned char> ok(T, 1);
+      // one pass per candidate scale: the first nonzero |J| (the K2000 instance: 1/2), then
+      // 1 and 1/2; each pass checks J = scale * q with |q| <= 127 and writes q
+      double first = 0.0;
+      for (int64_t k = 0; k < tot && first == 0.0; ++k) first = std::fabs(A[k]);
+      const int T = int(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())));
+      for (double cand : {first, 1.0, 0.5}) {
+        if (!(cand > 0.0) || !std::isfinite(cand)) continue;
+        std::vector<unsigned char> ok(64, 1);
         par_for(tot, [&](int64_t lo, int64_t hi, int t) {
           bool g = true;
           for (int64_t k = lo; k < hi; ++k) {
@@ -801,9 +816,13 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
             q[k] = int8_t(r);
           }
           ok[t] = g;
-        });
+        }, T);
         if (std::all_of(ok.begin(), ok.end(), [](unsigned char b) { return b != 0; })) {
+          pc.mark("classify");
+          // candidates coarser than the true grid are rejected above; a finer-than-needed one
+          // (first > min |J|) cannot pass, so cand is the operand scale
           dense_upload_int8(c->dn, n, q, cand, c->stream);
+          pc.mark("upload+operands");
           done = true;
           break;
         }
@@ -1031,6 +1050,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     if (P->trace_stride < 1) throw InvalidArg("trace_stride must be >= 1");
     for (int r = 0; r < R; ++r)
       if (!(alpha[r] > 0) || !(beta[r] > 0)) throw InvalidArg("alpha and beta must be positive");
+    PhaseClock pc("begin");
     c->prm = *P;
     c->R = R;
     c->begun = false;
@@ -1044,6 +1064,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     const size_t tb = c->f64 ? 8 : 4;
     c->J = csr_view(c, c->f64);
     c->sp = plan_small(c->J, P->solver, P->window_mode, c->f64);
+    pc.mark("views");
     c->dist = dist;
     if (dist) c->path = DCX_PATH_MULTIPASS;
     else if (use_tc) c->path = DCX_PATH_DENSE_TC;
@@ -1226,7 +1247,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
         float* x32 = reinterpret_cast<float*>(c->pin);
         par_for(tot, [&](int64_t lo, int64_t hi, int) {
           for (int64_t k = lo; k < hi; ++k) x32[k] = float(x0[k]);
-        });
+        }, 16);
+        pc.mark("x0 to f32");
         CK(cudaMemcpyAsync(src.p, x32, bytes, cudaMemcpyHostToDevice, c->stream));
         to_device_layout_s<float, float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<float>(), static_cast<float*>(a.x[0]), n, R);
       }
@@ -1238,6 +1260,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
       CK(cudaMemsetAsync(c->best.p, 1, tot, c->stream));
       if (c->states.p) CK(cudaMemcpyAsync(c->states.p, a.x[0], tot * tb, cudaMemcpyDeviceToDevice, c->stream));
       CK(cudaStreamSynchronize(c->stream));
+      pc.mark("x0 upload");
     }
     std::vector<RepCtl> h(R);
     for (int r = 0; r < R; ++r) {
@@ -1293,8 +1316,10 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     c->ring = c->ringp->p;
     c->ring_n = c->ringp->n;
     c->p_host = 0;
+    pc.mark("state+ring");
     if (c->path == DCX_PATH_MULTIPASS && !dist) build_graph(c);
     if (c->path == DCX_PATH_DENSE_TC) dense_begin(c->dn, c->mp, c->stream);
+    pc.mark("graph/dense_begin");
     CK(cudaEventRecord(c->ev0, c->stream));
     enqueue_start_clock(c->g.as<GState>(), c->stream);
     CK(cudaGetLastError());
@@ -1476,11 +1501,13 @@ int dcx_solve_step(dcx_ctx* c, int32_t* live) {
 }
 
 int dcx_solve_run(dcx_ctx* c) {
+  PhaseClock pc("run");
   int32_t live = 1;
   while (live) {
     int rc = dcx_solve_step(c, &live);
     if (rc != DCX_OK) return rc;
   }
+  pc.mark("steps");
   return DCX_OK;
 }
 
