@@ -52,6 +52,7 @@ from __future__ import annotations
 
 import contextlib
 import time
+import weakref
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -107,6 +108,8 @@ class RowBlocks:
     def position(self, j):
         """Index of spin j in the padded space."""
         j = np.asarray(j, dtype=np.int64)
+        if self.world == 1:
+            return j
         starts = np.array([r0 for r0, _ in self.blocks], dtype=np.int64)
         q = np.searchsorted(starts, j, side="right") - 1
         return q * self.B + (j - starts[q])
@@ -336,6 +339,38 @@ def halo_plan(ex: "Exchange", cols_padded, rb: RowBlocks) -> HaloPlan:
 
 
 _XGROUPS = {}
+_PLANS = {}
+
+
+def _block_plan(J, ex: "Exchange", exchange: str, tdev) -> dict:
+    """This rank's row block of J, ready to upload: the nnz-balanced partition, columns in the
+    padded space, or -- with the neighbour-only exchange -- in the compact [own | halo] space with
+    the rows ordered [interior | boundary] (dist.interior_first)."""
+    import torch
+
+    rb = RowBlocks(partition_rows(J.row_offsets, ex.world), J.n)
+    r0, r1 = rb.blocks[ex.rank]
+    n_rows, vals, cols, ro = local_block(J, rb, ex.rank)
+    # exchange plan: neighbour-only halo in a compact index space, or the all-gather of the padded space
+    use_halo, plan = False, None
+    if exchange != "allgather" and ex.world > 1:
+        plan = halo_plan(ex, cols, rb)
+        use_halo = exchange == "halo"
+        if exchange == "auto":
+            vol = torch.tensor([float(plan.volume), float(rb.n_space - rb.B)], dtype=torch.float64, device=tdev)
+            ex.all_reduce(vol, "sum")
+            use_halo = bool(vol[0] < 0.75 * vol[1])
+    bp = {"rb": rb, "r0": r0, "r1": r1, "n_rows": n_rows, "use_halo": use_halo}
+    if use_halo:
+        cc = compact_columns(cols, rb, ex.rank, plan)
+        send_old = plan.send_pos - ex.rank * rb.B
+        perm, inv, n_int = interior_first(n_rows, ro, cc, rb.B, send_old)
+        ro_p, vals_p, cc_p = permute_rows(perm, inv, ro, vals, cc, rb.B)
+        bp.update(plan=plan, perm=perm, inv=inv, n_int=n_int, send_old=send_old, space=rb.B + plan.volume, base=0,
+                  vals=vals_p, cols=cc_p, ro=ro_p)
+    else:
+        bp.update(space=rb.n_space, base=ex.rank * rb.B, vals=vals, cols=cols, ro=ro)
+    return bp
 
 
 def _exchange_group(group, world: int):
@@ -384,37 +419,27 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
     R, n = X0.shape
     if n != J.n:
         raise ValueError(f"x0 has {n} columns, expected {J.n}")
-    rb = RowBlocks(partition_rows(J.row_offsets, ex.world), J.n)
-    r0, r1 = rb.blocks[ex.rank]
-    n_rows, vals, cols, ro = local_block(J, rb, ex.rank)
     if _context is None:
         dev = _native.default_device() if device is None else int(device)
-        ctx = _native.Context(dev)
         tdev = torch.device("cuda", dev)
     else:
-        ctx, tdev = _context, torch.device("cpu")
-    # exchange plan (setup, once per solve): neighbour-only halo in a compact index space, or
-    # the all-gather of the padded space
-    use_halo = False
-    if exchange != "allgather" and ex.world > 1:
-        plan = halo_plan(ex, cols, rb)
-        use_halo = exchange == "halo"
-        if exchange == "auto":
-            vol = torch.tensor([float(plan.volume), float(rb.n_space - rb.B)], dtype=torch.float64, device=tdev)
-            ex.all_reduce(vol, "sum")
-            use_halo = bool(vol[0] < 0.75 * vol[1])
-    perm = None
-    if use_halo:
-        space, base = rb.B + plan.volume, 0
-        # rows [interior | boundary]: the interior pass overlaps the halo exchange of x_p
-        cc = compact_columns(cols, rb, ex.rank, plan)
-        send_old = plan.send_pos - ex.rank * rb.B
-        perm, inv, n_int = interior_first(n_rows, ro, cc, rb.B, send_old)
-        ro_p, vals_p, cc_p = permute_rows(perm, inv, ro, vals, cc, rb.B)
-        ctx.set_csr_block(n_rows, space, base, vals_p, cc_p, ro_p)
+        dev, tdev = None, torch.device("cpu")
+    # the block plan (partition, column remap, exchange plan, row order) and the context are
+    # made once per (coupling, group, rank, exchange, device) and reused by later solves; the
+    # block itself is uploaded again every solve (the caller's arrays may have changed)
+    key = (id(J), id(group), ex.world, ex.rank, exchange, dev)
+    cached = _PLANS.get(key) if _context is None else None
+    if cached is not None and cached["ref"]() is J:
+        bp, ctx = cached["plan"], cached["ctx"]
     else:
-        space, base = rb.n_space, ex.rank * rb.B
-        ctx.set_csr_block(n_rows, space, base, vals, cols, ro)
+        bp = _block_plan(J, ex, exchange, tdev)
+        ctx = _native.Context(dev) if _context is None else _context
+        if _context is None:
+            _PLANS[key] = {"ref": weakref.ref(J), "plan": bp, "ctx": ctx}
+    rb, r0, r1, n_rows, use_halo, space, base = (bp[k] for k in ("rb", "r0", "r1", "n_rows", "use_halo", "space",
+                                                                  "base"))
+    plan, perm, inv, n_int, send_old = (bp.get(k) for k in ("plan", "perm", "inv", "n_int", "send_old"))
+    ctx.set_csr_block(n_rows, space, base, bp["vals"], bp["cols"], bp["ro"])
     dt = torch.float64 if precision == "f64" else torch.float32
     X = [torch.zeros(space, R, dtype=dt, device=tdev) for _ in range(2)]
     qs = torch.zeros(R, _native.QSUM, dtype=torch.float64, device=tdev)
