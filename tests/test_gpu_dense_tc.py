@@ -139,6 +139,29 @@ def test_tc_padding_columns_stay_finite(n, solver):
         assert np.array_equal(p_.x, q_.x) and p_.energy == q_.energy and p_.iterations == q_.iterations
 
 
+@pytest.mark.parametrize("n,R", [(130, 1), (250, 5), (513, 100), (1000, 300), (767, 257)])
+def test_tc_shapes_sweep(n, R):
+    """Ragged spin counts and replica counts (padding replicas and spins, one CTA or pairs):
+    the first iterate matches the e4m3 emulation, every returned state and H is finite, and
+    the returned spins carry their exact energies, for DOCH and ADOCH."""
+    W = synth.dense_pm1(n, seed=n)
+    Jd = -0.5 * W
+    inst = dc.ProblemInstance(coupling=dc.maxcut_to_ising(dc.DenseCoupling(W, validate=False)))
+    p = dc.derive_params(inst.coupling, eta=0.2)
+    X0 = x0s(n, p.alpha, p.beta, range(R))
+    one = dc.solve_replicas(inst, "doch", p.alpha, p.beta, X0, max_iters=1, precision="f16tc")
+    assert one[0].path == "dense_tc"
+    for x0, r in zip(X0[:8], one[:8]):
+        emu = doch_first_iterate_emulation(Jd, x0, p.alpha, p.beta)
+        assert np.mean(np.isclose(r.x, emu, rtol=1e-5, atol=0)) >= 0.99
+    for solver in ("doch", "adoch"):
+        rs = dc.solve_replicas(inst, solver, p.alpha, p.beta, X0, max_iters=120, precision="f16tc")
+        E = dc.energies(inst.coupling, np.stack([r.spins for r in rs]))
+        np.testing.assert_array_equal(E, [r.energy for r in rs])
+        for r in rs:
+            assert np.all(np.isfinite(r.x)) and np.all(np.isfinite(np.asarray(r.h_values)))
+
+
 def test_tc_padding_ragged_sizes():
     rng = np.random.default_rng(4)
     n = 300
