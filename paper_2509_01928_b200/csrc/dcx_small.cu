@@ -5,6 +5,9 @@
 // For the G1-shape config (n = 800, 38,352 nnz) the pattern is 77 KB of uint16
 // column indices; there is no HBM traffic per iteration except the history
 // ring and best-spin copies.
+#include <cstdio>
+#include <cstdlib>
+
 #include "dcx_internal.h"
 
 namespace dcx {
@@ -20,6 +23,7 @@ struct SmallArgs {
   int col_is16;
   int ell;    // columns held as 32-row sliced ELL (V == 1): one conflict-free load per 32 rows and entry
   int pow2;   // uniform values, power-of-two scale: sum x_j, multiply once (bit-identical to sum v x_j)
+  int trace;  // DCX_SMALL_TRACE: phase stamps of block 0
 };
 
 __host__ __device__ constexpr int val_bytes(int vk) {
@@ -65,6 +69,9 @@ __device__ __forceinline__ void block_reduce(double* v, double (*sh)[NQ], double
   }
   __syncthreads();
 }
+
+// DCX_SMALL_TRACE: phase stamps of block 0, thread 0, iterations 10..73 (clock64)
+__device__ unsigned long long g_small_trace[64 * 4];
 
 template <typename T, int VK>
 __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
@@ -222,6 +229,8 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
   T* states = reinterpret_cast<T*>(a.states);
 
   while (p < s.p_end) {
+    const bool trc = s.trace && blockIdx.x == 0 && threadIdx.x == 0 && p >= 10 && p < 74;
+    if (trc) g_small_trace[(p - 10) * 4 + 0] = clock64();
     T* xc = (p & 1) ? xb1 : xb0;  // x_p
     T* xo = (p & 1) ? xb0 : xb1;  // DOCH: x_{p-1} -> x_{p+1}; ADOCH: x_{p-1}
     T* ac = (p & 1) ? axb1 : axb0;
@@ -294,7 +303,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
         row_done(i, acc, es);
       }
     }
+    if (trc) g_small_trace[(p - 10) * 4 + 1] = clock64();
     block_reduce(v, red, tot);
+    if (trc) g_small_trace[(p - 10) * 4 + 2] = clock64();
     if (threadIdx.x == 0) {
       const double now = double(globaltimer() - a.g->t0) * 1e-9;
       double t2[NQ];
@@ -355,6 +366,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(SmallArgs s) {
       if (c.pend == p)
         for (int i = threadIdx.x; i < n; i += blockDim.x) a.best[(int64_t)i * R + r] = xc[i] >= T(0) ? 1 : -1;
     }
+    if (trc) g_small_trace[(p - 10) * 4 + 3] = clock64();
     ++p;
     if (flag_stop) break;
   }
@@ -412,6 +424,7 @@ void launch_small(const MultiPass& m, const CsrDev& J, const SmallPlan& sp, int 
   s.p_end = p_end;
   s.ell = sp.ell ? int(J.ell) : 0;
   s.pow2 = J.pow2_uniform ? 1 : 0;
+  s.trace = std::getenv("DCX_SMALL_TRACE") != nullptr;
   if (m.f64) {
     switch (J.vk) {
       case VK_UNIFORM: launch_small_t<double, VK_UNIFORM>(s, sp, st); break;
@@ -428,6 +441,23 @@ void launch_small(const MultiPass& m, const CsrDev& J, const SmallPlan& sp, int 
       case VK_F32: launch_small_t<float, VK_F32>(s, sp, st); break;
       default: launch_small_t<float, VK_F64>(s, sp, st); break;
     }
+  }
+  if (s.trace) {
+    unsigned long long t[64 * 4];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(t, g_small_trace, sizeof(t));
+    double ph[3] = {0, 0, 0};
+    int cnt = 0;
+    for (int k = 0; k < 63; ++k) {
+      if (!t[k * 4] || !t[k * 4 + 3]) continue;
+      ph[0] += double(t[k * 4 + 1] - t[k * 4]);
+      ph[1] += double(t[k * 4 + 2] - t[k * 4 + 1]);
+      ph[2] += double(t[k * 4 + 3] - t[k * 4 + 2]);
+      ++cnt;
+    }
+    if (cnt)
+      std::fprintf(stderr, "[dcx small trace] cycles per iteration: pass %.0f | reduce %.0f | control+rest %.0f\n",
+                   ph[0] / cnt, ph[1] / cnt, ph[2] / cnt);
   }
 }
 
