@@ -21,7 +21,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t ph) {
   asm volatile("{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(a), "r"(ph) : "memory");
 }
 
-template <int CE, int LAYOUT = 0, bool RANDOM = false>
+template <int CE, int LAYOUT = 0, bool RANDOM = false, int SPIN = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int iters, int copy_kb, const char* gsrc, long long* out, int tmem_ld) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tmem_base;
@@ -69,6 +69,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int it
       ph ^= 1;
     }
   }
+  __shared__ __align__(8) uint64_t spinbar;
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&spinbar)), "r"(1) : "memory");
+    done = 0;
+  }
+  __syncthreads();
+  if (SPIN && threadIdx.x >= 128 && (threadIdx.x & 31) == 0 && ((threadIdx.x >> 5) - 4) < SPIN) {
+    // one lane per spinning warp polls an mbarrier phase that does not complete (as the kernel's
+    // producer / MMA issuer / epilogue do while they wait)
+    while (!done) {
+      uint32_t ok;
+      asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+                   : "=r"(ok) : "r"(smem_u32(&spinbar)), "r"(0) : "memory");
+    }
+  }
   if (tmem_ld && threadIdx.x >= 128) {
     // 4 warps (one per TMEM lane quadrant) read 3 x 16 columns and write 2 x 16 back, in a loop,
     // from columns 256.. (not the accumulator): the update's TMEM traffic
@@ -114,8 +130,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int it
                      smem_u32(&bar)), "h"(uint16_t(3)) : "memory");
     mbar_wait(smem_u32(&bar), 0);
     out[0] = clock64() - t0;
+    done = 1;
   } else if (rank == 1 && threadIdx.x == 0) {
     mbar_wait(smem_u32(&bar), 0);
+    done = 1;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+// 8 MMAs per stage, commit per stage to sbar[k % 4], wait for stage k - DEPTH + 1 before issuing
+// stage k + 1: the ring turnaround without TMA (MMA completion -> mbarrier -> waiting thread)
+__device__ __forceinline__ void mbar_wait_test(uint32_t a, uint32_t ph) {
+  asm volatile("{\n.reg .pred P1;\nWT_%=:\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra WT_%=;\n}\n" ::"r"(a), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_hint(uint32_t a, uint32_t ph) {
+  asm volatile("{\n.reg .pred P1;\nWH_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n@!P1 bra WH_%=;\n}\n" ::"r"(a), "r"(ph) : "memory");
+}
+template <int DEPTH, int WAITMODE = 0>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) ringbench(int stages, long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t bar[8];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = threadIdx.x; i < (4 * 16384 + 4 * 8192) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0x38383838u;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[k])), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base, idesc = idesc_f16(256, 128);
+  const uint32_t sa = smem_u32(base), sb = sa + 4 * 16384;
+  if (rank == 0 && threadIdx.x == 0) {
+    const long long t0 = clock64();
+    for (int k = 0; k < stages; ++k) {
+      if (k >= DEPTH) {
+        if (WAITMODE == 0) mbar_wait(smem_u32(&bar[(k - DEPTH) & 7]), ((k - DEPTH) >> 3) & 1);
+        else if (WAITMODE == 1) mbar_wait_hint(smem_u32(&bar[(k - DEPTH) & 7]), ((k - DEPTH) >> 3) & 1);
+        else if (WAITMODE == 2) mbar_wait_test(smem_u32(&bar[(k - DEPTH) & 7]), ((k - DEPTH) >> 3) & 1);
+        else if ((k & 3) == 0) mbar_wait(smem_u32(&bar[(k - DEPTH) & 7]), ((k - DEPTH) >> 3) & 1);  // every 4th stage
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint32_t acc = (k | m) ? 1u : 0u;
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                     "l"(sw128_desc(sa + (m >> 2) * 16384 + (m & 3) * 32)), "l"(sw128_desc(sb + (m >> 2) * 8192 + (m & 3) * 32)), "r"(idesc),
+                     "r"(acc) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                       smem_u32(&bar[k & 7])), "h"(uint16_t(3)) : "memory");
+    }
+    for (int k = (stages > DEPTH ? stages - DEPTH : 0); k < stages; ++k) mbar_wait(smem_u32(&bar[k & 7]), (k >> 3) & 1);
+    out[0] = clock64() - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -124,6 +201,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) bench(int it
 }
 
 int main() {
+  {
+    long long* dd;
+    cudaMalloc(&dd, 16);
+    const int sm = 4 * 16384 + 4 * 8192 + 1024;
+    cudaFuncSetAttribute(ringbench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(ringbench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(ringbench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(ringbench<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(ringbench<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    for (int rep = 0; rep < 2; ++rep) { ringbench<4, 1><<<128, 128, sm>>>(512, dd); cudaDeviceSynchronize(); }
+    {
+      long long h;
+      cudaMemcpy(&h, dd, 8, cudaMemcpyDeviceToHost);
+      printf("commit/wait ring depth 4, try_wait with suspend-time hint: %.1f cycles per stage\n", h / 512.0);
+    }
+    cudaFuncSetAttribute(ringbench<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(ringbench<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    for (int wm : {2, 3}) {
+      for (int rep = 0; rep < 2; ++rep) {
+        if (wm == 2) ringbench<4, 2><<<128, 128, sm>>>(512, dd);
+        else ringbench<4, 3><<<128, 128, sm>>>(512, dd);
+        cudaDeviceSynchronize();
+      }
+      long long h;
+      cudaMemcpy(&h, dd, 8, cudaMemcpyDeviceToHost);
+      printf("commit/wait ring depth 4, %s: %.1f cycles per stage\n", wm == 2 ? "test_wait loop" : "wait every 4th stage", h / 512.0);
+    }
+    for (int rep = 0; rep < 2; ++rep) { ringbench<8><<<128, 128, sm>>>(512, dd); cudaDeviceSynchronize(); }
+    {
+      long long h;
+      cudaMemcpy(&h, dd, 8, cudaMemcpyDeviceToHost);
+      printf("commit/wait ring depth 8: %.1f cycles per stage\n", h / 512.0);
+    }
+    for (int depth : {1, 2, 4}) {
+      for (int rep = 0; rep < 2; ++rep) {
+        if (depth == 1) ringbench<1><<<128, 128, sm>>>(512, dd);
+        else if (depth == 2) ringbench<2><<<128, 128, sm>>>(512, dd);
+        else ringbench<4><<<128, 128, sm>>>(512, dd);
+        cudaDeviceSynchronize();
+      }
+      long long h;
+      cudaMemcpy(&h, dd, 8, cudaMemcpyDeviceToHost);
+      printf("commit/wait ring depth %d (8 MMAs per stage): %.1f cycles per stage\n", depth, h / 512.0);
+    }
+  }
   long long* d;
   cudaMalloc(&d, 16);
   char* g;
@@ -136,6 +258,18 @@ int main() {
   cudaFuncSetAttribute(bench<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(bench<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(bench<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<8, 1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<8, 1, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int sp : {1, 4}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (sp == 1) bench<8, 1, false, 1><<<128, 256, smem>>>(256, 0, g, d, 0);
+      else bench<8, 1, false, 4><<<128, 256, smem>>>(256, 0, g, d, 0);
+      cudaDeviceSynchronize();
+    }
+    long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("%d warp(s) spinning on mbarrier.try_wait: %.1f cycles per MMA\n", sp, h / (256 * 16.0));
+  }
   for (int rep = 0; rep < 2; ++rep) {
     bench<8, 1, true><<<128, 256, smem>>>(256, 0, g, d, 0);
     cudaDeviceSynchronize();
