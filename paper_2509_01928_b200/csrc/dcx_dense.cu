@@ -143,7 +143,7 @@ struct Args {
   // Q (|q| <= 16, exact), kind::f8f6f4; the sign GEMM is e4m3 too (dS in {0, +-2}, f32 D2)
   int f8;
   float* dsc;      // f8: 2^-e of the replica's last written delta (resume), [Rpad]
-  int exp;         // timing experiments only (DCX_DENSE_EXP, wrong results): 1 skip A loads,
+  int exp;         // timing experiments only (DCX_DENSE_EXP in a -DDCX_DENSE_EXPERIMENTS build, wrong results): 1 skip A loads,
                    // 2 skip B loads, 4 skip GEMM2 (the sign GEMM); 8: spin (no sleep) on GEMM1 done;
                    // 32: wait for every tile's flag before the first GEMM1 stage (exact results)
 };
@@ -1842,7 +1842,9 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
   a.flags = reinterpret_cast<unsigned int*>(a.sync + d.Rpad / 128);
   a.dbg = reinterpret_cast<unsigned long long*>(d.dbg);
   a.exp = 0;
+#ifdef DCX_DENSE_EXPERIMENTS  // timing-only feed experiments (wrong results): never in a default build
   if (const char* e = std::getenv("DCX_DENSE_EXP")) a.exp = std::atoi(e);
+#endif
   a.cfg = m.args.cfg;
   a.n = int(d.n);
   a.npad = int(d.npad);
