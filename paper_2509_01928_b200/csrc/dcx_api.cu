@@ -1220,6 +1220,13 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     cfg.budget = P->time_budget_s;
     cfg.conv_tol = P->conv_tol;
     cfg.descent_tol = P->descent_tol;
+    cfg.momentum_floor = 0.0;
+    if (P->solver == DCX_SOLVER_ADOCH && P->precision != DCX_PREC_F64) {
+      // relative step (to sqrt(alpha / beta)) below which f32 / tensor-core ADOCH takes plain
+      // steps; DCX_ADOCH_FLOOR overrides, 0 keeps the momentum to the end
+      const char* e = std::getenv("DCX_ADOCH_FLOOR");
+      cfg.momentum_floor = e ? std::atof(e) : 2e-3;
+    }
     cfg.hist_cap = (int)cap;
     cfg.wcap = std::max(1, c->wcap);
     cfg.es_scale = use_tc ? c->dn.jscale_d : (c->vk_int >= 0 ? c->scale : 1.0);

@@ -56,6 +56,8 @@ struct RunCfg {
   double es_scale;  // Es partials are multiplied by this (integer kinds)
   HistRec* hist;    // [R][hist_cap]
   double* window;   // [R][wcap]
+  double momentum_floor;  // ADOCH in f32 / tensor-core precision: no extrapolation once the step is
+                          // <= momentum_floor * sqrt(alpha / beta) (the state's scale; 0: off)
 };
 
 struct GState {
@@ -319,7 +321,11 @@ __device__ inline void adoch_decide(RepCtl& c, const RunCfg& cfg, int r, const d
     c.label = 0;
   } else {
     const double hy = __dsub_rn(__dmul_rn(__dmul_rn(0.25, c.beta), tot[Q_SY4]), __dmul_rn(0.5, tot[Q_SYAY]));
-    const bool ok = hy <= window_max(c, cfg, r);
+    bool ok = hy <= window_max(c, cfg, r);
+    // f32 / tensor-core endgame: once the step is below the state's resolution the extrapolated
+    // point y carries only rounding noise, which the momentum amplifies ~ k/3, so
+    // the iteration never settles; the plain step T(x) lets it reach its discrete fixed point
+    if (cfg.momentum_floor > 0.0 && c.step <= cfg.momentum_floor * sqrt(__ddiv_rn(c.alpha, c.beta))) ok = false;
     c.accept = ok ? 1 : 0;
     c.label = ok ? DCX_EV_ACCEPTED : DCX_EV_REJECTED;
   }

@@ -179,7 +179,7 @@ def test_tc_padding_ragged_sizes():
     np.testing.assert_array_equal(dc.energies(J, np.stack([r.spins for r in full])), [r.energy for r in full])
 
 
-def k2_quality_gate(res, gk2, solver, stops=True):
+def k2_quality_gate(res, gk2, solver, stops=True, iter_rel=None):
     """SURVEY.md §8c G-quality on BASELINE configs[1], against the unmodified reference on
     the SAME 1024 seeds (tests/golden/golden_k2.npz):
       * stop reasons: the reference converges (step <= 1e-10, doch.py:220) on 1022 / 1024
@@ -205,8 +205,11 @@ def k2_quality_gate(res, gk2, solver, stops=True):
     assert len(res) == R
     if stops:
         assert conv.sum() >= (ref_st == 0).sum() - 0.02 * R, (conv.sum(), (ref_st == 0).sum())
-        se_it = np.sqrt(it.var(ddof=1) / R + ref_it.var(ddof=1) / R)
-        assert abs(it.mean() - ref_it.mean()) <= 4 * se_it, (it.mean(), ref_it.mean(), se_it)
+        if iter_rel is None:
+            se_it = np.sqrt(it.var(ddof=1) / R + ref_it.var(ddof=1) / R)
+            assert abs(it.mean() - ref_it.mean()) <= 4 * se_it, (it.mean(), ref_it.mean(), se_it)
+        else:
+            assert abs(it.mean() - ref_it.mean()) <= iter_rel * ref_it.mean(), (it.mean(), ref_it.mean())
     assert mannwhitneyu(e, ref_e, alternative="greater").pvalue >= 1e-3
     assert e.mean() <= ref_e.mean() + 3 * ref_e.std(ddof=1) / np.sqrt(R), (e.mean(), ref_e.mean())
     assert e.min() <= np.sort(ref_e)[2], (e.min(), np.sort(ref_e)[:3])
@@ -347,21 +350,22 @@ def test_tc_resumed_launches_equal_one_launch(gold, solver):
 
 def test_tc_adoch_k2000_quality_vs_reference_1024_seeds(gk2):
     """BASELINE configs[1] with ADOCH (economy window, q = 5): the reference's energy
-    distribution on the same 1024 seeds; energies exact for the returned spins; the accept
-    log has one entry per iteration.
+    distribution on the same 1024 seeds and its stop reasons (converged as often, mean
+    iterations within 15 %); energies exact for the returned spins; the accept log has one
+    entry per iteration.
 
-    Stop reasons are NOT the reference's at this precision: ADOCH's Nesterov momentum
-    amplifies the state's rounding noise by about 1 / (1 - c_k) ~ k / 3, so the absolute
-    1e-10 step test needs an f64 state and product (numpy emulations of the exact update
-    rule on seeds 0-4: f64 state + f64 product + f64 evaluation converge in 150-362
-    iterations; f32 state or f32 product never converge, with or without f16 operands).
-    The tensor-core run goes to max_iters; the f64 path keeps the reference's stop
-    reasons (test_k2000_f64_matches_reference_seeds below)."""
+    ADOCH's Nesterov momentum amplifies the state's rounding noise by about 1 / (1 - c_k) ~
+    k / 3 (numpy emulations of the exact update rule on seeds 0-4 converge only with an f64
+    state, product and evaluation), so at f32 / tensor-core precision the extrapolation is
+    dropped once the step falls below 2e-3 sqrt(alpha / beta) (RunCfg::momentum_floor) and
+    the plain steps settle on the discrete fixed point. Without it (DCX_ADOCH_FLOOR=0) the
+    run goes to max_iters; the f64 path keeps the reference's per-seed stop reasons
+    (test_k2000_f64_matches_reference_seeds below)."""
     inst = k2_instance()
     X0 = x0s(2000, gk2["alpha"], gk2["beta"], range(1024))
     res = dc.solve_replicas(inst, "adoch", gk2["alpha"], gk2["beta"], X0, max_iters=1000, precision="f16tc")
     assert res[0].path == "dense_tc"
-    k2_quality_gate(res, gk2, "adoch", stops=False)
+    k2_quality_gate(res, gk2, "adoch", stops=True, iter_rel=0.15)
     for r in res[:16]:
         assert dc.energy(inst.coupling, r.spins) == r.energy
         assert r.accepted[0] is True and len(r.accepted) == r.iterations  # as assemble_results builds it for every path
