@@ -426,6 +426,14 @@ __device__ __forceinline__ void tmem_ld4x16_wait(uint32_t a0, uint32_t a1, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3)
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld32_wait(uint32_t a0, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(a0)
+      : "memory");
+}
 // W = 32 or 24 consecutive TMEM columns of this warp's lane quadrant
 template <int W>
 __device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t* v) {
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
   using P = Pipe<NC, TN>;
   constexpr int HW = TN / 2;   // spin columns of one epilogue warp (its half of the tile)
   constexpr int W1 = HW - 32;  // width of its second chunk (32 or 24)
-  static_assert(W1 == 32 || W1 == 24, "tile widths 128 or 112");
+  static_assert(W1 == 32 || W1 == 24 || W1 == 0, "tile widths 128, 112 or 64");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment (SW128) by offset so the compiler keeps the shared address space
   unsigned char* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -593,9 +601,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = valid ? src[j] : 0u;
     tmem_st32(taddr, v);
+    if constexpr (W1 > 0) {
 #pragma unroll
-    for (int j = 0; j < W1; ++j) v[j] = valid ? src[32 + j] : 0u;
-    tmem_stw<W1>(taddr + 32, v);
+      for (int j = 0; j < W1; ++j) v[j] = valid ? src[32 + j] : 0u;
+      tmem_stw<W1>(taddr + 32, v);
+    }
   };
   if (epi) {
     const int64_t o = (int64_t)r * a.npad + i0 + h * HW;
@@ -1335,7 +1345,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
       {
         uint32_t v2[64];
         if constexpr (W1 == 32) tmem_ld64_wait(d2addr, d2addr + 32, v2);
-        else tmem_ld56_wait(d2addr, d2addr + 32, d2addr + 48, v2);
+        else if constexpr (W1 == 24) tmem_ld56_wait(d2addr, d2addr + 32, d2addr + 48, v2);
+        else tmem_ld32_wait(d2addr, v2);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sm.d2free));  // D2 drained: GEMM2(p+1) may overwrite it
@@ -1401,7 +1412,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     const int lim = max(0, min(HW, a.n - (i0 + h * HW)));
     uint32_t v[64];
     if constexpr (W1 == 32) tmem_ld64_wait(xaddr, xaddr + 32, v);
-    else tmem_ld56_wait(xaddr, xaddr + 32, xaddr + 48, v);
+    else if constexpr (W1 == 24) tmem_ld56_wait(xaddr, xaddr + 32, xaddr + 48, v);
+    else tmem_ld32_wait(xaddr, v);
     if (valid)  // s, for a later launch of this solve
 #pragma unroll
       for (int j = 0; j < HW; j += 4)
@@ -1423,7 +1435,8 @@ __global__ void __launch_bounds__(THREADS, 1) dense_doch_kernel(const __grid_con
     auto save_cols = [&](uint32_t taddr, uint32_t* dst) {
       uint32_t w[64];
       if constexpr (W1 == 32) tmem_ld64_wait(taddr, taddr + 32, w);
-      else tmem_ld56_wait(taddr, taddr + 32, taddr + 48, w);
+      else if constexpr (W1 == 24) tmem_ld56_wait(taddr, taddr + 32, taddr + 48, w);
+      else tmem_ld32_wait(taddr, w);
       if (valid)
 #pragma unroll
         for (int j = 0; j < HW; j += 4) *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
@@ -1692,7 +1705,8 @@ void dense_upload_int8(DenseDev& d, int64_t n, const int8_t* q_pinned, double sc
 
 static size_t dense_smem_bytes(int nc, int tn) {
   const size_t tiles = nc == 1 ? (tn == 112 ? tc::Pipe<1, 112>::TILES : tc::Pipe<1, 128>::TILES)
-                               : (tn == 112 ? tc::Pipe<2, 112>::TILES : tc::Pipe<2, 128>::TILES);
+                               : (tn == 112 ? tc::Pipe<2, 112>::TILES
+                                            : (tn == 64 ? tc::Pipe<2, 64>::TILES : tc::Pipe<2, 128>::TILES));
   return 1024 + tiles + sizeof(tc::Smem);
 }
 
@@ -1719,14 +1733,20 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   // spin tile width: 128, or 112 with DCX_DENSE_TN=112 (18 x 8 = 144 CTAs for K2000 x 1024
   // instead of 16 x 8 = 128). Measured: 18.14 vs 18.05 ms per solve -- an N = 112 MMA
   // issues no faster than an N = 128 one, so the extra SMs do not shorten the GEMMs
-  const int t112 = int((d.n + 111) / 112), t128 = int(d.npad / 128);
-  d.tn = 128;
+  const int t112 = int((d.n + 111) / 112), t128 = int(d.npad / 128), t64 = int(d.npad / 64);
+  // 64-wide tiles when the CTA pairs of every replica group fit the SMs (R <= 512 at K2000):
+  // half the update per CTA, 14.6 vs 16.8 us per iteration at R = 256 and 512
+  d.tn = (!d.ad && Rpad_new % 256 == 0 && t64 <= 32 && (Rpad_new / 128) * t64 <= nsm) ? 64 : 128;
   if (const char* e = std::getenv("DCX_DENSE_TN")) {
     const int want = std::atoi(e);
-    if (want == 128 || (want == 112 && t112 * 112 <= d.npad && t112 <= 32)) d.tn = want;
+    if (want == 128 || (want == 112 && t112 * 112 <= d.npad && t112 <= 32) ||
+        (want == 64 && t64 <= 32 && Rpad_new % 256 == 0 && (Rpad_new / 128) * t64 <= nsm))
+      d.tn = want;
+    else
+      d.tn = 128;
   }
   if (d.ad) d.tn = 128;  // the ADOCH kernel is built for 128-wide tiles
-  d.tiles_n = d.tn == 112 ? t112 : t128;
+  d.tiles_n = d.tn == 112 ? t112 : (d.tn == 64 ? t64 : t128);
   const int tiles = (d.Rpad / 128) * d.tiles_n;
   if (tiles > nsm || tiles > tc::MAX_FLAGS || d.tiles_n > 32)
     throw std::invalid_argument("tensor-core path: (R/128)*(n/128) tiles must fit the SM count (" +
@@ -1734,6 +1754,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   // CTA pairs (cta_group::2) when the replica count allows 256-replica groups
   d.nc = (d.Rpad % 256 == 0) ? 2 : 1;
   if (const char* e = std::getenv("DCX_DENSE_NC")) d.nc = std::atoi(e) == 2 && d.Rpad % 256 == 0 ? 2 : 1;
+  if (d.tn == 64) d.nc = 2;  // 64-wide tiles are built for CTA pairs only
   const size_t vec = size_t(d.Rpad) * d.npad;
   for (int b = 0; b < 2; ++b) {
     if (!reuse) {
@@ -1764,7 +1785,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
   // aligned stores); DCX_DENSE_F8=0 keeps f16 deltas and the int8 sign GEMM
   {
     const char* e = std::getenv("DCX_DENSE_F8");
-    d.f8 = d.f8ok && d.tn == 128 && !(e && std::atoi(e) == 0);
+    d.f8 = d.f8ok && (d.tn == 128 || d.tn == 64) && !(e && std::atoi(e) == 0);
   }
   if (!d.dsc) DCK(cudaMalloc(&d.dsc, sizeof(float) * d.Rpad));
   {
@@ -1807,6 +1828,7 @@ void dense_begin(DenseDev& d, MultiPass& m, cudaStream_t s) {
     else dense_set_smem<1, 128, false>();
   } else {
     if (d.tn == 112) dense_set_smem<2, 112, false>();
+    else if (d.tn == 64) dense_set_smem<2, 64, false>();
     else dense_set_smem<2, 128, false>();
   }
 }
@@ -1888,6 +1910,7 @@ static void launch_dense(DenseDev& d, MultiPass& m, int p_end, cudaStream_t s) {
     cfg.numAttrs = (coop && std::atoi(coop) == 0) ? 1 : 2;
     if (d.ad) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 128, true>, a));
     else if (d.tn == 112) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 112, false>, a));
+    else if (d.tn == 64) DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 64, false>, a));
     else DCK(cudaLaunchKernelEx(&cfg, tc::dense_doch_kernel<2, 128, false>, a));
   }
 }

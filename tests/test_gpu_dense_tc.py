@@ -265,6 +265,33 @@ def test_tc_operand_multicast_and_pair_variants_agree(gold):
             assert np.array_equal(a.x, b.x)
 
 
+@pytest.mark.parametrize("tn", ["64", "128"])
+def test_tc_spin_tile_widths_agree(gold, tn):
+    """64-wide spin tiles (the default when every replica group's CTA pairs fit the SMs, R <= 512
+    at K2000) and 128-wide ones: the first iterate matches the e4m3 emulation, returned spins
+    carry their exact energies, states stay finite, and a run resumed across launches equals
+    one launch."""
+    g = gold["k2"]
+    inst = k2_instance()
+    a, b = g["alpha"], g["beta"]
+    X0 = x0s(2000, a, b, range(256))
+    J = -0.5 * k2_W()
+    one = _run_with_env({"DCX_DENSE_TN": tn},
+                        lambda: dc.solve_replicas(inst, "doch", a, b, X0, max_iters=1, precision="f16tc"))
+    for x0, r in zip(X0[:16], one[:16]):
+        emu = doch_first_iterate_emulation(J, x0, a, b)
+        assert np.mean(np.isclose(r.x, emu, rtol=1e-5, atol=0)) >= 0.99
+    full = _run_with_env({"DCX_DENSE_TN": tn},
+                         lambda: dc.solve_replicas(inst, "doch", a, b, X0, max_iters=200, precision="f16tc"))
+    E = dc.energies(inst.coupling, np.stack([r.spins for r in full]))
+    np.testing.assert_array_equal(E, [r.energy for r in full])
+    assert all(np.all(np.isfinite(r.x)) for r in full)
+    chunked = _run_with_env({"DCX_DENSE_TN": tn}, lambda: dc.solve_replicas(
+        inst, "doch", a, b, X0, max_iters=200, precision="f16tc", chunk=37))
+    for p_, q_ in zip(full, chunked):
+        assert p_.iterations == q_.iterations and p_.energy == q_.energy and np.array_equal(p_.x, q_.x)
+
+
 def test_tc_112_wide_spin_tiles(gold):
     """DCX_DENSE_TN=112 (18 spin tiles of 112 for n = 2000, stages straddling two tiles'
     operand flags): the first iterate matches the f16-operand emulation and returned
