@@ -1257,7 +1257,15 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
         }, 16);
         pc.mark("x0 to f32");
         CK(cudaMemcpyAsync(src.p, x32, bytes, cudaMemcpyHostToDevice, c->stream));
+        if (timing_on()) {
+          CK(cudaStreamSynchronize(c->stream));
+          pc.mark("x0 H2D");
+        }
         to_device_layout_s<float, float><<<grid_for(tot), 256, 0, c->stream>>>(src.as<float>(), static_cast<float*>(a.x[0]), n, R);
+        if (timing_on()) {
+          CK(cudaStreamSynchronize(c->stream));
+          pc.mark("x0 layout");
+        }
       }
       CK(cudaMemsetAsync(a.x[1], 0, tot * tb, c->stream));
       if (ad) {
