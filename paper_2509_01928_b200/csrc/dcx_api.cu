@@ -1,7 +1,10 @@
 // libdcx C ABI (include/dcx.h): context, coupling upload, operator seam and
 // the chunked solve driver. No exception crosses the ABI.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -13,6 +16,9 @@
 #include <string>
 #include <thread>
 #include <vector>
+
+#include <emmintrin.h>
+#include <pthread.h>
 
 #include "dcx_internal.h"
 #include "dcx_dense.h"
@@ -71,7 +77,28 @@ struct InvalidArg : std::runtime_error {
 struct PinnedRing {
   HistRec* p = nullptr;
   size_t n = 0;
+  // the last run's history copy is left in flight (the host returns to the caller while
+  // it lands); readers wait on `ready` first
+  cudaEvent_t ready = nullptr;
+  bool pending = false;
+  void mark_pending(cudaStream_t s) {
+    if (!ready && cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess) {
+      ready = nullptr;
+      cudaStreamSynchronize(s);
+      return;
+    }
+    cudaEventRecord(ready, s);
+    pending = true;
+  }
+  void wait() {
+    if (pending) cudaEventSynchronize(ready);
+    pending = false;
+  }
   ~PinnedRing() {
+    if (ready) {
+      cudaEventSynchronize(ready);
+      cudaEventDestroy(ready);
+    }
     if (p) cudaFreeHost(p);
   }
 };
@@ -139,6 +166,14 @@ struct dcx_ctx {
   SmallPlan sp;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // the final history copy of a run goes out on its own stream (copy_hist defer): syncs of
+  // `stream` (result gathers, the next upload) do not wait for it; the next run's first
+  // write of `hist` waits for hist_copied
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t hist_go = nullptr, hist_copied = nullptr;
+  bool hist_inflight = false;
+  double* wdelta = nullptr;  // mapped pinned [R]: descent-warning deltas written by a kernel
+  size_t wdelta_n = 0;       // (no copy queued behind the in-flight history copy)
   double dev_seconds = 0.0;
   bool dist = false;              // dcx_dist_begin run: external iterate buffers, caller's collectives
   double *qs = nullptr, *qm = nullptr;
@@ -164,6 +199,11 @@ struct dcx_ctx {
     if (graph) cudaGraphExecDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (hstream) cudaStreamSynchronize(hstream);
+    if (wdelta) cudaFreeHost(wdelta);
+    if (hist_go) cudaEventDestroy(hist_go);
+    if (hist_copied) cudaEventDestroy(hist_copied);
+    if (hstream) cudaStreamDestroy(hstream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -208,23 +248,189 @@ int lanes_for_degree(double d) {
 }
 
 // Detect the narrowest exact storage of the coupling values.
-// Host passes over the uploaded arrays (10^8 entries at R8) run on all host threads:
-// f(lo, hi, t) over contiguous chunks [lo, hi) of [0, n), chunk t of T.
+// Host passes over the uploaded arrays (10^8 entries at R8) run on all host threads.
+// Host worker pool for par_for: spawning 16 threads per call cost 0.2-0.3 ms, paid
+// several times per solve (classify J, convert x0, CSR staging). Workers spin for a few
+// milliseconds after a job (the calls come in bursts) and then block.
+struct HostPool {
+  std::mutex run_mu;  // one parallel loop at a time
+  std::mutex mu;
+  std::condition_variable cv, cv_done;
+  std::atomic<uint64_t> gen{0};
+  std::atomic<int> pending{0};
+  const std::function<void(int)>* job = nullptr;
+  int T = 0;
+  std::vector<std::thread> th;
+  explicit HostPool(int n) {
+    for (int i = 1; i < n; ++i) th.emplace_back([this, i] { loop(i); });
+  }
+  int size() const { return int(th.size()) + 1; }
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      // spin up to 3 ms: waking a blocked worker on these hosts (KVM guests) cost ~0.4 ms
+      // per parallel loop, more than the loops themselves
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(3))
+        for (int s = 0; s < 64; ++s) _mm_pause();
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return gen.load(std::memory_order_acquire) != seen; });
+        seen = gen.load(std::memory_order_acquire);
+      }
+      if (id < T) (*job)(id);
+      if (pending.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+        std::lock_guard<std::mutex> lk(mu);
+        cv_done.notify_one();
+      }
+    }
+  }
+  void run(int t, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> g(run_mu);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      job = &f;
+      T = t;
+      pending.store(int(th.size()), std::memory_order_release);
+      gen.fetch_add(1, std::memory_order_acq_rel);
+    }
+    cv.notify_all();
+    f(0);
+    const auto t0 = std::chrono::steady_clock::now();  // the workers' share ends within microseconds
+    while (pending.load(std::memory_order_acquire) != 0 &&
+           std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(1))
+      _mm_pause();
+    std::unique_lock<std::mutex> lk(mu);
+    cv_done.wait(lk, [&] { return pending.load(std::memory_order_acquire) == 0; });
+  }
+};
+
+HostPool* g_pool = nullptr;
+std::mutex g_pool_mu;
+
+HostPool& host_pool() {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool) {
+    // a forked child has none of the parent's workers: it builds its own pool
+    static bool hooked = [] { return pthread_atfork(nullptr, nullptr, [] { g_pool = nullptr; }) == 0; }();
+    (void)hooked;
+    unsigned hw = std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
+    if (const char* e = std::getenv("DCX_HOST_THREADS"))
+      hw = unsigned(std::max(1, std::min(32, std::atoi(e))));
+    else if (const char* l = std::getenv("LOCAL_WORLD_SIZE"))  // torchrun: ranks on this node share the cores
+      hw = std::max(1u, hw / unsigned(std::max(1, std::atoi(l))));
+    g_pool = new HostPool(int(hw));  // never freed: workers live as long as the process
+  }
+  return *g_pool;
+}
+
+// f(lo, hi, t) over contiguous chunks [lo, hi) of [0, n), chunk t of T; chunk starts are
+// multiples of 64 elements so streaming stores (stream_fill) cover whole cache lines
 template <class F>
 static void par_for(int64_t n, F&& f, int max_threads = 32) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const int T = n < (int64_t(1) << 20) ? 1 : int(std::min<unsigned>(std::min<unsigned>(hw, 32u), unsigned(max_threads)));
-  if (T == 1) {
+  if (n < (int64_t(1) << 16)) {
     f(int64_t(0), n, 0);
     return;
   }
-  std::vector<std::thread> th;
-  const int64_t chunk = (n + T - 1) / T;
-  for (int t = 0; t < T; ++t) {
+  HostPool& pool = host_pool();
+  const int T = std::max(1, std::min(pool.size(), max_threads));
+  const int64_t chunk = ((n + T - 1) / T + 63) / 64 * 64;
+  const std::function<void(int)> body = [&](int t) {
     const int64_t lo = std::min(n, t * chunk), hi = std::min(n, lo + chunk);
-    th.emplace_back([&f, lo, hi, t] { f(lo, hi, t); });
+    if (lo < hi) f(lo, hi, t);
+  };
+  pool.run(T, body);
+}
+
+// dst[k] = f(k) for k in [lo, hi) with streaming (non-temporal) stores: the pinned staging
+// a DMA reads next must not sit dirty in 16 cores' private caches. Measured on the B200
+// hosts (KVM guests): 8 MB written by 16 threads then copied H2D at 6.6 GB/s with plain
+// stores, 51 GB/s with streaming stores.
+template <class T, class F>
+static inline void stream_fill(T* dst, int64_t lo, int64_t hi, F&& f) {
+  static_assert(16 % sizeof(T) == 0, "element size must divide 16");
+  constexpr int V = int(16 / sizeof(T));
+  int64_t k = lo;
+  for (; k < hi && (reinterpret_cast<uintptr_t>(dst + k) & 15); ++k) dst[k] = f(k);
+  for (; k + V <= hi; k += V) {
+    alignas(16) T tmp[V];
+    for (int j = 0; j < V; ++j) tmp[j] = f(k + j);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k), _mm_load_si128(reinterpret_cast<const __m128i*>(tmp)));
   }
-  for (auto& x : th) x.join();
+  for (; k < hi; ++k) dst[k] = f(k);
+  _mm_sfence();
+}
+// Round to nearest even without a libm call (std::nearbyint is one on the x86-64 baseline,
+// a call per entry): exact for |x| < 2^51; larger or non-finite x fail every caller's
+// |q| <= 127 / 32767 or q * scale == v check, as with nearbyint.
+static inline double rne(double x) {
+  const double m = 6755399441055744.0;  // 1.5 * 2^52
+  return (x + m) - m;
+}
+
+// dst[k] = int32(ci[k]) for k in [lo, hi), streamed; true if some index is outside [0, n_cols)
+// (SSE2: low and high 32-bit halves of four indices per step, n_cols < 2^31)
+static bool stage_columns(const int64_t* ci, int32_t* dst, int64_t lo, int64_t hi, int64_t n_cols) {
+  bool bad = false;
+  int64_t k = lo;
+  for (; k < hi && (reinterpret_cast<uintptr_t>(dst + k) & 15); ++k) {
+    bad |= uint64_t(ci[k]) >= uint64_t(n_cols);
+    dst[k] = int32_t(ci[k]);
+  }
+  const __m128i zero = _mm_setzero_si128(), last = _mm_set1_epi32(int32_t(n_cols - 1));
+  __m128i acc = zero;
+  for (; k + 4 <= hi; k += 4) {
+    const __m128 a = _mm_castsi128_ps(_mm_loadu_si128(reinterpret_cast<const __m128i*>(ci + k)));
+    const __m128 b = _mm_castsi128_ps(_mm_loadu_si128(reinterpret_cast<const __m128i*>(ci + k + 2)));
+    const __m128i l = _mm_castps_si128(_mm_shuffle_ps(a, b, _MM_SHUFFLE(2, 0, 2, 0)));
+    const __m128i h = _mm_castps_si128(_mm_shuffle_ps(a, b, _MM_SHUFFLE(3, 1, 3, 1)));
+    acc = _mm_or_si128(acc, _mm_or_si128(h, _mm_or_si128(_mm_cmplt_epi32(l, zero), _mm_cmpgt_epi32(l, last))));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k), l);
+  }
+  bad |= _mm_movemask_epi8(_mm_cmpeq_epi8(acc, zero)) != 0xFFFF;
+  for (; k < hi; ++k) {
+    bad |= uint64_t(ci[k]) >= uint64_t(n_cols);
+    dst[k] = int32_t(ci[k]);
+  }
+  _mm_sfence();
+  return bad;
+}
+
+// one pass over v[lo, hi): all finite, all equal to v0, min |nonzero| (SSE2, four
+// independent accumulators: a scalar min chain ran at a third of the memory rate)
+static void value_stats(const double* v, int64_t lo, int64_t hi, double v0, bool& fin, bool& uni, double& mn) {
+  const double inf = std::numeric_limits<double>::infinity();
+  const __m128d absm = _mm_castsi128_pd(_mm_set1_epi64x(0x7fffffffffffffffLL));
+  const __m128d big = _mm_set1_pd(std::numeric_limits<double>::max()), vinf = _mm_set1_pd(inf);
+  const __m128d z = _mm_setzero_pd(), w0 = _mm_set1_pd(v0);
+  __m128d m[4] = {vinf, vinf, vinf, vinf};
+  __m128d ok = _mm_cmpeq_pd(z, z), eq = ok;
+  int64_t k = lo;
+  for (; k + 8 <= hi; k += 8) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __m128d x = _mm_loadu_pd(v + k + 2 * j), a = _mm_and_pd(x, absm);
+      ok = _mm_and_pd(ok, _mm_cmple_pd(a, big));
+      eq = _mm_and_pd(eq, _mm_cmpeq_pd(x, w0));
+      const __m128d isz = _mm_cmpeq_pd(a, z);
+      m[j] = _mm_min_pd(m[j], _mm_or_pd(_mm_and_pd(isz, vinf), _mm_andnot_pd(isz, a)));
+    }
+  }
+  const __m128d mm = _mm_min_pd(_mm_min_pd(m[0], m[1]), _mm_min_pd(m[2], m[3]));
+  alignas(16) double t[2];
+  _mm_store_pd(t, mm);
+  double mnv = std::min(t[0], t[1]);
+  bool f = _mm_movemask_pd(ok) == 3, u = _mm_movemask_pd(eq) == 3;
+  for (; k < hi; ++k) {
+    const double x = v[k], a = std::fabs(x);
+    f &= a <= std::numeric_limits<double>::max();
+    u &= x == v0;
+    mnv = std::min(mnv, a == 0.0 ? inf : a);
+  }
+  fin = f;
+  uni = u;
+  mn = mnv;
 }
 
 void classify_values(const double* v, int64_t nnz, int& vk, double& scale) {
@@ -234,11 +440,7 @@ void classify_values(const double* v, int64_t nnz, int& vk, double& scale) {
   par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
     bool u = true, f = true;
     double mn = std::numeric_limits<double>::infinity();
-    for (int64_t e = lo; e < hi; ++e) {
-      f &= bool(std::isfinite(v[e]));
-      u &= v[e] == v[0];
-      if (v[e] != 0.0) mn = std::min(mn, std::fabs(v[e]));
-    }
+    value_stats(v, lo, hi, v[0], f, u, mn);
     uni[t] = u;
     fin[t] = f;
     mns[t] = mn;
@@ -260,7 +462,7 @@ void classify_values(const double* v, int64_t nnz, int& vk, double& scale) {
       double am = 0.0;
       for (int64_t e = lo; e < hi && okt; ++e) {
         const double q = v[e] / s;
-        if (q != std::nearbyint(q) || s * std::nearbyint(q) != v[e]) okt = false;
+        if (q != rne(q) || s * rne(q) != v[e]) okt = false;
         am = std::max(am, std::fabs(q));
       }
       oks[t] = okt;
@@ -363,6 +565,15 @@ __global__ void gather_final_state(const T* x0, const T* x1, const RepCtl* ctl, 
     const int k = max(0, ctl[r].k);
     out[o] = double(((k & 1) ? x1 : x0)[i * R + r]);
   }
+}
+// h_k - h_(k-1) at each replica's first descent violation k, NaN if none (the records sit
+// in place: record k of replica r at r * cap + k)
+__global__ void gather_warn_delta(const HistRec* hist, const RepCtl* ctl, int64_t cap, int R, double* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int k = ctl[r].warned;
+  out[r] = (k >= 1 && k <= ctl[r].k) ? hist[r * cap + k].h - hist[r * cap + k - 1].h
+                                     : __longlong_as_double(0x7ff8000000000000LL);
 }
 __global__ void gather_best(const int8_t* best, int64_t n, int R, int8_t* out) {
   const int64_t total = n * R;
@@ -510,8 +721,11 @@ int dcx_create(int device, dcx_ctx** out) {
   int rc = guarded(c, [&] {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreateWithFlags(&c->hist_go, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->hist_copied, cudaEventDisableTiming));
     if (const char* g = std::getenv("DCX_L2_FETCH")) {  // experiment: L2 fetch granularity of random gathers
       CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(g))));
       size_t v = 0;
@@ -607,6 +821,7 @@ static void detect_torus(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, 
 static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int64_t* ci, const double* v,
                       int64_t n_cols, int64_t row_base) {
   return guarded(c, [&] {
+    PhaseClock pc("set_csr");
     c->chunks.release();
     if (n < 1) throw InvalidArg("n must be >= 1");
     if (n_cols >= (int64_t(1) << 31)) throw InvalidArg("n >= 2^31 is not supported");
@@ -616,7 +831,8 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     if (ro[0] != 0 || ro[n] != nnz) throw InvalidArg("row_offsets must start at 0 and end at nnz");
     // row offsets and columns are converted straight into pinned staging (no host vectors
     // to zero-fill, DMA at full PCIe rate); the staging is kept for re-uploads
-    const size_t stage = size_t(n + 1) * 4 + size_t(nnz) * 4;
+    const size_t qoff = (size_t(n + 1) * 4 + size_t(nnz) * 4 + 63) / 64 * 64;  // int8/int16 values
+    const size_t stage = qoff + size_t(nnz) * 2;
     if (c->pin_bytes < stage) {
       if (c->pin) cudaFreeHost(c->pin);
       c->pin = nullptr;
@@ -630,29 +846,45 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     std::vector<int64_t> maxlens(32, 0);
     par_for(n + 1, [&](int64_t lo, int64_t hi, int t) {
       int64_t ml = 0;
-      for (int64_t i = lo; i < hi; ++i) {
+      bool b = false;
+      stream_fill(rp32, lo, hi, [&](int64_t i) {
         if (i > 0) {
-          if (ro[i] < ro[i - 1]) bad[t] = 1;
+          b |= ro[i] < ro[i - 1];
           ml = std::max<int64_t>(ml, ro[i] - ro[i - 1]);
         }
-        rp32[i] = uint32_t(ro[i]);
-      }
+        return uint32_t(ro[i]);
+      });
+      bad[t] = b;
       maxlens[t] = ml;
     });
     for (int t = 0; t < 32; ++t)
       if (bad[t]) throw InvalidArg("row_offsets must be nondecreasing");
     const int64_t row_maxlen = *std::max_element(maxlens.begin(), maxlens.end());
-    par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
-      for (int64_t e = lo; e < hi; ++e) {
-        if (ci[e] < 0 || ci[e] >= n_cols) bad[t] = 1;
-        c32[e] = int32_t(ci[e]);
+    c->have = false;  // the device arrays are overwritten from here on
+    c->rp.alloc((n + 1) * 4);
+    CK(cudaMemcpyAsync(c->rp.p, rp32, (n + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+    // 16 zero entries of padding: the R = 1 entry-parallel pass reads whole 16-byte vectors
+    c->col.alloc((nnz + 16) * 4);
+    CK(cudaMemsetAsync(static_cast<char*>(c->col.p) + nnz * 4, 0, 64, c->stream));
+    pc.mark("offsets");
+    // columns in pieces: the DMA of piece i overlaps the conversion of piece i + 1 and the
+    // last pieces' DMA the value classification below
+    const int64_t piece = std::max<int64_t>(int64_t(1) << 22, (nnz / 8 + 63) / 64 * 64);
+    for (int64_t e0 = 0; e0 < nnz; e0 += piece) {
+      const int64_t m = std::min(piece, nnz - e0);
+      std::fill(bad.begin(), bad.end(), 0);
+      par_for(m, [&](int64_t lo, int64_t hi, int t) { bad[t] = stage_columns(ci + e0, c32 + e0, lo, hi, n_cols); });
+      if (std::any_of(bad.begin(), bad.end(), [](unsigned char b) { return b != 0; })) {
+        CK(cudaStreamSynchronize(c->stream));
+        throw InvalidArg("column index out of range");
       }
-    });
-    for (int t = 0; t < 32; ++t)
-      if (bad[t]) throw InvalidArg("column index out of range");
+      CK(cudaMemcpyAsync(c->col.as<int32_t>() + e0, c32 + e0, size_t(m) * 4, cudaMemcpyHostToDevice, c->stream));
+    }
+    pc.mark("columns (+H2D issue)");
     int vk;
     double scale;
     classify_values(v, nnz, vk, scale);
+    pc.mark("classify");
     if (vk == VK_I8 || vk == VK_UNIFORM) {
       // the UNIFORM / I8 kernels sum q * sign(x) per row in f32, exact while
       // every row's sum of |q| stays below 2^24; longer rows use the int32
@@ -660,18 +892,13 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
       const int64_t maxlen = row_maxlen;
       if (maxlen * (vk == VK_I8 ? 127 : 1) >= (int64_t(1) << 24) && scale != 0.0) vk = VK_I16;
     }
-    c->have = false;
     c->torus_L = 0;
     c->n = n;
     c->n_cols = n_cols;
     c->row_base = row_base;
     c->nnz = nnz;
-    c->rp.alloc((n + 1) * 4);
-    CK(cudaMemcpy(c->rp.p, rp32, (n + 1) * 4, cudaMemcpyHostToDevice));
-    // 16 zero entries of padding: the R = 1 entry-parallel pass reads whole 16-byte vectors
-    c->col.alloc((nnz + 16) * 4);
-    CK(cudaMemset(static_cast<char*>(c->col.p) + nnz * 4, 0, 64));
-    if (nnz) CK(cudaMemcpy(c->col.p, c32, nnz * 4, cudaMemcpyHostToDevice));
+    CK(cudaStreamSynchronize(c->stream));
+    pc.mark("offsets+columns H2D");
     c->col16.release();
     if (n_cols <= 65536 && n == n_cols && nnz) {
       std::vector<uint16_t> c16(nnz);
@@ -686,19 +913,17 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     c->scale = scale;
     if (vk == VK_I8 || vk == VK_I16) {
       const int b = vk == VK_I8 ? 1 : 2;
-      std::vector<int16_t> q16;
-      std::vector<int8_t> q8;
-      if (b == 1) q8.resize(nnz); else q16.resize(nnz);
+      int8_t* q8 = reinterpret_cast<int8_t*>(c->pin + qoff);  // pinned staging, streamed
+      int16_t* q16 = reinterpret_cast<int16_t*>(c->pin + qoff);
       par_for(nnz, [&](int64_t lo, int64_t hi, int) {
-        for (int64_t e = lo; e < hi; ++e) {
-          const int q = int(std::nearbyint(v[e] / scale));
-          if (b == 1) q8[e] = int8_t(q); else q16[e] = int16_t(q);
-        }
+        if (b == 1) stream_fill(q8, lo, hi, [&](int64_t e) { return int8_t(rne(v[e] / scale)); });
+        else stream_fill(q16, lo, hi, [&](int64_t e) { return int16_t(rne(v[e] / scale)); });
       });
       c->vint.alloc((nnz + 16) * b);
       CK(cudaMemset(static_cast<char*>(c->vint.p) + nnz * b, 0, 16 * b));
-      CK(cudaMemcpy(c->vint.p, b == 1 ? (void*)q8.data() : (void*)q16.data(), nnz * b, cudaMemcpyHostToDevice));
-      if (b == 1 && n == n_cols && row_base == 0) detect_torus(c, n, nnz, ro, c32, q8.data());
+      CK(cudaMemcpy(c->vint.p, c->pin + qoff, nnz * b, cudaMemcpyHostToDevice));
+      if (b == 1 && n == n_cols && row_base == 0) detect_torus(c, n, nnz, ro, c32, q8);
+    pc.mark("values q + H2D");
     } else if (vk != VK_UNIFORM) {
       c->v64.alloc(nnz * 8);
       CK(cudaMemcpy(c->v64.p, v, nnz * 8, cudaMemcpyHostToDevice));
@@ -716,13 +941,14 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
         std::vector<double> qm(32, 0.0);
         par_for(nnz, [&](int64_t lo, int64_t hi, int t) {
           double m = 0.0;
-          for (int64_t e = lo; e < hi; ++e) m = std::max(m, std::fabs(std::nearbyint(v[e] / scale)));
+          for (int64_t e = lo; e < hi; ++e) m = std::max(m, std::fabs(rne(v[e] / scale)));
           qm[t] = m;
         });
         qmax = std::max(qmax, *std::max_element(qm.begin(), qm.end()));
       }
       c->es_row_bound = double(maxlen) * qmax;
     }
+    pc.mark("qmax");
     if (n_cols <= 65536 && n == n_cols)
       for (int64_t s0 = 0; s0 < n; s0 += 32) {
         int64_t mx = 0;
@@ -808,13 +1034,16 @@ int dcx_set_dense(dcx_ctx* c, int64_t n, const double* A) {
       for (double cand : {first, 1.0, 0.5}) {
         if (!(cand > 0.0) || !std::isfinite(cand)) continue;
         std::vector<unsigned char> ok(64, 1);
+        // J = cand * r exactly with |r| <= 127 (r found with the reciprocal, checked by the
+        // product: the device operand cand * q reproduces every entry bit for bit)
+        const double inv = 1.0 / cand;
         par_for(tot, [&](int64_t lo, int64_t hi, int t) {
           bool g = true;
-          for (int64_t k = lo; k < hi; ++k) {
-            const double v = A[k] / cand, r = std::nearbyint(v);
-            g &= (v == r) && std::fabs(r) <= 127.0 && r * cand == A[k];
-            q[k] = int8_t(r);
-          }
+          stream_fill(q, lo, hi, [&](int64_t k) {
+            const double r = rne(A[k] * inv);
+            g &= std::fabs(r) <= 127.0 && r * cand == A[k];
+            return int8_t(r);
+          });
           ok[t] = g;
         }, T);
         if (std::all_of(ok.begin(), ok.end(), [](unsigned char b) { return b != 0; })) {
@@ -1051,6 +1280,10 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     for (int r = 0; r < R; ++r)
       if (!(alpha[r] > 0) || !(beta[r] > 0)) throw InvalidArg("alpha and beta must be positive");
     PhaseClock pc("begin");
+    if (c->hist_inflight) {  // the last run's history copy still reads `hist`
+      CK(cudaEventSynchronize(c->hist_copied));
+      c->hist_inflight = false;
+    }
     c->prm = *P;
     c->R = R;
     c->begun = false;
@@ -1252,11 +1485,16 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
           c->pin_bytes = bytes;
         }
         float* x32 = reinterpret_cast<float*>(c->pin);
-        par_for(tot, [&](int64_t lo, int64_t hi, int) {
-          for (int64_t k = lo; k < hi; ++k) x32[k] = float(x0[k]);
-        }, 16);
-        pc.mark("x0 to f32");
-        CK(cudaMemcpyAsync(src.p, x32, bytes, cudaMemcpyHostToDevice, c->stream));
+        // in pieces: the DMA of piece i overlaps the rounding of piece i + 1
+        const int64_t piece = std::max<int64_t>(int64_t(1) << 18, (tot / 8 + 63) / 64 * 64);
+        for (int64_t k0 = 0; k0 < tot; k0 += piece) {
+          const int64_t m = std::min(piece, tot - k0);
+          par_for(m, [&](int64_t lo, int64_t hi, int) {
+            stream_fill(x32 + k0, lo, hi, [&](int64_t k) { return float(x0[k0 + k]); });
+          }, 16);
+          CK(cudaMemcpyAsync(src.as<float>() + k0, x32 + k0, size_t(m) * 4, cudaMemcpyHostToDevice, c->stream));
+        }
+        pc.mark("x0 to f32 + H2D issue");
         if (timing_on()) {
           CK(cudaStreamSynchronize(c->stream));
           pc.mark("x0 H2D");
@@ -1428,11 +1666,16 @@ int dcx_dist_finish(dcx_ctx* c) {
   });
 }
 
-static void drain(dcx_ctx* c) {
-  const int R = c->R;
-  CK(cudaMemcpyAsync(c->hctl.data(), c->ctl.p, sizeof(RepCtl) * R, cudaMemcpyDeviceToHost, c->stream));
+static void pull_ctl(dcx_ctx* c) {
+  CK(cudaMemcpyAsync(c->hctl.data(), c->ctl.p, sizeof(RepCtl) * c->R, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(&c->hg, c->g.p, sizeof(GState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+}
+
+// new history records -> the pinned ring. defer: the last drain of a run whose records
+// sit in place in the ring (ring_direct) leaves the copy in flight (PinnedRing::wait)
+static void copy_hist(dcx_ctx* c, bool defer) {
+  const int R = c->R;
   // new history entries: k in [lo, hi] over all replicas (replicas advance in lockstep)
   int64_t lo = std::numeric_limits<int64_t>::max(), hi = -1;
   for (int r = 0; r < R; ++r) {
@@ -1446,17 +1689,30 @@ static void drain(dcx_ctx* c) {
   if (hi < 0) return;
   const size_t rec = sizeof(HistRec);
   const size_t pitch = rec * c->cap;
+  const bool async = defer && c->ring_direct;
+  cudaStream_t cs = async ? c->hstream : c->stream;
   auto copy_cols = [&](int64_t k0, int64_t k1) {  // ring columns [k0, k1] without wrap
     CK(cudaMemcpy2DAsync(c->ring + k0, pitch, c->hist.as<HistRec>() + k0, pitch, rec * (k1 - k0 + 1), R,
-                         cudaMemcpyDeviceToHost, c->stream));
+                         cudaMemcpyDeviceToHost, cs));
   };
+  c->ringp->wait();  // an earlier deferred copy into this ring
+  if (async) {
+    CK(cudaEventRecord(c->hist_go, c->stream));
+    CK(cudaStreamWaitEvent(c->hstream, c->hist_go, 0));
+  }
   if (hi - lo + 1 >= c->cap) copy_cols(0, c->cap - 1);
   else {
     const int64_t a = lo % c->cap, b = hi % c->cap;
     if (a <= b) copy_cols(a, b);
     else { copy_cols(a, c->cap - 1); copy_cols(0, b); }
   }
-  CK(cudaStreamSynchronize(c->stream));
+  if (async) {
+    c->ringp->mark_pending(c->hstream);
+    CK(cudaEventRecord(c->hist_copied, c->hstream));
+    c->hist_inflight = true;
+  } else {
+    CK(cudaStreamSynchronize(c->stream));
+  }
   for (int r = 0; r < R; ++r) {
     const int64_t kr = c->hctl[r].k;
     if (c->ring_direct) {
@@ -1466,6 +1722,11 @@ static void drain(dcx_ctx* c) {
     auto& v = c->hh[r];
     for (int64_t k = (int64_t)v.size(); k <= kr; ++k) v.push_back(c->ring[(size_t)r * c->cap + (k % c->cap)]);
   }
+}
+
+static void drain(dcx_ctx* c) {
+  pull_ctl(c);
+  copy_hist(c, false);
 }
 
 int dcx_solve_step(dcx_ctx* c, int32_t* live) {
@@ -1498,7 +1759,7 @@ int dcx_solve_step(dcx_ctx* c, int32_t* live) {
     // device time of the solve ends with the last compute launch; history / result
     // downloads that follow belong to the end-to-end time only
     CK(cudaEventRecord(c->ev1, c->stream));
-    drain(c);
+    pull_ctl(c);
     bool alive = c->hg.live != 0 && c->hg.running > 0;
     if (c->path == DCX_PATH_PERSISTENT && c->p_host >= c->prm.max_iters + 1) alive = false;
     if (!alive) {
@@ -1508,9 +1769,10 @@ int dcx_solve_step(dcx_ctx* c, int32_t* live) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
       c->dev_seconds = ms * 1e-3;
-      drain(c);
+      pull_ctl(c);
       c->finished = true;
     }
+    copy_hist(c, !alive);
     if (live) *live = alive ? 1 : 0;
   });
 }
@@ -1545,6 +1807,7 @@ int dcx_result_history(dcx_ctx* c, int32_t r, int64_t from, int64_t count, doubl
                        int32_t* ev) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   if (!c->begun || r < 0 || r >= c->R) return fail(c, DCX_E_INVALID, "bad replica");
+  if (c->ringp) c->ringp->wait();
   if (from < 0 || count < 0 || from + count > c->nhist(r)) return fail(c, DCX_E_INVALID, "history range");
   for (int64_t k = 0; k < count; ++k) {
     const HistRec& q = c->rec(r, from + k);
@@ -1574,6 +1837,7 @@ int dcx_result_summaries(dcx_ctx* c, int64_t* iterations, int32_t* stop_reason, 
 int dcx_result_history_all(dcx_ctx* c, int64_t K, double* h, double* e, double* t, int32_t* ev) {
   if (!c) return fail(nullptr, DCX_E_INVALID, "ctx is NULL");
   if (!c->begun) return fail(c, DCX_E_STATE, "no run");
+  if (c->ringp) c->ringp->wait();
   auto rows = [&](int r0, int r1) {
     for (int r = r0; r < r1; ++r) {
       const int64_t cnt = std::min<int64_t>(K, c->nhist(r));
@@ -1870,9 +2134,26 @@ int dcx_result_detach(dcx_ctx* c, dcx_result** out) {
       res->hh = c->hh;  // (runs longer than the ring: the drained copies)
     }
     res->warn_delta.assign(R, std::numeric_limits<double>::quiet_NaN());
-    for (int r = 0; r < R; ++r) {
-      const int k = c->hctl[r].warned;
-      if (k >= 1 && k < res->nhist(r)) res->warn_delta[r] = res->rec(r, k).h - res->rec(r, k - 1).h;
+    if (c->ring_direct) {  // from the device records: the history copy may still be in flight
+      if (c->wdelta_n < size_t(R)) {
+        if (c->wdelta) cudaFreeHost(c->wdelta);
+        c->wdelta = nullptr;
+        c->wdelta_n = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->wdelta), size_t(R) * 8, cudaHostAllocMapped));
+        c->wdelta_n = size_t(R);
+      }
+      double* wd = nullptr;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&wd), c->wdelta, 0));
+      gather_warn_delta<<<int((R + 255) / 256), 256, 0, c->stream>>>(c->hist.as<HistRec>(), c->ctl.as<RepCtl>(),
+                                                                    c->cap, int(R), wd);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(c->stream));
+      std::copy(c->wdelta, c->wdelta + R, res->warn_delta.begin());
+    } else {
+      for (int r = 0; r < R; ++r) {
+        const int k = c->hctl[r].warned;
+        if (k >= 1 && k < res->nhist(r)) res->warn_delta[r] = res->rec(r, k).h - res->rec(r, k - 1).h;
+      }
     }
     CK(cudaStreamSynchronize(c->stream));
   });
@@ -1915,6 +2196,7 @@ int dcx_res_best_spins(dcx_result* res, int8_t* out) {
 
 int dcx_res_history_all(dcx_result* res, int64_t K, double* h, double* e, double* t, int32_t* ev) {
   if (!res) return fail(nullptr, DCX_E_INVALID, "result is NULL");
+  if (res->ring) res->ring->wait();
   history_rows(*res, res->R, K, h, e, t, ev);
   return DCX_OK;
 }
