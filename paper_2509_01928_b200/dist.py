@@ -500,22 +500,26 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
         if halo_done is not None:
             stream.wait_event(halo_done)
         ctx.dist_finish()
-        # gather best spins and final states of every row block (padded space)
-        pad = np.zeros((R, rb.B))
-        bs = ctx.best_spins().astype(np.float64)
-        pad[:, :n_rows] = bs if perm is None else bs[:, inv]
-        best_t = torch.from_numpy(pad.T.copy()).to(tdev)
-        full_b = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
-        full_b[ex.rank * rb.B:(ex.rank + 1) * rb.B] = best_t
-        ex.all_gather_rows(full_b, rb.B)
-        st = ctx.state()
-        pad[:, :n_rows] = st if perm is None else st[:, inv]
-        full_x = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
-        full_x[ex.rank * rb.B:(ex.rank + 1) * rb.B] = torch.from_numpy(pad.T.copy()).to(tdev)
-        ex.all_gather_rows(full_x, rb.B)
+        # best spins and final states of every row block, gathered to every rank (padded space);
+        # the spins cross as int8 (1 byte per entry), and one rank keeps its own arrays
+        bs, st = ctx.best_spins(), ctx.state()
+        if perm is not None:
+            bs, st = bs[:, inv], st[:, inv]
+        if ex.world == 1:
+            best, xs = bs.astype(np.float64), st
+        else:
+            lo = ex.rank * rb.B
+            full_b = torch.zeros(rb.n_space, R, dtype=torch.int8, device=tdev)
+            full_b[lo:lo + n_rows] = torch.from_numpy(np.ascontiguousarray(bs.T)).to(tdev)
+            ex.all_gather_rows(full_b, rb.B)
+            full_x = torch.zeros(rb.n_space, R, dtype=torch.float64, device=tdev)
+            full_x[lo:lo + n_rows] = torch.from_numpy(np.ascontiguousarray(st.T)).to(tdev)
+            ex.all_gather_rows(full_x, rb.B)
+            if stream is not None:
+                stream.synchronize()
+            best = rb.unpad(full_b.cpu().numpy().T).astype(np.float64)
+            xs = rb.unpad(full_x.cpu().numpy().T)
         if stream is not None:
             stream.synchronize()
-    best = rb.unpad(full_b.cpu().numpy().T)
-    xs = rb.unpad(full_x.cpu().numpy().T)
     return assemble_results(ctx, solver, R, best, xs, offset, getattr(instance, "cut_offset", None), seeds,
                             path="row-partitioned/" + ("halo" if use_halo else "allgather"))
