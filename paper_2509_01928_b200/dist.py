@@ -51,6 +51,7 @@ device buffers; with gloo (CPU transport) they are staged through host memory
 from __future__ import annotations
 
 import contextlib
+import os
 import time
 import weakref
 from dataclasses import dataclass
@@ -391,13 +392,17 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
                       lookback_q: int = 5, window_mode: str = "economy", trace_stride: int = 1,
                       time_budget: Optional[float] = None, precision: str = "f32",
                       seeds: Optional[Sequence[int]] = None, poll_every: int = 16,
-                      device: Optional[int] = None, exchange: str = "auto", _context=None) -> list:
+                      device: Optional[int] = None, exchange: str = "auto", graph: Optional[bool] = None,
+                      _context=None) -> list:
     """Row-partitioned ``solve_replicas``: the same R replicas, the coupling split by rows over the ranks
     of ``group`` (every rank passes the same instance and the same full ``x0`` [R][n]).
 
     Returns one SolveResult per replica on every rank (best spins and final x gathered to all ranks).
     ``exchange``: "allgather", "halo" (neighbour-only) or "auto" (halo when it moves < 3/4 of the
     all-gather rows summed over ranks). Both give bit-identical iterates.
+    ``graph``: replay the ``poll_every`` iterations between host polls as one CUDA graph (passes,
+    reductions, NCCL collectives and the exchange stream); default: environment ``DCX_DIST_GRAPH=1``.
+    NCCL process groups only; the iterates are the eager loop's.
     ``_context`` replaces the libdcx context (tests only).
     """
     import torch
@@ -470,35 +475,71 @@ def solve_distributed(instance, solver: str, alpha, beta, x0, *, group=None, max
                        qm.data_ptr())
         offset = time.perf_counter() - t_entry
         step(X[0])
-        p, live = 0, True
-        halo_done = None
+        st_ = {"p": 0, "halo_done": None}
+
+        def iterate():
+            p, halo_done = st_["p"], st_["halo_done"]
+            if perm is not None:
+                ctx.dist_pass_rows(0, n_int, 0)  # interior rows: own x only
+                if halo_done is not None:
+                    stream.wait_event(halo_done)  # the halo of x_p has landed
+                ctx.dist_pass_rows(n_int, n_rows, 1)
+                ctx.dist_reduce()
+            else:
+                ctx.dist_pass()
+            if ex.world > 1:
+                ex.combine(qs, qm)  # one collective for the SUM and MAX partials
+            ctx.dist_control()
+            p += 1
+            if overlap:  # x_{p+1} is final once control p ran: exchange it behind the next interior pass
+                ready = torch.cuda.Event()
+                ready.record(stream)
+                comm.wait_event(ready)
+                with torch.cuda.stream(comm):
+                    ex_x.halo_compact(X[p & 1], plan, send_local, rb.B)
+                    halo_done = torch.cuda.Event()
+                    halo_done.record(comm)
+            else:
+                step(X[p & 1])
+            st_["p"], st_["halo_done"] = p, halo_done
+
+        if graph is None:
+            graph = os.environ.get("DCX_DIST_GRAPH", "0") == "1"
+        use_graph = bool(graph) and stream is not None and not ex.host_staged
+        K = max(1, int(poll_every))
+        if use_graph:
+            K += K & 1  # an even chunk: every replay starts on the same iterate buffer parity
+        for _ in range(K):  # the first chunk eagerly (communicators, kernel attributes set up)
+            iterate()
+        live, _ = ctx.dist_poll()
+        if live and use_graph:
+            # the chunk ends joined (the last exchange waited for), so a replay depends on nothing
+            # recorded outside it; one interior pass per chunk loses its overlap
+            if st_["halo_done"] is not None:
+                stream.wait_event(st_["halo_done"])
+                st_["halo_done"] = None
+            g = torch.cuda.CUDAGraph()
+            # capture_begin / capture_end directly: torch.cuda.graph() would also run a full
+            # device synchronize and gc.collect() inside the solve
+            with torch.cuda.stream(stream):
+                g.capture_begin(capture_error_mode="thread_local")
+                try:
+                    for _ in range(K):
+                        iterate()
+                    if st_["halo_done"] is not None:
+                        stream.wait_event(st_["halo_done"])
+                        st_["halo_done"] = None
+                finally:
+                    g.capture_end()
+            while live:
+                g.replay()
+                live, _ = ctx.dist_poll()
         while live:
-            for _ in range(max(1, int(poll_every))):
-                if perm is not None:
-                    ctx.dist_pass_rows(0, n_int, 0)  # interior rows: own x only
-                    if halo_done is not None:
-                        stream.wait_event(halo_done)  # the halo of x_p has landed
-                    ctx.dist_pass_rows(n_int, n_rows, 1)
-                    ctx.dist_reduce()
-                else:
-                    ctx.dist_pass()
-                if ex.world > 1:
-                    ex.combine(qs, qm)  # one collective for the SUM and MAX partials
-                ctx.dist_control()
-                p += 1
-                if overlap:  # x_{p+1} is final once control p ran: exchange it behind the next interior pass
-                    ready = torch.cuda.Event()
-                    ready.record(stream)
-                    comm.wait_event(ready)
-                    with torch.cuda.stream(comm):
-                        ex_x.halo_compact(X[p & 1], plan, send_local, rb.B)
-                        halo_done = torch.cuda.Event()
-                        halo_done.record(comm)
-                else:
-                    step(X[p & 1])
+            for _ in range(K):
+                iterate()
             live, _ = ctx.dist_poll()
-        if halo_done is not None:
-            stream.wait_event(halo_done)
+        if st_["halo_done"] is not None:
+            stream.wait_event(st_["halo_done"])
         ctx.dist_finish()
         # best spins and final states of every row block, gathered to every rank (padded space);
         # the spins cross as int8 (1 byte per entry), and one rank keeps its own arrays

@@ -189,8 +189,12 @@ def _single_context(solver, precision, R, max_iters):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("solver,precision", [("doch", "f64"), ("doch", "f32"), ("adoch", "f64")])
-def test_row_partitioned_world1_nccl_equals_multipass(solver, precision):
+@pytest.mark.parametrize("solver,precision,exchange,graph", [
+    ("doch", "f64", "auto", False), ("doch", "f32", "auto", False), ("adoch", "f64", "auto", False),
+    # the iteration chunk replayed as a CUDA graph (passes, reductions, the exchange stream)
+    ("doch", "f64", "auto", True), ("adoch", "f64", "auto", True), ("doch", "f32", "halo", True),
+    ("adoch", "f64", "halo", True), ("doch", "f64", "halo", False)])
+def test_row_partitioned_world1_nccl_equals_multipass(solver, precision, exchange, graph):
     import torch.distributed as dist
 
     R, max_iters = 4, 150
@@ -199,7 +203,7 @@ def test_row_partitioned_world1_nccl_equals_multipass(solver, precision):
         dist.init_process_group("nccl", init_method=f"file://{td}/rdzv", rank=0, world_size=1)
         try:
             res = dd.solve_distributed(inst, solver, alpha, beta, X0, max_iters=max_iters, precision=precision,
-                                       device=0, poll_every=8)
+                                       device=0, poll_every=8, exchange=exchange, graph=graph)
         finally:
             dist.destroy_process_group()
     for a, b in zip(res, ref):
