@@ -399,10 +399,13 @@ def run_ours(args):
     per_iter = {"multipass": 2, "persistent": 0, "dense_tc": 0}.get(res[0].path, 2)
     chunk = 32
     its1 = int(its_max) + 1
+    # per solve, from the ncu launch list (profiles/r2_k2_launches.txt): the iteration kernels, then
+    # x0 layout, start clock, pack / flush, unpack, and the detached result's three gathers
+    # (final states, best spins, descent-warning deltas)
     if res[0].path == "multipass":
-        launches_total = args.steps * (per_iter * chunk * -(-its1 // chunk) + 4)
+        launches_total = args.steps * (per_iter * chunk * -(-its1 // chunk) + 7)
     else:
-        launches_total = args.steps * (-(-its1 // MAX_ITERS) + 3)
+        launches_total = args.steps * (-(-its1 // (MAX_ITERS + 1)) + 7)
     cpu = None
     if rank == 0 and world == 1:  # the unmodified reference on this host, bounded sample (~10-20 s)
         m = measure_reference(args.solver, 1, 1, step_seconds=15.0)
