@@ -17,7 +17,6 @@ the benchmark use.
 from __future__ import annotations
 
 import os
-import threading
 import time
 import warnings
 from dataclasses import dataclass, field, replace
@@ -217,7 +216,6 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
     ctx.begin(prm, alpha, beta, X0)
     offset = time.perf_counter() - t_entry
     cut_offset = getattr(instance, "cut_offset", None)
-    shells = None
     if callbacks and R == 1:
         # stream records to the callbacks in iteration order, chunk by chunk
         # the running best over recorded iterations is carried across chunks, so every
@@ -238,45 +236,12 @@ def solve_replicas(instance, solver: str, alpha, beta, x0, *, max_iters: int = 1
                         cb(rec)
                 fed = int(s.n_hist)
     else:
-        # large batches: the result objects are built on a helper thread while run() waits for
-        # the device (the call releases the GIL); the fields only the run decides are filled after
-        shells = _Shells(R, solver, seeds) if R >= _SHELL_MIN else None
         ctx.run()
     path_used = _native.PATH_NAME.get(int(ctx.summary(0).path_used))
-    return _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path_used, record_states,
-                              shells=None if callbacks and R == 1 else shells)
+    return _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path_used, record_states)
 
 
 _LAZY = object()  # a SolveResult field read from the detached run on first access
-_SHELL_MIN = 256  # batches from this size build their result objects during the run
-
-
-class _Shells:
-    """R result objects with every field the run does not decide, built on a helper thread."""
-
-    def __init__(self, R, solver, seeds):
-        self.out = []
-        base = dict(solver=solver, spins=_LAZY, trace=_LAZY, x=_LAZY, h_values=_LAZY,
-                    accepted=_LAZY if solver == "adoch" else None, states=None)
-        seed_l = [None] * R if seeds is None else list(seeds)
-        self._t = threading.Thread(target=self._build, args=(R, base, seed_l), daemon=True)
-        self._t.start()
-
-    def _build(self, R, base, seed_l):
-        new, cls, out = object.__new__, _LazySolveResult, self.out
-        for r0 in range(0, R, 32):
-            for r in range(r0, min(R, r0 + 32)):
-                o = new(cls)
-                d = o.__dict__
-                d.update(base)
-                d["seed"] = seed_l[r]
-                d["_r"] = r
-                out.append(o)
-            time.sleep(0)  # hand the GIL back: the caller's next launch must not wait a switch interval
-
-    def get(self):
-        self._t.join()
-        return self.out
 
 
 class _LazySolveResult(SolveResult):
@@ -338,7 +303,7 @@ class _Bulk:
         raise KeyError(kind)
 
 
-def _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path=None, record_states=False, shells=None):
+def _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path=None, record_states=False):
     """SolveResults of a finished run whose bulk arrays (final states, best spins, the
     history) are detached from the context and read only when a field is accessed: the
     energies, iterations and stop reasons come from the per-replica summaries."""
@@ -360,19 +325,6 @@ def _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path=None, rec
     bulk = _Bulk(res, solver, R, offset, cut_offset, iters, nh)
     it_l, be_l = iters.tolist(), bests.tolist()
     stop_l = [_native.STOP.get(v, "max_iters") for v in stops.tolist()]
-    if shells is not None:
-        out = shells.get()
-        for r, o in enumerate(out):
-            d = o.__dict__
-            d["energy"] = be_l[r]
-            d["iterations"] = it_l[r]
-            d["stop_reason"] = stop_l[r]
-            d["device_seconds"] = dev_s
-            d["path"] = path
-            d["_bulk"] = bulk
-            if states_l is not None:
-                d["states"] = states_l[r]
-        return out
     out = []
     append = out.append
     L = _LAZY

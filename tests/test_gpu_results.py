@@ -75,28 +75,3 @@ def test_lazy_result_is_a_solve_result():
     d = dataclasses.asdict(r)
     assert np.array_equal(d["x"], r.x) and len(d["trace"]) == len(r.trace)
     assert r.energy == dc.energy(inst.coupling, r.spins)
-
-
-def test_result_shells_built_during_the_run(monkeypatch):
-    """Batches of >= solvers._SHELL_MIN replicas build their result objects on a helper thread
-    while the run waits for the device: the results equal the ones built after the run."""
-    from paper_2509_01928_b200 import solvers
-
-    v, c, o, co = synth.g1_shape()
-    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(800, v, c, o, validate=False), cut_offset=co)
-    a, b = 6.108031887826326, 884913.7454957356
-    R = solvers._SHELL_MIN + 44
-    X0 = np.stack([dc.initial_state(800, a, b, np.random.default_rng(s)) for s in range(R)])
-    seeds = list(range(1000, 1000 + R))
-    for solver in ("doch", "adoch"):
-        shelled = dc.solve_replicas(inst, solver, a, b, X0, max_iters=40, precision="f32", seeds=seeds)
-        monkeypatch.setattr(solvers, "_SHELL_MIN", 10 ** 9)
-        plain = dc.solve_replicas(inst, solver, a, b, X0, max_iters=40, precision="f32", seeds=seeds)
-        monkeypatch.undo()
-        assert len(shelled) == len(plain) == R
-        for x, y in zip(shelled, plain):
-            assert type(x) is type(y)
-            assert x.seed == y.seed and x.path == y.path and x.device_seconds is not None
-            _same(_fields(x), _fields(y))
-        r2 = dataclasses.replace(shelled[5], seed=7)
-        assert r2.seed == 7 and r2.energy == shelled[5].energy and np.array_equal(r2.spins, shelled[5].spins)
