@@ -157,7 +157,7 @@ struct dcx_ctx {
   bool begun = false, finished = false, f64 = true;
   int path = DCX_PATH_MULTIPASS;
   int cap = 0, wcap = 0, chunk = 0, p_host = 0;
-  DevBuf ctl, g, hist, window, xb0, xb1, ax0, ax1, ay, best, states, part, spart;
+  DevBuf ctl, g, hist, window, xb0, xb1, xb2, ax0, ax1, ay, best, states, part, spart;
   DevBuf scratch;  // grow-only staging (x0 upload, result gathers): no cudaMalloc / cudaFree per call
   DevBuf xmaps;    // pass_rv row-gather TMA maps over the two iterate buffers
   DevBuf sgn0, sgn1;  // pass_torus sign words of x_p by pass parity
@@ -557,13 +557,15 @@ __global__ void from_device_layout(const T* src, double* dst, int64_t n, int R) 
 // final state of each replica (buffer by the parity of its last iteration),
 // [n][R] -> [R][n] f64, written coalesced for one device-to-host copy
 template <typename T>
-__global__ void gather_final_state(const T* x0, const T* x1, const RepCtl* ctl, int64_t n, int R, double* out) {
+__global__ void gather_final_state(const T* x0, const T* x1, const T* x2, int nbuf, const RepCtl* ctl, int64_t n,
+                                   int R, double* out) {
   const int64_t total = n * R;
   for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
     const int r = int(o / n);
     const int64_t i = o % n;
     const int k = max(0, ctl[r].k);
-    out[o] = double(((k & 1) ? x1 : x0)[i * R + r]);
+    const int slot = nbuf == 3 ? k % 3 : (k & 1);  // the buffer of x_k (xslot)
+    out[o] = double((slot == 0 ? x0 : (slot == 1 ? x1 : x2))[i * R + r]);
   }
 }
 // h_k - h_(k-1) at each replica's first descent violation k, NaN if none (the records sit
@@ -1327,12 +1329,23 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     if (c->chunk < 1) c->chunk = 1;
     // buffers
     const int64_t tot = n * R;
+    // three iterate buffers for DOCH on the CSR passes (pass_r1 / pass_r1w / pass_rv): x_{p-2}
+    // survives pass p, so the best-spin copy of x_q is made only when x_{q+1} does not improve on
+    // it -- at the end of an improvement streak, not after every improvement.
+    // Not on the row-partitioned (caller's two buffers), procedural, column-chunked or stencil
+    // passes; DCX_XBUF3=0 keeps two.
+    auto env_is = [](const char* k, const char* v) { const char* e = std::getenv(k); return e && std::strcmp(e, v) == 0; };
+    const int nbuf = (c->path == DCX_PATH_MULTIPASS && !dist && P->solver == DCX_SOLVER_DOCH && !c->proc &&
+                      !std::getenv("DCX_CHUNKS") && !env_is("DCX_TORUS", "1") && !env_is("DCX_XBUF3", "0"))
+                         ? 3 : 2;
     if (dist) {
       c->xb0.release();
       c->xb1.release();
+      c->xb2.release();
     } else {
       c->xb0.alloc(tot * tb);
       c->xb1.alloc(tot * tb);
+      if (nbuf == 3) c->xb2.alloc(tot * tb); else c->xb2.release();
     }
     const bool ad = P->solver == DCX_SOLVER_ADOCH;
     if (ad) { c->ax0.alloc(tot * tb); c->ax1.alloc(tot * tb); } else { c->ax0.release(); c->ax1.release(); }
@@ -1391,6 +1404,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.scale = c->J.scale;
     a.ctl = c->ctl.as<RepCtl>();
     a.g = c->g.as<GState>();
+    a.nbuf = nbuf;
+    a.x[2] = a.gx[2] = nullptr;
     if (dist) {  // own rows start at row_base of the caller's [n_cols][R] buffers
       a.gx[0] = xe0;
       a.gx[1] = xe1;
@@ -1399,6 +1414,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     } else {
       a.x[0] = a.gx[0] = c->xb0.p;
       a.x[1] = a.gx[1] = c->xb1.p;
+      if (nbuf == 3) a.x[2] = a.gx[2] = c->xb2.p;
     }
     a.ax[0] = c->ax0.p;
     a.ax[1] = c->ax1.p;
@@ -1407,7 +1423,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.states = c->states.p;
     a.part = c->part.as<double>();
     a.slots = slots;
-    a.xmap[0] = a.xmap[1] = nullptr;
+    a.xmap[0] = a.xmap[1] = a.xmap[2] = nullptr;
     a.proc_seed = c->J.proc_seed;
     a.torus_L = (!dist && c->torus_L > 0 && !c->proc) ? int32_t(c->torus_L) : 0;
     a.bond_r = c->bond_r.as<int8_t>();
@@ -1437,14 +1453,13 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     if (R > 1 && !c->proc && replica_vector_width(R, c->f64) > 1) {
       const char* e = std::getenv("DCX_RV_TMA");
       if (!(e && std::atoi(e) == 0)) {
-        alignas(64) unsigned char maps[2][128];
+        alignas(64) unsigned char maps[3][128] = {};
         const int vw = replica_vector_width(R, c->f64);
-        for (int k = 0; k < 2; ++k)
+        for (int k = 0; k < nbuf; ++k)
           encode_row_gather_map(maps[k], a.gx[k], uint64_t(R), uint64_t(c->n_cols), c->f64, uint32_t(32 * vw));
         c->xmaps.alloc(sizeof(maps));
         CK(cudaMemcpy(c->xmaps.p, maps, sizeof(maps), cudaMemcpyHostToDevice));
-        a.xmap[0] = c->xmaps.p;
-        a.xmap[1] = static_cast<char*>(c->xmaps.p) + 128;
+        for (int k = 0; k < 3; ++k) a.xmap[k] = k < nbuf ? static_cast<char*>(c->xmaps.p) + 128 * k : nullptr;
       }
     }
     // pass_rv lanes sum the spin energy of ceil(n / (8 grid)) rows; integer couplings keep that exact in f32
@@ -1515,6 +1530,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
         }
       }
       CK(cudaMemsetAsync(a.x[1], 0, tot * tb, c->stream));
+      if (a.x[2]) CK(cudaMemsetAsync(a.x[2], 0, tot * tb, c->stream));
       if (ad) {
         CK(cudaMemsetAsync(c->ax0.p, 0, tot * tb, c->stream));
         CK(cudaMemsetAsync(c->ax1.p, 0, tot * tb, c->stream));
@@ -1910,11 +1926,13 @@ int dcx_result_state(dcx_ctx* c, double* out) {
     if (tmp.bytes < size_t(tot) * 8) tmp.alloc(size_t(tot) * 8);
     if (c->f64)
       gather_final_state<double><<<grid_for(tot), 256, 0, c->stream>>>(
-          static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]),
+          static_cast<const double*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
           n, (int)R, tmp.as<double>());
     else
       gather_final_state<float><<<grid_for(tot), 256, 0, c->stream>>>(
-          static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]),
+          static_cast<const float*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
           n, (int)R, tmp.as<double>());
     CK(cudaMemcpyAsync(out, tmp.p, tot * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -2126,11 +2144,13 @@ int dcx_result_detach(dcx_ctx* c, dcx_result** out) {
     res->best = take_dev(c, size_t(tot));
     if (c->f64)
       gather_final_state<double><<<grid_for(tot), 256, 0, c->stream>>>(
-          static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]),
+          static_cast<const double*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
           n, (int)R, static_cast<double*>(res->x->p));
     else
       gather_final_state<float><<<grid_for(tot), 256, 0, c->stream>>>(
-          static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]), c->ctl.as<RepCtl>(),
+          static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]),
+          static_cast<const float*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
           n, (int)R, static_cast<double*>(res->x->p));
     gather_best<<<grid_for(tot), 256, 0, c->stream>>>(c->best.as<int8_t>(), n, (int)R, static_cast<int8_t*>(res->best->p));
     CK(cudaGetLastError());

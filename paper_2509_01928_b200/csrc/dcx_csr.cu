@@ -25,14 +25,14 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
   if (MODE == MODE_ADOCH_Y && p == 0) return;  // no extrapolation at k = 0
   const RowCtl<T> c = row_ctl<T>(a.ctl[0], p);
   const bool running = c.running;
-  if (!running && !(MODE == MODE_DOCH && c.pend == p - 1)) return;
+  if (!running && !(MODE == MODE_DOCH && c.pend == copy_iter(a, p) && c.pend >= 0)) return;
   const int lane = threadIdx.x & 31;
   const int sub = lane % V;
   const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // global warp
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   constexpr int RPW = 32 / V;  // rows per warp step
-  const T* xc = reinterpret_cast<const T*>(a.gx[p & 1]);  // gather source (all spins)
-  const T* xp = reinterpret_cast<const T*>(a.gx[(p + 1) & 1]);
+  const T* xc = reinterpret_cast<const T*>(a.gx[xslot(a, p)]);  // gather source (all spins)
+  const T* xp = reinterpret_cast<const T*>(a.gx[xslot(a, p + a.nbuf - 1)]);  // x_{p-1}
   const T cm = c.cm;
   const T scale = T(a.scale);
   RowOut<T, MODE> o;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) pass_r1(PassArgs a) {
     if (ok && sub == 0) {
       if (running) row_epilogue<T, MODE>(a, c, p, i, acc, double(es), o);
       else if (MODE == MODE_DOCH) {  // stopped: only the pending copy
-        a.best[i] = reinterpret_cast<const T*>(a.x[(p + 1) & 1])[i] >= T(0) ? 1 : -1;
+        a.best[i] = reinterpret_cast<const T*>(a.x[xslot(a, p + 1)])[i] >= T(0) ? 1 : -1;
       }
     }
   }
@@ -176,14 +176,14 @@ __global__ void __launch_bounds__(256) pass_r1w(PassArgs a) {
   if (MODE == MODE_ADOCH_Y && p == 0) return;  // no extrapolation at k = 0
   const RowCtl<T> c = row_ctl<T>(a.ctl[0], p);
   const bool running = c.running;
-  if (!running && !(MODE == MODE_DOCH && c.pend == p - 1)) return;
+  if (!running && !(MODE == MODE_DOCH && c.pend == copy_iter(a, p) && c.pend >= 0)) return;
   __shared__ float sx[8][R1W_SLOT];
   __shared__ int8_t sq[VK == VK_I8 ? 8 : 1][VK == VK_I8 ? R1W_SLOT : 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const T* xc = reinterpret_cast<const T*>(a.gx[p & 1]);
-  const T* xp = reinterpret_cast<const T*>(a.gx[(p + 1) & 1]);
+  const T* xc = reinterpret_cast<const T*>(a.gx[xslot(a, p)]);
+  const T* xp = reinterpret_cast<const T*>(a.gx[xslot(a, p + a.nbuf - 1)]);  // x_{p-1}
   const T cm = c.cm;
   const T scale = T(a.scale);
   const int64_t n = a.cfg.n;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256) pass_r1w(PassArgs a) {
     if (ok) {
       if (running) row_epilogue<T, MODE>(a, c, p, i, acc, double(es), o);
       else if (MODE == MODE_DOCH) {  // stopped: only the pending copy
-        a.best[i] = reinterpret_cast<const T*>(a.x[(p + 1) & 1])[i] >= T(0) ? 1 : -1;
+        a.best[i] = reinterpret_cast<const T*>(a.x[xslot(a, p + 1)])[i] >= T(0) ? 1 : -1;
       }
     }
   }
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
     if (lane_on) {
       const RepCtl& c = a.ctl[r0 + v];
       run[v] = c.status == DCX_STOP_RUNNING;
-      copy[v] = MODE == MODE_DOCH && p > 0 && c.pend == p - 1;
+      copy[v] = MODE == MODE_DOCH && c.pend >= 0 && c.pend == copy_iter(a, p);
       alpha[v] = T(c.alpha);
       beta[v] = T(c.beta);
       ibeta[v] = inv_beta(beta[v]);
@@ -410,9 +410,9 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
   // nothing to do for this replica chunk (block-uniform: the chunk is per block)
   if (!__syncthreads_or(any_run || any_copy)) return;
   const bool warp_run = __any_sync(0xffffffffu, any_run);
-  const T* xc = reinterpret_cast<const T*>(a.x[p & 1]);
-  const T* xp = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
-  T* xn_buf = reinterpret_cast<T*>(a.x[(p + 1) & 1]);
+  const T* xc = reinterpret_cast<const T*>(a.x[xslot(a, p)]);
+  const T* xp = reinterpret_cast<const T*>(a.x[xslot(a, p + a.nbuf - 1)]);  // x_{p-1}
+  T* xn_buf = reinterpret_cast<T*>(a.x[xslot(a, p + 1)]);  // x_{p+1} (holds the copy iterate)
   const T scale = T(a.scale);
   // per-replica partials over this warp's rows, in T (f32 mode: a few hundred
   // rows per lane, summed in double across warps and blocks); the step max is
@@ -435,8 +435,8 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
   const int64_t S = int64_t(gridDim.x) * 8;
   int64_t i = int64_t(blockIdx.x) * 8 + warp;
   const uint32_t rowb = uint32_t(R) * uint32_t(sizeof(T));  // bytes per spin row of x
-  const char* xcb = reinterpret_cast<const char*>(reinterpret_cast<const T*>(a.gx[p & 1]) + r0);  // gathers
-  const char* xpb = reinterpret_cast<const char*>(reinterpret_cast<const T*>(a.gx[(p + 1) & 1]) + r0);
+  const char* xcb = reinterpret_cast<const char*>(reinterpret_cast<const T*>(a.gx[xslot(a, p)]) + r0);  // gathers
+  const char* xpb = reinterpret_cast<const char*>(reinterpret_cast<const T*>(a.gx[xslot(a, p + a.nbuf - 1)]) + r0);
   // stage s of this warp, edge e, this lane: stage_mem + ((s*8 + warp)*G + e)*32*CB + lane*CB
   const uint32_t st_base = smem_u32(stage_mem) + uint32_t((warp * G * 32 + lane) * CB);
   constexpr uint32_t ST_STRIDE = 8u * G * 32 * CB;  // between stages
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(256, (VW * sizeof(T) >= 16) ? 2 : 3) pass_rv(P
   // TMA staging (a.xmap set): one tile::gather4 per four staged edges, issued by
   // lane 0 with the columns the batch registers hold, completion on an mbarrier
   const bool tma = G > 0 && a.xmap[0] != nullptr;
-  const void* xmap = a.xmap[p & 1];
+  const void* xmap = a.xmap[xslot(a, p)];
   const int cb = int(blockIdx.y) * 32 * VW;  // first replica of this block's chunk
   constexpr uint32_t CHUNK = 32u * CB;
   __shared__ __align__(8) uint64_t stage_bar[8][2];
@@ -1280,7 +1280,9 @@ __global__ void flush_best(PassArgs a) {
        idx += int64_t(gridDim.x) * blockDim.x) {
     const int r = int(idx % R);
     const int pe = a.ctl[r].pend;
-    if (pe >= 0 && pe == P) a.best[idx] = reinterpret_cast<const T*>(a.x[pe & 1])[idx] >= T(0) ? 1 : -1;
+    // not yet copied by a pass: pend > the copy iterate of the last pass (x_P; with three
+    // buffers also x_{P-1}), both still in their buffers
+    if (pe >= 0 && pe > copy_iter(a, P)) a.best[idx] = reinterpret_cast<const T*>(a.x[xslot(a, pe)])[idx] >= T(0) ? 1 : -1;
   }
 }
 

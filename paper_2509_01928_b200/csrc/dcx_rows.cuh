@@ -36,12 +36,12 @@ __device__ __forceinline__ RowCtl<T> row_ctl(const RepCtl& c, int p) {
 template <typename T, int MODE>
 __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RowCtl<T>& c, int p, int64_t idx, T acc,
                                              double esrow, RowOut<T, MODE>& o) {
-  const T* xcur = reinterpret_cast<const T*>(a.x[p & 1]);
-  T* xnext = reinterpret_cast<T*>(a.x[(p + 1) & 1]);
+  const T* xcur = reinterpret_cast<const T*>(a.x[xslot(a, p)]);
+  T* xnext = reinterpret_cast<T*>(a.x[xslot(a, p + 1)]);
   const T alpha = c.alpha;
   if constexpr (MODE == MODE_ADOCH_Y) {
     // acc = J y ; y recomputed identically to the gather
-    const T* xprev = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
+    const T* xprev = reinterpret_cast<const T*>(a.x[xslot(a, p + a.nbuf - 1)]);
     T yi = extrap(xcur[idx], xprev[idx], c.cm);
     T ayi = shifted(acc, alpha, yi);
     reinterpret_cast<T*>(a.ay)[idx] = ayi;
@@ -57,8 +57,8 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RowCtl<T>&
     o.sxax += double(xi) * double(ax);
     o.es += (xi >= T(0) ? esrow : -esrow);
     if constexpr (MODE == MODE_DOCH) {
-      // pending best-spin copy of x_{p-1}, still held in the write buffer
-      if (c.pend == p - 1 && p > 0) a.best[idx] = xnext[idx] >= T(0) ? 1 : -1;
+      // pending best-spin copy (x_{p-1}, or x_{p-2} with three buffers), still held in the write buffer
+      if (c.pend == copy_iter(a, p) && c.pend >= 0) a.best[idx] = xnext[idx] >= T(0) ? 1 : -1;
       if (c.running) {
         T xn = tmap_pass(ax, c.beta, c.ibeta);
         xnext[idx] = xn;
@@ -70,7 +70,7 @@ __device__ __forceinline__ void row_epilogue(const PassArgs& a, const RowCtl<T>&
       T* axb = reinterpret_cast<T*>(a.ax[p & 1]);
       axb[idx] = ax;
       if (p > 0 && a.cfg.window_mode == DCX_WINDOW_ECONOMY) {
-        const T* xprev = reinterpret_cast<const T*>(a.x[(p + 1) & 1]);
+        const T* xprev = reinterpret_cast<const T*>(a.x[xslot(a, p + a.nbuf - 1)]);
         const T* axprev = reinterpret_cast<const T*>(a.ax[(p + 1) & 1]);
         T yi = extrap(xi, xprev[idx], c.cm);
         T ayi = extrap(ax, axprev[idx], c.cm);
