@@ -247,7 +247,6 @@ int lanes_for_degree(double d) {
   return 32;
 }
 
-// Detect the narrowest exact storage of the coupling values (DESIGN.md §3).
 // Host passes over the uploaded arrays (10^8 entries at R8) run on all host threads.
 // Host worker pool for par_for: spawning 16 threads per call cost 0.2-0.3 ms, paid
 // several times per solve (classify J, convert x0, CSR staging). Workers spin for a few
@@ -433,6 +432,7 @@ static void value_stats(const double* v, int64_t lo, int64_t hi, double v0, bool
   mn = mnv;
 }
 
+// Detect the narrowest exact storage of the coupling values (DESIGN.md §3).
 void classify_values(const double* v, int64_t nnz, int& vk, double& scale) {
   if (nnz == 0) { vk = VK_UNIFORM; scale = 0.0; return; }
   std::vector<unsigned char> uni(32, 1), fin(32, 1);
