@@ -253,3 +253,34 @@ def test_torus_stencil_bitwise_equals_csr_pass(solver):
         assert a_.energy == b_.energy and np.array_equal(a_.x, b_.x) and np.array_equal(a_.spins, b_.spins)
         assert [t.energy for t in a_.trace] == [t.energy for t in b_.trace]
         assert np.array_equal(np.asarray(a_.h_values), np.asarray(b_.h_values))
+
+
+def _golden(name):
+    import json
+    from pathlib import Path
+
+    return json.loads((Path(__file__).resolve().parent / "golden" / f"golden_{name}.json").read_text())
+
+
+def test_t6_200_iterations_seed0_equals_reference(t6):
+    """The unmodified reference's 200-iteration DOCH run on the T6 torus, seed 0, f64 on the host
+    (tests/golden/make_golden_t6.py): the f32 device run of replica 0 (one of the bench's 256)
+    ends on the same best energy."""
+    inst, J, alpha, beta, X0 = t6
+    g = _golden("t6")
+    assert (g["alpha"], g["beta"], g["iterations"]) == (alpha, beta, 200)
+    r = dc.solve_replicas(inst, "doch", alpha, beta, X0, max_iters=200, precision="f32")
+    assert r[0].energy == g["best_energy"]
+    assert r[0].energy == dc.energy(inst.coupling, r[0].spins)
+
+
+def test_e7_200_iterations_equals_reference(e7):
+    """The unmodified reference's 200-iteration DOCH run on E7, seed 0, with derive_params at
+    eta = 1 (tests/golden/make_golden_e7.py): the f32 device run reaches the same best cut."""
+    n, v, c, o, co = e7
+    g = _golden("e7")
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False), cut_offset=co)
+    assert co == g["cut_offset"]
+    X0 = dc.initial_state(n, g["alpha"], g["beta"], np.random.default_rng(0))[None, :]
+    r = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=200, precision="f32")[0]
+    assert co - r.energy == g["best_cut"]
