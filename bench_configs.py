@@ -97,6 +97,9 @@ def reference_quality(name):
         if name == "e7":
             g = json.loads((gdir / "golden_e7.json").read_text())
             return g["best_cut"], f"best cut of one {g['iterations']}-iteration reference DOCH run (seed 0)"
+        if name == "r8":
+            g = json.loads((gdir / "golden_r8.json").read_text())
+            return g["best_cut"], f"best cut of one {g['iterations']}-iteration reference DOCH run (seed 0)"
         if name == "t6":  # a spin glass: quality = -best energy (no cut offset)
             g = json.loads((gdir / "golden_t6.json").read_text())
             return -g["best_energy"], f"-(best energy) of one {g['iterations']}-iteration reference DOCH run (seed 0)"

@@ -284,3 +284,17 @@ def test_e7_200_iterations_equals_reference(e7):
     X0 = dc.initial_state(n, g["alpha"], g["beta"], np.random.default_rng(0))[None, :]
     r = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=200, precision="f32")[0]
     assert co - r.energy == g["best_cut"]
+
+
+def test_r8_20_iterations_equals_reference():
+    """The unmodified reference's DOCH run on R8 (n = 1e8, seed 0, derive_params at eta = 1) for
+    the bench's 20 iterations (tests/golden/make_golden_r8.py): the f32 device run reaches the
+    same best cut."""
+    g = _golden("r8")
+    n = 10**8
+    v, c, o, co = synth.random_regular3(n, seed=0, device=0)
+    assert co == g["cut_offset"]
+    inst = dc.ProblemInstance(coupling=dc.CsrCoupling(n, v, c, o, validate=False), cut_offset=co)
+    X0 = dc.initial_state(n, g["alpha"], g["beta"], np.random.default_rng(0))[None, :]
+    r = dc.solve_replicas(inst, "doch", g["alpha"], g["beta"], X0, max_iters=g["iterations"], precision="f32")[0]
+    assert co - r.energy == g["best_cut"]
