@@ -17,6 +17,7 @@ the benchmark use.
 from __future__ import annotations
 
 import os
+import sys
 import time
 import warnings
 from dataclasses import dataclass, field, replace
@@ -303,6 +304,21 @@ class _Bulk:
         raise KeyError(kind)
 
 
+def _warn_site(stacklevel):
+    """warnings.warn(msg, RuntimeWarning, stacklevel) from the caller of this function's caller,
+    with the frame looked up once for a batch of per-replica warnings (warn_explicit with the
+    filename, line, module and registry warnings.warn would derive: the same filters apply)."""
+    try:
+        f = sys._getframe(stacklevel)
+    except ValueError:
+        g, fname, line = sys.__dict__, "sys", 1
+    else:
+        g, fname, line = f.f_globals, f.f_code.co_filename, f.f_lineno
+    module = g.get("__name__", "<string>")
+    registry = g.setdefault("__warningregistry__", {})
+    return lambda msg: warnings.warn_explicit(msg, RuntimeWarning, fname, line, module, registry)
+
+
 def _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path=None, record_states=False):
     """SolveResults of a finished run whose bulk arrays (final states, best spins, the
     history) are detached from the context and read only when a field is accessed: the
@@ -319,9 +335,9 @@ def _assemble_detached(ctx, solver, R, offset, cut_offset, seeds, path=None, rec
     warned = np.nonzero(warn >= 0)[0] if solver == "doch" else ()
     if len(warned):
         wd = res.warn_delta()
+        warn_at = _warn_site(4)
         for r in warned:
-            warnings.warn(f"Hamiltonian increased by {wd[r]:.3e} at iteration {int(warn[r])}",
-                          RuntimeWarning, stacklevel=4)
+            warn_at(f"Hamiltonian increased by {wd[r]:.3e} at iteration {int(warn[r])}")
     bulk = _Bulk(res, solver, R, offset, cut_offset, iters, nh)
     it_l, be_l = iters.tolist(), bests.tolist()
     stop_l = [_native.STOP.get(v, "max_iters") for v in stops.tolist()]
