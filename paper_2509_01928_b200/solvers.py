@@ -374,10 +374,10 @@ def assemble_results(ctx, solver, R, best, xs, offset, cut_offset, seeds, path=N
     nh_l, it_l, be_l = nh.tolist(), iters.tolist(), bests.tolist()
     stop_l = [_native.STOP.get(v, "max_iters") for v in stops.tolist()]
     warned = np.nonzero(warn >= 0)[0] if solver == "doch" else ()
+    warn_at = _warn_site(4) if len(warned) else None
     for r in warned:
         k = int(warn[r])
-        warnings.warn(f"Hamiltonian increased by {H[r, k] - H[r, k - 1]:.3e} at iteration {k}",
-                      RuntimeWarning, stacklevel=4)
+        warn_at(f"Hamiltonian increased by {H[r, k] - H[r, k - 1]:.3e} at iteration {k}")
     out = []
     append = out.append
     for r in range(R):
