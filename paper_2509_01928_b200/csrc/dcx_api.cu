@@ -157,7 +157,7 @@ struct dcx_ctx {
   bool begun = false, finished = false, f64 = true;
   int path = DCX_PATH_MULTIPASS;
   int cap = 0, wcap = 0, chunk = 0, p_host = 0;
-  DevBuf ctl, g, hist, window, xb0, xb1, xb2, ax0, ax1, ay, best, states, part, spart;
+  DevBuf ctl, g, hist, window, xb0, xb1, xb2, xb3, ax0, ax1, ay, best, states, part, spart;
   DevBuf scratch;  // grow-only staging (x0 upload, result gathers): no cudaMalloc / cudaFree per call
   DevBuf xmaps;    // pass_rv row-gather TMA maps over the two iterate buffers
   DevBuf sgn0, sgn1;  // pass_torus sign words of x_p by pass parity
@@ -557,15 +557,15 @@ __global__ void from_device_layout(const T* src, double* dst, int64_t n, int R) 
 // final state of each replica (buffer by the parity of its last iteration),
 // [n][R] -> [R][n] f64, written coalesced for one device-to-host copy
 template <typename T>
-__global__ void gather_final_state(const T* x0, const T* x1, const T* x2, int nbuf, const RepCtl* ctl, int64_t n,
-                                   int R, double* out) {
+__global__ void gather_final_state(const T* x0, const T* x1, const T* x2, const T* x3, int nbuf, const RepCtl* ctl,
+                                   int64_t n, int R, double* out) {
   const int64_t total = n * R;
   for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
     const int r = int(o / n);
     const int64_t i = o % n;
     const int k = max(0, ctl[r].k);
-    const int slot = nbuf == 3 ? k % 3 : (k & 1);  // the buffer of x_k (xslot)
-    out[o] = double((slot == 0 ? x0 : (slot == 1 ? x1 : x2))[i * R + r]);
+    const int slot = nbuf == 2 ? (k & 1) : (nbuf == 4 ? (k & 3) : k % 3);  // the buffer of x_k (xslot)
+    out[o] = double((slot == 0 ? x0 : (slot == 1 ? x1 : (slot == 2 ? x2 : x3)))[i * R + r]);
   }
 }
 // h_k - h_(k-1) at each replica's first descent violation k, NaN if none (the records sit
@@ -1335,17 +1335,20 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     // Not on the row-partitioned (caller's two buffers), procedural, column-chunked or stencil
     // passes; DCX_XBUF3=0 keeps two.
     auto env_is = [](const char* k, const char* v) { const char* e = std::getenv(k); return e && std::strcmp(e, v) == 0; };
-    const int nbuf = (c->path == DCX_PATH_MULTIPASS && !dist && P->solver == DCX_SOLVER_DOCH && !c->proc &&
-                      !std::getenv("DCX_CHUNKS") && !env_is("DCX_TORUS", "1") && !env_is("DCX_XBUF3", "0"))
-                         ? 3 : 2;
+    int nbuf = (c->path == DCX_PATH_MULTIPASS && !dist && P->solver == DCX_SOLVER_DOCH && !c->proc &&
+                !std::getenv("DCX_CHUNKS") && !env_is("DCX_TORUS", "1") && !env_is("DCX_XBUF3", "0"))
+                   ? 3 : 2;
+    if (const char* e = std::getenv("DCX_XBUF"); e && nbuf > 2) nbuf = std::max(2, std::min(4, std::atoi(e)));
     if (dist) {
       c->xb0.release();
       c->xb1.release();
       c->xb2.release();
+      c->xb3.release();
     } else {
       c->xb0.alloc(tot * tb);
       c->xb1.alloc(tot * tb);
-      if (nbuf == 3) c->xb2.alloc(tot * tb); else c->xb2.release();
+      if (nbuf >= 3) c->xb2.alloc(tot * tb); else c->xb2.release();
+      if (nbuf >= 4) c->xb3.alloc(tot * tb); else c->xb3.release();
     }
     const bool ad = P->solver == DCX_SOLVER_ADOCH;
     if (ad) { c->ax0.alloc(tot * tb); c->ax1.alloc(tot * tb); } else { c->ax0.release(); c->ax1.release(); }
@@ -1405,7 +1408,7 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     a.ctl = c->ctl.as<RepCtl>();
     a.g = c->g.as<GState>();
     a.nbuf = nbuf;
-    a.x[2] = a.gx[2] = nullptr;
+    a.x[2] = a.gx[2] = a.x[3] = a.gx[3] = nullptr;
     if (dist) {  // own rows start at row_base of the caller's [n_cols][R] buffers
       a.gx[0] = xe0;
       a.gx[1] = xe1;
@@ -1414,7 +1417,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     } else {
       a.x[0] = a.gx[0] = c->xb0.p;
       a.x[1] = a.gx[1] = c->xb1.p;
-      if (nbuf == 3) a.x[2] = a.gx[2] = c->xb2.p;
+      if (nbuf >= 3) a.x[2] = a.gx[2] = c->xb2.p;
+      if (nbuf >= 4) a.x[3] = a.gx[3] = c->xb3.p;
     }
     a.ax[0] = c->ax0.p;
     a.ax[1] = c->ax1.p;
@@ -1453,13 +1457,13 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
     if (R > 1 && !c->proc && replica_vector_width(R, c->f64) > 1) {
       const char* e = std::getenv("DCX_RV_TMA");
       if (!(e && std::atoi(e) == 0)) {
-        alignas(64) unsigned char maps[3][128] = {};
+        alignas(64) unsigned char maps[4][128] = {};
         const int vw = replica_vector_width(R, c->f64);
         for (int k = 0; k < nbuf; ++k)
           encode_row_gather_map(maps[k], a.gx[k], uint64_t(R), uint64_t(c->n_cols), c->f64, uint32_t(32 * vw));
         c->xmaps.alloc(sizeof(maps));
         CK(cudaMemcpy(c->xmaps.p, maps, sizeof(maps), cudaMemcpyHostToDevice));
-        for (int k = 0; k < 3; ++k) a.xmap[k] = k < nbuf ? static_cast<char*>(c->xmaps.p) + 128 * k : nullptr;
+        for (int k = 0; k < 4; ++k) a.xmap[k] = k < nbuf ? static_cast<char*>(c->xmaps.p) + 128 * k : nullptr;
       }
     }
     // pass_rv lanes sum the spin energy of ceil(n / (8 grid)) rows; integer couplings keep that exact in f32
@@ -1530,7 +1534,8 @@ static void begin_impl(dcx_ctx* c, const dcx_params* P, int32_t R, const double*
         }
       }
       CK(cudaMemsetAsync(a.x[1], 0, tot * tb, c->stream));
-      if (a.x[2]) CK(cudaMemsetAsync(a.x[2], 0, tot * tb, c->stream));
+      for (int k = 2; k < 4; ++k)
+        if (a.x[k]) CK(cudaMemsetAsync(a.x[k], 0, tot * tb, c->stream));
       if (ad) {
         CK(cudaMemsetAsync(c->ax0.p, 0, tot * tb, c->stream));
         CK(cudaMemsetAsync(c->ax1.p, 0, tot * tb, c->stream));
@@ -1927,12 +1932,14 @@ int dcx_result_state(dcx_ctx* c, double* out) {
     if (c->f64)
       gather_final_state<double><<<grid_for(tot), 256, 0, c->stream>>>(
           static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]),
-          static_cast<const double*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
+          static_cast<const double*>(c->mp.args.x[2]), static_cast<const double*>(c->mp.args.x[3]), c->mp.args.nbuf,
+          c->ctl.as<RepCtl>(),
           n, (int)R, tmp.as<double>());
     else
       gather_final_state<float><<<grid_for(tot), 256, 0, c->stream>>>(
           static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]),
-          static_cast<const float*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
+          static_cast<const float*>(c->mp.args.x[2]), static_cast<const float*>(c->mp.args.x[3]), c->mp.args.nbuf,
+          c->ctl.as<RepCtl>(),
           n, (int)R, tmp.as<double>());
     CK(cudaMemcpyAsync(out, tmp.p, tot * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -2145,12 +2152,14 @@ int dcx_result_detach(dcx_ctx* c, dcx_result** out) {
     if (c->f64)
       gather_final_state<double><<<grid_for(tot), 256, 0, c->stream>>>(
           static_cast<const double*>(c->mp.args.x[0]), static_cast<const double*>(c->mp.args.x[1]),
-          static_cast<const double*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
+          static_cast<const double*>(c->mp.args.x[2]), static_cast<const double*>(c->mp.args.x[3]), c->mp.args.nbuf,
+          c->ctl.as<RepCtl>(),
           n, (int)R, static_cast<double*>(res->x->p));
     else
       gather_final_state<float><<<grid_for(tot), 256, 0, c->stream>>>(
           static_cast<const float*>(c->mp.args.x[0]), static_cast<const float*>(c->mp.args.x[1]),
-          static_cast<const float*>(c->mp.args.x[2]), c->mp.args.nbuf, c->ctl.as<RepCtl>(),
+          static_cast<const float*>(c->mp.args.x[2]), static_cast<const float*>(c->mp.args.x[3]), c->mp.args.nbuf,
+          c->ctl.as<RepCtl>(),
           n, (int)R, static_cast<double*>(res->x->p));
     gather_best<<<grid_for(tot), 256, 0, c->stream>>>(c->best.as<int8_t>(), n, (int)R, static_cast<int8_t*>(res->best->p));
     CK(cudaGetLastError());

@@ -54,8 +54,8 @@ struct PassArgs {
   double scale;
   RepCtl* ctl;
   GState* g;
-  void* x[3];      // iterate buffers (xslot below), layout [n][R], at this context's own rows
-  void* gx[3];     // the same buffers at spin 0: the gather source (== x unless row-partitioned)
+  void* x[4];      // iterate buffers (xslot below), layout [n][R], at this context's own rows
+  void* gx[4];     // the same buffers at spin 0: the gather source (== x unless row-partitioned)
   void* ax[2];     // ADOCH (J+aI)x_p by parity
   void* ay;        // ADOCH exact (J+aI)y
   int8_t* best;    // best spins [n][R]
@@ -63,7 +63,7 @@ struct PassArgs {
   double* part;    // pass partials [R][NQ][slots]
   int32_t slots;
   int32_t es_f32;  // pass_rv: per-lane spin-energy sums exact in f32 (integer couplings, bounded rows)
-  const void* xmap[3];  // pass_rv: tile::gather4 maps over gx[0..2] (device copies), or null (cp.async staging)
+  const void* xmap[4];  // pass_rv: tile::gather4 maps over gx[0..nbuf) (device copies), or null (cp.async staging)
   long long proc_seed;  // procedural coupling (vk == VK_PROC): seed of sin(i*j + seed)
   // 2-D periodic L x L lattice detected at upload (dcx_api.cu detect_torus): the stencil
   // pass reads the bonds instead of the CSR. torus_L = 0: not a lattice
@@ -75,16 +75,18 @@ struct PassArgs {
   // pass p + 1 reads them instead of x_p
   uint32_t* sgnw[2];
   ChunkArgs chunks;  // C > 0: the R = 1 pass runs as C column-chunk sweeps + a row epilogue
-  // iterate buffers in rotation: 2 (by pass parity) or 3 (DOCH multipass: x_{p-2} survives pass p,
-  // so the best-spin copy of x_q is made only when x_{q+1} does not improve on it)
+  // iterate buffers in rotation: 2 (by pass parity), or 3 / 4 (DOCH multipass: x_{p-nbuf+1} survives
+  // pass p, so the best-spin copy of x_q is made only when none of the next nbuf - 2 iterates improves on it)
   int32_t nbuf;
   RunCfg cfg;
 };
 
 // the buffer holding x_q (q >= 0)
-__host__ __device__ __forceinline__ int xslot(const PassArgs& a, int q) { return a.nbuf == 3 ? q % 3 : (q & 1); }
-// pass p copies sign(x_q) into the best spins when q = pend is this pass's copy iterate: x_{p-1}
-// (two buffers) or x_{p-2} (three), in both cases the buffer pass p overwrites (xslot(a, p + 1))
+__host__ __device__ __forceinline__ int xslot(const PassArgs& a, int q) {
+  return a.nbuf == 2 ? (q & 1) : (a.nbuf == 4 ? (q & 3) : q % 3);
+}
+// pass p copies sign(x_q) into the best spins when q = pend is this pass's copy iterate x_{p-nbuf+1}
+// (x_{p-1} with two buffers), the buffer pass p overwrites (xslot(a, p + 1))
 __host__ __device__ __forceinline__ int copy_iter(const PassArgs& a, int p) { return p - a.nbuf + 1; }
 
 struct MultiPass {

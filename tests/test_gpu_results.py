@@ -80,9 +80,9 @@ def test_lazy_result_is_a_solve_result():
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 @pytest.mark.parametrize("R", [1, 8])
 def test_three_iterate_buffers_equal_two(monkeypatch, precision, R):
-    """DOCH on the CSR passes rotates three iterate buffers so the best-spin copy waits for the
-    end of an improvement streak (PassArgs::nbuf); DCX_XBUF3=0 keeps two, copying after every
-    improvement. Everything a caller sees is identical, including the best spins of runs that
+    """DOCH on the CSR passes rotates three (DCX_XBUF=4: four) iterate buffers so the best-spin
+    copy waits for the end of an improvement streak (PassArgs::nbuf); DCX_XBUF3=0 keeps two,
+    copying after every improvement. Everything a caller sees is identical, including the best spins of runs that
     end on an improvement, on a non-improving iterate, by convergence and by max_iters."""
     v, c, o, co = synth.g1_shape()
     inst = dc.ProblemInstance(coupling=dc.CsrCoupling(800, v, c, o, validate=False), cut_offset=co)
@@ -91,10 +91,14 @@ def test_three_iterate_buffers_equal_two(monkeypatch, precision, R):
     for iters in (1, 2, 3, 17, 300):
         kw = dict(max_iters=iters, precision=precision, path="multipass")
         three = [_fields(r) for r in dc.solve_replicas(inst, "doch", a, b, X0, **kw)]
+        monkeypatch.setenv("DCX_XBUF", "4")
+        four = [_fields(r) for r in dc.solve_replicas(inst, "doch", a, b, X0, **kw)]
+        monkeypatch.delenv("DCX_XBUF")
         monkeypatch.setenv("DCX_XBUF3", "0")
         two = [_fields(r) for r in dc.solve_replicas(inst, "doch", a, b, X0, **kw)]
         monkeypatch.delenv("DCX_XBUF3")
-        for x, y in zip(three, two):
+        for x, y, z in zip(three, two, four):
             _same(x, y)
+            _same(z, y)
         for r in dc.solve_replicas(inst, "doch", a, b, X0, **kw):
             assert r.energy == dc.energy(inst.coupling, r.spins)
