@@ -252,19 +252,31 @@ int lanes_for_degree(double d) {
 // several times per solve (classify J, convert x0, CSR staging). Workers spin for a few
 // milliseconds after a job (the calls come in bursts) and then block.
 struct HostPool {
+  // A parallel loop is a set of blocks taken from a shared counter by the calling thread and by
+  // whichever workers are awake: a worker whose virtual CPU the host does not schedule for a
+  // while (measured: single uploads stalled 0.5-0.9 s when the loop waited for every worker's
+  // fixed share) only misses the blocks the others took. The loop is done when every block is;
+  // a worker that wakes after that finds the loop closed and never touches it.
   std::mutex run_mu;  // one parallel loop at a time
   std::mutex mu;
   std::condition_variable cv, cv_done;
   std::atomic<uint64_t> gen{0};
-  std::atomic<int> pending{0};
+  std::atomic<int> next{0}, done{0};
+  int nblk = 0, active = 0;
+  bool open = false;
   const std::function<void(int)>* job = nullptr;
-  int T = 0;
   std::vector<std::thread> th;
   explicit HostPool(int n) {
-    for (int i = 1; i < n; ++i) th.emplace_back([this, i] { loop(i); });
+    for (int i = 1; i < n; ++i) th.emplace_back([this] { loop(); });
   }
   int size() const { return int(th.size()) + 1; }
-  void loop(int id) {
+  void work() {  // blocks until none is left
+    for (int b; (b = next.fetch_add(1, std::memory_order_acq_rel)) < nblk;) {
+      (*job)(b);
+      done.fetch_add(1, std::memory_order_acq_rel);
+    }
+  }
+  void loop() {
     uint64_t seen = 0;
     for (;;) {
       // spin up to 3 ms: waking a blocked worker on these hosts (KVM guests) cost ~0.4 ms
@@ -277,31 +289,32 @@ struct HostPool {
         std::unique_lock<std::mutex> lk(mu);
         cv.wait(lk, [&] { return gen.load(std::memory_order_acquire) != seen; });
         seen = gen.load(std::memory_order_acquire);
+        if (!open) continue;  // that loop finished without this worker
+        ++active;
       }
-      if (id < T) (*job)(id);
-      if (pending.fetch_sub(1, std::memory_order_acq_rel) == 1) {
-        std::lock_guard<std::mutex> lk(mu);
-        cv_done.notify_one();
-      }
+      work();
+      std::lock_guard<std::mutex> lk(mu);
+      if (--active == 0) cv_done.notify_one();
     }
   }
-  void run(int t, const std::function<void(int)>& f) {
+  // f(b) for every block b in [0, blocks)
+  void run(int blocks, const std::function<void(int)>& f) {
     std::lock_guard<std::mutex> g(run_mu);
     {
       std::lock_guard<std::mutex> lk(mu);
       job = &f;
-      T = t;
-      pending.store(int(th.size()), std::memory_order_release);
+      nblk = blocks;
+      next.store(0, std::memory_order_relaxed);
+      done.store(0, std::memory_order_relaxed);
+      open = true;
       gen.fetch_add(1, std::memory_order_acq_rel);
     }
     cv.notify_all();
-    f(0);
-    const auto t0 = std::chrono::steady_clock::now();  // the workers' share ends within microseconds
-    while (pending.load(std::memory_order_acquire) != 0 &&
-           std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(1))
-      _mm_pause();
+    work();
+    while (done.load(std::memory_order_acquire) < blocks) _mm_pause();  // blocks other threads hold
     std::unique_lock<std::mutex> lk(mu);
-    cv_done.wait(lk, [&] { return pending.load(std::memory_order_acquire) == 0; });
+    open = false;  // late workers skip this loop
+    cv_done.wait(lk, [&] { return active == 0; });  // workers still inside finished their last block
   }
 };
 
@@ -324,8 +337,9 @@ HostPool& host_pool() {
   return *g_pool;
 }
 
-// f(lo, hi, t) over contiguous chunks [lo, hi) of [0, n), chunk t of T; chunk starts are
-// multiples of 64 elements so streaming stores (stream_fill) cover whole cache lines
+// f(lo, hi, t) over contiguous blocks [lo, hi) of [0, n), block t < 32 (callers keep one result
+// slot per block); block starts are multiples of 64 elements so streaming stores (stream_fill)
+// cover whole cache lines
 template <class F>
 static void par_for(int64_t n, F&& f, int max_threads = 32) {
   if (n < (int64_t(1) << 16)) {
@@ -333,13 +347,15 @@ static void par_for(int64_t n, F&& f, int max_threads = 32) {
     return;
   }
   HostPool& pool = host_pool();
-  const int T = std::max(1, std::min(pool.size(), max_threads));
-  const int64_t chunk = ((n + T - 1) / T + 63) / 64 * 64;
+  // up to 32 blocks (callers keep one result slot per block), two per thread
+  const int T = std::max(1, std::min({pool.size(), max_threads, 16}));
+  const int blocks = std::min(32, 2 * T);
+  const int64_t chunk = ((n + blocks - 1) / blocks + 63) / 64 * 64;
   const std::function<void(int)> body = [&](int t) {
     const int64_t lo = std::min(n, t * chunk), hi = std::min(n, lo + chunk);
     if (lo < hi) f(lo, hi, t);
   };
-  pool.run(T, body);
+  pool.run(blocks, body);
 }
 
 // dst[k] = f(k) for k in [lo, hi) with streaming (non-temporal) stores: the pinned staging
@@ -784,9 +800,7 @@ int dcx_set_csr_block(dcx_ctx* c, int64_t n_rows, int64_t n_cols, int64_t row_ba
 // with +-1 integer values, symmetric. Recognised here so the stencil pass (pass_torus,
 // dcx_csr.cu) can read two int8 bond arrays instead of the CSR.
 static void detect_torus(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, const int32_t* col, const int8_t* q) {
-  c->torus_L = 0;
-  c->bond_r.release();
-  c->bond_d.release();
+  c->torus_L = 0;  // the bond buffers are kept for a re-upload of the same size (no cudaFree / cudaMalloc)
   const int64_t L = int64_t(std::llround(std::sqrt(double(n))));
   if (L < 3 || L * L != n || nnz != 4 * n) return;
   std::vector<int8_t> br(n), bd(n), bl(n), bu(n);
@@ -822,10 +836,13 @@ static void detect_torus(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, 
     }
   });
   if (!ok) return;
+  PhaseClock pc("detect_torus");
+  pc.mark("classify bonds");
   c->bond_r.alloc(n);
   c->bond_d.alloc(n);
   CK(cudaMemcpy(c->bond_r.p, br.data(), n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->bond_d.p, bd.data(), n, cudaMemcpyHostToDevice));
+  pc.mark("bond upload");
   c->torus_L = L;
 }
 
@@ -909,6 +926,7 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
     c->row_base = row_base;
     c->nnz = nnz;
     CK(cudaStreamSynchronize(c->stream));
+    pc.mark("columns H2D wait");
     pc.mark("offsets+columns H2D");
     c->col16.release();
     if (n_cols <= 65536 && n == n_cols && nnz) {
@@ -930,9 +948,11 @@ static int upload_csr(dcx_ctx* c, int64_t n, int64_t nnz, const int64_t* ro, con
         if (b == 1) stream_fill(q8, lo, hi, [&](int64_t e) { return int8_t(rne(v[e] / scale)); });
         else stream_fill(q16, lo, hi, [&](int64_t e) { return int16_t(rne(v[e] / scale)); });
       });
+      pc.mark("values q");
       c->vint.alloc((nnz + 16) * b);
       CK(cudaMemset(static_cast<char*>(c->vint.p) + nnz * b, 0, 16 * b));
       CK(cudaMemcpy(c->vint.p, c->pin + qoff, nnz * b, cudaMemcpyHostToDevice));
+      pc.mark("values H2D");
       if (b == 1 && n == n_cols && row_base == 0) detect_torus(c, n, nnz, ro, c32, q8);
     pc.mark("values q + H2D");
     } else if (vk != VK_UNIFORM) {
